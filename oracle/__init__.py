@@ -1,0 +1,18 @@
+"""oracle/ -- TEST INFRASTRUCTURE for the B200 PSD-projection path. NOT PRODUCT CODE.
+
+A plain, slow, obviously-correct CPU implementation of what the hot path computes
+(arXiv:1912.02767, Rontsis/Goulart/Nakatsukasa, PAPER.md):
+
+  exact.py    Pi_{S+}(A) by its definition: cyclic Jacobi (jacobi.c,
+              GvL Alg. 8.5.3) then both closed forms V+L+V+^T and A - V-L-V-^T.
+  lobpcg.py   Rayleigh-Ritz (Alg. 2) and LOBPCG for the positive
+              eigenpairs (Alg. 3) step by step, with the side rule
+              (PAPER.md:505), negation and the Theorem-3 bound.
+  philox.py   Philox4x32-10 counter-based RNG + Box-Muller (the random expansion/cold
+              block of Alg. 3 line 8; generator reading R11 in DESIGN.md).
+  checks.py   Moreau/KKT certificate, Theorem-3 exact right-hand side (perp term by Jacobi).
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs
+may import this package. It shares no code with paper_1912_02767_b200/ and never imports it.
+Parity unpinned: none (every function is pinned in tests/test_oracle_*.py).
+"""
