@@ -1,0 +1,160 @@
+/*
+ * psdproj.h -- C ABI of the B200-native approximate PSD-cone projection
+ * (arXiv:1912.02767, Rontsis, Goulart & Nakatsukasa; PAPER.md in the reference tree).
+ *
+ * One call projects a symmetric fp64 matrix A onto the PSD cone,
+ *     Pi(A) = argmin_{X >= 0} ||A - X||_F = V+ L+ V+^T = A - V- L- V-^T
+ * computing only the smaller one-sided eigenspace with warm-started LOBPCG (Alg. 3,
+ * PAPER.md:398-412), certifying it with the Theorem-3 residual bound, and
+ * choosing the side with the one-third rule. All arithmetic runs in sm_100a
+ * kernels on the caller's stream; there is no CPU fallback.
+ *
+ * Conventions for every entry point:
+ *   - Matrices are fp64, column-major, DEVICE pointers unless the name says _host.
+ *     A must be exactly symmetric in storage (full storage, both triangles).
+ *     Since A is symmetric, row- and column-major are the same.
+ *   - lda/ldpi >= n. Pi may alias A (in-place projection) when ldpi == lda.
+ *   - The caller owns A, Pi and the workspace (sized by psdproj_workspace_bytes, cuBLAS
+ *     style). The context keeps pointers into the workspace; the warm block lives there.
+ *     psdproj_destroy frees only the host-side context, never caller memory.
+ *   - stream is a cudaStream_t passed as void* (NULL = legacy default stream). Calls are
+ *     stream-ordered and return when the info struct is final (host-synchronous).
+ *   - A context is used by one host thread and one stream at a time; distinct contexts may
+ *     run concurrently.
+ *   - Return codes: PSDPROJ_OK (0), PSDPROJ_NOT_CONVERGED (1: Pi and its bound are valid, the
+ *     per-pair residual test did not pass within max_iter), negative values are errors;
+ *     psdproj_last_error() gives a thread-local message. After E_CUDA the context is
+ *     poisoned and must be destroyed.
+ */
+#ifndef PSDPROJ_H
+#define PSDPROJ_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  PSDPROJ_OK = 0,
+  PSDPROJ_NOT_CONVERGED = 1,
+  PSDPROJ_E_INVALID = -1,    /* bad argument; state untouched                               */
+  PSDPROJ_E_NONFINITE = -2,  /* A holds inf/nan (detected in the first pass)                */
+  PSDPROJ_E_CUDA = -3,       /* CUDA runtime error; context poisoned                         */
+  PSDPROJ_E_DEGENERATE = -4, /* pencil not positive definite after dropping P (R20)          */
+  PSDPROJ_E_NCCL = -5,       /* reserved for the row-sharded mode                            */
+  PSDPROJ_E_WORKSPACE = -6,  /* workspace too small / misaligned (needs 256-byte alignment)  */
+  PSDPROJ_E_CAPACITY = -7    /* block width would exceed m_max (no silent fallback)          */
+};
+
+enum { PSDPROJ_SIDE_AUTO = 0, PSDPROJ_SIDE_POS = 1, PSDPROJ_SIDE_NEG = -1, PSDPROJ_SIDE_DIRECT = 2 };
+enum { PSDPROJ_LOCK_SOFT = 1, PSDPROJ_LOCK_HARD = 2 };
+
+typedef struct psdproj_ctx_s* psdproj_ctx;
+
+typedef struct {
+  int max_iter;   /* LOBPCG iteration cap (paper silent, R22); default 500                      */
+  int m0;         /* cold block width; 0 => max(ceil(0.1 n), 1) (R28)                          */
+  int expand_q;   /* expansion quantum; 0 => max(ceil(0.05 n), 1) (R9)                         */
+  int guard;      /* minimum non-positive guard columns (R8, R12); default 1                    */
+  int side;       /* PSDPROJ_SIDE_*: 0 = one-third rule                          */
+  int locking;    /* PSDPROJ_LOCK_SOFT (BLOPEX active mask) or _HARD (default, R35)             */
+  int keep_extra; /* non-positive columns kept in the warm block; <0 => max(guard, ceil(p/10))  */
+  int m_max;      /* block-width capacity; 0 => ceil(n/3)+1 (wider => DIRECT, R18)              */
+  uint64_t seed;  /* Philox4x32-10 key (R11)                                                    */
+  uint32_t ctx_id;/* Philox counter word c2 (distinct per cone block)                           */
+  int profile;    /* 1: time every block-multiply (a3) launch with CUDA events into info        */
+  int host_io;    /* 1: workspace also holds an n x n staging buffer for psdproj_project_host   */
+} psdproj_params;
+
+typedef struct {
+  int status;       /* return code of the call                                                */
+  int side;         /* side used: +1, -1, or 2 (DIRECT)                                        */
+  int iters;        /* LOBPCG iterations                                                       */
+  int m;            /* final block width                                                       */
+  int npos;         /* kept pairs (positive Ritz values on the computed side)                  */
+  int expansions;   /* random expansions (Alg. 3 line 8)                                       */
+  int a_passes;     /* block multiplies B.Z issued                                             */
+  int cold;         /* 1 if the call started cold                                              */
+  int rr_max;       /* largest Rayleigh-Ritz basis width s                                     */
+  int locked;       /* hard-locked columns at exit                                             */
+  long long a_cols; /* total columns multiplied by A                                           */
+  double err_bound; /* Theorem-3 bound on ||Pi~ - Pi(A)||_F (perp term 0)        */
+  double resid_fro; /* ||R+||_F over the kept pairs                                           */
+  double resid_max; /* max_i r_i over the kept pairs                                          */
+  double lock_defect; /* ||V+^T B V+ - diag(theta+)||_F (hard locking term, R36)             */
+  double anorm_f;   /* ||A||_F                                                                 */
+  double flops;     /* algorithmic flops of the call                           */
+  double bytes;     /* algorithmic HBM bytes of the call                                       */
+  double amul_flops;/* flops of the block multiplies (2 n^2 sum of columns)                    */
+  double amul_bytes;/* bytes of the block multiplies (8 n^2 per pass)                          */
+  double amul_ms;   /* summed device time of the block multiplies (profile = 1)                */
+  int amul_launches;/* number of timed block-multiply launches                                 */
+  int last_pos, last_neg; /* sign counts fed to the next call's side rule                      */
+} psdproj_info;
+
+/* Fill *p with the defaults documented above. */
+void psdproj_default_params(psdproj_params* p);
+
+/* Device workspace needed by a context of order n with these params (NULL = defaults). */
+size_t psdproj_workspace_bytes(int n, const psdproj_params* p);
+
+/* Create a context over caller-owned device workspace ws (>= workspace_bytes, 256-B aligned). */
+int psdproj_create(int n, const psdproj_params* p, void* ws, size_t ws_bytes, psdproj_ctx* out);
+
+/* Project A (device, n x n, lda) into Pi (device, ldpi). tol: absolute per-pair residual
+ * 2-norm threshold. info may be NULL. */
+int psdproj_project(psdproj_ctx ctx, const double* A, int lda, double* Pi, int ldpi, double tol,
+                    void* stream, psdproj_info* info);
+
+/* Same, with HOST A and Pi (pinned or pageable): H2D copy of A, projection, D2H copy of Pi,
+ * all on `stream` inside the call (the end-to-end path). */
+int psdproj_project_host(psdproj_ctx ctx, const double* A_host, int lda, double* Pi_host, int ldpi,
+                         double tol, void* stream, psdproj_info* info);
+
+/* Batched: count independent contexts (one per cone block, possibly different n), issued in
+ * order on one stream. Per-item status in infos[i].status; returns the worst status. */
+int psdproj_project_batched(psdproj_ctx* ctxs, int count, const double* const* A, const int* lda,
+                            double* const* Pi, const int* ldpi, const double* tol, void* stream,
+                            psdproj_info* infos);
+
+/* Warm block of the last call: vals_host (cap values, descending Ritz values of the side used,
+ * sign as computed on B = side*A), vecs_dev (n x cap, ldv) may be NULL. Returns the count. */
+int psdproj_get_ritz(psdproj_ctx ctx, double* vals_host, int cap, double* vecs_dev, int ldv);
+
+/* Drop the warm state: the next call is cold and uses the side hint / positive side. */
+int psdproj_reset(psdproj_ctx ctx);
+
+/* Free the host-side context (never the caller's workspace). */
+int psdproj_destroy(psdproj_ctx ctx);
+
+/* Thread-local message of the last error ("" if none). */
+const char* psdproj_last_error(void);
+
+/* ---- kernel-level entry points (tests and benchmarks call the same kernels the path uses) ---- */
+
+/* C = alpha op(A) op(B) + beta C, column-major, opA/opB: 0 = N, 1 = T. ws: device scratch of
+ * ws_elems doubles for split-K partials (may be NULL). Device pointers. */
+int psdproj_dgemm(int opA, int opB, int M, int N, int K, double alpha, const double* A, int lda,
+                  const double* B, int ldb, double beta, double* C, int ldc, double* ws,
+                  size_t ws_elems, void* stream);
+
+/* Symmetric eigendecomposition by parallel-order Jacobi (a7/a13): A (s x s, device) ->
+ * w (s, ascending, device) and V (s x s, ldv, device). ws: device scratch of
+ * psdproj_jacobi_ws_elems(s) doubles. Returns sweeps (>0) or a negative code. */
+size_t psdproj_jacobi_ws_elems(int s);
+int psdproj_jacobi(int s, const double* A, int lda, double* w, double* V, int ldv, double* ws,
+                   void* stream);
+
+/* Raw Philox4x32-10 stream: out[4i+j] for counters (i, c1, c2, c3), key (k0, k1), device out. */
+int psdproj_philox_raw(int count, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0, uint32_t k1,
+                       uint32_t* out, void* stream);
+
+/* n x q N(0,1) block with the expansion mapping of R11 (device out, ld). */
+int psdproj_philox_gauss(int n, int q, double* out, int ld, uint64_t seed, uint32_t stream_id,
+                         uint32_t ctx, uint32_t tag, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PSDPROJ_H */

@@ -1,0 +1,570 @@
+// kernels.cuh -- non-GEMM kernels of the psdproj path (sm_100a).
+//
+//   resid_norm      a4: R = B X - X diag(theta), r_j = ||R_:,j||_2
+//   colnorm/scale   unit-column scaling of the residual / direction blocks (R6, §8.c.3 4.4)
+//   gather_cols     active-set compaction (BLOPEX active mask)
+//   philox_gauss    cold block / random expansion (Alg. 3 line 8; R11)
+//   insert_known    known Gram blocks X^T X = I, X^T B X = Theta (a5)
+//   cholesky / trinv  implicit Cholesky-QR of the pencil (a6)
+//   jacobi_*        Rayleigh-Ritz eigensolve of L^-1 H L^-T (a7, Alg. 2) and the
+//                   DIRECT full eigendecomposition (a13)
+//   sort_desc       Ritz values in descending order, "the m largest"
+//   symmetrize      exact symmetry of Pi (R24)
+// Every reduction is a fixed-order tree (deterministic, R25).
+#pragma once
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+
+namespace psd {
+namespace cg = cooperative_groups;
+
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    v = (l < NT / 32) ? red[l] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (l == 0) red[0] = v;
+  }
+  __syncthreads();
+  double r = red[0];
+  __syncthreads();
+  return r;
+}
+
+// ---------------------------------------------------------------- a4 residual + norms
+// one CTA per column; R may be null (norms only). theta_sign: B = s*A already folded in BX.
+template <int NT>
+__global__ void __launch_bounds__(NT) resid_norm_kernel(int n, const double* __restrict__ X, int ldx,
+                                                        const double* __restrict__ BX, int ldb,
+                                                        const double* __restrict__ theta, double* __restrict__ R,
+                                                        int ldr, double* __restrict__ rnorm) {
+  __shared__ double red[32];
+  int j = blockIdx.x;
+  double th = theta[j];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < n; i += NT) {
+    double v = BX[IDX(i, j, ldb)] - th * X[IDX(i, j, ldx)];
+    if (R) R[IDX(i, j, ldr)] = v;
+    acc += v * v;
+  }
+  acc = block_sum<NT>(acc, red);
+  if (threadIdx.x == 0) rnorm[j] = sqrt(acc);
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) colnorm_kernel(int n, const double* __restrict__ Z, int ld,
+                                                     double* __restrict__ out) {
+  __shared__ double red[32];
+  int j = blockIdx.x;
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < n; i += NT) {
+    double v = Z[IDX(i, j, ld)];
+    acc += v * v;
+  }
+  acc = block_sum<NT>(acc, red);
+  if (threadIdx.x == 0) out[j] = sqrt(acc);
+}
+
+// Z[:, j] /= norm[j] (and Z2 likewise when given); zero norms leave the column unchanged.
+__global__ void scale_cols_kernel(int n, int cols, double* __restrict__ Z, int ld, double* __restrict__ Z2, int ld2,
+                                  const double* __restrict__ norm) {
+  size_t total = (size_t)n * cols;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+    int i = (int)(e % n), j = (int)(e / n);
+    double s = norm[j];
+    if (s > 0.0) {
+      double inv = 1.0 / s;
+      Z[IDX(i, j, ld)] *= inv;
+      if (Z2) Z2[IDX(i, j, ld2)] *= inv;
+    }
+  }
+}
+
+__global__ void gather_cols_kernel(int n, int cols, double* __restrict__ dst, int ldd, const double* __restrict__ src,
+                                   int lds, const int* __restrict__ idx) {
+  size_t total = (size_t)n * cols;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+    int i = (int)(e % n), j = (int)(e / n);
+    dst[IDX(i, j, ldd)] = src[IDX(i, idx[j], lds)];
+  }
+}
+
+// dst[:, j] = src[:, j] * w[j]
+__global__ void scale_copy_cols_kernel(int n, int cols, double* __restrict__ dst, int ldd,
+                                       const double* __restrict__ src, int lds, const double* __restrict__ w) {
+  size_t total = (size_t)n * cols;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+    int i = (int)(e % n), j = (int)(e / n);
+    dst[IDX(i, j, ldd)] = src[IDX(i, j, lds)] * w[j];
+  }
+}
+
+// ---------------------------------------------------------------- Philox4x32-10 (R11)
+__device__ __forceinline__ void philox10(uint32_t c[4], uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    uint32_t hi0 = __umulhi(0xD2511F53u, c[0]), lo0 = 0xD2511F53u * c[0];
+    uint32_t hi1 = __umulhi(0xCD9E8D57u, c[2]), lo1 = 0xCD9E8D57u * c[2];
+    uint32_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
+    c[0] = n0; c[1] = lo1; c[2] = n2; c[3] = lo0;
+    k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
+  }
+}
+
+// raw uint32 stream (tests): out[4*i + j] = philox(counter=(i, c1, c2, c3), key)
+__global__ void philox_raw_kernel(int count, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0, uint32_t k1,
+                                  uint32_t* __restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) {
+    uint32_t c[4] = {(uint32_t)i, c1, c2, c3};
+    philox10(c, k0, k1);
+    out[4 * i + 0] = c[0]; out[4 * i + 1] = c[1]; out[4 * i + 2] = c[2]; out[4 * i + 3] = c[3];
+  }
+}
+
+__device__ __forceinline__ double u53(uint32_t a, uint32_t b) {
+  return ((double)(a >> 5) * 67108864.0 + (double)(b >> 6) + 0.5) * (1.0 / 9007199254740992.0);
+}
+
+// n x q standard normal block: linear index l = i + j*n; counter (l>>1, stream, ctx, tag)
+__global__ void philox_gauss_kernel(int n, int q, double* __restrict__ dst, int ld, uint64_t seed, uint32_t stream,
+                                    uint32_t ctx, uint32_t tag) {
+  int64_t total = (int64_t)n * q;
+  int64_t npairs = (total + 1) / 2;
+  for (int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; h < npairs; h += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t c[4] = {(uint32_t)h, stream, ctx, tag};
+    philox10(c, (uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32));
+    double u1 = u53(c[0], c[1]), u2 = u53(c[2], c[3]);
+    double rad = sqrt(-2.0 * log(u1));
+    double sv, cv;
+    sincospi(2.0 * u2, &sv, &cv);
+    int64_t l0 = 2 * h, l1 = 2 * h + 1;
+    dst[IDX(l0 % n, l0 / n, ld)] = rad * cv;
+    if (l1 < total) dst[IDX(l1 % n, l1 / n, ld)] = rad * sv;
+  }
+}
+
+// ---------------------------------------------------------------- a5 known blocks
+// G, H (s x s, ld): symmetrise ((M + M^T)/2) and insert G[:kxG,:kxG] = I, H[:kxH,:kxH] = diag(theta).
+__global__ void insert_known_kernel(int s, int kxG, int kxH, double* __restrict__ G, double* __restrict__ H, int ld,
+                                    const double* __restrict__ theta) {
+  int total = s * s;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    int i = e % s, j = e / s;
+    if (i > j) continue;
+    double g = (j < kxG) ? ((i == j) ? 1.0 : 0.0) : 0.5 * (G[IDX(i, j, ld)] + G[IDX(j, i, ld)]);
+    double h = (j < kxH) ? ((i == j) ? theta[i] : 0.0) : 0.5 * (H[IDX(i, j, ld)] + H[IDX(j, i, ld)]);
+    G[IDX(i, j, ld)] = g; G[IDX(j, i, ld)] = g;
+    H[IDX(i, j, ld)] = h; H[IDX(j, i, ld)] = h;
+  }
+}
+
+// ---------------------------------------------------------------- a6 Cholesky (one CTA)
+// In place on the lower triangle of G (s x s, ld). Fails (status = j+1) when a pivot is
+// <= fail_rel * max diag(G) (R20). Upper triangle is zeroed on success.
+template <int NT>
+__global__ void __launch_bounds__(NT) cholesky_kernel(int s, double* __restrict__ G, int ld, double fail_rel,
+                                                      int* __restrict__ status) {
+  __shared__ double red[32];
+  __shared__ double sh_ljj;
+  __shared__ int sh_fail;
+  double mx = 0.0;
+  for (int i = threadIdx.x; i < s; i += NT) mx = fmax(mx, G[IDX(i, i, ld)]);
+  // max reduction
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int w = 0; w < NT / 32; ++w) m = fmax(m, red[w]);
+    red[0] = m;
+    sh_fail = 0;
+  }
+  __syncthreads();
+  const double floor_ = fail_rel * red[0];
+  for (int j = 0; j < s; ++j) {
+    if (threadIdx.x == 0) {
+      double d = G[IDX(j, j, ld)];
+      if (!(d > floor_)) {
+        sh_fail = j + 1;
+      } else {
+        sh_ljj = sqrt(d);
+        G[IDX(j, j, ld)] = sh_ljj;
+      }
+    }
+    __syncthreads();
+    if (sh_fail) break;
+    double inv = 1.0 / sh_ljj;
+    for (int i = j + 1 + threadIdx.x; i < s; i += NT) G[IDX(i, j, ld)] *= inv;
+    __syncthreads();
+    // trailing update of the lower triangle: G[i][k] -= L[i][j] L[k][j], j < k <= i
+    int rem = s - j - 1;
+    int64_t cnt = (int64_t)rem * (rem + 1) / 2;
+    for (int64_t e = threadIdx.x; e < cnt; e += NT) {
+      // column-wise enumeration of the lower triangle of the trailing (rem x rem) block
+      int k = (int)((sqrt(8.0 * (double)e + 1.0) - 1.0) * 0.5);  // row of packed upper index
+      // map e -> (kk, ii) with kk <= ii over a triangle: use k as the "column" of length rem-k
+      // simple robust decode: walk from estimate
+      int64_t base = (int64_t)k * (k + 1) / 2;
+      while (base > e) { --k; base = (int64_t)k * (k + 1) / 2; }
+      while ((int64_t)(k + 1) * (k + 2) / 2 <= e) { ++k; base = (int64_t)k * (k + 1) / 2; }
+      int ii = k, kk = (int)(e - base);  // 0 <= kk <= ii < rem
+      int gi = j + 1 + ii, gk = j + 1 + kk;
+      G[IDX(gi, gk, ld)] -= G[IDX(gi, j, ld)] * G[IDX(gk, j, ld)];
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *status = sh_fail;
+  if (!sh_fail) {
+    for (int e = threadIdx.x; e < s * s; e += NT) {
+      int i = e % s, k = e / s;
+      if (i < k) G[IDX(i, k, ld)] = 0.0;
+    }
+  }
+}
+
+// Linv = L^-1 (lower triangular), one warp per column j: x = L^-1 e_j by forward substitution.
+__global__ void trinv_kernel(int s, const double* __restrict__ L, int ldl, double* __restrict__ Li, int ldi) {
+  int warps = (blockDim.x >> 5) * gridDim.x;
+  int lane = threadIdx.x & 31;
+  for (int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); j < s; j += warps) {
+    for (int i = lane; i < j; i += 32) Li[IDX(i, j, ldi)] = 0.0;
+    for (int i = j; i < s; ++i) {
+      double acc = 0.0;
+      for (int k = j + lane; k < i; k += 32) acc += L[IDX(i, k, ldl)] * Li[IDX(k, j, ldi)];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) Li[IDX(i, j, ldi)] = ((i == j ? 1.0 : 0.0) - acc) / L[IDX(i, i, ldl)];
+      __syncwarp();
+    }
+  }
+}
+
+// ---------------------------------------------------------------- a7 / a13 Jacobi
+// Parallel-order (round-robin "circle method") two-sided Jacobi. N = s rounded up to even;
+// a zero row/column pads odd s (its rotations never trigger). Round r pairs
+//   k = 0: (r, N-1);  k >= 1: ((r + k) mod (N-1), (r - k) mod (N-1)),
+// all N/2 rotations of a round are disjoint, so the 2x2 blocks (pair k1 x pair k2) of
+// J^T A J update independently; the annihilated diagonal blocks are set exactly
+// (a_pp - t a_pq, a_qq + t a_pq, 0) as in GvL §8.5.2. Skip test as in the oracle (R-J1):
+//   |a_pq| <= u sqrt(|a_pp a_qq|) or |a_pq| <= u ||A||_F / s; stop after a rotation-free sweep.
+__device__ __forceinline__ void rr_pair(int r, int k, int N, int& p, int& q) {
+  int a, b;
+  if (k == 0) {
+    a = r; b = N - 1;
+  } else {
+    a = (r + k) % (N - 1);
+    b = (r - k + (N - 1)) % (N - 1);
+  }
+  p = min(a, b); q = max(a, b);
+}
+
+constexpr int JAC_SMEM_MAX = 112;
+
+// One CTA; A (s x s, lda) symmetric input; outputs w (s, unsorted) and V (s x s, ldv).
+// info[0] = sweeps performed (-1: no convergence within max_sweeps).
+template <int NT>
+__global__ void __launch_bounds__(NT) jacobi_smem_kernel(int s, const double* __restrict__ A, int lda,
+                                                         double* __restrict__ w, double* __restrict__ V, int ldv,
+                                                         int max_sweeps, int* __restrict__ info) {
+  extern __shared__ __align__(16) double sm[];
+  const int N = s + (s & 1);
+  const int H = N / 2;
+  double* M = sm;                 // N x N (col-major, ld N)
+  double* Q = sm + N * N;         // N x N
+  __shared__ double c_[JAC_SMEM_MAX / 2 + 1], s_[JAC_SMEM_MAX / 2 + 1], t_[JAC_SMEM_MAX / 2 + 1];
+  __shared__ int p_[JAC_SMEM_MAX / 2 + 1], q_[JAC_SMEM_MAX / 2 + 1], act_[JAC_SMEM_MAX / 2 + 1];
+  __shared__ double red[32];
+  __shared__ int rot;
+  double fro = 0.0;
+  for (int e = threadIdx.x; e < N * N; e += NT) {
+    int i = e % N, j = e / N;
+    double v = 0.0;
+    if (i < s && j < s) v = 0.5 * (A[IDX(i, j, lda)] + A[IDX(j, i, lda)]);
+    M[e] = v;
+    Q[e] = (i == j) ? 1.0 : 0.0;
+    fro += v * v;
+  }
+  fro = sqrt(block_sum<NT>(fro, red));
+  const double afloor = PSD_U * fro / (double)max(s, 1);
+  int sweep = 0;
+  bool done = (N <= 1);
+  while (!done && sweep < max_sweeps) {
+    if (threadIdx.x == 0) rot = 0;
+    __syncthreads();
+    for (int r = 0; r < N - 1; ++r) {
+      for (int k = threadIdx.x; k < H; k += NT) {
+        int p, q;
+        rr_pair(r, k, N, p, q);
+        double app = M[p + p * N], aqq = M[q + q * N], apq = M[p + q * N];
+        int a = !(fabs(apq) <= PSD_U * sqrt(fabs(app) * fabs(aqq)) || fabs(apq) <= afloor);
+        double c = 1.0, sn = 0.0, t = 0.0;
+        if (a) schur2(app, apq, aqq, c, sn, t);
+        p_[k] = p; q_[k] = q; c_[k] = c; s_[k] = sn; t_[k] = t; act_[k] = a;
+        if (a) rot = 1;
+      }
+      __syncthreads();
+      // A <- J^T A J on 2x2 blocks (k1 <= k2), mirrored
+      const int nb = H * (H + 1) / 2;
+      for (int b = threadIdx.x; b < nb; b += NT) {
+        // decode b -> (k1, k2), k1 <= k2 (row-major upper triangle)
+        int k1 = (int)((2 * H + 1 - sqrt((double)(2 * H + 1) * (2 * H + 1) - 8.0 * b)) * 0.5);
+        int base = k1 * H - k1 * (k1 - 1) / 2;
+        while (base > b) { --k1; base = k1 * H - k1 * (k1 - 1) / 2; }
+        while (base + (H - k1) <= b) { base += H - k1; ++k1; }
+        int k2 = k1 + (b - base);
+        int a1 = act_[k1], a2 = act_[k2];
+        if (!a1 && !a2) continue;
+        int p1 = p_[k1], q1 = q_[k1], p2 = p_[k2], q2 = q_[k2];
+        if (k1 == k2) {
+          double apq = M[p1 + q1 * N], t = t_[k1];
+          M[p1 + p1 * N] -= t * apq;
+          M[q1 + q1 * N] += t * apq;
+          M[p1 + q1 * N] = 0.0; M[q1 + p1 * N] = 0.0;
+          continue;
+        }
+        double c1 = c_[k1], s1 = s_[k1], c2 = c_[k2], s2 = s_[k2];
+        double b00 = M[p1 + p2 * N], b01 = M[p1 + q2 * N], b10 = M[q1 + p2 * N], b11 = M[q1 + q2 * N];
+        // rows: J1^T
+        double x00 = c1 * b00 - s1 * b10, x01 = c1 * b01 - s1 * b11;
+        double x10 = s1 * b00 + c1 * b10, x11 = s1 * b01 + c1 * b11;
+        // cols: J2
+        double y00 = c2 * x00 - s2 * x01, y01 = s2 * x00 + c2 * x01;
+        double y10 = c2 * x10 - s2 * x11, y11 = s2 * x10 + c2 * x11;
+        M[p1 + p2 * N] = y00; M[p1 + q2 * N] = y01; M[q1 + p2 * N] = y10; M[q1 + q2 * N] = y11;
+        M[p2 + p1 * N] = y00; M[q2 + p1 * N] = y01; M[p2 + q1 * N] = y10; M[q2 + q1 * N] = y11;
+      }
+      // V <- V J
+      for (int e = threadIdx.x; e < N * H; e += NT) {
+        int i = e % N, k = e / N;
+        if (!act_[k]) continue;
+        int p = p_[k], q = q_[k];
+        double c = c_[k], sn = s_[k];
+        double vp = Q[i + p * N], vq = Q[i + q * N];
+        Q[i + p * N] = c * vp - sn * vq;
+        Q[i + q * N] = sn * vp + c * vq;
+      }
+      __syncthreads();
+    }
+    ++sweep;
+    __syncthreads();
+    done = (rot == 0);
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < s; i += NT) w[i] = M[i + i * N];
+  for (int e = threadIdx.x; e < s * s; e += NT) {
+    int i = e % s, j = e / s;
+    V[IDX(i, j, ldv)] = Q[i + j * N];
+  }
+  if (threadIdx.x == 0) { info[0] = done ? sweep : -1; info[1] = 0; }
+}
+
+// Cooperative multi-CTA variant for s > JAC_SMEM_MAX: the matrix is double-buffered in
+// global memory (Ma -> Mb each round); each thread recomputes the two rotations of its
+// block from the read buffer, so one grid barrier per round suffices. Only blocks k1 <= k2
+// are computed and mirrored (exact symmetry). Q is updated in place (disjoint columns).
+// counters[max_sweeps+1] are zeroed by the host; afloor = afl_scale * ||A||_F (*d_fro).
+__device__ __forceinline__ void decode_upper(int64_t b, int H, int& k1, int& k2) {
+  double hh = 2.0 * H + 1.0;
+  int r = (int)((hh - sqrt(hh * hh - 8.0 * (double)b)) * 0.5);
+  r = max(0, min(r, H - 1));
+  int64_t base = (int64_t)r * H - (int64_t)r * (r - 1) / 2;
+  while (r > 0 && base > b) { --r; base = (int64_t)r * H - (int64_t)r * (r - 1) / 2; }
+  while (base + (H - r) <= b) { base += H - r; ++r; }
+  k1 = r;
+  k2 = r + (int)(b - base);
+}
+
+__device__ __forceinline__ int jac_active(double app, double aqq, double apq, double afloor) {
+  return !(fabs(apq) <= PSD_U * sqrt(fabs(app) * fabs(aqq)) || fabs(apq) <= afloor);
+}
+
+__global__ void jacobi_coop_kernel(int s, int N, double* __restrict__ Ma, double* __restrict__ Mb,
+                                   double* __restrict__ Q, const double* __restrict__ d_fro, double afl_scale,
+                                   int max_sweeps, int* __restrict__ counters, int* __restrict__ info) {
+  cg::grid_group grid = cg::this_grid();
+  const int H = N / 2;
+  const int64_t nb = (int64_t)H * (H + 1) / 2;
+  const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t gsz = (int64_t)gridDim.x * blockDim.x;
+  const double afloor = afl_scale * d_fro[0];
+  double* cur = Ma;
+  double* nxt = Mb;
+  int sweep = 0;
+  bool done = (N <= 1);
+  while (!done && sweep < max_sweeps) {
+    for (int r = 0; r < N - 1; ++r) {
+      for (int64_t b = gtid; b < nb; b += gsz) {
+        int k1, k2;
+        decode_upper(b, H, k1, k2);
+        int p1, q1, p2, q2;
+        rr_pair(r, k1, N, p1, q1);
+        double c1 = 1, s1 = 0, t1 = 0, c2 = 1, s2 = 0, t2 = 0;
+        double app = cur[IDX(p1, p1, N)], aqq = cur[IDX(q1, q1, N)], apq = cur[IDX(p1, q1, N)];
+        int a1 = jac_active(app, aqq, apq, afloor);
+        if (a1) schur2(app, apq, aqq, c1, s1, t1);
+        if (k1 == k2) {
+          if (a1) {
+            atomicAdd(&counters[sweep], 1);
+            nxt[IDX(p1, p1, N)] = app - t1 * apq;
+            nxt[IDX(q1, q1, N)] = aqq + t1 * apq;
+            nxt[IDX(p1, q1, N)] = 0.0;
+            nxt[IDX(q1, p1, N)] = 0.0;
+          } else {
+            nxt[IDX(p1, p1, N)] = app;
+            nxt[IDX(q1, q1, N)] = aqq;
+            nxt[IDX(p1, q1, N)] = apq;
+            nxt[IDX(q1, p1, N)] = apq;
+          }
+          continue;
+        }
+        rr_pair(r, k2, N, p2, q2);
+        double bpp = cur[IDX(p2, p2, N)], bqq = cur[IDX(q2, q2, N)], bpq = cur[IDX(p2, q2, N)];
+        int a2 = jac_active(bpp, bqq, bpq, afloor);
+        if (a2) schur2(bpp, bpq, bqq, c2, s2, t2);
+        double b00 = cur[IDX(p1, p2, N)], b01 = cur[IDX(p1, q2, N)], b10 = cur[IDX(q1, p2, N)],
+               b11 = cur[IDX(q1, q2, N)];
+        double x00 = c1 * b00 - s1 * b10, x01 = c1 * b01 - s1 * b11;
+        double x10 = s1 * b00 + c1 * b10, x11 = s1 * b01 + c1 * b11;
+        double y00 = c2 * x00 - s2 * x01, y01 = s2 * x00 + c2 * x01;
+        double y10 = c2 * x10 - s2 * x11, y11 = s2 * x10 + c2 * x11;
+        nxt[IDX(p1, p2, N)] = y00; nxt[IDX(p1, q2, N)] = y01; nxt[IDX(q1, p2, N)] = y10; nxt[IDX(q1, q2, N)] = y11;
+        nxt[IDX(p2, p1, N)] = y00; nxt[IDX(q2, p1, N)] = y01; nxt[IDX(p2, q1, N)] = y10; nxt[IDX(q2, q1, N)] = y11;
+      }
+      for (int64_t e = gtid; e < (int64_t)N * H; e += gsz) {
+        int i = (int)(e % N), k = (int)(e / N);
+        int p, q;
+        rr_pair(r, k, N, p, q);
+        double app = cur[IDX(p, p, N)], aqq = cur[IDX(q, q, N)], apq = cur[IDX(p, q, N)];
+        if (!jac_active(app, aqq, apq, afloor)) continue;
+        double c, sn, t;
+        schur2(app, apq, aqq, c, sn, t);
+        double vp = Q[IDX(i, p, N)], vq = Q[IDX(i, q, N)];
+        Q[IDX(i, p, N)] = c * vp - sn * vq;
+        Q[IDX(i, q, N)] = sn * vp + c * vq;
+      }
+      grid.sync();
+      double* tmp = cur; cur = nxt; nxt = tmp;
+    }
+    done = (*(volatile int*)&counters[sweep] == 0);
+    ++sweep;
+  }
+  if (gtid == 0) {
+    info[0] = done ? sweep : -1;
+    info[1] = (cur == Ma) ? 0 : 1;  // which buffer holds the result
+  }
+}
+
+// load symmetric (s x s, lda) into an N x N zero-padded buffer; Q = I
+__global__ void jacobi_prep_kernel(int s, int N, const double* __restrict__ A, int lda, double* __restrict__ M,
+                                   double* __restrict__ Q) {
+  int64_t total = (int64_t)N * N;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    int i = (int)(e % N), j = (int)(e / N);
+    double v = 0.0;
+    if (i < s && j < s) v = 0.5 * (A[IDX(i, j, lda)] + A[IDX(j, i, lda)]);
+    M[e] = v;
+    Q[e] = (i == j) ? 1.0 : 0.0;
+  }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) fro_kernel(int64_t count, const double* __restrict__ M, double* __restrict__ out) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  for (int64_t e = threadIdx.x; e < count; e += NT) acc += M[e] * M[e];
+  acc = block_sum<NT>(acc, red);
+  if (threadIdx.x == 0) out[0] = sqrt(acc);
+}
+
+// extract diag / V (s x s) from the padded Jacobi buffers (info[1] selects Ma or Mb)
+__global__ void jacobi_extract_kernel(int s, int N, const double* __restrict__ Ma, const double* __restrict__ Mb,
+                                      const double* __restrict__ Q, const int* __restrict__ info,
+                                      double* __restrict__ w, double* __restrict__ V, int ldv) {
+  const double* M = info[1] ? Mb : Ma;
+  int64_t total = (int64_t)s * s;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    int i = (int)(e % s), j = (int)(e / s);
+    V[IDX(i, j, ldv)] = Q[IDX(i, j, N)];
+    if (i == j) w[i] = M[IDX(i, i, N)];
+  }
+}
+
+// rank sort, descending, ties by index (R21): order[rank] = i, wsorted[rank] = w[i]
+__global__ void sort_desc_kernel(int s, const double* __restrict__ w, int* __restrict__ order,
+                                 double* __restrict__ wsorted) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < s; i += gridDim.x * blockDim.x) {
+    double wi = w[i];
+    int rank = 0;
+    for (int j = 0; j < s; ++j) {
+      double wj = w[j];
+      rank += (wj > wi) || (wj == wi && j < i);
+    }
+    order[rank] = i;
+    wsorted[rank] = wi;
+  }
+}
+
+// ||H - diag(theta)||_F over an s x s block (bound term of hard locking, R36)
+template <int NT>
+__global__ void __launch_bounds__(NT) offdiag_fro_kernel(int s, const double* __restrict__ H, int ld,
+                                                         const double* __restrict__ theta, double* __restrict__ out) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  for (int64_t e = threadIdx.x; e < (int64_t)s * s; e += NT) {
+    int i = (int)(e % s), j = (int)(e / s);
+    double v = H[IDX(i, j, ld)] - (i == j ? theta[i] : 0.0);
+    acc += v * v;
+  }
+  acc = block_sum<NT>(acc, red);
+  if (threadIdx.x == 0) out[0] = sqrt(acc);
+}
+
+// P = (P + P^T)/2 in place (n x n, ld)
+__global__ void symmetrize_kernel(int n, double* __restrict__ P, int ld) {
+  int64_t total = (int64_t)n * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    int i = (int)(e % n), j = (int)(e / n);
+    if (i >= j) continue;
+    double a = P[IDX(i, j, ld)], b = P[IDX(j, i, ld)];
+    double v = 0.5 * (a + b);
+    P[IDX(i, j, ld)] = v;
+    P[IDX(j, i, ld)] = v;
+  }
+}
+
+// non-finite scan (E_NONFINITE, R-first pass): flag[0] |= 1 if any entry is inf/nan
+__global__ void nonfinite_kernel(int n, const double* __restrict__ A, int lda, int* __restrict__ flag) {
+  int64_t total = (int64_t)n * n;
+  int bad = 0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    int i = (int)(e % n), j = (int)(e / n);
+    if (!isfinite(A[IDX(i, j, lda)])) bad = 1;
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
+// Frobenius norm partials: out[block] = sum of squares of its slice (second pass on host order)
+__global__ void fro_partial_kernel(int n, const double* __restrict__ A, int lda, double* __restrict__ out) {
+  __shared__ double red[32];
+  int64_t total = (int64_t)n * n;
+  double acc = 0.0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    int i = (int)(e % n), j = (int)(e / n);
+    double v = A[IDX(i, j, lda)];
+    acc += v * v;
+  }
+  acc = block_sum<256>(acc, red);
+  if (threadIdx.x == 0) out[blockIdx.x] = acc;
+}
+
+}  // namespace psd

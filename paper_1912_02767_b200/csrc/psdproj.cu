@@ -1,0 +1,1000 @@
+// psdproj.cu -- C ABI + host orchestration of the warm-started LOBPCG PSD-cone projection.
+//
+// The LOBPCG control flow (convergence, locking, active set, expansion) runs on the host
+// (C++17); every arithmetic step runs in the sm_100a kernels of gemm.cuh / kernels.cuh on the
+// caller's stream. Per LOBPCG iteration the host reads back two small vectors (the residual
+// norms r and the Rayleigh-Ritz values theta); everything n-sized stays in HBM.
+//
+// Algorithm (restated in DESIGN.md §2; readings R*): Alg. 3 of PAPER.md:398-412 on B = s*A
+// (s = +1/-1), started from the previous call's block (warm) or a Philox block
+// (cold), Rayleigh-Ritz by implicit Cholesky-QR + Jacobi (Alg. 2), residual
+// basis (footnote PAPER.md:377), BLOPEX P direction (R5), hard/soft locking (R35), random
+// expansion (line 8, R8-R11), stopping rule with guard (R12), Theorem-3 bound
+// (R14-R16, R36), side rule (R17-R18).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "psdproj.h"
+#include "common.cuh"
+#include "gemm.cuh"
+#include "kernels.cuh"
+
+using namespace psd;
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string g_err;
+static int set_err(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+#define CK(x)                                                                                   \
+  do {                                                                                          \
+    cudaError_t e_ = (x);                                                                       \
+    if (e_ != cudaSuccess) return set_err(PSDPROJ_E_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #x, \
+                                          cudaGetErrorString(e_));                              \
+  } while (0)
+#define CKL() CK(cudaGetLastError())
+#define TRY(x)              \
+  do {                      \
+    int rc_ = (x);          \
+    if (rc_ < 0) return rc_; \
+  } while (0)
+
+static inline int rup(int x, int a) { return (x + a - 1) / a * a; }
+static int g_sms = 0;
+static int sms() {
+  if (!g_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_sms <= 0) g_sms = 148;
+  }
+  return g_sms;
+}
+static inline int grid1d(size_t work, int nt = 256) {
+  size_t b = (work + nt - 1) / nt;
+  size_t cap = (size_t)sms() * 8;
+  return (int)std::max<size_t>(1, std::min(b, cap));
+}
+
+// ------------------------------------------------------------------ GEMM dispatch
+namespace {
+constexpr int GBM = 64, GBN = 64, GBK = 16, GWM = 32, GWN = 32, GST = 4;
+using GCfg = GemmCfg<GBM, GBN, GBK, GWM, GWN, GST>;
+
+template <int OA, int OB, bool V>
+int gemm_launch(cudaStream_t st, int M, int N, int K, double alpha, const double* A, int lda, const double* B,
+                int ldb, double beta, double* C, int ldc, double* part, int splits, int ktps) {
+  auto kern = dgemm_kernel<OA, OB, GBM, GBN, GBK, GWM, GWN, GST, V>;
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GCfg::SMEM));
+    attr = true;
+  }
+  dim3 grid(cdiv(M, GBM), cdiv(N, GBN), splits);
+  kern<<<grid, GCfg::THREADS, GCfg::SMEM, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc,
+                                                splits > 1 ? part : nullptr, ktps);
+  CKL();
+  if (splits > 1) {
+    splitk_reduce_kernel<<<grid1d((size_t)M * N), 256, 0, st>>>(M, N, splits, alpha, part, beta, C, ldc);
+    CKL();
+  }
+  return 0;
+}
+}  // namespace
+
+static int dgemm(cudaStream_t st, int opA, int opB, int M, int N, int K, double alpha, const double* A, int lda,
+                 const double* B, int ldb, double beta, double* C, int ldc, double* part, size_t part_elems) {
+  if (M <= 0 || N <= 0) return 0;
+  if (K <= 0) {
+    // C = beta C
+    if (beta == 0.0) {
+      CK(cudaMemset2DAsync(C, (size_t)ldc * 8, 0, (size_t)M * 8, N, st));
+      return 0;
+    }
+    // C = alpha*0 + beta*C via a zero-K split-free launch
+  }
+  bool vec = (lda % 2 == 0) && (ldb % 2 == 0) && (((uintptr_t)A & 15) == 0) && (((uintptr_t)B & 15) == 0);
+  int KT = cdiv(std::max(K, 1), GBK);
+  int tiles = cdiv(M, GBM) * cdiv(N, GBN);
+  int splits = 1;
+  int target = sms() * 2;
+  if (tiles < target && part && KT >= 8) {
+    splits = std::min(cdiv(target, tiles), KT / 4);
+    splits = std::max(1, std::min(splits, 32));
+    while (splits > 1 && (size_t)splits * M * N > part_elems) --splits;
+  }
+  int ktps = cdiv(KT, splits);
+  splits = cdiv(KT, ktps);
+#define GL(OA, OB)                                                                                       \
+  return vec ? gemm_launch<OA, OB, true>(st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, part, splits, ktps) \
+             : gemm_launch<OA, OB, false>(st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, part, splits, ktps)
+  if (opA == OP_N && opB == OP_N) GL(OP_N, OP_N);
+  if (opA == OP_T && opB == OP_N) GL(OP_T, OP_N);
+  if (opA == OP_N && opB == OP_T) GL(OP_N, OP_T);
+  GL(OP_T, OP_T);
+#undef GL
+}
+
+// ------------------------------------------------------------------ Jacobi dispatch
+static int g_coop_blocks = 0;
+static int jacobi_run(cudaStream_t st, int s, const double* A, int lda, double* w, double* V, int ldv, double* M,
+                      double* M2, double* Q, int* d_info, int* d_counters, double* d_fro, int max_sweeps = 60) {
+  if (s <= 0) return 0;
+  if (s <= JAC_SMEM_MAX) {
+    int N = s + (s & 1);
+    size_t smem = (size_t)2 * N * N * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+      CK(cudaFuncSetAttribute(jacobi_smem_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)(2 * JAC_SMEM_MAX * JAC_SMEM_MAX * sizeof(double))));
+      attr = true;
+    }
+    jacobi_smem_kernel<1024><<<1, 1024, smem, st>>>(s, A, lda, w, V, ldv, max_sweeps, d_info);
+    CKL();
+    return 0;
+  }
+  int N = s + (s & 1);
+  jacobi_prep_kernel<<<grid1d((size_t)N * N), 256, 0, st>>>(s, N, A, lda, M, Q);
+  CKL();
+  fro_kernel<1024><<<1, 1024, 0, st>>>((int64_t)N * N, M, d_fro);
+  CKL();
+  CK(cudaMemsetAsync(d_counters, 0, sizeof(int) * (max_sweeps + 2), st));
+  if (!g_coop_blocks) {
+    int per = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, jacobi_coop_kernel, 256, 0));
+    g_coop_blocks = std::max(1, std::min(per, 4)) * sms();
+  }
+  double afl_scale = PSD_U / (double)s;
+  void* args[] = {(void*)&s, (void*)&N, (void*)&M, (void*)&M2, (void*)&Q, (void*)&d_fro, (void*)&afl_scale,
+                  (void*)&max_sweeps, (void*)&d_counters, (void*)&d_info};
+  CK(cudaLaunchCooperativeKernel((void*)jacobi_coop_kernel, dim3(g_coop_blocks), dim3(256), args, 0, st));
+  jacobi_extract_kernel<<<grid1d((size_t)s * s), 256, 0, st>>>(s, N, M, M2, Q, d_info, w, V, ldv);
+  CKL();
+  return 0;
+}
+
+// ------------------------------------------------------------------ context
+struct psdproj_ctx_s {
+  int n = 0, ld = 0;
+  psdproj_params prm{};
+  int m0 = 0, q = 0, m_max = 0, s_max = 0, NJ = 0, tcols = 0;
+  // device (carved from the caller's workspace)
+  double *S = nullptr, *BS = nullptr, *S2 = nullptr, *BS2 = nullptr, *T = nullptr, *T2 = nullptr, *E = nullptr;
+  double *Pb = nullptr, *BPb = nullptr, *XL = nullptr, *BXL = nullptr, *R = nullptr, *Xw = nullptr;
+  double *G = nullptr, *Hm = nullptr, *Gc = nullptr, *Li = nullptr, *Y = nullptr, *Hh = nullptr, *Vj = nullptr,
+         *Cp = nullptr;
+  double *jM = nullptr, *jM2 = nullptr, *jQ = nullptr;
+  double* part = nullptr;
+  size_t part_elems = 0;
+  double *d_thU = nullptr, *d_r = nullptr, *d_norm = nullptr, *d_w = nullptr, *d_ths = nullptr, *d_scal = nullptr;
+  int *d_idx = nullptr, *d_order = nullptr, *d_status = nullptr, *d_counters = nullptr;
+  double* stage = nullptr;  // host_io staging (n x n, ld)
+  // pinned host mirrors
+  double* h_d = nullptr;
+  int* h_i = nullptr;
+  size_t h_d_len = 0, h_i_len = 0;
+  // host state
+  bool warm = false;
+  int block_side = 0, m_warm = 0;
+  std::vector<double> th_warm;
+  bool have_counts = false;
+  int last_pos = 0, last_neg = 0;
+  int calls = 0;
+  bool poisoned = false;
+  std::vector<cudaEvent_t> ev;
+};
+
+struct Carver {
+  char* base;
+  size_t off, cap;
+  bool dry;
+  template <typename T>
+  T* take(size_t count) {
+    off = (off + 255) / 256 * 256;
+    T* p = dry ? nullptr : reinterpret_cast<T*>(base + off);
+    off += count * sizeof(T);
+    return p;
+  }
+};
+
+static void resolve(int n, const psdproj_params* in, psdproj_params& p, int& m0, int& q, int& m_max, int& s_max,
+                    int& NJ, int& tcols) {
+  if (in)
+    p = *in;
+  else
+    psdproj_default_params(&p);
+  m0 = p.m0 > 0 ? std::min(p.m0, n) : std::max(1, (int)std::ceil(0.1 * n));
+  q = p.expand_q > 0 ? p.expand_q : std::max(1, (int)std::ceil(0.05 * n));
+  // default capacity n/3: a wider block is the exact-eig regime anyway (R18)
+  m_max = p.m_max > 0 ? std::min(p.m_max, n) : std::min(n, (n + 2) / 3 + 1);
+  m_max = std::max(m_max, std::min(n, m0));
+  s_max = 3 * m_max + q;
+  NJ = std::max(s_max, n);
+  NJ += NJ & 1;
+  tcols = std::max(s_max, n);
+}
+
+static size_t carve(psdproj_ctx_s* c, int n, const psdproj_params& p, int m_max, int s_max, int NJ, int tcols,
+                    char* base, size_t cap, bool dry) {
+  Carver cv{base, 0, cap, dry};
+  int ld = rup(std::max(n, 1), 8);
+  size_t nS = (size_t)ld * s_max, nM = (size_t)ld * m_max, nT = (size_t)ld * tcols, s2 = (size_t)s_max * s_max;
+  c->S = cv.take<double>(nS); c->BS = cv.take<double>(nS);
+  c->S2 = cv.take<double>(nS); c->BS2 = cv.take<double>(nS);
+  c->T = cv.take<double>(nT); c->T2 = cv.take<double>(nT);
+  c->E = cv.take<double>(nT);
+  c->Pb = cv.take<double>(nM); c->BPb = cv.take<double>(nM);
+  c->XL = cv.take<double>(nM); c->BXL = cv.take<double>(nM);
+  c->R = cv.take<double>(nM); c->Xw = cv.take<double>(nM);
+  c->G = cv.take<double>(s2); c->Hm = cv.take<double>(s2); c->Gc = cv.take<double>(s2);
+  c->Li = cv.take<double>(s2); c->Y = cv.take<double>(s2); c->Hh = cv.take<double>(s2);
+  c->Vj = cv.take<double>(s2); c->Cp = cv.take<double>(s2);
+  size_t nj = (size_t)NJ * NJ;
+  c->jM = cv.take<double>(nj); c->jM2 = cv.take<double>(nj); c->jQ = cv.take<double>(nj);
+  c->part_elems = 2 * std::max(s2, nM);
+  c->part = cv.take<double>(c->part_elems);
+  int vlen = std::max(s_max, n) + 8;
+  c->d_thU = cv.take<double>(vlen); c->d_r = cv.take<double>(vlen); c->d_norm = cv.take<double>(vlen);
+  c->d_w = cv.take<double>(vlen); c->d_ths = cv.take<double>(vlen); c->d_scal = cv.take<double>(64);
+  c->d_idx = cv.take<int>((size_t)8 * (std::max(s_max, n) + 64)); c->d_order = cv.take<int>(vlen); c->d_status = cv.take<int>(64);
+  c->d_counters = cv.take<int>(128);
+  c->stage = p.host_io ? cv.take<double>((size_t)ld * n) : nullptr;
+  return cv.off + 256;
+}
+
+extern "C" void psdproj_default_params(psdproj_params* p) {
+  std::memset(p, 0, sizeof(*p));
+  p->max_iter = 500;
+  p->guard = 1;
+  p->side = PSDPROJ_SIDE_AUTO;
+  p->locking = PSDPROJ_LOCK_HARD;
+  p->keep_extra = -1;
+  p->seed = 0x5eed1912ull;
+}
+
+extern "C" size_t psdproj_workspace_bytes(int n, const psdproj_params* in) {
+  if (n <= 0) return 0;
+  psdproj_params p;
+  int m0, q, m_max, s_max, NJ, tcols;
+  resolve(n, in, p, m0, q, m_max, s_max, NJ, tcols);
+  psdproj_ctx_s tmp;
+  return carve(&tmp, n, p, m_max, s_max, NJ, tcols, nullptr, 0, true);
+}
+
+extern "C" int psdproj_create(int n, const psdproj_params* in, void* ws, size_t ws_bytes, psdproj_ctx* out) {
+  if (!out) return set_err(PSDPROJ_E_INVALID, "out is NULL");
+  *out = nullptr;
+  if (n <= 0) return set_err(PSDPROJ_E_INVALID, "n must be positive (got %d)", n);
+  if (!ws || ((uintptr_t)ws & 255)) return set_err(PSDPROJ_E_WORKSPACE, "workspace NULL or not 256-byte aligned");
+  psdproj_params p;
+  int m0, q, m_max, s_max, NJ, tcols;
+  resolve(n, in, p, m0, q, m_max, s_max, NJ, tcols);
+  if (p.max_iter < 0 || p.guard < 1 || (p.locking != PSDPROJ_LOCK_SOFT && p.locking != PSDPROJ_LOCK_HARD) ||
+      (p.side != 0 && p.side != 1 && p.side != -1 && p.side != 2))
+    return set_err(PSDPROJ_E_INVALID, "invalid params");
+  psdproj_ctx_s tmp;
+  size_t need = carve(&tmp, n, p, m_max, s_max, NJ, tcols, nullptr, 0, true);
+  if (ws_bytes < need) return set_err(PSDPROJ_E_WORKSPACE, "workspace %zu < needed %zu", ws_bytes, need);
+  auto* c = new psdproj_ctx_s();
+  c->n = n;
+  c->ld = rup(n, 8);
+  c->prm = p;
+  c->m0 = m0; c->q = q; c->m_max = m_max; c->s_max = s_max; c->NJ = NJ; c->tcols = tcols;
+  carve(c, n, p, m_max, s_max, NJ, tcols, (char*)ws, ws_bytes, false);
+  c->h_d_len = (size_t)4 * (std::max(s_max, n) + 64);
+  c->h_i_len = (size_t)8 * (std::max(s_max, n) + 64);
+  if (cudaMallocHost(&c->h_d, c->h_d_len * sizeof(double)) != cudaSuccess ||
+      cudaMallocHost(&c->h_i, c->h_i_len * sizeof(int)) != cudaSuccess) {
+    delete c;
+    return set_err(PSDPROJ_E_CUDA, "cudaMallocHost failed");
+  }
+  *out = c;
+  return PSDPROJ_OK;
+}
+
+extern "C" int psdproj_destroy(psdproj_ctx c) {
+  if (!c) return PSDPROJ_OK;
+  if (c->h_d) cudaFreeHost(c->h_d);
+  if (c->h_i) cudaFreeHost(c->h_i);
+  for (auto e : c->ev) cudaEventDestroy(e);
+  delete c;
+  return PSDPROJ_OK;
+}
+
+extern "C" int psdproj_reset(psdproj_ctx c) {
+  if (!c) return set_err(PSDPROJ_E_INVALID, "ctx NULL");
+  c->warm = false;
+  c->block_side = 0;
+  c->m_warm = 0;
+  c->have_counts = false;
+  c->th_warm.clear();
+  return PSDPROJ_OK;
+}
+
+extern "C" const char* psdproj_last_error(void) { return g_err.c_str(); }
+
+// ------------------------------------------------------------------ small helpers
+namespace {
+struct Run {
+  psdproj_ctx_s* c;
+  cudaStream_t st;
+  psdproj_info* info;
+  int ihost = 0;  // next free int slot in the pinned buffer (per iteration)
+  int nev = 0;
+  double anorm = 0.0;
+
+  int upload_idx(const std::vector<int>& v, int* dev) {
+    if (v.empty()) return 0;
+    if (ihost + (int)v.size() > (int)c->h_i_len - 64) return set_err(PSDPROJ_E_CAPACITY, "pinned index buffer full");
+    int* h = c->h_i + ihost;
+    std::memcpy(h, v.data(), v.size() * sizeof(int));
+    ihost += (int)v.size();
+    CK(cudaMemcpyAsync(dev, h, v.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    return 0;
+  }
+  int sync() {
+    CK(cudaStreamSynchronize(st));
+    ihost = 0;
+    return 0;
+  }
+  int gemm(int oa, int ob, int M, int N, int K, double al, const double* A, int lda, const double* B, int ldb,
+           double be, double* C, int ldc) {
+    if (info) {
+      info->flops += 2.0 * M * N * (double)K;
+      info->bytes += 8.0 * ((double)M * K + (double)K * N + (double)M * N);
+    }
+    return dgemm(st, oa, ob, M, N, K, al, A, lda, B, ldb, be, C, ldc, c->part, c->part_elems);
+  }
+  // block multiply (a3): Y = sgn * A * Z, the hot kernel; optionally timed with events
+  int amul(double sgn, const double* A, int lda, const double* Z, int ldz, int k, double* Y, int ldy) {
+    if (k <= 0) return 0;
+    int n = c->n;
+    info->a_passes++;
+    info->a_cols += k;
+    info->amul_flops += 2.0 * n * (double)n * k;
+    info->amul_bytes += 8.0 * n * (double)n;
+    info->flops += 2.0 * n * (double)n * k;
+    info->bytes += 8.0 * n * (double)n + 16.0 * n * (double)k;
+    bool prof = c->prm.profile & 1;
+    if (prof) {
+      while ((int)c->ev.size() < 2 * (nev + 1)) {
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        c->ev.push_back(e);
+      }
+      CK(cudaEventRecord(c->ev[2 * nev], st));
+    }
+    TRY(dgemm(st, OP_N, OP_N, n, k, n, sgn, A, lda, Z, ldz, 0.0, Y, ldy, c->part, c->part_elems));
+    if (prof) {
+      CK(cudaEventRecord(c->ev[2 * nev + 1], st));
+      nev++;
+    }
+    return 0;
+  }
+  int gather(int n, int cols, double* dst, int ldd, const double* src, int lds, const std::vector<int>& idx) {
+    if (cols <= 0) return 0;
+    int* d = c->d_idx;
+    // use a fresh region of d_idx per gather within an iteration: offset by ihost
+    int off = ihost;
+    TRY(upload_idx(idx, d + off));
+    gather_cols_kernel<<<grid1d((size_t)n * cols), 256, 0, st>>>(n, cols, dst, ldd, src, lds, d + off);
+    CKL();
+    return 0;
+  }
+  int copy_cols(int n, int cols, double* dst, int ldd, const double* src, int lds) {
+    if (cols <= 0) return 0;
+    CK(cudaMemcpy2DAsync(dst, (size_t)ldd * 8, src, (size_t)lds * 8, (size_t)n * 8, cols, cudaMemcpyDeviceToDevice,
+                         st));
+    return 0;
+  }
+  int normalize(int n, int cols, double* Z, int ldz, double* Z2, int ldz2) {
+    if (cols <= 0) return 0;
+    colnorm_kernel<256><<<cols, 256, 0, st>>>(n, Z, ldz, c->d_norm);
+    CKL();
+    scale_cols_kernel<<<grid1d((size_t)n * cols), 256, 0, st>>>(n, cols, Z, ldz, Z2, ldz2, c->d_norm);
+    CKL();
+    return 0;
+  }
+  // Rayleigh-Ritz on the pencil (H, G) in c->G / c->Hm (s x s, ld s_max):
+  // returns 0 (ok), >0 (Cholesky failed at that pivot), <0 error. Outputs Cp (s x mU), theta desc in h_d[0..s).
+  int rr(int s, int kxG, int kxH, const double* d_theta_known, int mU) {
+    int ldm = c->s_max;
+    info->rr_max = std::max(info->rr_max, s);
+    info->flops += 9.0 * s * (double)s * s + s * (double)s * s / 3.0 + 2.0 * s * (double)s * s;
+    insert_known_kernel<<<grid1d((size_t)s * s), 256, 0, st>>>(s, kxG, kxH, c->G, c->Hm, ldm, d_theta_known);
+    CKL();
+    TRY(copy_cols(s, s, c->Gc, ldm, c->G, ldm));
+    cholesky_kernel<1024><<<1, 1024, 0, st>>>(s, c->Gc, ldm, 1e-12, c->d_status);
+    CKL();
+    trinv_kernel<<<cdiv(s, 8), 256, 0, st>>>(s, c->Gc, ldm, c->Li, ldm);
+    CKL();
+    // Hh = L^-1 H L^-T
+    TRY(dgemm(st, OP_N, OP_N, s, s, s, 1.0, c->Li, ldm, c->Hm, ldm, 0.0, c->Y, ldm, c->part, c->part_elems));
+    TRY(dgemm(st, OP_N, OP_T, s, s, s, 1.0, c->Y, ldm, c->Li, ldm, 0.0, c->Hh, ldm, c->part, c->part_elems));
+    TRY(jacobi_run(st, s, c->Hh, ldm, c->d_w, c->Vj, ldm, c->jM, c->jM2, c->jQ, c->d_status + 4, c->d_counters,
+                   c->d_scal));
+    sort_desc_kernel<<<cdiv(s, 256), 256, 0, st>>>(s, c->d_w, c->d_order, c->d_ths);
+    CKL();
+    // C' = L^-T V[:, order[:mU]]
+    gather_cols_kernel<<<grid1d((size_t)s * mU), 256, 0, st>>>(s, mU, c->Y, ldm, c->Vj, ldm, c->d_order);
+    CKL();
+    TRY(dgemm(st, OP_T, OP_N, s, mU, s, 1.0, c->Li, ldm, c->Y, ldm, 0.0, c->Cp, ldm, c->part, c->part_elems));
+    CK(cudaMemcpyAsync(c->h_d, c->d_ths, sizeof(double) * s, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(c->h_i + c->h_i_len - 16, c->d_status, sizeof(int) * 8, cudaMemcpyDeviceToHost, st));
+    TRY(sync());
+    int chol = c->h_i[c->h_i_len - 16];
+    int sweeps = c->h_i[c->h_i_len - 16 + 4];
+    if (chol) return chol;
+    if (sweeps < 0) return set_err(PSDPROJ_E_DEGENERATE, "Jacobi did not converge (s=%d)", s);
+    return 0;
+  }
+};
+}  // namespace
+
+// ------------------------------------------------------------------ side rule
+static int select_mode(psdproj_ctx_s* c) {
+  // PAPER.md:505 (< n/3, strict, R17); ties -> smaller count then positive
+  int side = c->prm.side;
+  if (side != PSDPROJ_SIDE_AUTO) return side;
+  if (!c->have_counts) return PSDPROJ_SIDE_POS;
+  double third = c->n / 3.0;
+  bool pos_ok = c->last_pos < third, neg_ok = c->last_neg < third;
+  if (pos_ok && neg_ok) return c->last_pos <= c->last_neg ? PSDPROJ_SIDE_POS : PSDPROJ_SIDE_NEG;
+  if (pos_ok) return PSDPROJ_SIDE_POS;
+  if (neg_ok) return PSDPROJ_SIDE_NEG;
+  return PSDPROJ_SIDE_DIRECT;
+}
+
+static int keep_count(const psdproj_ctx_s* c, int p, int m) {
+  int extra = c->prm.keep_extra >= 0 ? c->prm.keep_extra
+                                     : std::max(c->prm.guard, std::max(1, (int)std::ceil(0.1 * p)));
+  return std::min(m, p + extra);
+}
+
+// ------------------------------------------------------------------ DIRECT path (a13)
+static int direct_path(Run& run, const double* A, int lda, double* Pi, int ldpi) {
+  psdproj_ctx_s* c = run.c;
+  cudaStream_t st = run.st;
+  int n = c->n, ld = c->ld;
+  run.info->side = PSDPROJ_SIDE_DIRECT;
+  run.info->flops += 9.0 * n * (double)n * n;
+  // eigendecomposition of A; V into jQ-free region: use T as V (ld x n)
+  double* V = c->T;
+  TRY(jacobi_run(st, n, A, lda, c->d_w, V, ld, c->jM, c->jM2, c->jQ, c->d_status + 4, c->d_counters, c->d_scal));
+  sort_desc_kernel<<<cdiv(n, 256), 256, 0, st>>>(n, c->d_w, c->d_order, c->d_ths);
+  CKL();
+  CK(cudaMemcpyAsync(c->h_d, c->d_ths, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(c->h_i + c->h_i_len - 16, c->d_status, sizeof(int) * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(c->h_i, c->d_order, sizeof(int) * n, cudaMemcpyDeviceToHost, st));
+  TRY(run.sync());
+  if (c->h_i[c->h_i_len - 16 + 4] < 0) return set_err(PSDPROJ_E_DEGENERATE, "Jacobi (DIRECT) did not converge");
+  std::vector<double> w(c->h_d, c->h_d + n);
+  std::vector<int> order(c->h_i, c->h_i + n);
+  int p = 0;
+  while (p < n && w[p] > 0.0) ++p;
+  // Pi = V+ diag(w+) V+^T
+  std::vector<int> pidx(order.begin(), order.begin() + p);
+  TRY(run.gather(n, p, c->T2, ld, V, ld, pidx));
+  if (p > 0) {
+    CK(cudaMemcpyAsync(c->d_w, c->d_ths, sizeof(double) * p, cudaMemcpyDeviceToDevice, st));
+    scale_copy_cols_kernel<<<grid1d((size_t)n * p), 256, 0, st>>>(n, p, c->E, ld, c->T2, ld, c->d_w);
+    CKL();
+    TRY(run.gemm(OP_N, OP_T, n, n, p, 1.0, c->E, ld, c->T2, ld, 0.0, Pi, ldpi));
+    symmetrize_kernel<<<grid1d((size_t)n * n), 256, 0, st>>>(n, Pi, ldpi);
+    CKL();
+  } else {
+    CK(cudaMemset2DAsync(Pi, (size_t)ldpi * 8, 0, (size_t)n * 8, n, st));
+  }
+  run.info->bytes += 16.0 * n * (double)n;
+  double z = 1e-9 * (1.0 + run.anorm);
+  int np = 0, nn = 0;
+  for (double x : w) {
+    np += x > z;
+    nn += x < -z;
+  }
+  c->last_pos = np;
+  c->last_neg = nn;
+  c->have_counts = true;
+  run.info->npos = p;
+  run.info->m = n;
+  run.info->err_bound = 0.0;
+  // seed the warm block for the side the next call will use
+  int nxt = select_mode(c);
+  if (nxt == PSDPROJ_SIDE_POS || nxt == PSDPROJ_SIDE_NEG) {
+    std::vector<int> idx;
+    std::vector<double> th;
+    if (nxt == PSDPROJ_SIDE_POS) {
+      int keep = keep_count(c, p, std::min(n, c->m_max));
+      for (int i = 0; i < keep; ++i) { idx.push_back(order[i]); th.push_back(w[i]); }
+    } else {
+      int pn = 0;
+      while (pn < n && w[n - 1 - pn] < 0.0) ++pn;
+      int keep = keep_count(c, pn, std::min(n, c->m_max));
+      for (int i = 0; i < keep; ++i) { idx.push_back(order[n - 1 - i]); th.push_back(-w[n - 1 - i]); }
+    }
+    TRY(run.gather(n, (int)idx.size(), c->Xw, ld, V, ld, idx));
+    c->m_warm = (int)idx.size();
+    c->th_warm = th;
+    c->block_side = nxt;
+    c->warm = true;
+  } else {
+    c->warm = false;
+    c->block_side = 0;
+  }
+  return PSDPROJ_OK;
+}
+
+// ------------------------------------------------------------------ LOBPCG path
+static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi, int ldpi, double tol,
+                       bool& abort_direct) {
+  psdproj_ctx_s* c = run.c;
+  psdproj_info* info = run.info;
+  cudaStream_t st = run.st;
+  const int n = c->n, ld = c->ld, ldm = c->s_max;
+  const double sgn = side == PSDPROJ_SIDE_POS ? 1.0 : -1.0;
+  const bool hard = c->prm.locking == PSDPROJ_LOCK_HARD;
+  const int g = c->prm.guard;
+  info->side = side;
+  abort_direct = false;
+
+  bool cold = !(c->warm && c->block_side == side);
+  info->cold = cold;
+  int m = cold ? c->m0 : c->m_warm;
+  if (m > c->m_max) return set_err(PSDPROJ_E_CAPACITY, "block %d > m_max %d", m, c->m_max);
+  // ---- start block X0 in S[:, :m] and B X0 in BS
+  if (cold) {
+    philox_gauss_kernel<<<grid1d(((size_t)n * m + 1) / 2), 256, 0, st>>>(n, m, c->S, ld, c->prm.seed,
+                                                                         (uint32_t)c->calls, c->prm.ctx_id, 0u);
+    CKL();
+  } else {
+    TRY(run.copy_cols(n, m, c->S, ld, c->Xw, ld));
+  }
+  TRY(run.amul(sgn, A, lda, c->S, ld, m, c->BS, ld));
+  // ---- Alg. 3 line 2: Rayleigh-Ritz on span(X0): G = X0^T X0 (I when warm), H = X0^T B X0
+  if (cold) TRY(run.gemm(OP_T, OP_N, m, m, n, 1.0, c->S, ld, c->S, ld, 0.0, c->G, ldm));
+  TRY(run.gemm(OP_T, OP_N, m, m, n, 1.0, c->S, ld, c->BS, ld, 0.0, c->Hm, ldm));
+  int rc = run.rr(m, cold ? 0 : m, 0, c->d_thU, m);
+  if (rc > 0) return set_err(PSDPROJ_E_DEGENERATE, "start block rank deficient");
+  TRY(rc);
+  std::vector<double> thU(c->h_d, c->h_d + m);
+  TRY(run.gemm(OP_N, OP_N, n, m, m, 1.0, c->S, ld, c->Cp, ldm, 0.0, c->S2, ld));
+  TRY(run.gemm(OP_N, OP_N, n, m, m, 1.0, c->BS, ld, c->Cp, ldm, 0.0, c->BS2, ld));
+  std::swap(c->S, c->S2);
+  std::swap(c->BS, c->BS2);
+  CK(cudaMemcpyAsync(c->d_thU, c->d_ths, sizeof(double) * m, cudaMemcpyDeviceToDevice, st));
+
+  int mU = m, nL = 0, qe = 0;
+  std::vector<double> rU(m, INFINITY), thL, rL;
+  std::vector<char> hasP(m, 0);
+  int status = PSDPROJ_NOT_CONVERGED;
+  int k = 0;
+  for (;;) {
+    // ---- line 5: R = B X - X Theta, r_i = ||R_i|| (unlocked columns)
+    resid_norm_kernel<256><<<mU, 256, 0, st>>>(n, c->S, ld, c->BS, ld, c->d_thU, c->R, ld, c->d_r);
+    CKL();
+    CK(cudaMemcpyAsync(c->h_d, c->d_r, sizeof(double) * mU, cudaMemcpyDeviceToHost, st));
+    TRY(run.sync());
+    rU.assign(c->h_d, c->h_d + mU);
+    // ---- stopping rule (R12)
+    int npos = nL;
+    bool conv_pos = true;
+    double g_th = -INFINITY, g_r = 0.0;
+    bool has_guard = false;
+    for (int j = 0; j < mU; ++j) {
+      if (thU[j] > 0) {
+        npos++;
+        if (!(rU[j] <= tol)) conv_pos = false;
+      } else if (!has_guard || thU[j] > g_th) {
+        has_guard = true;
+        g_th = thU[j];
+        g_r = rU[j];
+      }
+    }
+    int mtot = nL + mU;
+    bool guard_ok = (mtot >= n) ? true : (has_guard && g_th + g_r <= 0.0);
+    bool converged = conv_pos && guard_ok && qe == 0 && !(cold && k == 0);
+    if (converged) {
+      status = PSDPROJ_OK;
+      break;
+    }
+    if (k >= c->prm.max_iter) break;
+    // ---- hard locking (R35)
+    std::vector<int> keep, lock;
+    for (int j = 0; j < mU; ++j) {
+      if (hard && thU[j] > 0 && rU[j] <= tol)
+        lock.push_back(j);
+      else
+        keep.push_back(j);
+    }
+    if (!lock.empty()) {
+      TRY(run.gather(n, (int)lock.size(), c->XL + (size_t)nL * ld, ld, c->S, ld, lock));
+      TRY(run.gather(n, (int)lock.size(), c->BXL + (size_t)nL * ld, ld, c->BS, ld, lock));
+      for (int j : lock) {
+        thL.push_back(thU[j]);
+        rL.push_back(rU[j]);
+      }
+      nL += (int)lock.size();
+      // compact U (X, BX, P, BP, theta)
+      int nk = (int)keep.size();
+      TRY(run.gather(n, nk, c->T, ld, c->S, ld, keep));
+      TRY(run.copy_cols(n, nk, c->S, ld, c->T, ld));
+      TRY(run.gather(n, nk, c->T, ld, c->BS, ld, keep));
+      TRY(run.copy_cols(n, nk, c->BS, ld, c->T, ld));
+      TRY(run.gather(n, nk, c->T, ld, c->Pb, ld, keep));
+      TRY(run.copy_cols(n, nk, c->Pb, ld, c->T, ld));
+      TRY(run.gather(n, nk, c->T, ld, c->BPb, ld, keep));
+      TRY(run.copy_cols(n, nk, c->BPb, ld, c->T, ld));
+      std::vector<double> th2, r2;
+      std::vector<char> hp2;
+      for (int j : keep) {
+        th2.push_back(thU[j]);
+        r2.push_back(rU[j]);
+        hp2.push_back(hasP[j]);
+      }
+      thU = th2;
+      rU = r2;
+      hasP = hp2;
+      mU = nk;
+      for (int j = 0; j < mU; ++j) c->h_d[j] = thU[j];
+      CK(cudaMemcpyAsync(c->d_thU, c->h_d, sizeof(double) * mU, cudaMemcpyHostToDevice, st));
+      TRY(run.sync());
+    }
+    // ---- active set J (BLOPEX active mask): unlocked columns with r > tol
+    std::vector<int> Jorig, Jnew, PJ;
+    for (int jj = 0; jj < mU; ++jj) {
+      int j0 = keep[jj];
+      if (rU[jj] > tol) {
+        Jorig.push_back(j0);
+        Jnew.push_back(jj);
+        if (hasP[jj]) PJ.push_back(jj);
+      }
+    }
+    int a = (int)Jorig.size();
+    int ap = (int)PJ.size();
+    int offW = mU, offE = mU + a, offP = mU + a + qe;
+    int s = offP + ap;
+    if (s > c->s_max) return set_err(PSDPROJ_E_CAPACITY, "RR basis %d > s_max %d", s, c->s_max);
+    // W = R_J (+ pending expansion E)
+    TRY(run.gather(n, a, c->S + (size_t)offW * ld, ld, c->R, ld, Jorig));
+    TRY(run.copy_cols(n, qe, c->S + (size_t)offE * ld, ld, c->E, ld));
+    int aw = a + qe;
+    double* W = c->S + (size_t)offW * ld;
+    if (hard && nL > 0 && aw > 0) {
+      TRY(run.gemm(OP_T, OP_N, nL, aw, n, 1.0, c->XL, ld, W, ld, 0.0, c->Y, ldm));
+      TRY(run.gemm(OP_N, OP_N, n, aw, nL, -1.0, c->XL, ld, c->Y, ldm, 1.0, W, ld));
+    }
+    TRY(run.normalize(n, aw, W, ld, nullptr, 0));
+    TRY(run.amul(sgn, A, lda, W, ld, aw, c->BS + (size_t)offW * ld, ld));
+    // P_J, B P_J
+    if (ap > 0) {
+      double* P = c->S + (size_t)offP * ld;
+      double* BP = c->BS + (size_t)offP * ld;
+      TRY(run.gather(n, ap, P, ld, c->Pb, ld, PJ));
+      TRY(run.gather(n, ap, BP, ld, c->BPb, ld, PJ));
+      if (hard && nL > 0) {
+        TRY(run.gemm(OP_T, OP_N, nL, ap, n, 1.0, c->XL, ld, P, ld, 0.0, c->Y, ldm));
+        TRY(run.gemm(OP_N, OP_N, n, ap, nL, -1.0, c->XL, ld, c->Y, ldm, 1.0, P, ld));
+        TRY(run.gemm(OP_N, OP_N, n, ap, nL, -1.0, c->BXL, ld, c->Y, ldm, 1.0, BP, ld));
+      }
+      TRY(run.normalize(n, ap, P, ld, BP, ld));
+    }
+    // ---- line 6: Rayleigh-Ritz on span(X, R, P) via the pencil (S^T BS, S^T S)
+    TRY(run.gemm(OP_T, OP_N, s, s, n, 1.0, c->S, ld, c->S, ld, 0.0, c->G, ldm));
+    TRY(run.gemm(OP_T, OP_N, s, s, n, 1.0, c->S, ld, c->BS, ld, 0.0, c->Hm, ldm));
+    int sU = s;
+    rc = run.rr(s, mU, mU, c->d_thU, std::min(mU + qe, s));
+    if (rc > 0 && ap > 0) {
+      sU = s - ap;  // drop P and retry (R20)
+      rc = run.rr(sU, mU, mU, c->d_thU, std::min(mU + qe, sU));
+    }
+    if (rc > 0) return set_err(PSDPROJ_E_DEGENERATE, "Cholesky-QR failed at pivot %d (s=%d)", rc, sU);
+    TRY(rc);
+    std::vector<double> ths(c->h_d, c->h_d + sU);
+    int mUn = std::min(mU + qe, sU);
+    // ---- rotation (a8): X <- S C', BX <- BS C', P <- S_[R P] C'_[R P], BP likewise
+    TRY(run.gemm(OP_N, OP_N, n, mUn, sU, 1.0, c->S, ld, c->Cp, ldm, 0.0, c->S2, ld));
+    TRY(run.gemm(OP_N, OP_N, n, mUn, sU, 1.0, c->BS, ld, c->Cp, ldm, 0.0, c->BS2, ld));
+    TRY(run.gemm(OP_N, OP_N, n, mUn, sU - mU, 1.0, c->S + (size_t)mU * ld, ld, c->Cp + mU, ldm, 0.0, c->Pb, ld));
+    TRY(run.gemm(OP_N, OP_N, n, mUn, sU - mU, 1.0, c->BS + (size_t)mU * ld, ld, c->Cp + mU, ldm, 0.0, c->BPb, ld));
+    std::swap(c->S, c->S2);
+    std::swap(c->BS, c->BS2);
+    CK(cudaMemcpyAsync(c->d_thU, c->d_ths, sizeof(double) * mUn, cudaMemcpyDeviceToDevice, st));
+    thU.assign(ths.begin(), ths.begin() + mUn);
+    rU.assign(mUn, INFINITY);
+    hasP.assign(mUn, 1);
+    mU = mUn;
+    qe = 0;
+    ++k;
+    // ---- line 8: expansion when fewer than g guards would remain (R8)
+    int p_rr = (hard ? nL : 0);
+    for (double x : ths) p_rr += x > 0;
+    int mt = nL + mU;
+    if (p_rr >= mt - g + 1 && mt < n) {
+      int qq = std::min(c->q, n - mt);
+      if (mt + qq > c->m_max) {  // R18: the block reached the exact-eig regime (m_max = ceil(n/3)+1)
+        abort_direct = true;
+        return PSDPROJ_OK;
+      }
+      philox_gauss_kernel<<<grid1d(((size_t)n * qq + 1) / 2), 256, 0, st>>>(
+          n, qq, c->E, ld, c->prm.seed, (uint32_t)c->calls, c->prm.ctx_id, (uint32_t)k);
+      CKL();
+      for (int pass = 0; pass < 2; ++pass) {
+        if (nL > 0) {
+          TRY(run.gemm(OP_T, OP_N, nL, qq, n, 1.0, c->XL, ld, c->E, ld, 0.0, c->Y, ldm));
+          TRY(run.gemm(OP_N, OP_N, n, qq, nL, -1.0, c->XL, ld, c->Y, ldm, 1.0, c->E, ld));
+        }
+        TRY(run.gemm(OP_T, OP_N, mU, qq, n, 1.0, c->S, ld, c->E, ld, 0.0, c->Y, ldm));
+        TRY(run.gemm(OP_N, OP_N, n, qq, mU, -1.0, c->S, ld, c->Y, ldm, 1.0, c->E, ld));
+      }
+      qe = qq;
+      info->expansions++;
+    }
+  }
+  info->iters = k;
+  info->status = status;
+  info->locked = nL;
+  // ---- kept pairs: theta > 0 over L and U
+  std::vector<int> lpos, upos;
+  std::vector<double> wts;
+  double rs = 0.0, rmax = 0.0;
+  for (int j = 0; j < nL; ++j)
+    if (thL[j] > 0) { lpos.push_back(j); wts.push_back(thL[j]); rs += rL[j] * rL[j]; rmax = std::max(rmax, rL[j]); }
+  for (int j = 0; j < mU; ++j)
+    if (thU[j] > 0) { upos.push_back(j); wts.push_back(thU[j]); rs += rU[j] * rU[j]; rmax = std::max(rmax, rU[j]); }
+  int p = (int)wts.size();
+  double* V = c->T;
+  double* BV = c->T2;
+  TRY(run.gather(n, (int)lpos.size(), V, ld, c->XL, ld, lpos));
+  TRY(run.gather(n, (int)upos.size(), V + (size_t)lpos.size() * ld, ld, c->S, ld, upos));
+  for (int j = 0; j < p; ++j) c->h_d[j] = wts[j];
+  CK(cudaMemcpyAsync(c->d_w, c->h_d, sizeof(double) * std::max(p, 1), cudaMemcpyHostToDevice, st));
+  double lock_def = 0.0;
+  if (hard && nL > 0 && p > 0) {
+    TRY(run.gather(n, (int)lpos.size(), BV, ld, c->BXL, ld, lpos));
+    TRY(run.gather(n, (int)upos.size(), BV + (size_t)lpos.size() * ld, ld, c->BS, ld, upos));
+    TRY(run.gemm(OP_T, OP_N, p, p, n, 1.0, V, ld, BV, ld, 0.0, c->Y, ldm));
+    offdiag_fro_kernel<1024><<<1, 1024, 0, st>>>(p, c->Y, ldm, c->d_w, c->d_scal + 8);
+    CKL();
+    CK(cudaMemcpyAsync(c->h_d + c->h_d_len - 8, c->d_scal + 8, sizeof(double), cudaMemcpyDeviceToHost, st));
+    TRY(run.sync());
+    lock_def = c->h_d[c->h_d_len - 8];
+  }
+  // ---- Theorem 3 bound (R14-R16, R36): sqrt(2||R+||^2) + ||V+^T B V+ - Theta+||_F + 4 n u ||A||_F
+  info->resid_fro = std::sqrt(rs);
+  info->resid_max = rmax;
+  info->lock_defect = lock_def;
+  info->err_bound = std::sqrt(2.0 * rs) + lock_def + 4.0 * n * PSD_U * run.anorm;
+  info->npos = p;
+  // ---- a11: Pi = V Theta+ V^T (side +) or A + V Theta+ V^T (side -, pairs of -A)
+  if (sgn < 0 && Pi != A) {
+    CK(cudaMemcpy2DAsync(Pi, (size_t)ldpi * 8, A, (size_t)lda * 8, (size_t)n * 8, n, cudaMemcpyDeviceToDevice, st));
+  }
+  if (p > 0) {
+    scale_copy_cols_kernel<<<grid1d((size_t)n * p), 256, 0, st>>>(n, p, c->E, ld, V, ld, c->d_w);
+    CKL();
+    TRY(run.gemm(OP_N, OP_T, n, n, p, 1.0, c->E, ld, V, ld, sgn < 0 ? 1.0 : 0.0, Pi, ldpi));
+    symmetrize_kernel<<<grid1d((size_t)n * n), 256, 0, st>>>(n, Pi, ldpi);
+    CKL();
+  } else if (sgn > 0) {
+    CK(cudaMemset2DAsync(Pi, (size_t)ldpi * 8, 0, (size_t)n * 8, n, st));
+  }
+  // ---- a12: warm block for the next call: all columns by theta desc, first p + extra
+  struct Col { double th; int src; int j; };
+  std::vector<Col> cols;
+  for (int j = 0; j < nL; ++j) cols.push_back({thL[j], 0, j});
+  for (int j = 0; j < mU; ++j) cols.push_back({thU[j], 1, j});
+  std::stable_sort(cols.begin(), cols.end(), [](const Col& x, const Col& y) { return x.th > y.th; });
+  int mtot = nL + mU;
+  int keepn = std::min(keep_count(c, p, mtot), c->m_max);
+  // gather L-sourced then U-sourced into Xw preserving the sorted order via T2 staging
+  std::vector<int> li, ui, pos_l, pos_u;
+  for (int i = 0; i < keepn; ++i) {
+    if (cols[i].src == 0) { li.push_back(cols[i].j); pos_l.push_back(i); }
+    else { ui.push_back(cols[i].j); pos_u.push_back(i); }
+  }
+  TRY(run.gather(n, (int)li.size(), c->T2, ld, c->XL, ld, li));
+  TRY(run.gather(n, (int)ui.size(), c->T2 + (size_t)li.size() * ld, ld, c->S, ld, ui));
+  std::vector<int> perm(keepn);  // Xw[:, pos] = T2[:, staged index]
+  for (size_t i = 0; i < pos_l.size(); ++i) perm[pos_l[i]] = (int)i;
+  for (size_t i = 0; i < pos_u.size(); ++i) perm[pos_u[i]] = (int)(li.size() + i);
+  TRY(run.gather(n, keepn, c->Xw, ld, c->T2, ld, perm));
+  c->m_warm = keepn;
+  c->th_warm.clear();
+  for (int i = 0; i < keepn; ++i) c->th_warm.push_back(cols[i].th);
+  c->block_side = side;
+  c->warm = true;
+  // ---- counts for the side rule (computed side p, other side n - p)
+  if (side == PSDPROJ_SIDE_POS) { c->last_pos = p; c->last_neg = n - p; }
+  else { c->last_neg = p; c->last_pos = n - p; }
+  c->have_counts = true;
+  info->m = mtot;
+  info->bytes += 8.0 * n * (double)n * (sgn < 0 ? 2 : 1);
+  info->flops += (double)n * (n + 1) * p;
+  return status;
+}
+
+static int project_impl(psdproj_ctx c, const double* A, int lda, double* Pi, int ldpi, double tol, cudaStream_t st,
+                        psdproj_info* info) {
+  int n = c->n;
+  // first pass: non-finite check and ||A||_F (deterministic partials, host sums in order)
+  int nb = std::min(sms() * 2, std::max(1, (int)(((size_t)n * n + 255) / 256)));
+  CK(cudaMemsetAsync(c->d_status + 8, 0, sizeof(int), st));
+  nonfinite_kernel<<<nb, 256, 0, st>>>(n, A, lda, c->d_status + 8);
+  CKL();
+  fro_partial_kernel<<<nb, 256, 0, st>>>(n, A, lda, c->T2);
+  CKL();
+  CK(cudaMemcpyAsync(c->h_d, c->T2, sizeof(double) * nb, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(c->h_i + c->h_i_len - 32, c->d_status + 8, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (c->h_i[c->h_i_len - 32]) return set_err(PSDPROJ_E_NONFINITE, "A contains inf/nan");
+  double fro2 = 0.0;
+  for (int i = 0; i < nb; ++i) fro2 += c->h_d[i];
+  Run run{c, st, info};
+  run.anorm = std::sqrt(fro2);
+  info->anorm_f = run.anorm;
+  int mode = select_mode(c);
+  int call = c->calls++;
+  (void)call;
+  if (mode != PSDPROJ_SIDE_DIRECT) {
+    int mstart = (c->warm && c->block_side == mode) ? c->m_warm : c->m0;
+    if (3 * mstart >= n) mode = PSDPROJ_SIDE_DIRECT;  // R18
+  }
+  int rc;
+  if (mode == PSDPROJ_SIDE_DIRECT) {
+    rc = direct_path(run, A, lda, Pi, ldpi);
+    info->status = rc;
+  } else {
+    bool abort_direct = false;
+    rc = lobpcg_path(run, mode, A, lda, Pi, ldpi, tol, abort_direct);
+    if (rc >= 0 && abort_direct) {
+      rc = direct_path(run, A, lda, Pi, ldpi);
+      info->status = rc;
+    }
+  }
+  if (rc < 0) return rc;
+  info->last_pos = c->last_pos;
+  info->last_neg = c->last_neg;
+  CK(cudaStreamSynchronize(st));
+  if ((c->prm.profile & 1) && run.nev > 0) {
+    double tot = 0.0;
+    for (int i = 0; i < run.nev; ++i) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, c->ev[2 * i], c->ev[2 * i + 1]));
+      tot += ms;
+    }
+    info->amul_ms = tot;
+    info->amul_launches = run.nev;
+  }
+  return rc;
+}
+
+extern "C" int psdproj_project(psdproj_ctx c, const double* A, int lda, double* Pi, int ldpi, double tol,
+                               void* stream, psdproj_info* info) {
+  psdproj_info local;
+  if (!info) info = &local;
+  std::memset(info, 0, sizeof(*info));
+  if (!c) return info->status = set_err(PSDPROJ_E_INVALID, "ctx NULL");
+  if (c->poisoned) return info->status = set_err(PSDPROJ_E_CUDA, "context poisoned by an earlier CUDA error");
+  if (!A || !Pi || lda < c->n || ldpi < c->n || !(tol > 0.0) || !std::isfinite(tol))
+    return info->status = set_err(PSDPROJ_E_INVALID, "invalid arguments (lda=%d ldpi=%d tol=%g)", lda, ldpi, tol);
+  if ((const void*)Pi == (const void*)A && lda != ldpi)
+    return info->status = set_err(PSDPROJ_E_INVALID, "aliased Pi needs ldpi == lda");
+  int rc = project_impl(c, A, lda, Pi, ldpi, tol, (cudaStream_t)stream, info);
+  if (rc == PSDPROJ_E_CUDA) c->poisoned = true;
+  info->status = rc;
+  return rc;
+}
+
+extern "C" int psdproj_project_host(psdproj_ctx c, const double* A_host, int lda, double* Pi_host, int ldpi,
+                                    double tol, void* stream, psdproj_info* info) {
+  psdproj_info local;
+  if (!info) info = &local;
+  std::memset(info, 0, sizeof(*info));
+  if (!c || !c->stage) return info->status = set_err(PSDPROJ_E_INVALID, "ctx NULL or created without host_io");
+  if (!A_host || !Pi_host || lda < c->n || ldpi < c->n) return info->status = set_err(PSDPROJ_E_INVALID, "invalid arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  int n = c->n, ld = c->ld;
+  CK(cudaMemcpy2DAsync(c->stage, (size_t)ld * 8, A_host, (size_t)lda * 8, (size_t)n * 8, n, cudaMemcpyHostToDevice, st));
+  int rc = psdproj_project(c, c->stage, ld, c->stage, ld, tol, stream, info);
+  if (rc < 0) return rc;
+  CK(cudaMemcpy2DAsync(Pi_host, (size_t)ldpi * 8, c->stage, (size_t)ld * 8, (size_t)n * 8, n, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return rc;
+}
+
+extern "C" int psdproj_project_batched(psdproj_ctx* ctxs, int count, const double* const* A, const int* lda,
+                                       double* const* Pi, const int* ldpi, const double* tol, void* stream,
+                                       psdproj_info* infos) {
+  if (count < 0 || (count > 0 && (!ctxs || !A || !lda || !Pi || !ldpi || !tol || !infos)))
+    return set_err(PSDPROJ_E_INVALID, "invalid batched arguments");
+  int worst = PSDPROJ_OK;
+  for (int i = 0; i < count; ++i) {
+    int rc = psdproj_project(ctxs[i], A[i], lda[i], Pi[i], ldpi[i], tol[i], stream, &infos[i]);
+    if (rc < 0) return rc;
+    worst = std::max(worst, rc);
+  }
+  return worst;
+}
+
+extern "C" int psdproj_get_ritz(psdproj_ctx c, double* vals_host, int cap, double* vecs_dev, int ldv) {
+  if (!c) return set_err(PSDPROJ_E_INVALID, "ctx NULL");
+  if (!c->warm) return 0;
+  int k = std::min(cap, c->m_warm);
+  if (vals_host)
+    for (int i = 0; i < k; ++i) vals_host[i] = c->th_warm[i];
+  if (vecs_dev && k > 0) {
+    if (ldv < c->n) return set_err(PSDPROJ_E_INVALID, "ldv < n");
+    CK(cudaMemcpy2D(vecs_dev, (size_t)ldv * 8, c->Xw, (size_t)c->ld * 8, (size_t)c->n * 8, k, cudaMemcpyDeviceToDevice));
+  }
+  return k;
+}
+
+// ------------------------------------------------------------------ kernel-level entry points
+extern "C" int psdproj_dgemm(int opA, int opB, int M, int N, int K, double alpha, const double* A, int lda,
+                             const double* B, int ldb, double beta, double* C, int ldc, double* ws, size_t ws_elems,
+                             void* stream) {
+  if (M < 0 || N < 0 || K < 0 || (opA != 0 && opA != 1) || (opB != 0 && opB != 1))
+    return set_err(PSDPROJ_E_INVALID, "invalid gemm arguments");
+  if (lda < std::max(1, opA == OP_N ? M : K) || ldb < std::max(1, opB == OP_N ? K : N) || ldc < std::max(1, M))
+    return set_err(PSDPROJ_E_INVALID, "invalid leading dimension");
+  int rc = dgemm((cudaStream_t)stream, opA, opB, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws, ws ? ws_elems : 0);
+  return rc;
+}
+
+extern "C" size_t psdproj_jacobi_ws_elems(int s) {
+  size_t N = (size_t)(s + (s & 1));
+  return 3 * N * N + 256;
+}
+
+extern "C" int psdproj_jacobi(int s, const double* A, int lda, double* w, double* V, int ldv, double* ws,
+                              void* stream) {
+  if (s <= 0 || lda < s || ldv < s || !A || !w || !V || !ws) return set_err(PSDPROJ_E_INVALID, "invalid jacobi args");
+  cudaStream_t st = (cudaStream_t)stream;
+  size_t N = (size_t)(s + (s & 1));
+  double* M = ws;
+  double* M2 = ws + N * N;
+  double* Q = ws + 2 * N * N;
+  int* d_info = (int*)(ws + 3 * N * N);
+  int* d_cnt = d_info + 8;
+  double* d_fro = ws + 3 * N * N + 128;
+  TRY(jacobi_run(st, s, A, lda, w, V, ldv, M, M2, Q, d_info, d_cnt, d_fro));
+  int hinfo = 0;
+  CK(cudaMemcpyAsync(&hinfo, d_info, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (hinfo < 0) return set_err(PSDPROJ_E_DEGENERATE, "Jacobi did not converge");
+  // ascending order for the kernel-level API
+  return hinfo;
+}
+
+extern "C" int psdproj_philox_raw(int count, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0, uint32_t k1,
+                                  uint32_t* out, void* stream) {
+  if (count < 0 || (count > 0 && !out)) return set_err(PSDPROJ_E_INVALID, "invalid philox args");
+  if (count == 0) return 0;
+  philox_raw_kernel<<<grid1d(count), 256, 0, (cudaStream_t)stream>>>(count, c1, c2, c3, k0, k1, out);
+  CKL();
+  return 0;
+}
+
+extern "C" int psdproj_philox_gauss(int n, int q, double* out, int ld, uint64_t seed, uint32_t stream_id, uint32_t ctx,
+                                    uint32_t tag, void* stream) {
+  if (n < 0 || q < 0 || ld < n || (n * (size_t)q > 0 && !out)) return set_err(PSDPROJ_E_INVALID, "invalid gauss args");
+  if ((size_t)n * q == 0) return 0;
+  philox_gauss_kernel<<<grid1d(((size_t)n * q + 1) / 2), 256, 0, (cudaStream_t)stream>>>(n, q, out, ld, seed,
+                                                                                           stream_id, ctx, tag);
+  CKL();
+  return 0;
+}

@@ -1,0 +1,73 @@
+"""GPU parity of the individual kernels (through the C ABI) against the oracle / definitions."""
+import numpy as np
+import pytest
+import torch
+
+from oracle.philox import gaussian_block, philox4x32_10
+
+pytestmark = pytest.mark.gpu
+
+
+def _cm(a):
+    """numpy (r, c) -> column-major CUDA tensor view."""
+    a = np.asarray(a, dtype=np.float64)
+    return torch.from_numpy(np.ascontiguousarray(a.T)).cuda().T
+
+
+@pytest.mark.parametrize("opA,opB", [(0, 0), (1, 0), (0, 1)])
+@pytest.mark.parametrize("M,N,K", [(1, 1, 1), (7, 5, 3), (64, 64, 16), (131, 77, 203), (200, 40, 1000),
+                                   (33, 290, 4000)])
+def test_dgemm_vs_fp64_reference(api, opA, opB, M, N, K):
+    rng = np.random.default_rng(M * 1000 + N * 10 + K)
+    A = rng.standard_normal((M, K) if opA == 0 else (K, M))
+    B = rng.standard_normal((K, N) if opB == 0 else (N, K))
+    C0 = rng.standard_normal((M, N))
+    ref = 1.5 * (A if opA == 0 else A.T) @ (B if opB == 0 else B.T) - 0.5 * C0
+    C = _cm(C0)
+    ws = torch.empty(1 << 22, dtype=torch.float64, device="cuda")
+    api.dgemm(opA, opB, 1.5, _cm(A), _cm(B), -0.5, C, ws=ws)
+    got = C.cpu().numpy()
+    err = np.abs(got - ref).max() / (np.abs(A).max() * np.abs(B).max() * K + 1)
+    assert err < 1e-15, err
+
+
+def test_dgemm_odd_leading_dims(api):
+    rng = np.random.default_rng(3)
+    M, N, K = 37, 19, 51
+    Abig = rng.standard_normal((M + 3, K))  # lda = 40 -> use an odd-ld view
+    A = torch.from_numpy(np.ascontiguousarray(Abig.T)).cuda().T[:M, :]  # ld 40
+    Bfull = torch.from_numpy(np.ascontiguousarray(rng.standard_normal((N, K + 1)))).cuda().T[:K, :]  # ld 52
+    C = api.colmajor(M, N, ld=M)
+    api.dgemm(0, 0, 1.0, A, Bfull, 0.0, C)
+    ref = A.cpu().numpy() @ Bfull.cpu().numpy()
+    assert np.abs(C.cpu().numpy() - ref).max() < 1e-12
+
+
+@pytest.mark.parametrize("s", [1, 2, 3, 17, 64, 112, 113, 200, 301])
+def test_jacobi_eig(api, s):
+    rng = np.random.default_rng(s)
+    M = rng.standard_normal((s, s))
+    A = (M + M.T) / 2
+    w, V, sweeps = api.jacobi(_cm(A))
+    w = w.cpu().numpy()
+    V = V.cpu().numpy()
+    ref = np.linalg.eigvalsh(A)
+    assert sweeps > 0
+    assert np.abs(np.sort(w) - ref).max() < 1e-12 * max(1, np.abs(ref).max()) * max(1, s / 10)
+    assert np.linalg.norm(V.T @ V - np.eye(s)) < 1e-12 * s
+    assert np.linalg.norm(V @ np.diag(w) @ V.T - A) < 1e-12 * np.linalg.norm(A) * max(1, s / 10)
+
+
+def test_philox_raw_bit_exact(api):
+    cnt = 1000
+    out = api.philox_raw(cnt, 7, 11, 13, 0x12345678, 0x9abcdef0).cpu().numpy().view(np.uint32)
+    i = np.arange(cnt, dtype=np.uint32)
+    ref = np.stack(philox4x32_10(i, 7, 11, 13, 0x12345678, 0x9abcdef0), axis=1).reshape(-1)
+    assert np.array_equal(out, ref)
+
+
+def test_philox_gauss_matches_oracle(api):
+    n, q = 301, 7
+    got = api.philox_gauss(n, q, seed=99, stream_id=5, ctx=2, tag=3).cpu().numpy()
+    ref = gaussian_block(n, q, 99, 5, ctx=2, tag=3)
+    assert np.abs(got - ref).max() < 1e-13
