@@ -91,6 +91,7 @@ typedef struct {
   double amul_ms;   /* summed device time of the block multiplies (profile = 1)                */
   int amul_launches;/* number of timed block-multiply launches                                 */
   int last_pos, last_neg; /* sign counts fed to the next call's side rule                      */
+  int launches;     /* kernels this call launched (all of them libpsdproj's own)               */
 } psdproj_info;
 
 /* Fill *p with the defaults documented above. */

@@ -41,7 +41,7 @@ class Info(ctypes.Structure):
         ("resid_max", ctypes.c_double), ("lock_defect", ctypes.c_double), ("anorm_f", ctypes.c_double),
         ("flops", ctypes.c_double), ("bytes", ctypes.c_double), ("amul_flops", ctypes.c_double),
         ("amul_bytes", ctypes.c_double), ("amul_ms", ctypes.c_double), ("amul_launches", ctypes.c_int),
-        ("last_pos", ctypes.c_int), ("last_neg", ctypes.c_int),
+        ("last_pos", ctypes.c_int), ("last_neg", ctypes.c_int), ("launches", ctypes.c_int),
     ]
 
     def as_dict(self):

@@ -46,7 +46,12 @@ static int set_err(int code, const char* fmt, ...) {
     if (e_ != cudaSuccess) return set_err(PSDPROJ_E_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #x, \
                                           cudaGetErrorString(e_));                              \
   } while (0)
-#define CKL() CK(cudaGetLastError())
+static thread_local long long g_launches = 0;  // kernels issued by this thread (info.launches)
+#define CKL()              \
+  do {                     \
+    ++g_launches;          \
+    CK(cudaGetLastError()); \
+  } while (0)
 #define TRY(x)              \
   do {                      \
     int rc_ = (x);          \
@@ -162,6 +167,7 @@ static int jacobi_run(cudaStream_t st, int s, const double* A, int lda, double* 
   void* args[] = {(void*)&s, (void*)&N, (void*)&M, (void*)&M2, (void*)&Q, (void*)&d_fro, (void*)&afl_scale,
                   (void*)&max_sweeps, (void*)&d_counters, (void*)&d_info};
   CK(cudaLaunchCooperativeKernel((void*)jacobi_coop_kernel, dim3(g_coop_blocks), dim3(256), args, 0, st));
+  ++g_launches;
   jacobi_extract_kernel<<<grid1d((size_t)s * s), 256, 0, st>>>(s, N, M, M2, Q, d_info, w, V, ldv);
   CKL();
   return 0;
@@ -844,6 +850,7 @@ static int project_impl(psdproj_ctx c, const double* A, int lda, double* Pi, int
   double fro2 = 0.0;
   for (int i = 0; i < nb; ++i) fro2 += c->h_d[i];
   Run run{c, st, info};
+  long long launches0 = g_launches - 2;  // count the two first-pass kernels
   run.anorm = std::sqrt(fro2);
   info->anorm_f = run.anorm;
   int mode = select_mode(c);
@@ -868,6 +875,7 @@ static int project_impl(psdproj_ctx c, const double* A, int lda, double* Pi, int
   if (rc < 0) return rc;
   info->last_pos = c->last_pos;
   info->last_neg = c->last_neg;
+  info->launches = (int)(g_launches - launches0);
   CK(cudaStreamSynchronize(st));
   if ((c->prm.profile & 1) && run.nev > 0) {
     double tot = 0.0;
