@@ -21,10 +21,12 @@ __host__ __device__ inline int64_t cdiv64(int64_t a, int64_t b) { return (a + b 
 // the CPU restatement; the two are written independently).
 __device__ __forceinline__ void schur2(double app, double apq, double aqq, double& c, double& s,
                                        double& t) {
-  double tau = (aqq - app) / (2.0 * apq);
-  double r = sqrt(1.0 + tau * tau);
-  t = (tau >= 0.0) ? 1.0 / (tau + r) : -1.0 / (r - tau);
-  c = rsqrt(1.0 + t * t);
+  // tau = (aqq - app) / (2 apq), t = sign(tau) / (|tau| + sqrt(1 + tau^2)) rewritten with
+  // d = aqq - app, e = 2 apq as t = sgn(d) e / (|d| + hypot(d, e)) (one division, one sqrt)
+  double d = aqq - app, e = 2.0 * apq;
+  double h = sqrt(fma(d, d, e * e));
+  t = (d >= 0.0 ? e : -e) / (fabs(d) + h);
+  c = rsqrt(fma(t, t, 1.0));
   s = t * c;
 }
 

@@ -152,14 +152,17 @@ __global__ void philox_gauss_kernel(int n, int q, double* __restrict__ dst, int 
 }
 
 // ---------------------------------------------------------------- a5 known blocks
-// G, H (s x s, ld): symmetrise ((M + M^T)/2) and insert G[:kxG,:kxG] = I, H[:kxH,:kxH] = diag(theta).
+// G, H (s x s, ld): symmetrise ((M + M^T)/2) and insert G[:kxG,:] = [I 0] (the directions are
+// orthogonalised against X before the Gram), H[:kxH,:kxH] = diag(theta).
 __global__ void insert_known_kernel(int s, int kxG, int kxH, double* __restrict__ G, double* __restrict__ H, int ld,
                                     const double* __restrict__ theta) {
   int total = s * s;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
     int i = e % s, j = e / s;
     if (i > j) continue;
-    double g = (j < kxG) ? ((i == j) ? 1.0 : 0.0) : 0.5 * (G[IDX(i, j, ld)] + G[IDX(j, i, ld)]);
+    // i <= j: i < kxG <= j is the X-W/P cross block, zero after the orthogonalisation
+    double g = (j < kxG) ? ((i == j) ? 1.0 : 0.0)
+                         : (i < kxG ? 0.0 : 0.5 * (G[IDX(i, j, ld)] + G[IDX(j, i, ld)]));
     double h = (j < kxH) ? ((i == j) ? theta[i] : 0.0) : 0.5 * (H[IDX(i, j, ld)] + H[IDX(j, i, ld)]);
     G[IDX(i, j, ld)] = g; G[IDX(j, i, ld)] = g;
     H[IDX(i, j, ld)] = h; H[IDX(j, i, ld)] = h;
@@ -272,17 +275,22 @@ constexpr int JAC_SMEM_MAX = 112;
 
 // One CTA; A (s x s, lda) symmetric input; outputs w (s, unsorted) and V (s x s, ldv).
 // info[0] = sweeps performed (-1: no convergence within max_sweeps).
+// Each thread owns a fixed set of (pair-slot k1 <= pair-slot k2) blocks (decoded once) and a
+// fixed set of (row, pair-slot) entries of V; per round only the rotation parameters change.
 template <int NT>
 __global__ void __launch_bounds__(NT) jacobi_smem_kernel(int s, const double* __restrict__ A, int lda,
                                                          double* __restrict__ w, double* __restrict__ V, int ldv,
                                                          int max_sweeps, int* __restrict__ info) {
   extern __shared__ __align__(16) double sm[];
+  constexpr int HM = JAC_SMEM_MAX / 2;
+  constexpr int MAXB = (HM * (HM + 1) / 2 + NT - 1) / NT;
   const int N = s + (s & 1);
   const int H = N / 2;
-  double* M = sm;                 // N x N (col-major, ld N)
-  double* Q = sm + N * N;         // N x N
-  __shared__ double c_[JAC_SMEM_MAX / 2 + 1], s_[JAC_SMEM_MAX / 2 + 1], t_[JAC_SMEM_MAX / 2 + 1];
-  __shared__ int p_[JAC_SMEM_MAX / 2 + 1], q_[JAC_SMEM_MAX / 2 + 1], act_[JAC_SMEM_MAX / 2 + 1];
+  const int L = N + 1;     // odd leading dimension: column-strided accesses hit distinct banks
+  double* M = sm;          // N x N (col-major, ld L)
+  double* Q = sm + N * L;  // N x N (ld L)
+  __shared__ double c_[HM], s_[HM], t_[HM];
+  __shared__ int p_[HM], q_[HM], act_[HM];
   __shared__ double red[32];
   __shared__ int rot;
   double fro = 0.0;
@@ -290,12 +298,27 @@ __global__ void __launch_bounds__(NT) jacobi_smem_kernel(int s, const double* __
     int i = e % N, j = e / N;
     double v = 0.0;
     if (i < s && j < s) v = 0.5 * (A[IDX(i, j, lda)] + A[IDX(j, i, lda)]);
-    M[e] = v;
-    Q[e] = (i == j) ? 1.0 : 0.0;
+    M[i + j * L] = v;
+    Q[i + j * L] = (i == j) ? 1.0 : 0.0;
     fro += v * v;
   }
   fro = sqrt(block_sum<NT>(fro, red));
-  const double afloor = PSD_U * fro / (double)max(s, 1);
+  const double afloor = PSD_U * fro;  // absolute floor u ||A||_F (R39)
+  // fixed block ownership
+  const int nb = H * (H + 1) / 2;
+  int bk1[MAXB], bk2[MAXB];
+  int myb = 0;
+#pragma unroll
+  for (int j = 0; j < MAXB; ++j) {
+    int b = threadIdx.x + j * NT;
+    bk1[j] = 0; bk2[j] = 0;
+    if (b < nb) {
+      int r = 0, base = 0;
+      while (base + (H - r) <= b) { base += H - r; ++r; }
+      bk1[j] = r; bk2[j] = r + (b - base);
+      myb = j + 1;
+    }
+  }
   int sweep = 0;
   bool done = (N <= 1);
   while (!done && sweep < max_sweeps) {
@@ -305,7 +328,7 @@ __global__ void __launch_bounds__(NT) jacobi_smem_kernel(int s, const double* __
       for (int k = threadIdx.x; k < H; k += NT) {
         int p, q;
         rr_pair(r, k, N, p, q);
-        double app = M[p + p * N], aqq = M[q + q * N], apq = M[p + q * N];
+        double app = M[p + p * L], aqq = M[q + q * L], apq = M[p + q * L];
         int a = !(fabs(apq) <= PSD_U * sqrt(fabs(app) * fabs(aqq)) || fabs(apq) <= afloor);
         double c = 1.0, sn = 0.0, t = 0.0;
         if (a) schur2(app, apq, aqq, c, sn, t);
@@ -313,57 +336,51 @@ __global__ void __launch_bounds__(NT) jacobi_smem_kernel(int s, const double* __
         if (a) rot = 1;
       }
       __syncthreads();
-      // A <- J^T A J on 2x2 blocks (k1 <= k2), mirrored
-      const int nb = H * (H + 1) / 2;
-      for (int b = threadIdx.x; b < nb; b += NT) {
-        // decode b -> (k1, k2), k1 <= k2 (row-major upper triangle)
-        int k1 = (int)((2 * H + 1 - sqrt((double)(2 * H + 1) * (2 * H + 1) - 8.0 * b)) * 0.5);
-        int base = k1 * H - k1 * (k1 - 1) / 2;
-        while (base > b) { --k1; base = k1 * H - k1 * (k1 - 1) / 2; }
-        while (base + (H - k1) <= b) { base += H - k1; ++k1; }
-        int k2 = k1 + (b - base);
+#pragma unroll
+      for (int j = 0; j < MAXB; ++j) {
+        if (j >= myb) break;
+        int k1 = bk1[j], k2 = bk2[j];
         int a1 = act_[k1], a2 = act_[k2];
         if (!a1 && !a2) continue;
-        int p1 = p_[k1], q1 = q_[k1], p2 = p_[k2], q2 = q_[k2];
+        int p1 = p_[k1], q1 = q_[k1];
         if (k1 == k2) {
-          double apq = M[p1 + q1 * N], t = t_[k1];
-          M[p1 + p1 * N] -= t * apq;
-          M[q1 + q1 * N] += t * apq;
-          M[p1 + q1 * N] = 0.0; M[q1 + p1 * N] = 0.0;
+          double apq = M[p1 + q1 * L], t = t_[k1];
+          M[p1 + p1 * L] -= t * apq;
+          M[q1 + q1 * L] += t * apq;
+          M[p1 + q1 * L] = 0.0; M[q1 + p1 * L] = 0.0;
           continue;
         }
+        int p2 = p_[k2], q2 = q_[k2];
         double c1 = c_[k1], s1 = s_[k1], c2 = c_[k2], s2 = s_[k2];
-        double b00 = M[p1 + p2 * N], b01 = M[p1 + q2 * N], b10 = M[q1 + p2 * N], b11 = M[q1 + q2 * N];
-        // rows: J1^T
+        double b00 = M[p1 + p2 * L], b01 = M[p1 + q2 * L], b10 = M[q1 + p2 * L], b11 = M[q1 + q2 * L];
         double x00 = c1 * b00 - s1 * b10, x01 = c1 * b01 - s1 * b11;
         double x10 = s1 * b00 + c1 * b10, x11 = s1 * b01 + c1 * b11;
-        // cols: J2
         double y00 = c2 * x00 - s2 * x01, y01 = s2 * x00 + c2 * x01;
         double y10 = c2 * x10 - s2 * x11, y11 = s2 * x10 + c2 * x11;
-        M[p1 + p2 * N] = y00; M[p1 + q2 * N] = y01; M[q1 + p2 * N] = y10; M[q1 + q2 * N] = y11;
-        M[p2 + p1 * N] = y00; M[q2 + p1 * N] = y01; M[p2 + q1 * N] = y10; M[q2 + q1 * N] = y11;
+        M[p1 + p2 * L] = y00; M[p1 + q2 * L] = y01; M[q1 + p2 * L] = y10; M[q1 + q2 * L] = y11;
+        M[p2 + p1 * L] = y00; M[q2 + p1 * L] = y01; M[p2 + q1 * L] = y10; M[q2 + q1 * L] = y11;
       }
       // V <- V J
       for (int e = threadIdx.x; e < N * H; e += NT) {
-        int i = e % N, k = e / N;
+        int k = e / N;
         if (!act_[k]) continue;
+        int i = e - k * N;
         int p = p_[k], q = q_[k];
         double c = c_[k], sn = s_[k];
-        double vp = Q[i + p * N], vq = Q[i + q * N];
-        Q[i + p * N] = c * vp - sn * vq;
-        Q[i + q * N] = sn * vp + c * vq;
+        double vp = Q[i + p * L], vq = Q[i + q * L];
+        Q[i + p * L] = c * vp - sn * vq;
+        Q[i + q * L] = sn * vp + c * vq;
       }
       __syncthreads();
     }
     ++sweep;
-    __syncthreads();
     done = (rot == 0);
     __syncthreads();
   }
-  for (int i = threadIdx.x; i < s; i += NT) w[i] = M[i + i * N];
+  for (int i = threadIdx.x; i < s; i += NT) w[i] = M[i + i * L];
   for (int e = threadIdx.x; e < s * s; e += NT) {
     int i = e % s, j = e / s;
-    V[IDX(i, j, ldv)] = Q[i + j * N];
+    V[IDX(i, j, ldv)] = Q[i + j * L];
   }
   if (threadIdx.x == 0) { info[0] = done ? sweep : -1; info[1] = 0; }
 }
@@ -374,8 +391,8 @@ __global__ void __launch_bounds__(NT) jacobi_smem_kernel(int s, const double* __
 // are computed and mirrored (exact symmetry). Q is updated in place (disjoint columns).
 // counters[max_sweeps+1] are zeroed by the host; afloor = afl_scale * ||A||_F (*d_fro).
 __device__ __forceinline__ void decode_upper(int64_t b, int H, int& k1, int& k2) {
-  double hh = 2.0 * H + 1.0;
-  int r = (int)((hh - sqrt(hh * hh - 8.0 * (double)b)) * 0.5);
+  float hh = 2.0f * H + 1.0f;
+  int r = (int)((hh - sqrtf(fmaxf(hh * hh - 8.0f * (float)b, 0.0f))) * 0.5f);
   r = max(0, min(r, H - 1));
   int64_t base = (int64_t)r * H - (int64_t)r * (r - 1) / 2;
   while (r > 0 && base > b) { --r; base = (int64_t)r * H - (int64_t)r * (r - 1) / 2; }
@@ -388,12 +405,21 @@ __device__ __forceinline__ int jac_active(double app, double aqq, double apq, do
   return !(fabs(apq) <= PSD_U * sqrt(fabs(app) * fabs(aqq)) || fabs(apq) <= afloor);
 }
 
-__global__ void jacobi_coop_kernel(int s, int N, double* __restrict__ Ma, double* __restrict__ Mb,
-                                   double* __restrict__ Q, const double* __restrict__ d_fro, double afl_scale,
-                                   int max_sweeps, int* __restrict__ counters, int* __restrict__ info) {
+// One CTA per SM, one grid barrier per round. At the start of a round every CTA computes the
+// rotation parameters of all N/2 pairs from the read buffer into shared memory (redundant
+// across CTAs, no extra barrier), then updates its share of the k1 <= k2 blocks into the
+// write buffer (mirrored) and its share of V's column pairs in place.
+constexpr int JAC_COOP_MAXH = 1280;
+__global__ void __launch_bounds__(512) jacobi_coop_kernel(int s, int N, double* __restrict__ Ma,
+                                                          double* __restrict__ Mb, double* __restrict__ Q,
+                                                          const double* __restrict__ d_fro, double afl_scale,
+                                                          int max_sweeps, int* __restrict__ counters,
+                                                          int* __restrict__ info) {
   cg::grid_group grid = cg::this_grid();
+  __shared__ double sc[JAC_COOP_MAXH], ss[JAC_COOP_MAXH], st_[JAC_COOP_MAXH], sapq[JAC_COOP_MAXH];
+  __shared__ unsigned char sact[JAC_COOP_MAXH];
   const int H = N / 2;
-  const int64_t nb = (int64_t)H * (H + 1) / 2;
+  const int64_t nb = (int64_t)H * H;  // all (k1, k2), k1 fastest: coalesced rows p1 = r + k1
   const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t gsz = (int64_t)gridDim.x * blockDim.x;
   const double afloor = afl_scale * d_fro[0];
@@ -403,20 +429,29 @@ __global__ void jacobi_coop_kernel(int s, int N, double* __restrict__ Ma, double
   bool done = (N <= 1);
   while (!done && sweep < max_sweeps) {
     for (int r = 0; r < N - 1; ++r) {
+      int cnt = 0;
+      for (int k = threadIdx.x; k < H; k += blockDim.x) {
+        int p, q;
+        rr_pair(r, k, N, p, q);
+        double app = cur[IDX(p, p, N)], aqq = cur[IDX(q, q, N)], apq = cur[IDX(p, q, N)];
+        int a = jac_active(app, aqq, apq, afloor);
+        double c = 1.0, sn = 0.0, t = 0.0;
+        if (a) schur2(app, apq, aqq, c, sn, t);
+        sc[k] = c; ss[k] = sn; st_[k] = t; sapq[k] = apq; sact[k] = (unsigned char)a;
+        cnt += a;
+      }
+      if (blockIdx.x == 0 && cnt) atomicAdd(&counters[sweep], cnt);
+      __syncthreads();
       for (int64_t b = gtid; b < nb; b += gsz) {
-        int k1, k2;
-        decode_upper(b, H, k1, k2);
-        int p1, q1, p2, q2;
+        int k1 = (int)(b % H), k2 = (int)(b / H);
+        int p1, q1;
         rr_pair(r, k1, N, p1, q1);
-        double c1 = 1, s1 = 0, t1 = 0, c2 = 1, s2 = 0, t2 = 0;
-        double app = cur[IDX(p1, p1, N)], aqq = cur[IDX(q1, q1, N)], apq = cur[IDX(p1, q1, N)];
-        int a1 = jac_active(app, aqq, apq, afloor);
-        if (a1) schur2(app, apq, aqq, c1, s1, t1);
         if (k1 == k2) {
-          if (a1) {
-            atomicAdd(&counters[sweep], 1);
-            nxt[IDX(p1, p1, N)] = app - t1 * apq;
-            nxt[IDX(q1, q1, N)] = aqq + t1 * apq;
+          double app = cur[IDX(p1, p1, N)], aqq = cur[IDX(q1, q1, N)], apq = sapq[k1];
+          if (sact[k1]) {
+            double t = st_[k1];
+            nxt[IDX(p1, p1, N)] = app - t * apq;
+            nxt[IDX(q1, q1, N)] = aqq + t * apq;
             nxt[IDX(p1, q1, N)] = 0.0;
             nxt[IDX(q1, p1, N)] = 0.0;
           } else {
@@ -427,27 +462,24 @@ __global__ void jacobi_coop_kernel(int s, int N, double* __restrict__ Ma, double
           }
           continue;
         }
+        int p2, q2;
         rr_pair(r, k2, N, p2, q2);
-        double bpp = cur[IDX(p2, p2, N)], bqq = cur[IDX(q2, q2, N)], bpq = cur[IDX(p2, q2, N)];
-        int a2 = jac_active(bpp, bqq, bpq, afloor);
-        if (a2) schur2(bpp, bpq, bqq, c2, s2, t2);
+        double c1 = sc[k1], s1 = ss[k1], c2 = sc[k2], s2 = ss[k2];
         double b00 = cur[IDX(p1, p2, N)], b01 = cur[IDX(p1, q2, N)], b10 = cur[IDX(q1, p2, N)],
                b11 = cur[IDX(q1, q2, N)];
         double x00 = c1 * b00 - s1 * b10, x01 = c1 * b01 - s1 * b11;
         double x10 = s1 * b00 + c1 * b10, x11 = s1 * b01 + c1 * b11;
-        double y00 = c2 * x00 - s2 * x01, y01 = s2 * x00 + c2 * x01;
-        double y10 = c2 * x10 - s2 * x11, y11 = s2 * x10 + c2 * x11;
-        nxt[IDX(p1, p2, N)] = y00; nxt[IDX(p1, q2, N)] = y01; nxt[IDX(q1, p2, N)] = y10; nxt[IDX(q1, q2, N)] = y11;
-        nxt[IDX(p2, p1, N)] = y00; nxt[IDX(q2, p1, N)] = y01; nxt[IDX(p2, q1, N)] = y10; nxt[IDX(q2, q1, N)] = y11;
+        nxt[IDX(p1, p2, N)] = c2 * x00 - s2 * x01;
+        nxt[IDX(p1, q2, N)] = s2 * x00 + c2 * x01;
+        nxt[IDX(q1, p2, N)] = c2 * x10 - s2 * x11;
+        nxt[IDX(q1, q2, N)] = s2 * x10 + c2 * x11;
       }
       for (int64_t e = gtid; e < (int64_t)N * H; e += gsz) {
         int i = (int)(e % N), k = (int)(e / N);
+        if (!sact[k]) continue;
         int p, q;
         rr_pair(r, k, N, p, q);
-        double app = cur[IDX(p, p, N)], aqq = cur[IDX(q, q, N)], apq = cur[IDX(p, q, N)];
-        if (!jac_active(app, aqq, apq, afloor)) continue;
-        double c, sn, t;
-        schur2(app, apq, aqq, c, sn, t);
+        double c = sc[k], sn = ss[k];
         double vp = Q[IDX(i, p, N)], vq = Q[IDX(i, q, N)];
         Q[IDX(i, p, N)] = c * vp - sn * vq;
         Q[IDX(i, q, N)] = sn * vp + c * vq;
@@ -461,6 +493,113 @@ __global__ void jacobi_coop_kernel(int s, int N, double* __restrict__ Ma, double
   if (gtid == 0) {
     info[0] = done ? sweep : -1;
     info[1] = (cur == Ma) ? 0 : 1;  // which buffer holds the result
+  }
+}
+
+// Cluster variant: one thread-block cluster of CS CTAs (CS <= 16, non-portable) runs the whole
+// Jacobi; the matrix stays in global memory (L2-resident) double-buffered, reads bypass L1
+// (ld.global.cg), and rounds are separated by the cluster barrier (release/acquire), which
+// is an order of magnitude cheaper than a grid-wide barrier. Every CTA computes all rotation
+// parameters of the round itself (identical inputs -> identical decisions, no exchange).
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ unsigned cluster_ctarank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+
+constexpr int JAC_CL_MAXH = 1280;
+__global__ void __launch_bounds__(1024) jacobi_cluster_kernel(int s, int N, double* __restrict__ Ma,
+                                                              double* __restrict__ Mb, double* __restrict__ Q,
+                                                              const double* __restrict__ d_fro, double afl_scale,
+                                                              int max_sweeps, int* __restrict__ info) {
+  __shared__ double sc[JAC_CL_MAXH], ss[JAC_CL_MAXH], st_[JAC_CL_MAXH], sapq[JAC_CL_MAXH];
+  __shared__ unsigned char sact[JAC_CL_MAXH];
+  __shared__ int srot;
+  const int H = N / 2;
+  const int CS = (int)gridDim.x;  // the grid is exactly one cluster
+  const int64_t nb = (int64_t)H * H;
+  const int64_t gtid = (int64_t)cluster_ctarank() * blockDim.x + threadIdx.x;
+  const int64_t gsz = (int64_t)CS * blockDim.x;
+  const double afloor = afl_scale * __ldcg(d_fro);
+  double* cur = Ma;
+  double* nxt = Mb;
+  int sweep = 0;
+  bool done = (N <= 1);
+  while (!done && sweep < max_sweeps) {
+    if (threadIdx.x == 0) srot = 0;
+    __syncthreads();
+    for (int r = 0; r < N - 1; ++r) {
+      int any = 0;
+      for (int k = threadIdx.x; k < H; k += blockDim.x) {
+        int p, q;
+        rr_pair(r, k, N, p, q);
+        double app = __ldcg(cur + IDX(p, p, N)), aqq = __ldcg(cur + IDX(q, q, N)), apq = __ldcg(cur + IDX(p, q, N));
+        int a = jac_active(app, aqq, apq, afloor);
+        double c = 1.0, sn = 0.0, t = 0.0;
+        if (a) schur2(app, apq, aqq, c, sn, t);
+        sc[k] = c; ss[k] = sn; st_[k] = t; sapq[k] = apq; sact[k] = (unsigned char)a;
+        any |= a;
+      }
+      if (any) srot = 1;
+      __syncthreads();
+      for (int64_t b = gtid; b < nb; b += gsz) {
+        int k1 = (int)(b % H), k2 = (int)(b / H);
+        int p1, q1;
+        rr_pair(r, k1, N, p1, q1);
+        if (k1 == k2) {
+          double app = __ldcg(cur + IDX(p1, p1, N)), aqq = __ldcg(cur + IDX(q1, q1, N)), apq = sapq[k1];
+          if (sact[k1]) {
+            double t = st_[k1];
+            nxt[IDX(p1, p1, N)] = app - t * apq;
+            nxt[IDX(q1, q1, N)] = aqq + t * apq;
+            nxt[IDX(p1, q1, N)] = 0.0;
+            nxt[IDX(q1, p1, N)] = 0.0;
+          } else {
+            nxt[IDX(p1, p1, N)] = app;
+            nxt[IDX(q1, q1, N)] = aqq;
+            nxt[IDX(p1, q1, N)] = apq;
+            nxt[IDX(q1, p1, N)] = apq;
+          }
+          continue;
+        }
+        int p2, q2;
+        rr_pair(r, k2, N, p2, q2);
+        double c1 = sc[k1], s1 = ss[k1], c2 = sc[k2], s2 = ss[k2];
+        double b00 = __ldcg(cur + IDX(p1, p2, N)), b01 = __ldcg(cur + IDX(p1, q2, N));
+        double b10 = __ldcg(cur + IDX(q1, p2, N)), b11 = __ldcg(cur + IDX(q1, q2, N));
+        double x00 = c1 * b00 - s1 * b10, x01 = c1 * b01 - s1 * b11;
+        double x10 = s1 * b00 + c1 * b10, x11 = s1 * b01 + c1 * b11;
+        nxt[IDX(p1, p2, N)] = c2 * x00 - s2 * x01;
+        nxt[IDX(p1, q2, N)] = s2 * x00 + c2 * x01;
+        nxt[IDX(q1, p2, N)] = c2 * x10 - s2 * x11;
+        nxt[IDX(q1, q2, N)] = s2 * x10 + c2 * x11;
+      }
+      for (int64_t e = gtid; e < (int64_t)N * H; e += gsz) {
+        int k = (int)(e / N);
+        if (!sact[k]) continue;
+        int i = (int)(e - (int64_t)k * N);
+        int p, q;
+        rr_pair(r, k, N, p, q);
+        double c = sc[k], sn = ss[k];
+        double vp = __ldcg(Q + IDX(i, p, N)), vq = __ldcg(Q + IDX(i, q, N));
+        Q[IDX(i, p, N)] = c * vp - sn * vq;
+        Q[IDX(i, q, N)] = sn * vp + c * vq;
+      }
+      cluster_sync_all();
+      double* tmp = cur; cur = nxt; nxt = tmp;
+    }
+    __syncthreads();
+    done = (srot == 0);
+    ++sweep;
+    __syncthreads();
+  }
+  if (gtid == 0) {
+    info[0] = done ? sweep : -1;
+    info[1] = (cur == Ma) ? 0 : 1;
   }
 }
 
@@ -527,6 +666,11 @@ __global__ void __launch_bounds__(NT) offdiag_fro_kernel(int s, const double* __
   }
   acc = block_sum<NT>(acc, red);
   if (threadIdx.x == 0) out[0] = sqrt(acc);
+}
+
+__global__ void fill_identity_kernel(int k, double* __restrict__ M, int ld) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < k) M[IDX(i, i, ld)] = 1.0;
 }
 
 // P = (P + P^T)/2 in place (n x n, ld)

@@ -17,6 +17,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -139,16 +140,21 @@ static int g_coop_blocks = 0;
 static int jacobi_run(cudaStream_t st, int s, const double* A, int lda, double* w, double* V, int ldv, double* M,
                       double* M2, double* Q, int* d_info, int* d_counters, double* d_fro, int max_sweeps = 60) {
   if (s <= 0) return 0;
-  if (s <= JAC_SMEM_MAX) {
+  static int smem_max = -1;
+  if (smem_max < 0) {
+    smem_max = JAC_SMEM_MAX;
+    if (const char* e = getenv("PSDPROJ_JACOBI_SMEM_MAX")) smem_max = std::min(JAC_SMEM_MAX, atoi(e));
+  }
+  if (s <= smem_max) {
     int N = s + (s & 1);
-    size_t smem = (size_t)2 * N * N * sizeof(double);
+    size_t smem = (size_t)2 * N * (N + 1) * sizeof(double);
     static bool attr = false;
     if (!attr) {
-      CK(cudaFuncSetAttribute(jacobi_smem_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)(2 * JAC_SMEM_MAX * JAC_SMEM_MAX * sizeof(double))));
+      CK(cudaFuncSetAttribute(jacobi_smem_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)(2 * JAC_SMEM_MAX * (JAC_SMEM_MAX + 1) * sizeof(double))));
       attr = true;
     }
-    jacobi_smem_kernel<1024><<<1, 1024, smem, st>>>(s, A, lda, w, V, ldv, max_sweeps, d_info);
+    jacobi_smem_kernel<512><<<1, 512, smem, st>>>(s, A, lda, w, V, ldv, max_sweeps, d_info);
     CKL();
     return 0;
   }
@@ -158,16 +164,47 @@ static int jacobi_run(cudaStream_t st, int s, const double* A, int lda, double* 
   fro_kernel<1024><<<1, 1024, 0, st>>>((int64_t)N * N, M, d_fro);
   CKL();
   CK(cudaMemsetAsync(d_counters, 0, sizeof(int) * (max_sweeps + 2), st));
-  if (!g_coop_blocks) {
-    int per = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, jacobi_coop_kernel, 256, 0));
-    g_coop_blocks = std::max(1, std::min(per, 4)) * sms();
+  int mode = 1;  // 1 = cluster, 2 = cooperative grid
+  if (const char* e = getenv("PSDPROJ_JACOBI_MODE")) mode = atoi(e);
+  double afl_scale = PSD_U;  // absolute floor u ||A||_F (R39)
+  if (mode == 1) {
+    static bool attr = false;
+    if (!attr) {
+      CK(cudaFuncSetAttribute(jacobi_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      attr = true;
+    }
+    if (N / 2 > JAC_CL_MAXH) return set_err(PSDPROJ_E_CAPACITY, "Jacobi size %d > %d", s, 2 * JAC_CL_MAXH);
+    int cs = s <= 160 ? 8 : 16;
+    if (const char* e = getenv("PSDPROJ_JACOBI_CS")) cs = std::max(1, std::min(16, atoi(e)));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cs);
+    cfg.blockDim = dim3(1024);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, jacobi_cluster_kernel, s, N, M, M2, Q, (const double*)d_fro, afl_scale, max_sweeps,
+                          d_info));
+    ++g_launches;
+  } else {
+    if (!g_coop_blocks) {
+      int per = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, jacobi_coop_kernel, 512, 0));
+      if (per < 1) return set_err(PSDPROJ_E_CUDA, "jacobi_coop_kernel cannot be co-resident");
+      g_coop_blocks = sms();  // one CTA per SM: the grid barrier is the per-round cost
+      if (const char* e = getenv("PSDPROJ_JACOBI_CTAS")) g_coop_blocks = std::max(1, std::min(atoi(e), sms()));
+    }
+    if (N / 2 > JAC_COOP_MAXH) return set_err(PSDPROJ_E_CAPACITY, "Jacobi size %d > %d", s, 2 * JAC_COOP_MAXH);
+    void* args[] = {(void*)&s, (void*)&N, (void*)&M, (void*)&M2, (void*)&Q, (void*)&d_fro, (void*)&afl_scale,
+                    (void*)&max_sweeps, (void*)&d_counters, (void*)&d_info};
+    CK(cudaLaunchCooperativeKernel((void*)jacobi_coop_kernel, dim3(g_coop_blocks), dim3(512), args, 0, st));
+    ++g_launches;
   }
-  double afl_scale = PSD_U / (double)s;
-  void* args[] = {(void*)&s, (void*)&N, (void*)&M, (void*)&M2, (void*)&Q, (void*)&d_fro, (void*)&afl_scale,
-                  (void*)&max_sweeps, (void*)&d_counters, (void*)&d_info};
-  CK(cudaLaunchCooperativeKernel((void*)jacobi_coop_kernel, dim3(g_coop_blocks), dim3(256), args, 0, st));
-  ++g_launches;
   jacobi_extract_kernel<<<grid1d((size_t)s * s), 256, 0, st>>>(s, N, M, M2, Q, d_info, w, V, ldv);
   CKL();
   return 0;
@@ -423,11 +460,21 @@ struct Run {
     info->flops += 9.0 * s * (double)s * s + s * (double)s * s / 3.0 + 2.0 * s * (double)s * s;
     insert_known_kernel<<<grid1d((size_t)s * s), 256, 0, st>>>(s, kxG, kxH, c->G, c->Hm, ldm, d_theta_known);
     CKL();
-    TRY(copy_cols(s, s, c->Gc, ldm, c->G, ldm));
-    cholesky_kernel<1024><<<1, 1024, 0, st>>>(s, c->Gc, ldm, 1e-12, c->d_status);
-    CKL();
-    trinv_kernel<<<cdiv(s, 8), 256, 0, st>>>(s, c->Gc, ldm, c->Li, ldm);
-    CKL();
+    // G = [I 0; 0 D]: factor only the direction block D = L22 L22^T (size t = s - kxG)
+    const int kx = kxG, t = s - kxG;
+    CK(cudaMemset2DAsync(c->Li, (size_t)ldm * 8, 0, (size_t)s * 8, s, st));
+    if (kx > 0) {
+      fill_identity_kernel<<<cdiv(kx, 256), 256, 0, st>>>(kx, c->Li, ldm);
+      CKL();
+    }
+    CK(cudaMemsetAsync(c->d_status, 0, sizeof(int), st));
+    if (t > 0) {
+      TRY(copy_cols(t, t, c->Gc, ldm, c->G + kx + (size_t)kx * ldm, ldm));
+      cholesky_kernel<1024><<<1, 1024, 0, st>>>(t, c->Gc, ldm, 1e-12, c->d_status);
+      CKL();
+      trinv_kernel<<<cdiv(t, 8), 256, 0, st>>>(t, c->Gc, ldm, c->Li + kx + (size_t)kx * ldm, ldm);
+      CKL();
+    }
     // Hh = L^-1 H L^-T
     TRY(dgemm(st, OP_N, OP_N, s, s, s, 1.0, c->Li, ldm, c->Hm, ldm, 0.0, c->Y, ldm, c->part, c->part_elems));
     TRY(dgemm(st, OP_N, OP_T, s, s, s, 1.0, c->Y, ldm, c->Li, ldm, 0.0, c->Hh, ldm, c->part, c->part_elems));
@@ -444,7 +491,7 @@ struct Run {
     TRY(sync());
     int chol = c->h_i[c->h_i_len - 16];
     int sweeps = c->h_i[c->h_i_len - 16 + 4];
-    if (chol) return chol;
+    if (chol) return chol + kx;
     if (sweeps < 0) return set_err(PSDPROJ_E_DEGENERATE, "Jacobi did not converge (s=%d)", s);
     return 0;
   }
@@ -683,6 +730,10 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
       TRY(run.gemm(OP_T, OP_N, nL, aw, n, 1.0, c->XL, ld, W, ld, 0.0, c->Y, ldm));
       TRY(run.gemm(OP_N, OP_N, n, aw, nL, -1.0, c->XL, ld, c->Y, ldm, 1.0, W, ld));
     }
+    if (aw > 0) {  // W <- W - X_U (X_U^T W): the pencil's X-block of G becomes [I 0]
+      TRY(run.gemm(OP_T, OP_N, mU, aw, n, 1.0, c->S, ld, W, ld, 0.0, c->Y, ldm));
+      TRY(run.gemm(OP_N, OP_N, n, aw, mU, -1.0, c->S, ld, c->Y, ldm, 1.0, W, ld));
+    }
     TRY(run.normalize(n, aw, W, ld, nullptr, 0));
     TRY(run.amul(sgn, A, lda, W, ld, aw, c->BS + (size_t)offW * ld, ld));
     // P_J, B P_J
@@ -696,10 +747,15 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
         TRY(run.gemm(OP_N, OP_N, n, ap, nL, -1.0, c->XL, ld, c->Y, ldm, 1.0, P, ld));
         TRY(run.gemm(OP_N, OP_N, n, ap, nL, -1.0, c->BXL, ld, c->Y, ldm, 1.0, BP, ld));
       }
+      TRY(run.gemm(OP_T, OP_N, mU, ap, n, 1.0, c->S, ld, P, ld, 0.0, c->Y, ldm));
+      TRY(run.gemm(OP_N, OP_N, n, ap, mU, -1.0, c->S, ld, c->Y, ldm, 1.0, P, ld));
+      TRY(run.gemm(OP_N, OP_N, n, ap, mU, -1.0, c->BS, ld, c->Y, ldm, 1.0, BP, ld));
       TRY(run.normalize(n, ap, P, ld, BP, ld));
     }
     // ---- line 6: Rayleigh-Ritz on span(X, R, P) via the pencil (S^T BS, S^T S)
-    TRY(run.gemm(OP_T, OP_N, s, s, n, 1.0, c->S, ld, c->S, ld, 0.0, c->G, ldm));
+    // only the direction block of G is needed (X^T X = I, X^T [W P] = 0 by construction)
+    TRY(run.gemm(OP_T, OP_N, s - mU, s - mU, n, 1.0, c->S + (size_t)mU * ld, ld, c->S + (size_t)mU * ld, ld, 0.0,
+                 c->G + mU + (size_t)mU * ldm, ldm));
     TRY(run.gemm(OP_T, OP_N, s, s, n, 1.0, c->S, ld, c->BS, ld, 0.0, c->Hm, ldm));
     int sU = s;
     rc = run.rr(s, mU, mU, c->d_thU, std::min(mU + qe, s));
