@@ -147,6 +147,14 @@ size_t psdproj_jacobi_ws_elems(int s);
 int psdproj_jacobi(int s, const double* A, int lda, double* w, double* V, int ldv, double* ws,
                    void* stream);
 
+/* Top-m eigenpairs of a symmetric s x s matrix by the path's Rayleigh-Ritz eigensolver (a7):
+ * Householder tridiagonalisation, bisection, inverse iteration, back-transformation.
+ * w (m, device, DESCENDING), V (s x m, ldv, device), npos (device int: #eigenvalues > 0).
+ * ws: device scratch of psdproj_eigh_ws_elems(s, m) doubles. */
+size_t psdproj_eigh_ws_elems(int s, int m);
+int psdproj_eigh(int s, const double* A, int lda, int m, double* w, double* V, int ldv, int* npos,
+                 double* ws, void* stream);
+
 /* Raw Philox4x32-10 stream: out[4i+j] for counters (i, c1, c2, c3), key (k0, k1), device out. */
 int psdproj_philox_raw(int count, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0, uint32_t k1,
                        uint32_t* out, void* stream);

@@ -19,7 +19,8 @@ EXPORTS = [
     "psdproj_default_params", "psdproj_workspace_bytes", "psdproj_create", "psdproj_project",
     "psdproj_project_host", "psdproj_project_batched", "psdproj_get_ritz", "psdproj_reset",
     "psdproj_destroy", "psdproj_last_error", "psdproj_dgemm", "psdproj_jacobi_ws_elems",
-    "psdproj_jacobi", "psdproj_philox_raw", "psdproj_philox_gauss",
+    "psdproj_jacobi", "psdproj_philox_raw", "psdproj_philox_gauss", "psdproj_eigh_ws_elems",
+    "psdproj_eigh",
 ]
 
 
@@ -79,10 +80,13 @@ def load(path=SO_PATH):
     L.psdproj_jacobi_ws_elems.argtypes = [i]
     L.psdproj_jacobi_ws_elems.restype = sz
     L.psdproj_jacobi.argtypes = [i, vp, i, vp, vp, i, vp, vp]
+    L.psdproj_eigh_ws_elems.argtypes = [i, i]
+    L.psdproj_eigh_ws_elems.restype = sz
+    L.psdproj_eigh.argtypes = [i, vp, i, i, vp, vp, i, vp, vp, vp]
     L.psdproj_philox_raw.argtypes = [i, u32, u32, u32, u32, u32, vp, vp]
     L.psdproj_philox_gauss.argtypes = [i, i, vp, i, u64, u32, u32, u32, vp]
     special = ("psdproj_default_params", "psdproj_workspace_bytes", "psdproj_last_error",
-               "psdproj_jacobi_ws_elems")
+               "psdproj_jacobi_ws_elems", "psdproj_eigh_ws_elems")
     for name in EXPORTS:
         if name not in special:
             getattr(L, name).restype = ctypes.c_int

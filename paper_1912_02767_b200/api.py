@@ -183,6 +183,20 @@ def jacobi(A, stream=None):
     return w, V, sweeps
 
 
+def eigh(A, m=None, stream=None):
+    """Top-m eigenpairs (descending) by the path's tridiagonal eigensolver: (w, V, npos)."""
+    L = _lib.load()
+    s = A.shape[0]
+    m = s if m is None else m
+    w = torch.empty(max(m, 1), dtype=torch.float64, device=A.device)
+    V = colmajor(s, max(m, 1), device=A.device)
+    npos = torch.zeros(1, dtype=torch.int32, device=A.device)
+    ws = torch.empty(int(L.psdproj_eigh_ws_elems(s, m)), dtype=torch.float64, device=A.device)
+    check(L.psdproj_eigh(s, _ptr(A), _ld_sym(A), m, _ptr(w), _ptr(V), s, _ptr(npos), _ptr(ws), _stream_ptr(stream)),
+          "psdproj_eigh")
+    return w[:m], V[:, :m], int(npos.item())
+
+
 def philox_raw(count, c1, c2, c3, k0, k1, device="cuda", stream=None):
     L = _lib.load()
     out = torch.empty(4 * count, dtype=torch.int32, device=device)

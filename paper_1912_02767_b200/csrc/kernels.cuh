@@ -668,6 +668,19 @@ __global__ void __launch_bounds__(NT) offdiag_fro_kernel(int s, const double* __
   if (threadIdx.x == 0) out[0] = sqrt(acc);
 }
 
+__global__ void count_pos_kernel(int s, const double* __restrict__ w, int* __restrict__ out) {
+  __shared__ int cnt;
+  if (threadIdx.x == 0) cnt = 0;
+  __syncthreads();
+  int c = 0;
+  for (int i = threadIdx.x; i < s; i += blockDim.x) c += w[i] > 0.0;
+  atomicAdd(&cnt, c);
+  __syncthreads();
+  if (threadIdx.x == 0) *out = cnt;
+}
+
+__global__ void set_int_kernel(int* p, int v) { *p = v; }
+
 __global__ void fill_identity_kernel(int k, double* __restrict__ M, int ld) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < k) M[IDX(i, i, ld)] = 1.0;

@@ -27,6 +27,7 @@
 #include "common.cuh"
 #include "gemm.cuh"
 #include "kernels.cuh"
+#include "tridiag.cuh"
 
 using namespace psd;
 
@@ -210,6 +211,53 @@ static int jacobi_run(cudaStream_t st, int s, const double* A, int lda, double* 
   return 0;
 }
 
+// ------------------------------------------------------------------ tridiagonal eigensolver (a7)
+// Top-m eigenpairs (descending) of the symmetric s x s matrix H: Householder tridiagonalisation,
+// multisection bisection, inverse iteration + clustered MGS, back-transformation (tridiag.cuh).
+static int eigh_top(cudaStream_t st, int s, const double* Hs, int ldh, int m, double* lam, double* Yv, int ldy,
+                    int* npos, double* td, double* te, double* ttau, double* te2, double* tbounds, double* tscr,
+                    double* tG, int ldg, double* Vh, int ldv) {
+  // tridiag dynamic smem: [M s(s+1) when s <= TRI_SMEM_MAX] sv[s] sp[s + 8 s]
+  const size_t vecs = (size_t)s * 10;
+  size_t dyn = ((s <= TRI_SMEM_MAX) ? (size_t)s * (s + 1) : 0) + vecs;
+  dyn *= sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(tridiag_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)((size_t)(TRI_SMEM_MAX * (TRI_SMEM_MAX + 1) + 10 * TRI_SMEM_MAX) * sizeof(double))));
+    CK(cudaFuncSetAttribute(tri_inviter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    CK(cudaFuncSetAttribute(tri_bisect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    attr = true;
+  }
+  if (s > TRI_SMEM_MAX && dyn > 200 * 1024) return set_err(PSDPROJ_E_CAPACITY, "tridiag smem %zu for s=%d", dyn, s);
+  if (s > 32 * TRI_BT_PER_LANE) return set_err(PSDPROJ_E_CAPACITY, "eigensolver supports s <= %d", 32 * TRI_BT_PER_LANE);
+  tridiag_kernel<1024><<<1, 1024, dyn, st>>>(s, Hs, ldh, td, te, ttau, Vh, ldv, tG, ldg);
+  CKL();
+  tri_prep_kernel<<<1, 1024, 0, st>>>(s, td, te, te2, tbounds);
+  CKL();
+  tri_bisect_kernel<<<cdiv(m + 1, 8), 256, (size_t)2 * s * sizeof(double), st>>>(s, m, td, te2, tbounds, lam, npos);
+  CKL();
+  if (m > 0) {
+    // inverse iteration: vectors per CTA so that 6 s doubles each fit in shared memory
+    int vpb = (int)std::min<size_t>(64, (220 * 1024) / ((size_t)6 * s * sizeof(double)));
+    int smem_ok = vpb >= 1;
+    if (!smem_ok) vpb = 64;
+    size_t ism = smem_ok ? (size_t)6 * s * vpb * sizeof(double) : 0;
+    for (int pass = 0; pass < 2; ++pass) {
+      tri_inviter_kernel<<<cdiv(m, vpb), vpb, ism, st>>>(s, m, td, te, lam, tbounds, Yv, ldy, tscr, pass ? 1 : 2,
+                                                         pass, smem_ok);
+      CKL();
+      tri_cluster_mgs_kernel<1024><<<1, 1024, 0, st>>>(s, m, lam, tbounds, Yv, ldy);
+      CKL();
+    }
+    if (s > 2) {
+      tri_backtransform_kernel<<<cdiv(m, 8), 256, 0, st>>>(s, m, Vh, ldv, ttau, Yv, ldy);
+      CKL();
+    }
+  }
+  return 0;
+}
+
 // ------------------------------------------------------------------ context
 struct psdproj_ctx_s {
   int n = 0, ld = 0;
@@ -226,6 +274,11 @@ struct psdproj_ctx_s {
   double *d_thU = nullptr, *d_r = nullptr, *d_norm = nullptr, *d_w = nullptr, *d_ths = nullptr, *d_scal = nullptr;
   int *d_idx = nullptr, *d_order = nullptr, *d_status = nullptr, *d_counters = nullptr;
   double* stage = nullptr;  // host_io staging (n x n, ld)
+  // tridiagonal eigensolver scratch (a7)
+  double *td = nullptr, *te = nullptr, *ttau = nullptr, *te2 = nullptr, *tbounds = nullptr, *tscr = nullptr,
+         *tG = nullptr;
+  int* tnpos = nullptr;
+  size_t tscr_elems = 0;
   // pinned host mirrors
   double* h_d = nullptr;
   int* h_i = nullptr;
@@ -296,6 +349,11 @@ static size_t carve(psdproj_ctx_s* c, int n, const psdproj_params& p, int m_max,
   c->d_idx = cv.take<int>((size_t)8 * (std::max(s_max, n) + 64)); c->d_order = cv.take<int>(vlen); c->d_status = cv.take<int>(64);
   c->d_counters = cv.take<int>(128);
   c->stage = p.host_io ? cv.take<double>((size_t)ld * n) : nullptr;
+  c->td = cv.take<double>(vlen); c->te = cv.take<double>(vlen); c->ttau = cv.take<double>(vlen);
+  c->te2 = cv.take<double>(vlen); c->tbounds = cv.take<double>(8); c->tnpos = cv.take<int>(8);
+  c->tscr_elems = (size_t)6 * s_max * (size_t)(std::min(s_max, m_max + (s_max - 3 * m_max)) + 1);
+  c->tscr = cv.take<double>(c->tscr_elems);
+  c->tG = cv.take<double>(s2);
   return cv.off + 256;
 }
 
@@ -377,6 +435,7 @@ struct Run {
   cudaStream_t st;
   psdproj_info* info;
   int ihost = 0;  // next free int slot in the pinned buffer (per iteration)
+  int rr_npos = 0;  // positive Ritz values among all s of the last Rayleigh-Ritz (expansion test)
   int nev = 0;
   double anorm = 0.0;
 
@@ -452,6 +511,11 @@ struct Run {
     CKL();
     return 0;
   }
+  int tri_eig(int s, const double* Hs, int ldh, int m, double* lam, double* Yv, int ldy, int* npos) {
+    if ((size_t)6 * s * (size_t)m > c->tscr_elems) return set_err(PSDPROJ_E_CAPACITY, "eigensolver scratch");
+    return eigh_top(st, s, Hs, ldh, m, lam, Yv, ldy, npos, c->td, c->te, c->ttau, c->te2, c->tbounds, c->tscr, c->tG,
+                    c->s_max, c->Vj, c->s_max);
+  }
   // Rayleigh-Ritz on the pencil (H, G) in c->G / c->Hm (s x s, ld s_max):
   // returns 0 (ok), >0 (Cholesky failed at that pivot), <0 error. Outputs Cp (s x mU), theta desc in h_d[0..s).
   int rr(int s, int kxG, int kxH, const double* d_theta_known, int mU) {
@@ -478,19 +542,38 @@ struct Run {
     // Hh = L^-1 H L^-T
     TRY(dgemm(st, OP_N, OP_N, s, s, s, 1.0, c->Li, ldm, c->Hm, ldm, 0.0, c->Y, ldm, c->part, c->part_elems));
     TRY(dgemm(st, OP_N, OP_T, s, s, s, 1.0, c->Y, ldm, c->Li, ldm, 0.0, c->Hh, ldm, c->part, c->part_elems));
-    TRY(jacobi_run(st, s, c->Hh, ldm, c->d_w, c->Vj, ldm, c->jM, c->jM2, c->jQ, c->d_status + 4, c->d_counters,
-                   c->d_scal));
-    sort_desc_kernel<<<cdiv(s, 256), 256, 0, st>>>(s, c->d_w, c->d_order, c->d_ths);
-    CKL();
-    // C' = L^-T V[:, order[:mU]]
-    gather_cols_kernel<<<grid1d((size_t)s * mU), 256, 0, st>>>(s, mU, c->Y, ldm, c->Vj, ldm, c->d_order);
-    CKL();
+    // eigensolver choice by measured crossover: tridiagonal path while the matrix fits in shared memory (s <= 160),
+    // cooperative Jacobi above (single-SM tridiagonalisation in global memory is L2-bandwidth bound)
+    static int rr_mode = -1;  // 0 auto, 1 jacobi, 2 tridiag
+    if (rr_mode < 0) {
+      const char* e = getenv("PSDPROJ_RR");
+      rr_mode = !e ? 0 : (std::string(e) == "jacobi" ? 1 : (std::string(e) == "tridiag" ? 2 : 0));
+    }
+    bool use_jacobi = rr_mode == 1 || (rr_mode == 0 && s > TRI_SMEM_MAX);
+    if (use_jacobi) {
+      TRY(jacobi_run(st, s, c->Hh, ldm, c->d_w, c->Vj, ldm, c->jM, c->jM2, c->jQ, c->d_status + 4, c->d_counters,
+                     c->d_scal));
+      sort_desc_kernel<<<cdiv(s, 256), 256, 0, st>>>(s, c->d_w, c->d_order, c->d_ths);
+      CKL();
+      count_pos_kernel<<<1, 256, 0, st>>>(s, c->d_w, c->tnpos);
+      CKL();
+      // C' = L^-T V[:, order[:mU]]
+      gather_cols_kernel<<<grid1d((size_t)s * mU), 256, 0, st>>>(s, mU, c->Y, ldm, c->Vj, ldm, c->d_order);
+      CKL();
+    } else {
+      TRY(tri_eig(s, c->Hh, ldm, mU, c->d_ths, c->Y, ldm, c->tnpos));
+      CK(cudaMemsetAsync(c->d_status + 4, 0, sizeof(int), st));
+      set_int_kernel<<<1, 1, 0, st>>>(c->d_status + 4, 1);
+      CKL();
+    }
     TRY(dgemm(st, OP_T, OP_N, s, mU, s, 1.0, c->Li, ldm, c->Y, ldm, 0.0, c->Cp, ldm, c->part, c->part_elems));
-    CK(cudaMemcpyAsync(c->h_d, c->d_ths, sizeof(double) * s, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(c->h_d, c->d_ths, sizeof(double) * mU, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(c->h_i + c->h_i_len - 16, c->d_status, sizeof(int) * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(c->h_i + c->h_i_len - 24, c->tnpos, sizeof(int), cudaMemcpyDeviceToHost, st));
     TRY(sync());
     int chol = c->h_i[c->h_i_len - 16];
     int sweeps = c->h_i[c->h_i_len - 16 + 4];
+    rr_npos = c->h_i[c->h_i_len - 24];
     if (chol) return chol + kx;
     if (sweeps < 0) return set_err(PSDPROJ_E_DEGENERATE, "Jacobi did not converge (s=%d)", s);
     return 0;
@@ -623,7 +706,7 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
   int rc = run.rr(m, cold ? 0 : m, 0, c->d_thU, m);
   if (rc > 0) return set_err(PSDPROJ_E_DEGENERATE, "start block rank deficient");
   TRY(rc);
-  std::vector<double> thU(c->h_d, c->h_d + m);
+  std::vector<double> thU(c->h_d, c->h_d + m);  // all m values (the initial RR keeps m of m)
   TRY(run.gemm(OP_N, OP_N, n, m, m, 1.0, c->S, ld, c->Cp, ldm, 0.0, c->S2, ld));
   TRY(run.gemm(OP_N, OP_N, n, m, m, 1.0, c->BS, ld, c->Cp, ldm, 0.0, c->BS2, ld));
   std::swap(c->S, c->S2);
@@ -765,8 +848,9 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
     }
     if (rc > 0) return set_err(PSDPROJ_E_DEGENERATE, "Cholesky-QR failed at pivot %d (s=%d)", rc, sU);
     TRY(rc);
-    std::vector<double> ths(c->h_d, c->h_d + sU);
     int mUn = std::min(mU + qe, sU);
+    std::vector<double> ths(c->h_d, c->h_d + mUn);
+    const int rr_npos = run.rr_npos;
     // ---- rotation (a8): X <- S C', BX <- BS C', P <- S_[R P] C'_[R P], BP likewise
     TRY(run.gemm(OP_N, OP_N, n, mUn, sU, 1.0, c->S, ld, c->Cp, ldm, 0.0, c->S2, ld));
     TRY(run.gemm(OP_N, OP_N, n, mUn, sU, 1.0, c->BS, ld, c->Cp, ldm, 0.0, c->BS2, ld));
@@ -782,8 +866,7 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
     qe = 0;
     ++k;
     // ---- line 8: expansion when fewer than g guards would remain (R8)
-    int p_rr = (hard ? nL : 0);
-    for (double x : ths) p_rr += x > 0;
+    int p_rr = (hard ? nL : 0) + rr_npos;  // positive RR values among all sU (R8)
     int mt = nL + mU;
     if (p_rr >= mt - g + 1 && mt < n) {
       int qq = std::min(c->q, n - mt);
@@ -1060,5 +1143,27 @@ extern "C" int psdproj_philox_gauss(int n, int q, double* out, int ld, uint64_t 
   philox_gauss_kernel<<<grid1d(((size_t)n * q + 1) / 2), 256, 0, (cudaStream_t)stream>>>(n, q, out, ld, seed,
                                                                                            stream_id, ctx, tag);
   CKL();
+  return 0;
+}
+
+extern "C" size_t psdproj_eigh_ws_elems(int s, int m) {
+  return (size_t)5 * s + 64 + (size_t)6 * s * (size_t)std::max(m, 1) + 2 * (size_t)s * s + 64;
+}
+
+extern "C" int psdproj_eigh(int s, const double* A, int lda, int m, double* w, double* V, int ldv, int* npos,
+                            double* ws, void* stream) {
+  if (s <= 0 || m < 0 || m > s || lda < s || ldv < s || !A || !w || !V || !npos || !ws)
+    return set_err(PSDPROJ_E_INVALID, "invalid eigh args");
+  cudaStream_t st = (cudaStream_t)stream;
+  double* td = ws;
+  double* te = td + s;
+  double* ttau = te + s;
+  double* te2 = ttau + s;
+  double* tb = te2 + s + 8;
+  double* tscr = tb + 56;
+  double* tG = tscr + (size_t)6 * s * (size_t)std::max(m, 1);
+  double* Vh = tG + (size_t)s * s;
+  TRY(eigh_top(st, s, A, lda, m, w, V, ldv, npos, td, te, ttau, te2, tb, tscr, tG, s, Vh, s));
+  CK(cudaStreamSynchronize(st));
   return 0;
 }

@@ -71,3 +71,39 @@ def test_philox_gauss_matches_oracle(api):
     got = api.philox_gauss(n, q, seed=99, stream_id=5, ctx=2, tag=3).cpu().numpy()
     ref = gaussian_block(n, q, 99, 5, ctx=2, tag=3)
     assert np.abs(got - ref).max() < 1e-13
+
+
+@pytest.mark.parametrize("s,m", [(1, 1), (2, 2), (3, 1), (17, 17), (64, 20), (160, 60), (161, 161), (300, 100),
+                                 (500, 170)])
+def test_eigh_tridiagonal(api, s, m):
+    rng = np.random.default_rng(1000 + s)
+    M = rng.standard_normal((s, s))
+    A = (M + M.T) / 2
+    w, V, npos = api.eigh(_cm(A), m)
+    w = w.cpu().numpy()
+    V = V.cpu().numpy()
+    ref = np.linalg.eigvalsh(A)[::-1][:m]
+    scale = max(1.0, np.abs(ref).max())
+    assert np.abs(w - ref).max() <= 1e-12 * scale * max(1, s / 20)
+    assert npos == int(np.sum(np.linalg.eigvalsh(A) > 0))
+    assert np.linalg.norm(V.T @ V - np.eye(m)) <= 1e-11 * max(1, s / 20)
+    R = A @ V - V * w
+    assert np.linalg.norm(R, axis=0).max() <= 1e-11 * scale * max(1, s / 20)
+
+
+def test_eigh_clustered_spectrum(api):
+    """Planted spectrum with a tight near-zero cluster (the C3-R regime of the RR pencil)."""
+    from workloads.generators import haar_q, planted
+    rng = np.random.default_rng(5)
+    s = 240
+    lam = np.concatenate([10.0 ** rng.uniform(-3, 2, 40), -(10.0 ** rng.uniform(-3, 2, 180)),
+                          rng.uniform(-1e-9, 1e-9, 20)])
+    A = planted(haar_q(rng, s), lam)
+    m = 80
+    w, V, npos = api.eigh(_cm(A), m)
+    w = w.cpu().numpy()
+    V = V.cpu().numpy()
+    ref = np.sort(lam)[::-1][:m]
+    assert np.abs(w - ref).max() <= 1e-12 * 100 * 5
+    assert np.linalg.norm(V.T @ V - np.eye(m)) <= 1e-10
+    assert np.linalg.norm(A @ V - V * w, axis=0).max() <= 1e-10 * 100
