@@ -63,7 +63,7 @@ typedef struct {
   int m_max;      /* block-width capacity; 0 => ceil(n/3)+1 (wider => DIRECT, R18)              */
   uint64_t seed;  /* Philox4x32-10 key (R11)                                                    */
   uint32_t ctx_id;/* Philox counter word c2 (distinct per cone block)                           */
-  int profile;    /* 1: time every block-multiply (a3) launch with CUDA events into info        */
+  int profile;    /* bit 0: time every block-multiply (a3) launch; bit 1: per-phase timing       */
   int host_io;    /* 1: workspace also holds an n x n staging buffer for psdproj_project_host   */
 } psdproj_params;
 
@@ -92,6 +92,9 @@ typedef struct {
   int amul_launches;/* number of timed block-multiply launches                                 */
   int last_pos, last_neg; /* sign counts fed to the next call's side rule                      */
   int launches;     /* kernels this call launched (all of them libpsdproj's own)               */
+  double phase_ms[8]; /* profile & 2: device time per phase: 0 block multiply, 1 W/P projection,
+                         2 Gram/pencil, 3 Cholesky + L^-1 H L^-T, 4 RR eigensolve, 5 rotation,
+                         6 residual norms, 7 host round trips / locking / assembly            */
 } psdproj_info;
 
 /* Fill *p with the defaults documented above. */

@@ -43,10 +43,13 @@ class Info(ctypes.Structure):
         ("flops", ctypes.c_double), ("bytes", ctypes.c_double), ("amul_flops", ctypes.c_double),
         ("amul_bytes", ctypes.c_double), ("amul_ms", ctypes.c_double), ("amul_launches", ctypes.c_int),
         ("last_pos", ctypes.c_int), ("last_neg", ctypes.c_int), ("launches", ctypes.c_int),
+        ("phase_ms", ctypes.c_double * 8),
     ]
 
     def as_dict(self):
-        return {f: getattr(self, f) for f, _ in self._fields_}
+        d = {f: getattr(self, f) for f, _ in self._fields_}
+        d["phase_ms"] = list(self.phase_ms)
+        return d
 
 
 _lib = None

@@ -1,0 +1,567 @@
+// cluster_la.cuh -- latency-bound small dense linear algebra of the Rayleigh-Ritz step (a6, a7)
+// on one thread-block cluster (up to 16 CTAs on 16 SMs), the matrix distributed column-cyclically
+// over the CTAs' shared memory and exchanged through distributed shared memory (DSMEM).
+//
+//   cholesky_cluster_kernel  G = L L^T of the direction-block Gram (a6, implicit Cholesky-QR,
+//                            PAPER.md:395-397); one cluster barrier per column.
+//   tridiag_cluster_kernel   Householder tridiagonalisation Q^T H Q = T of the Rayleigh-Ritz
+//                            matrix (a7, the eigensolve of Alg. 2); two cluster
+//                            barriers per column.
+//
+// Why a cluster: both factorizations are s sequential column steps. One CTA streams the whole
+// trailing matrix through one SM's shared memory per step (s = 400: 1.3 MB does not fit); a
+// grid-wide barrier costs microseconds. A 16-CTA cluster holds s <= 640 in 16 x 227 KB of shared
+// memory, its barrier costs ~0.2 us (B300_MICROARCH.md: cluster.sync ~380 cycles) and every CTA
+// only touches its own s/16 columns per step.
+//
+// Column g lives in CTA (g % CS) at local column g / CS (leading dimension = matrix order).
+// Conventions match tridiag.cuh (LAPACK dsytd2, lower): reflector j has v[j+1] = 1, stored in
+// column j of Vh for the back-transformation kernel there.
+#pragma once
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+
+namespace psd {
+
+namespace cg = cooperative_groups;
+
+constexpr int CLA_NT = 512;
+constexpr int CLA_MAX = 640;  // largest order held in a 16-CTA cluster's shared memory
+constexpr int CLA_SMEM_BYTES = 226 * 1024;  // dynamic smem cap (227 KB minus the static arrays)
+
+__device__ __forceinline__ void cla_cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ unsigned cla_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+template <typename T>
+__device__ __forceinline__ T* cla_remote(T* p, unsigned rank) {
+  return cg::this_cluster().map_shared_rank(p, rank);
+}
+
+__device__ __forceinline__ double cla_block_sum(double v, double* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();  // red may still be read by a previous call
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    v = (l < (int)(blockDim.x >> 5)) ? red[l] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (l == 0) red[32] = v;
+  }
+  __syncthreads();
+  return red[32];
+}
+
+// ------------------------------------------------------------------ Cholesky (a6)
+// Blocked right-looking Cholesky on a cluster. Column blocks of CHOL_NB columns are dealt
+// block-cyclically (block b -> CTA b % CS, full column storage, ld = t). Per block: the owner
+// factors its panel with CTA barriers only, one cluster barrier publishes it, every CTA copies the
+// panel (DSMEM) and applies the rank-CHOL_NB update to its own later columns. t/CHOL_NB cluster
+// barriers instead of t.
+// In place on G (t x t, ld): lower triangle <- L, upper <- 0. status = j + 1 when pivot j is
+// <= fail_rel * max diag(G) (R20), else 0.
+constexpr int CHOL_NB = 8;
+__host__ __device__ inline int chol_local_cols(int t, int CS) { return cdiv(cdiv(t, CHOL_NB), CS) * CHOL_NB; }
+__host__ __device__ inline size_t chol_smem_doubles(int t, int CS) {
+  return (size_t)chol_local_cols(t, CS) * t + (size_t)CHOL_NB * t + 16;
+}
+
+__global__ void __launch_bounds__(CLA_NT) cholesky_cluster_kernel(int t, double* __restrict__ G, int ld,
+                                                                   double fail_rel, int* __restrict__ status) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ double red[33];
+  __shared__ int sh_bad;
+  const int CS = (int)gridDim.x;
+  const unsigned rank = cla_rank();
+  const int ncl = chol_local_cols(t, CS);
+  double* Al = sm;                      // ncl x t: local column lc = lb * NB + c <-> global (lb * CS + rank) * NB + c
+  double* pl = Al + (size_t)ncl * t;    // NB x t: local copy of the current panel
+  double* xch = pl + (size_t)CHOL_NB * t;  // [0] max diag part, [1..2] fail flag by parity
+  const int tid = threadIdx.x, NT = blockDim.x;
+  const int warp = tid >> 5, lane = tid & 31, nw = NT >> 5;
+  auto gcol = [&](int lc) { return ((lc / CHOL_NB) * CS + (int)rank) * CHOL_NB + (lc % CHOL_NB); };
+  for (int e = tid; e < ncl * t; e += NT) {
+    int lc = e / t, i = e - lc * t, g = gcol(lc);
+    Al[e] = (g < t) ? G[IDX(i, g, ld)] : 0.0;
+  }
+  __syncthreads();
+  double mx = 0.0;
+  for (int lc = tid; lc < ncl; lc += NT) {
+    int g = gcol(lc);
+    if (g < t) mx = fmax(mx, Al[(size_t)lc * t + g]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) red[warp] = mx;
+  __syncthreads();
+  if (tid == 0) {
+    double m = 0.0;
+    for (int w = 0; w < nw; ++w) m = fmax(m, red[w]);
+    xch[0] = m;
+    xch[1] = xch[2] = 0.0;
+  }
+  cla_cluster_sync();
+  if (tid < 32) {
+    double m = (tid < CS) ? *cla_remote(xch, (unsigned)tid) : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (tid == 0) red[32] = m;
+  }
+  __syncthreads();
+  const double floor_ = fail_rel * red[32];
+  const int nblk = cdiv(t, CHOL_NB);
+  int fail = 0;
+  for (int b = 0; b < nblk; ++b) {
+    const int owner = b % CS, par = b & 1, j0 = b * CHOL_NB, jb = min(CHOL_NB, t - j0);
+    if ((int)rank == owner) {
+      double* P = Al + (size_t)(b / CS) * CHOL_NB * t;  // panel columns c = 0..jb-1, rows j0..t-1
+      if (tid == 0) sh_bad = 0;
+      for (int k = 0; k < jb; ++k) {
+        const int j = j0 + k;
+        __syncthreads();
+        const double dj = P[(size_t)k * t + j];
+        if (!(dj > floor_)) {
+          if (tid == 0) sh_bad = j + 1;
+          break;  // uniform: every thread read the same dj
+        }
+        const double ljj = sqrt(dj), inv = 1.0 / ljj;
+        double* pc = P + (size_t)k * t;
+        __syncthreads();
+        for (int i = j + tid; i < t; i += NT) pc[i] = (i == j) ? ljj : pc[i] * inv;
+        __syncthreads();
+        // rank-1 update of the remaining panel columns c > k, rows i >= j0 + c
+        for (int c = k + 1 + warp; c < jb; c += nw) {
+          double* qc = P + (size_t)c * t;
+          const double lg = pc[j0 + c];
+          for (int i = j0 + c + lane; i < t; i += 32) qc[i] -= pc[i] * lg;
+        }
+      }
+      __syncthreads();
+      if (tid == 0) xch[1 + par] = (double)sh_bad;
+    }
+    cla_cluster_sync();  // the panel (in the owner's Al) and its status are visible
+    {
+      const double f = *cla_remote(xch + 1 + par, (unsigned)owner);
+      if (f != 0.0) {
+        fail = (int)f;
+        break;
+      }
+    }
+    const int jn = j0 + jb;  // first column after the panel
+    if (jn < t) {
+      const double* P = cla_remote(Al + (size_t)(b / CS) * CHOL_NB * t, (unsigned)owner);
+      for (int e = tid; e < jb * (t - jn); e += NT) {
+        int c = e / (t - jn), i = jn + (e - c * (t - jn));
+        pl[(size_t)c * t + i] = P[(size_t)c * t + i];
+      }
+      __syncthreads();
+      // own columns g >= jn: G[i][g] -= sum_c L[i][j0+c] L[g][j0+c], i >= g
+      for (int lc = warp; lc < ncl; lc += nw) {
+        const int g = gcol(lc);
+        if (g < jn || g >= t) continue;
+        double lgc[CHOL_NB];
+#pragma unroll
+        for (int c = 0; c < CHOL_NB; ++c) lgc[c] = (c < jb) ? pl[(size_t)c * t + g] : 0.0;
+        double* col = Al + (size_t)lc * t;
+        for (int i = g + lane; i < t; i += 32) {
+          double acc = col[i];
+#pragma unroll
+          for (int c = 0; c < CHOL_NB; ++c)
+            if (c < jb) acc -= pl[(size_t)c * t + i] * lgc[c];
+          col[i] = acc;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (rank == 0 && tid == 0) *status = fail;
+  if (!fail) {
+    for (int e = tid; e < ncl * t; e += NT) {
+      int lc = e / t, i = e - lc * t, g = gcol(lc);
+      if (g < t) G[IDX(i, g, ld)] = (i >= g) ? Al[e] : 0.0;
+    }
+  }
+  cla_cluster_sync();  // no CTA leaves while its shared memory may still be read
+}
+
+// ------------------------------------------------------------------ tridiagonalisation (a7)
+// A (s x s, lda) symmetric (symmetrised on load, never modified). Outputs d[s], e[s-1], tau[s-2]
+// and the reflectors in Vh (s x s, ldv: column j rows j+1..s-1).
+// Column g lives in CTA g % CS (local column g / CS, ld = s). The rank-2 update of step j-1 is
+// applied lazily, fused with the matrix-vector product of step j (one pass over the own columns
+// per step), except for column j, which the owner's warp 0 updates eagerly before forming the
+// Householder vector of step j. Step j:
+//   owner(j), warp 0:  column j <- step j-1 update; Householder vector v_j, tau_j -> vloc[par]
+//   B1 (cluster barrier)
+//   all:  v_j, tau_j <- owner's vloc[par] (DSMEM)
+//         for own g > j: A[:, g] -= v' a'_g + p' v'_g (step j-1: a' = p'_g - 2 K' v'_g);
+//                        p_g = tau_j A[:, g] . v_j; per-warp partials of p . v_j
+//   B2
+//   all:  ploc[par] <- p (DSMEM gather); warp 0: K_j = tau_j / 2 * sum(partials)
+__host__ __device__ inline size_t tri_smem_doubles(int s, int CS) {
+  return (size_t)cdiv(s, CS) * s + 5 * (size_t)s + 3 * (size_t)cdiv(s, CS) + 2 * 32 + 16 + 160;
+}
+
+// PL = rows per lane (s <= 32 PL): the row vectors of a step (v', p' of the pending update and
+// v_j) are held in registers, so each own column costs PL independent smem loads and stores.
+template <int PL, int TNT>
+__global__ void __launch_bounds__(TNT) tridiag_cluster_kernel(int s, const double* __restrict__ A, int lda,
+                                                                  double* __restrict__ d, double* __restrict__ e,
+                                                                  double* __restrict__ tau, double* __restrict__ Vh,
+                                                                  int ldv, long long* __restrict__ prof) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ double Kbuf[2];
+  __shared__ double wsum[2];
+  long long pt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long tprev = 0;
+#define TRI_T(k)                  \
+  if (prof && threadIdx.x == 0) { \
+    long long tn = clock64();     \
+    pt[k] += tn - tprev;          \
+    tprev = tn;                   \
+  }
+  const int CS = (int)gridDim.x;
+  const unsigned rank = cla_rank();
+  const int ncl = cdiv(s, CS);
+  double* Al = sm;                      // ncl x s, own columns
+  double* vloc = Al + (size_t)ncl * s;  // 2 x s (parity): [tau_j at index j | v_j at j+1..s-1]
+  double* ploc = vloc + 2 * (size_t)s;  // 2 x s (parity): gathered p_j (all rows)
+  double* pbuf = ploc + 2 * (size_t)s;  // own entries of p_j (global column index), read remotely
+  double* wpart = pbuf + s;             // per-warp partials of p.v (32)
+  double* dl = wpart + 64;              // d, e, tau of own columns (local column index); written out at the end
+  double* el = dl + ncl;
+  double* tl = el + ncl;
+  const int tid = threadIdx.x, NT = blockDim.x;
+  const int warp = tid >> 5, lane = tid & 31, nw = NT >> 5;
+  // every row loop below reads whole 32-row groups unconditionally (rows >= s hit later arrays or
+  // the 160-double tail pad; they are multiplied by zero and never stored), so smem starts zeroed
+  for (size_t q = (size_t)ncl * s + tid; q < tri_smem_doubles(s, CS); q += NT) sm[q] = 0.0;
+  for (int q = tid; q < ncl * s; q += NT) {
+    int lc = q / s, i = q - lc * s, g = (int)rank + CS * lc;
+    Al[q] = (g < s) ? 0.5 * (A[IDX(i, g, lda)] + A[IDX(g, i, lda)]) : 0.0;
+  }
+  __syncthreads();
+  if (prof && threadIdx.x == 0) tprev = clock64();
+  for (int j = 0; j + 2 < s; ++j) {
+    const int owner = j % CS, par = j & 1, pp = par ^ 1;
+    const bool pend = j > 0;  // step j-1's update is pending on columns > j
+    if ((int)rank == owner && warp == 0) {
+      // eager update of column j with step j-1 (rows >= j) fused with sigma = sum_{i >= j+2} x_i^2
+      double* col = Al + (size_t)(j / CS) * s;
+      const double* vp = vloc + (size_t)pp * s;
+      const double* pq = ploc + (size_t)pp * s;
+      double ag = 0.0, bg = 0.0;
+      if (pend) {
+        bg = vp[j];
+        ag = pq[j] - 2.0 * Kbuf[pp] * bg;
+      }
+      double x[PL];
+      const double* cp = col + j + lane;
+#pragma unroll
+      for (int q = 0; q < PL; ++q) x[q] = cp[32 * q];
+      if (pend) {
+        const double* vpp = vp + j + lane;
+        const double* pqq = pq + j + lane;
+#pragma unroll
+        for (int q = 0; q < PL; ++q) x[q] = fma(-vpp[32 * q], ag, fma(-pqq[32 * q], bg, x[q]));
+      }
+      double acc = 0.0;
+#pragma unroll
+      for (int q = 0; q < PL; ++q) {
+        const int i = j + lane + 32 * q;
+        const double xs = (i >= j + 2 && i < s) ? x[q] : 0.0;
+        acc = fma(xs, xs, acc);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      const double sigma = acc;
+      const double alpha = __shfl_sync(0xffffffffu, x[0], 1);  // row j + 1 sits in lane 1, slot 0
+      const double dj = __shfl_sync(0xffffffffu, x[0], 0);
+      double tj, beta, scale;
+      if (sigma == 0.0) {
+        tj = 0.0;
+        beta = alpha;
+        scale = 0.0;
+      } else {
+        const double mu = sqrt(fma(alpha, alpha, sigma));
+        beta = (alpha <= 0.0) ? mu : -mu;
+        tj = (beta - alpha) / beta;
+        scale = 1.0 / (alpha - beta);
+      }
+      // no global stores inside the loop: a release barrier would wait for them to reach L2
+      double* vb = vloc + (size_t)par * s;
+      if (lane == 0) {
+        dl[j / CS] = dj;
+        el[j / CS] = beta;
+        tl[j / CS] = tj;
+        vb[j] = tj;
+      }
+#pragma unroll
+      for (int q = 0; q < PL; ++q) {  // v_j -> broadcast buffer and (reflector storage) column j
+        const int i = j + lane + 32 * q;
+        if (i > j && i < s) {
+          const double v = (i == j + 1) ? 1.0 : x[q] * scale;
+          vb[i] = v;
+          col[i] = v;
+        }
+      }
+    }
+    TRI_T(0);
+    cla_cluster_sync();  // B1: v_j, tau_j visible; step j-1 finished everywhere
+    TRI_T(1);
+    double* vj = vloc + (size_t)par * s;
+    if ((int)rank != owner) {
+      const double* ov = cla_remote(vj, (unsigned)owner);
+      int i = j + tid;
+      for (; i + NT < s; i += 2 * NT) {
+        const double a = ov[i], b = ov[i + NT];
+        vj[i] = a;
+        vj[i + NT] = b;
+      }
+      if (i < s) vj[i] = ov[i];
+    }
+    __syncthreads();
+    TRI_T(2);
+    const double tj = vj[j];
+    const double Kp = pend ? Kbuf[pp] : 0.0;
+    // row vectors in registers: rows i = j + 1 + lane + 32 q (rows >= s read finite padding, masked)
+    double rv[PL], rp[PL], rj[PL];
+    {
+      const double* vp = vloc + (size_t)pp * s + j + 1 + lane;
+      const double* pq = ploc + (size_t)pp * s + j + 1 + lane;
+      const double* vv = vj + j + 1 + lane;
+      const double pm = pend ? 1.0 : 0.0;
+#pragma unroll
+      for (int q = 0; q < PL; ++q) {
+        const bool ok = j + 1 + lane + 32 * q < s;
+        rv[q] = ok ? pm * vp[32 * q] : 0.0;
+        rp[q] = ok ? pm * pq[32 * q] : 0.0;
+        rj[q] = ok ? vv[32 * q] : 0.0;
+      }
+    }
+    const int lc0 = (j + 1 > (int)rank) ? (j + 1 - (int)rank + CS - 1) / CS : 0;
+    double part = 0.0;
+    for (int lc = lc0 + warp; lc < ncl; lc += nw) {
+      const int g = (int)rank + CS * lc;
+      if (g >= s) break;
+      double* col = Al + (size_t)lc * s;
+      double bg = 0.0, ag = 0.0;
+      if (pend) {
+        bg = vloc[(size_t)pp * s + g];
+        ag = ploc[(size_t)pp * s + g] - 2.0 * Kp * bg;
+      }
+      double x[PL];
+      double* cp = col + j + 1 + lane;
+#pragma unroll
+      for (int q = 0; q < PL; ++q) x[q] = cp[32 * q];
+      double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+      for (int q = 0; q < PL; ++q) {
+        x[q] = fma(-rv[q], ag, fma(-rp[q], bg, x[q]));
+        if (q & 1)
+          a1 = fma(x[q], rj[q], a1);
+        else
+          a0 = fma(x[q], rj[q], a0);
+      }
+      if (pend) {
+#pragma unroll
+        for (int q = 0; q < PL; ++q)
+          if (j + 1 + lane + 32 * q < s) cp[32 * q] = x[q];
+      }
+      double acc = a0 + a1;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      acc *= tj;
+      if (lane == 0) pbuf[g] = acc;
+      part = fma(acc, vj[g], part);
+    }
+    if (lane == 0) wpart[warp] = part;
+    __syncthreads();
+    if (warp == 0) {
+      double pv = (lane < nw) ? wpart[lane] : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) pv += __shfl_xor_sync(0xffffffffu, pv, o);
+      if (lane == 0) wsum[par] = pv;
+    }
+    TRI_T(3);
+    cla_cluster_sync();  // B2: p_j entries and per-CTA partial sums visible
+    TRI_T(4);
+    double* pj = ploc + (size_t)par * s;
+    {
+      int i = j + 1 + tid;
+      for (; i + NT < s; i += 2 * NT) {
+        const double a = *cla_remote(pbuf + i, (unsigned)(i & (CS - 1)));
+        const double b = *cla_remote(pbuf + i + NT, (unsigned)((i + NT) & (CS - 1)));
+        pj[i] = a;
+        pj[i + NT] = b;
+      }
+      if (i < s) pj[i] = *cla_remote(pbuf + i, (unsigned)(i & (CS - 1)));
+    }
+    if (warp == nw - 1) {
+      double pv = (lane < CS) ? *cla_remote(wsum + par, (unsigned)lane) : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) pv += __shfl_xor_sync(0xffffffffu, pv, o);
+      if (lane == 0) Kbuf[par] = 0.5 * tj * pv;
+    }
+    TRI_T(5);
+    __syncthreads();
+    TRI_T(6);
+  }
+  if (prof && threadIdx.x == 0)
+    for (int k = 0; k < 8; ++k) prof[rank * 8 + k] = pt[k];
+#undef TRI_T
+  // pending update of the last step on columns s-2, s-1 (rows >= s-2), then the trailing 2 x 2
+  if (s >= 3) {
+    const int jl = s - 3, pl = jl & 1;
+    const double* vp = vloc + (size_t)pl * s;
+    const double* pq = ploc + (size_t)pl * s;
+    const double Kp = Kbuf[pl];
+    if (tid < 4) {
+      const int g = s - 2 + (tid >> 1), i = s - 2 + (tid & 1);
+      if ((int)rank == g % CS) {
+        double* col = Al + (size_t)(g / CS) * s;
+        const double bg = vp[g], ag = pq[g] - 2.0 * Kp * bg;
+        col[i] -= vp[i] * ag + pq[i] * bg;
+      }
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    if (s >= 2) {
+      int g = s - 2;
+      if ((int)rank == g % CS) {
+        d[g] = Al[(size_t)(g / CS) * s + g];
+        e[g] = Al[(size_t)(g / CS) * s + g + 1];
+      }
+      g = s - 1;
+      if ((int)rank == g % CS) d[g] = Al[(size_t)(g / CS) * s + g];
+    } else if (rank == 0) {
+      d[0] = Al[0];
+    }
+  }
+  // reflectors (own columns g <= s-3, rows g+1..s-1) and d, e, tau of the own columns
+  for (int q = tid; q < ncl * s; q += NT) {
+    int lc = q / s, i = q - lc * s, g = (int)rank + CS * lc;
+    if (g + 2 < s && i > g) Vh[IDX(i, g, ldv)] = Al[q];
+  }
+  for (int lc = tid; lc < ncl; lc += NT) {
+    int g = (int)rank + CS * lc;
+    if (g + 2 < s) {
+      d[g] = dl[lc];
+      e[g] = el[lc];
+      tau[g] = tl[lc];
+    }
+  }
+  cla_cluster_sync();  // no CTA leaves while its shared memory may still be read
+}
+
+// Back-transformation Y <- Q Y, Q = H_0 H_1 ... H_{s-3} (apply H_{s-3} first): one warp per
+// column (held in registers), reflectors staged through shared memory in panels of BT_PB
+// (coalesced loads shared by the CTA's warps instead of per-warp L2 round trips).
+constexpr int BT_PB = 16;
+constexpr int BT_PER_LANE = 40;  // s <= 1280
+template <int PL>
+__global__ void __launch_bounds__(256) backtransform_panel_kernel(int s, int m, const double* __restrict__ Vh, int ldv,
+                                                                  const double* __restrict__ tau,
+                                                                  double* __restrict__ y, int ldy) {
+  extern __shared__ __align__(16) double pv[];  // BT_PB x s
+  __shared__ double ptau[BT_PB];
+  const int lane = threadIdx.x & 31;
+  const int col = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const bool active = col < m;
+  double* yc = y + (size_t)(active ? col : 0) * ldy;
+  double r[PL];
+#pragma unroll
+  for (int q = 0; q < PL; ++q) {
+    int k = lane + 32 * q;
+    r[q] = (active && k < s) ? yc[k] : 0.0;
+  }
+  const int nref = s - 2;  // reflectors 0 .. s-3
+  for (int hi = nref - 1; hi >= 0; hi -= BT_PB) {
+    const int lo = max(0, hi - BT_PB + 1);
+    __syncthreads();
+    for (int q = threadIdx.x; q < (hi - lo + 1) * s; q += blockDim.x) {
+      int c = q / s, i = q - c * s, j = lo + c;
+      pv[(size_t)c * s + i] = (i > j) ? __ldg(Vh + IDX(i, j, ldv)) : 0.0;
+    }
+    if (threadIdx.x < hi - lo + 1) ptau[threadIdx.x] = __ldg(tau + lo + threadIdx.x);
+    __syncthreads();
+    if (!active) continue;
+    for (int j = hi; j >= lo; --j) {
+      const double tj = ptau[j - lo];
+      if (tj == 0.0) continue;
+      const double* v = pv + (size_t)(j - lo) * s;
+      double acc = 0.0;
+#pragma unroll
+      for (int q = 0; q < PL; ++q) {
+        int k = lane + 32 * q;
+        if (k < s) acc = fma(v[k], r[q], acc);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      acc *= tj;
+#pragma unroll
+      for (int q = 0; q < PL; ++q) {
+        int k = lane + 32 * q;
+        if (k < s) r[q] = fma(-acc, v[k], r[q]);
+      }
+    }
+  }
+  if (!active) return;
+#pragma unroll
+  for (int q = 0; q < PL; ++q) {
+    int k = lane + 32 * q;
+    if (k < s) yc[k] = r[q];
+  }
+}
+
+// ------------------------------------------------------------------ helpers for the RR step
+// Li = L^-1 (t x t lower, ldl -> ldi), one warp per column j, column-oriented forward
+// substitution: x = e_j; for k >= j: x_k /= L_kk; x_{k+1:} -= x_k L_{k+1:,k} (coalesced column reads).
+__global__ void __launch_bounds__(256) trinv_cols_kernel(int t, const double* __restrict__ L, int ldl,
+                                                         double* __restrict__ Li, int ldi) {
+  extern __shared__ __align__(16) double xs[];  // (blockDim/32) x t
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int j = blockIdx.x * (blockDim.x >> 5) + w;
+  if (j >= t) return;
+  double* x = xs + (size_t)w * t;
+  for (int i = lane; i < t; i += 32) x[i] = (i == j) ? 1.0 : 0.0;
+  __syncwarp();
+  for (int k = j; k < t; ++k) {
+    const double xk = x[k] / __ldg(L + IDX(k, k, ldl));
+    __syncwarp();
+    if (lane == 0) x[k] = xk;
+    const double* lc = L + IDX(0, k, ldl);
+    for (int i = k + 1 + lane; i < t; i += 32) x[i] -= xk * __ldg(lc + i);
+    __syncwarp();
+  }
+  for (int i = lane; i < t; i += 32) Li[IDX(i, j, ldi)] = (i >= j) ? x[i] : 0.0;
+}
+
+// Newton-Schulz step towards the polar factor: Z = 1.5 I - 0.5 M for M = Y^T Y (m x m), and
+// dev = max |M - I| accumulated into *dev (as a non-negative double's bit pattern, atomicMax).
+__global__ void ns_coeff_kernel(int m, const double* __restrict__ M, int ldm, double* __restrict__ Z, int ldz,
+                                unsigned long long* __restrict__ dev) {
+  double mx = 0.0;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < (int64_t)m * m;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    int i = (int)(q % m), k = (int)(q / m);
+    double mik = M[IDX(i, k, ldm)], id = (i == k) ? 1.0 : 0.0;
+    Z[IDX(i, k, ldz)] = 1.5 * id - 0.5 * mik;
+    mx = fmax(mx, fabs(mik - id));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0 && mx > 0.0) atomicMax(dev, (unsigned long long)__double_as_longlong(mx));
+}
+
+}  // namespace psd

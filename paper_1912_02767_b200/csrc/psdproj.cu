@@ -28,6 +28,7 @@
 #include "gemm.cuh"
 #include "kernels.cuh"
 #include "tridiag.cuh"
+#include "cluster_la.cuh"
 
 using namespace psd;
 
@@ -211,16 +212,104 @@ static int jacobi_run(cudaStream_t st, int s, const double* A, int lda, double* 
   return 0;
 }
 
+// ------------------------------------------------------------------ cluster launch helpers
+// cluster size for a cluster_la.cuh kernel of order s: the preferred size (PSDPROJ_CLA_CS overrides),
+// doubled until the kernel's shared-memory footprint fits; 0 if it does not fit in 16 CTAs
+static int cla_cluster_size(int s, size_t (*smem_doubles)(int, int)) {
+  static int forced = -1;
+  if (forced < 0) {
+    const char* e = getenv("PSDPROJ_CLA_CS");
+    forced = e ? std::max(1, std::min(16, atoi(e))) : 0;
+  }
+  int cs = forced ? forced : (s > 160 ? 16 : (s > 64 ? 8 : 4));
+  while (cs < 16 && smem_doubles(s, cs) * sizeof(double) > (size_t)CLA_SMEM_BYTES) cs *= 2;
+  return smem_doubles(s, cs) * sizeof(double) <= (size_t)CLA_SMEM_BYTES ? cs : 0;
+}
+
+template <typename... KArgs, typename... Args>
+static int launch_cluster(void (*kern)(KArgs...), int cs, int nt, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cs);
+  cfg.blockDim = dim3(nt);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, kern, args...));
+  ++g_launches;
+  return 0;
+}
+
+static int cla_attrs() {
+  static bool done = false;
+  if (done) return 0;
+  const int mx = CLA_SMEM_BYTES;
+  CK(cudaFuncSetAttribute(tridiag_cluster_kernel<4, 512>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  CK(cudaFuncSetAttribute(tridiag_cluster_kernel<4, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  CK(cudaFuncSetAttribute(tridiag_cluster_kernel<8, 512>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  CK(cudaFuncSetAttribute(tridiag_cluster_kernel<8, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  CK(cudaFuncSetAttribute(tridiag_cluster_kernel<14, 256>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  CK(cudaFuncSetAttribute(tridiag_cluster_kernel<14, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  CK(cudaFuncSetAttribute(tridiag_cluster_kernel<20, 256>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  CK(cudaFuncSetAttribute(tridiag_cluster_kernel<20, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  CK(cudaFuncSetAttribute(cholesky_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  CK(cudaFuncSetAttribute(cholesky_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  CK(cudaFuncSetAttribute(trinv_cols_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  const int bmx = (int)(BT_PB * 32 * BT_PER_LANE * sizeof(double));
+  CK(cudaFuncSetAttribute(backtransform_panel_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, bmx));
+  CK(cudaFuncSetAttribute(backtransform_panel_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, bmx));
+  CK(cudaFuncSetAttribute(backtransform_panel_kernel<24>, cudaFuncAttributeMaxDynamicSharedMemorySize, bmx));
+  CK(cudaFuncSetAttribute(backtransform_panel_kernel<BT_PER_LANE>, cudaFuncAttributeMaxDynamicSharedMemorySize, bmx));
+  done = true;
+  return 0;
+}
+
+// L = chol(G) in place (t x t, ld); status = failing pivot + 1 or 0 (a6, R20)
+static int cholesky_run(cudaStream_t st, int t, double* G, int ld, int* d_status) {
+  TRY(cla_attrs());
+  if (int cs = cla_cluster_size(t, chol_smem_doubles)) {
+    return launch_cluster(cholesky_cluster_kernel, cs, CLA_NT, chol_smem_doubles(t, cs) * sizeof(double), st, t, G, ld,
+                          1e-12, d_status);
+  }
+  cholesky_kernel<1024><<<1, 1024, 0, st>>>(t, G, ld, 1e-12, d_status);
+  CKL();
+  return 0;
+}
+
+// Li = L^-1 (lower triangular t x t)
+static int trinv_run(cudaStream_t st, int t, const double* L, int ldl, double* Li, int ldi) {
+  TRY(cla_attrs());
+  const int wpb = 4;
+  trinv_cols_kernel<<<cdiv(t, wpb), 32 * wpb, (size_t)wpb * t * sizeof(double), st>>>(t, L, ldl, Li, ldi);
+  CKL();
+  return 0;
+}
+
 // ------------------------------------------------------------------ tridiagonal eigensolver (a7)
-// Top-m eigenpairs (descending) of the symmetric s x s matrix H: Householder tridiagonalisation,
-// multisection bisection, inverse iteration + clustered MGS, back-transformation (tridiag.cuh).
+// Top-m eigenpairs (descending) of the symmetric s x s matrix H: Householder tridiagonalisation
+// (cluster_la.cuh for s <= CLA_MAX, one CTA above), multisection bisection, inverse iteration,
+// back-transformation (tridiag.cuh), then two Newton-Schulz steps towards the polar factor
+// Y <- Y (3I - Y^T Y)/2 restore orthonormality lost inside tight eigenvalue clusters (any
+// orthonormal basis of a cluster's invariant subspace diagonalises H to the cluster width).
+// With mgs = true the slow robust path (clustered modified Gram-Schmidt, dstein's rule) is used.
+struct EighScratch {
+  double *td, *te, *ttau, *te2, *tbounds, *tscr, *tG;
+  int ldg;
+  double* Vh;
+  int ldv;
+  double *nsM, *nsZ, *nsY;  // m x m, m x m, s x m (ld = ldv)
+  unsigned long long* dev;   // NS deviation (double bits)
+  size_t tscr_elems;
+};
+
 static int eigh_top(cudaStream_t st, int s, const double* Hs, int ldh, int m, double* lam, double* Yv, int ldy,
-                    int* npos, double* td, double* te, double* ttau, double* te2, double* tbounds, double* tscr,
-                    double* tG, int ldg, double* Vh, int ldv) {
-  // tridiag dynamic smem: [M s(s+1) when s <= TRI_SMEM_MAX] sv[s] sp[s + 8 s]
-  const size_t vecs = (size_t)s * 10;
-  size_t dyn = ((s <= TRI_SMEM_MAX) ? (size_t)s * (s + 1) : 0) + vecs;
-  dyn *= sizeof(double);
+                    int* npos, const EighScratch& w, double* part, size_t part_elems, bool mgs) {
+  TRY(cla_attrs());
   static bool attr = false;
   if (!attr) {
     CK(cudaFuncSetAttribute(tridiag_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -229,30 +318,87 @@ static int eigh_top(cudaStream_t st, int s, const double* Hs, int ldh, int m, do
     CK(cudaFuncSetAttribute(tri_bisect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     attr = true;
   }
-  if (s > TRI_SMEM_MAX && dyn > 200 * 1024) return set_err(PSDPROJ_E_CAPACITY, "tridiag smem %zu for s=%d", dyn, s);
   if (s > 32 * TRI_BT_PER_LANE) return set_err(PSDPROJ_E_CAPACITY, "eigensolver supports s <= %d", 32 * TRI_BT_PER_LANE);
-  tridiag_kernel<1024><<<1, 1024, dyn, st>>>(s, Hs, ldh, td, te, ttau, Vh, ldv, tG, ldg);
+  static int tri_mode = -1;  // 0 auto, 1 force one-CTA
+  if (tri_mode < 0) tri_mode = getenv("PSDPROJ_TRI_ONECTA") ? 1 : 0;
+  int tcs = (tri_mode == 0 && s > 64) ? cla_cluster_size(s, tri_smem_doubles) : 0;
+  if (tcs) {
+    static long long* dprof = nullptr;
+    static int want_prof = getenv("PSDPROJ_TRI_PROF") ? 1 : 0;
+    if (want_prof && !dprof) CK(cudaMalloc(&dprof, 16 * 8 * sizeof(long long)));
+    const size_t tsm = tri_smem_doubles(s, tcs) * sizeof(double);
+    if (s <= 32 * 4)
+      TRY(launch_cluster(tridiag_cluster_kernel<4, 512>, tcs, 512, tsm, st, s, Hs, ldh, w.td, w.te, w.ttau, w.Vh, w.ldv, dprof));
+    else if (s <= 32 * 8)
+      TRY(launch_cluster(tridiag_cluster_kernel<8, 512>, tcs, 512, tsm, st, s, Hs, ldh, w.td, w.te, w.ttau, w.Vh, w.ldv, dprof));
+    else if (s <= 32 * 14)
+      TRY(launch_cluster(tridiag_cluster_kernel<14, 256>, tcs, 256, tsm, st, s, Hs, ldh, w.td, w.te, w.ttau, w.Vh, w.ldv, dprof));
+    else
+      TRY(launch_cluster(tridiag_cluster_kernel<20, 256>, tcs, 256, tsm, st, s, Hs, ldh, w.td, w.te, w.ttau, w.Vh, w.ldv, dprof));
+    if (want_prof) {
+      long long h[128];
+      CK(cudaStreamSynchronize(st));
+      CK(cudaMemcpy(h, dprof, sizeof(h), cudaMemcpyDeviceToHost));
+      for (int r = 0; r < std::min(tcs, 3); ++r)
+        fprintf(stderr, "tri prof s=%d cs=%d rank %d: house %lld B1 %lld vcopy %lld fused %lld B2 %lld gatherK %lld sync %lld (cycles/step)\n",
+                s, tcs, r, h[r * 8 + 0] / (s - 2), h[r * 8 + 1] / (s - 2), h[r * 8 + 2] / (s - 2), h[r * 8 + 3] / (s - 2),
+                h[r * 8 + 4] / (s - 2), h[r * 8 + 5] / (s - 2), h[r * 8 + 6] / (s - 2));
+    }
+  } else {
+    const size_t vecs = (size_t)s * 10;
+    size_t dyn = ((s <= TRI_SMEM_MAX) ? (size_t)s * (s + 1) : 0) + vecs;
+    dyn *= sizeof(double);
+    if (s > TRI_SMEM_MAX && dyn > 200 * 1024) return set_err(PSDPROJ_E_CAPACITY, "tridiag smem %zu for s=%d", dyn, s);
+    tridiag_kernel<1024><<<1, 1024, dyn, st>>>(s, Hs, ldh, w.td, w.te, w.ttau, w.Vh, w.ldv, w.tG, w.ldg);
+    CKL();
+  }
+  tri_prep_kernel<<<1, 1024, 0, st>>>(s, w.td, w.te, w.te2, w.tbounds);
   CKL();
-  tri_prep_kernel<<<1, 1024, 0, st>>>(s, td, te, te2, tbounds);
+  tri_bisect_kernel<<<cdiv(m + 1, 8), 256, (size_t)2 * s * sizeof(double), st>>>(s, m, w.td, w.te2, w.tbounds, lam, npos);
   CKL();
-  tri_bisect_kernel<<<cdiv(m + 1, 8), 256, (size_t)2 * s * sizeof(double), st>>>(s, m, td, te2, tbounds, lam, npos);
-  CKL();
-  if (m > 0) {
-    // inverse iteration: vectors per CTA so that 6 s doubles each fit in shared memory
-    int vpb = (int)std::min<size_t>(64, (220 * 1024) / ((size_t)6 * s * sizeof(double)));
-    int smem_ok = vpb >= 1;
-    if (!smem_ok) vpb = 64;
-    size_t ism = smem_ok ? (size_t)6 * s * vpb * sizeof(double) : 0;
+  if (m <= 0) return 0;
+  // inverse iteration: vectors per CTA so that 6 s doubles each fit in shared memory
+  int vpb = (int)std::min<size_t>(64, (220 * 1024) / ((size_t)6 * s * sizeof(double)));
+  int smem_ok = vpb >= 1;
+  if (!smem_ok) vpb = 64;
+  if (!smem_ok && (size_t)6 * s * (size_t)m > w.tscr_elems) return set_err(PSDPROJ_E_CAPACITY, "eigensolver scratch");
+  size_t ism = smem_ok ? (size_t)6 * s * vpb * sizeof(double) : 0;
+  if (mgs) {
     for (int pass = 0; pass < 2; ++pass) {
-      tri_inviter_kernel<<<cdiv(m, vpb), vpb, ism, st>>>(s, m, td, te, lam, tbounds, Yv, ldy, tscr, pass ? 1 : 2,
-                                                         pass, smem_ok);
+      tri_inviter_kernel<<<cdiv(m, vpb), vpb, ism, st>>>(s, m, w.td, w.te, lam, w.tbounds, Yv, ldy, w.tscr,
+                                                         pass ? 1 : 2, pass, smem_ok);
       CKL();
-      tri_cluster_mgs_kernel<1024><<<1, 1024, 0, st>>>(s, m, lam, tbounds, Yv, ldy);
+      tri_cluster_mgs_kernel<1024><<<1, 1024, 0, st>>>(s, m, lam, w.tbounds, Yv, ldy);
       CKL();
     }
-    if (s > 2) {
-      tri_backtransform_kernel<<<cdiv(m, 8), 256, 0, st>>>(s, m, Vh, ldv, ttau, Yv, ldy);
+  } else {
+    tri_inviter_kernel<<<cdiv(m, vpb), vpb, ism, st>>>(s, m, w.td, w.te, lam, w.tbounds, Yv, ldy, w.tscr, 3, 0,
+                                                       smem_ok);
+    CKL();
+  }
+  if (s > 2) {
+    const size_t bsm = (size_t)BT_PB * s * sizeof(double);
+    if (s <= 32 * 8)
+      backtransform_panel_kernel<8><<<cdiv(m, 8), 256, bsm, st>>>(s, m, w.Vh, w.ldv, w.ttau, Yv, ldy);
+    else if (s <= 32 * 16)
+      backtransform_panel_kernel<16><<<cdiv(m, 8), 256, bsm, st>>>(s, m, w.Vh, w.ldv, w.ttau, Yv, ldy);
+    else if (s <= 32 * 24)
+      backtransform_panel_kernel<24><<<cdiv(m, 8), 256, bsm, st>>>(s, m, w.Vh, w.ldv, w.ttau, Yv, ldy);
+    else
+      backtransform_panel_kernel<BT_PER_LANE><<<cdiv(m, 8), 256, bsm, st>>>(s, m, w.Vh, w.ldv, w.ttau, Yv, ldy);
+    CKL();
+  }
+  if (!mgs) {
+    // two Newton-Schulz steps; dev records max|Y^T Y - I| before the second step
+    for (int it = 0; it < 2; ++it) {
+      TRY(dgemm(st, OP_T, OP_N, m, m, s, 1.0, Yv, ldy, Yv, ldy, 0.0, w.nsM, m, part, part_elems));
+      if (it == 1) CK(cudaMemsetAsync(w.dev, 0, sizeof(unsigned long long), st));
+      ns_coeff_kernel<<<grid1d((size_t)m * m), 256, 0, st>>>(m, w.nsM, m, w.nsZ, m,
+                                                              it == 1 ? w.dev : w.dev + 1);
       CKL();
+      TRY(dgemm(st, OP_N, OP_N, s, m, m, 1.0, Yv, ldy, w.nsZ, m, 0.0, w.nsY, w.ldv, part, part_elems));
+      CK(cudaMemcpy2DAsync(Yv, (size_t)ldy * 8, w.nsY, (size_t)w.ldv * 8, (size_t)s * 8, m, cudaMemcpyDeviceToDevice,
+                           st));
     }
   }
   return 0;
@@ -292,6 +438,7 @@ struct psdproj_ctx_s {
   int calls = 0;
   bool poisoned = false;
   std::vector<cudaEvent_t> ev;
+  std::vector<cudaEvent_t> pev;  // phase-timing events (profile & 2)
 };
 
 struct Carver {
@@ -412,6 +559,7 @@ extern "C" int psdproj_destroy(psdproj_ctx c) {
   if (c->h_d) cudaFreeHost(c->h_d);
   if (c->h_i) cudaFreeHost(c->h_i);
   for (auto e : c->ev) cudaEventDestroy(e);
+  for (auto e : c->pev) cudaEventDestroy(e);
   delete c;
   return PSDPROJ_OK;
 }
@@ -438,6 +586,21 @@ struct Run {
   int rr_npos = 0;  // positive Ritz values among all s of the last Rayleigh-Ritz (expansion test)
   int nev = 0;
   double anorm = 0.0;
+  std::vector<int> marks;  // phase id of each recorded phase event (profile & 2)
+
+  // phase boundary: the GPU time from this mark to the next is charged to phase ph
+  int mark(int ph) {
+    if (!(c->prm.profile & 2)) return 0;
+    size_t k = marks.size();
+    while (c->pev.size() <= k) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      c->pev.push_back(e);
+    }
+    CK(cudaEventRecord(c->pev[k], st));
+    marks.push_back(ph);
+    return 0;
+  }
 
   int upload_idx(const std::vector<int>& v, int* dev) {
     if (v.empty()) return 0;
@@ -511,10 +674,18 @@ struct Run {
     CKL();
     return 0;
   }
-  int tri_eig(int s, const double* Hs, int ldh, int m, double* lam, double* Yv, int ldy, int* npos) {
-    if ((size_t)6 * s * (size_t)m > c->tscr_elems) return set_err(PSDPROJ_E_CAPACITY, "eigensolver scratch");
-    return eigh_top(st, s, Hs, ldh, m, lam, Yv, ldy, npos, c->td, c->te, c->ttau, c->te2, c->tbounds, c->tscr, c->tG,
-                    c->s_max, c->Vj, c->s_max);
+  EighScratch eig_scratch() {
+    EighScratch w;
+    w.td = c->td; w.te = c->te; w.ttau = c->ttau; w.te2 = c->te2; w.tbounds = c->tbounds; w.tscr = c->tscr;
+    w.tG = c->tG; w.ldg = c->s_max; w.Vh = c->Vj; w.ldv = c->s_max;
+    // free while the eigensolver runs: G/Hm were consumed by the Cholesky copy and L^-1 H, Gc (L) by trinv
+    w.nsM = c->G; w.nsZ = c->Hm; w.nsY = c->Gc;
+    w.dev = reinterpret_cast<unsigned long long*>(c->d_scal + 16);
+    w.tscr_elems = c->tscr_elems;
+    return w;
+  }
+  int tri_eig(int s, const double* Hs, int ldh, int m, double* lam, double* Yv, int ldy, int* npos, bool mgs) {
+    return eigh_top(st, s, Hs, ldh, m, lam, Yv, ldy, npos, eig_scratch(), c->part, c->part_elems, mgs);
   }
   // Rayleigh-Ritz on the pencil (H, G) in c->G / c->Hm (s x s, ld s_max):
   // returns 0 (ok), >0 (Cholesky failed at that pivot), <0 error. Outputs Cp (s x mU), theta desc in h_d[0..s).
@@ -522,6 +693,7 @@ struct Run {
     int ldm = c->s_max;
     info->rr_max = std::max(info->rr_max, s);
     info->flops += 9.0 * s * (double)s * s + s * (double)s * s / 3.0 + 2.0 * s * (double)s * s;
+    TRY(mark(3));
     insert_known_kernel<<<grid1d((size_t)s * s), 256, 0, st>>>(s, kxG, kxH, c->G, c->Hm, ldm, d_theta_known);
     CKL();
     // G = [I 0; 0 D]: factor only the direction block D = L22 L22^T (size t = s - kxG)
@@ -534,22 +706,21 @@ struct Run {
     CK(cudaMemsetAsync(c->d_status, 0, sizeof(int), st));
     if (t > 0) {
       TRY(copy_cols(t, t, c->Gc, ldm, c->G + kx + (size_t)kx * ldm, ldm));
-      cholesky_kernel<1024><<<1, 1024, 0, st>>>(t, c->Gc, ldm, 1e-12, c->d_status);
-      CKL();
-      trinv_kernel<<<cdiv(t, 8), 256, 0, st>>>(t, c->Gc, ldm, c->Li + kx + (size_t)kx * ldm, ldm);
-      CKL();
+      TRY(cholesky_run(st, t, c->Gc, ldm, c->d_status));
+      TRY(trinv_run(st, t, c->Gc, ldm, c->Li + kx + (size_t)kx * ldm, ldm));
     }
     // Hh = L^-1 H L^-T
     TRY(dgemm(st, OP_N, OP_N, s, s, s, 1.0, c->Li, ldm, c->Hm, ldm, 0.0, c->Y, ldm, c->part, c->part_elems));
     TRY(dgemm(st, OP_N, OP_T, s, s, s, 1.0, c->Y, ldm, c->Li, ldm, 0.0, c->Hh, ldm, c->part, c->part_elems));
     // eigensolver choice by measured crossover: tridiagonal path while the matrix fits in shared memory (s <= 160),
     // cooperative Jacobi above (single-SM tridiagonalisation in global memory is L2-bandwidth bound)
+    TRY(mark(4));
     static int rr_mode = -1;  // 0 auto, 1 jacobi, 2 tridiag
     if (rr_mode < 0) {
       const char* e = getenv("PSDPROJ_RR");
       rr_mode = !e ? 0 : (std::string(e) == "jacobi" ? 1 : (std::string(e) == "tridiag" ? 2 : 0));
     }
-    bool use_jacobi = rr_mode == 1 || (rr_mode == 0 && s > TRI_SMEM_MAX);
+    bool use_jacobi = rr_mode == 1;
     if (use_jacobi) {
       TRY(jacobi_run(st, s, c->Hh, ldm, c->d_w, c->Vj, ldm, c->jM, c->jM2, c->jQ, c->d_status + 4, c->d_counters,
                      c->d_scal));
@@ -561,12 +732,14 @@ struct Run {
       gather_cols_kernel<<<grid1d((size_t)s * mU), 256, 0, st>>>(s, mU, c->Y, ldm, c->Vj, ldm, c->d_order);
       CKL();
     } else {
-      TRY(tri_eig(s, c->Hh, ldm, mU, c->d_ths, c->Y, ldm, c->tnpos));
+      TRY(tri_eig(s, c->Hh, ldm, mU, c->d_ths, c->Y, ldm, c->tnpos, false));
       CK(cudaMemsetAsync(c->d_status + 4, 0, sizeof(int), st));
       set_int_kernel<<<1, 1, 0, st>>>(c->d_status + 4, 1);
       CKL();
+      CK(cudaMemcpyAsync(c->h_d + c->h_d_len - 16, c->d_scal + 16, sizeof(double), cudaMemcpyDeviceToHost, st));
     }
     TRY(dgemm(st, OP_T, OP_N, s, mU, s, 1.0, c->Li, ldm, c->Y, ldm, 0.0, c->Cp, ldm, c->part, c->part_elems));
+    TRY(mark(7));
     CK(cudaMemcpyAsync(c->h_d, c->d_ths, sizeof(double) * mU, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(c->h_i + c->h_i_len - 16, c->d_status, sizeof(int) * 8, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(c->h_i + c->h_i_len - 24, c->tnpos, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -575,6 +748,13 @@ struct Run {
     int sweeps = c->h_i[c->h_i_len - 16 + 4];
     rr_npos = c->h_i[c->h_i_len - 24];
     if (chol) return chol + kx;
+    if (!use_jacobi && !(c->h_d[c->h_d_len - 16] <= 1e-7)) {
+      // Newton-Schulz could not restore orthonormality (near-multiple eigenvalues): robust path
+      TRY(tri_eig(s, c->Hh, ldm, mU, c->d_ths, c->Y, ldm, c->tnpos, true));
+      TRY(dgemm(st, OP_T, OP_N, s, mU, s, 1.0, c->Li, ldm, c->Y, ldm, 0.0, c->Cp, ldm, c->part, c->part_elems));
+      CK(cudaMemcpyAsync(c->h_d, c->d_ths, sizeof(double) * mU, cudaMemcpyDeviceToHost, st));
+      TRY(sync());
+    }
     if (sweeps < 0) return set_err(PSDPROJ_E_DEGENERATE, "Jacobi did not converge (s=%d)", s);
     return 0;
   }
@@ -610,14 +790,27 @@ static int direct_path(Run& run, const double* A, int lda, double* Pi, int ldpi)
   run.info->flops += 9.0 * n * (double)n * n;
   // eigendecomposition of A; V into jQ-free region: use T as V (ld x n)
   double* V = c->T;
-  TRY(jacobi_run(st, n, A, lda, c->d_w, V, ld, c->jM, c->jM2, c->jQ, c->d_status + 4, c->d_counters, c->d_scal));
-  sort_desc_kernel<<<cdiv(n, 256), 256, 0, st>>>(n, c->d_w, c->d_order, c->d_ths);
-  CKL();
-  CK(cudaMemcpyAsync(c->h_d, c->d_ths, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(c->h_i + c->h_i_len - 16, c->d_status, sizeof(int) * 8, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(c->h_i, c->d_order, sizeof(int) * n, cudaMemcpyDeviceToHost, st));
-  TRY(run.sync());
-  if (c->h_i[c->h_i_len - 16 + 4] < 0) return set_err(PSDPROJ_E_DEGENERATE, "Jacobi (DIRECT) did not converge");
+  static int dmode = -1;  // 1: Jacobi for DIRECT (PSDPROJ_RR=jacobi)
+  if (dmode < 0) dmode = (getenv("PSDPROJ_RR") && std::string(getenv("PSDPROJ_RR")) == "jacobi") ? 1 : 0;
+  if (dmode == 0 && n <= 32 * TRI_BT_PER_LANE) {
+    // tridiagonal eigensolver, all n pairs, descending; order = identity
+    TRY(run.tri_eig(n, A, lda, n, c->d_ths, V, ld, c->tnpos, false));
+    CK(cudaMemcpyAsync(c->h_d + c->h_d_len - 16, c->d_scal + 16, sizeof(double), cudaMemcpyDeviceToHost, st));
+    TRY(run.sync());
+    if (!(c->h_d[c->h_d_len - 16] <= 1e-7)) TRY(run.tri_eig(n, A, lda, n, c->d_ths, V, ld, c->tnpos, true));
+    CK(cudaMemcpyAsync(c->h_d, c->d_ths, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    TRY(run.sync());
+    for (int i = 0; i < n; ++i) c->h_i[i] = i;
+  } else {
+    TRY(jacobi_run(st, n, A, lda, c->d_w, V, ld, c->jM, c->jM2, c->jQ, c->d_status + 4, c->d_counters, c->d_scal));
+    sort_desc_kernel<<<cdiv(n, 256), 256, 0, st>>>(n, c->d_w, c->d_order, c->d_ths);
+    CKL();
+    CK(cudaMemcpyAsync(c->h_d, c->d_ths, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(c->h_i + c->h_i_len - 16, c->d_status, sizeof(int) * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(c->h_i, c->d_order, sizeof(int) * n, cudaMemcpyDeviceToHost, st));
+    TRY(run.sync());
+    if (c->h_i[c->h_i_len - 16 + 4] < 0) return set_err(PSDPROJ_E_DEGENERATE, "Jacobi (DIRECT) did not converge");
+  }
   std::vector<double> w(c->h_d, c->h_d + n);
   std::vector<int> order(c->h_i, c->h_i + n);
   int p = 0;
@@ -720,6 +913,7 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
   int k = 0;
   for (;;) {
     // ---- line 5: R = B X - X Theta, r_i = ||R_i|| (unlocked columns)
+    TRY(run.mark(6));
     resid_norm_kernel<256><<<mU, 256, 0, st>>>(n, c->S, ld, c->BS, ld, c->d_thU, c->R, ld, c->d_r);
     CKL();
     CK(cudaMemcpyAsync(c->h_d, c->d_r, sizeof(double) * mU, cudaMemcpyDeviceToHost, st));
@@ -749,6 +943,7 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
     }
     if (k >= c->prm.max_iter) break;
     // ---- hard locking (R35)
+    TRY(run.mark(7));
     std::vector<int> keep, lock;
     for (int j = 0; j < mU; ++j) {
       if (hard && thU[j] > 0 && rU[j] <= tol)
@@ -805,6 +1000,7 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
     int s = offP + ap;
     if (s > c->s_max) return set_err(PSDPROJ_E_CAPACITY, "RR basis %d > s_max %d", s, c->s_max);
     // W = R_J (+ pending expansion E)
+    TRY(run.mark(1));
     TRY(run.gather(n, a, c->S + (size_t)offW * ld, ld, c->R, ld, Jorig));
     TRY(run.copy_cols(n, qe, c->S + (size_t)offE * ld, ld, c->E, ld));
     int aw = a + qe;
@@ -818,7 +1014,9 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
       TRY(run.gemm(OP_N, OP_N, n, aw, mU, -1.0, c->S, ld, c->Y, ldm, 1.0, W, ld));
     }
     TRY(run.normalize(n, aw, W, ld, nullptr, 0));
+    TRY(run.mark(0));
     TRY(run.amul(sgn, A, lda, W, ld, aw, c->BS + (size_t)offW * ld, ld));
+    TRY(run.mark(1));
     // P_J, B P_J
     if (ap > 0) {
       double* P = c->S + (size_t)offP * ld;
@@ -837,6 +1035,7 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
     }
     // ---- line 6: Rayleigh-Ritz on span(X, R, P) via the pencil (S^T BS, S^T S)
     // only the direction block of G is needed (X^T X = I, X^T [W P] = 0 by construction)
+    TRY(run.mark(2));
     TRY(run.gemm(OP_T, OP_N, s - mU, s - mU, n, 1.0, c->S + (size_t)mU * ld, ld, c->S + (size_t)mU * ld, ld, 0.0,
                  c->G + mU + (size_t)mU * ldm, ldm));
     TRY(run.gemm(OP_T, OP_N, s, s, n, 1.0, c->S, ld, c->BS, ld, 0.0, c->Hm, ldm));
@@ -852,6 +1051,7 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
     std::vector<double> ths(c->h_d, c->h_d + mUn);
     const int rr_npos = run.rr_npos;
     // ---- rotation (a8): X <- S C', BX <- BS C', P <- S_[R P] C'_[R P], BP likewise
+    TRY(run.mark(5));
     TRY(run.gemm(OP_N, OP_N, n, mUn, sU, 1.0, c->S, ld, c->Cp, ldm, 0.0, c->S2, ld));
     TRY(run.gemm(OP_N, OP_N, n, mUn, sU, 1.0, c->BS, ld, c->Cp, ldm, 0.0, c->BS2, ld));
     TRY(run.gemm(OP_N, OP_N, n, mUn, sU - mU, 1.0, c->S + (size_t)mU * ld, ld, c->Cp + mU, ldm, 0.0, c->Pb, ld));
@@ -866,6 +1066,7 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
     qe = 0;
     ++k;
     // ---- line 8: expansion when fewer than g guards would remain (R8)
+    TRY(run.mark(7));
     int p_rr = (hard ? nL : 0) + rr_npos;  // positive RR values among all sU (R8)
     int mt = nL + mU;
     if (p_rr >= mt - g + 1 && mt < n) {
@@ -889,6 +1090,7 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
       info->expansions++;
     }
   }
+  TRY(run.mark(7));
   info->iters = k;
   info->status = status;
   info->locked = nL;
@@ -1016,6 +1218,15 @@ static int project_impl(psdproj_ctx c, const double* A, int lda, double* Pi, int
   info->last_neg = c->last_neg;
   info->launches = (int)(g_launches - launches0);
   CK(cudaStreamSynchronize(st));
+  if ((c->prm.profile & 2) && !run.marks.empty()) {
+    TRY(run.mark(7));
+    CK(cudaEventSynchronize(c->pev[run.marks.size() - 1]));
+    for (size_t i = 0; i + 1 < run.marks.size(); ++i) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, c->pev[i], c->pev[i + 1]));
+      info->phase_ms[run.marks[i]] += ms;
+    }
+  }
   if ((c->prm.profile & 1) && run.nev > 0) {
     double tot = 0.0;
     for (int i = 0; i < run.nev; ++i) {
@@ -1147,7 +1358,8 @@ extern "C" int psdproj_philox_gauss(int n, int q, double* out, int ld, uint64_t 
 }
 
 extern "C" size_t psdproj_eigh_ws_elems(int s, int m) {
-  return (size_t)5 * s + 64 + (size_t)6 * s * (size_t)std::max(m, 1) + 2 * (size_t)s * s + 64;
+  size_t mm = (size_t)std::max(m, 1);
+  return (size_t)5 * s + 64 + (size_t)6 * s * mm + 2 * (size_t)s * s + 2 * mm * mm + (size_t)s * mm + 64;
 }
 
 extern "C" int psdproj_eigh(int s, const double* A, int lda, int m, double* w, double* V, int ldv, int* npos,
@@ -1155,15 +1367,30 @@ extern "C" int psdproj_eigh(int s, const double* A, int lda, int m, double* w, d
   if (s <= 0 || m < 0 || m > s || lda < s || ldv < s || !A || !w || !V || !npos || !ws)
     return set_err(PSDPROJ_E_INVALID, "invalid eigh args");
   cudaStream_t st = (cudaStream_t)stream;
-  double* td = ws;
-  double* te = td + s;
-  double* ttau = te + s;
-  double* te2 = ttau + s;
-  double* tb = te2 + s + 8;
-  double* tscr = tb + 56;
-  double* tG = tscr + (size_t)6 * s * (size_t)std::max(m, 1);
-  double* Vh = tG + (size_t)s * s;
-  TRY(eigh_top(st, s, A, lda, m, w, V, ldv, npos, td, te, ttau, te2, tb, tscr, tG, s, Vh, s));
+  size_t mm = (size_t)std::max(m, 1);
+  EighScratch e;
+  e.td = ws;
+  e.te = e.td + s;
+  e.ttau = e.te + s;
+  e.te2 = e.ttau + s;
+  e.tbounds = e.te2 + s + 8;
+  e.dev = reinterpret_cast<unsigned long long*>(e.tbounds + 16);
+  e.tscr = e.tbounds + 56;
+  e.tscr_elems = (size_t)6 * s * mm;
+  e.tG = e.tscr + e.tscr_elems;
+  e.ldg = s;
+  e.Vh = e.tG + (size_t)s * s;
+  e.ldv = s;
+  e.nsM = e.Vh + (size_t)s * s;
+  e.nsZ = e.nsM + mm * mm;
+  e.nsY = e.nsZ + mm * mm;
+  TRY(eigh_top(st, s, A, lda, m, w, V, ldv, npos, e, nullptr, 0, false));
+  double dev = 0.0;
+  CK(cudaMemcpyAsync(&dev, e.dev, sizeof(double), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  if (!(dev <= 1e-7)) {
+    TRY(eigh_top(st, s, A, lda, m, w, V, ldv, npos, e, nullptr, 0, true));
+    CK(cudaStreamSynchronize(st));
+  }
   return 0;
 }

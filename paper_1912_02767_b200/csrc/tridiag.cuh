@@ -159,6 +159,17 @@ __global__ void __launch_bounds__(NT) tridiag_kernel(int s, const double* __rest
   }
 }
 
+// 1/x from the hardware approximation (rcp.approx.ftz.f64) plus two Newton steps: within an ulp
+// or two of the IEEE quotient, several times cheaper than the division (latency-bound recurrences).
+__device__ __forceinline__ double fast_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
 // Sturm count: number of eigenvalues of T (d, e2 = e^2) strictly below x (GvL §8.4.1).
 __device__ __forceinline__ int sturm_count(int s, const double* __restrict__ d, const double* __restrict__ e2,
                                            double x, double pivmin) {
@@ -167,7 +178,7 @@ __device__ __forceinline__ int sturm_count(int s, const double* __restrict__ d, 
   if (fabs(q) < pivmin) q = -pivmin;
   cnt += q < 0.0;
   for (int i = 1; i < s; ++i) {
-    q = (d[i] - x) - e2[i - 1] / q;
+    q = (d[i] - x) - e2[i - 1] * fast_rcp(q);
     if (fabs(q) < pivmin) q = -pivmin;
     cnt += q < 0.0;
   }
@@ -294,14 +305,14 @@ __global__ void tri_inviter_kernel(int s, int m, const double* __restrict__ d, c
     double dk = DD(k), lk = DL(k);
     if (fabs(dk) >= fabs(lk)) {
       if (dk == 0.0) dk = eps_piv;
-      double fact = lk / dk;
+      double fact = lk * fast_rcp(dk);
       DD(k) = dk;
       DL(k) = fact;
       DD(k + 1) -= fact * DU(k);
       DU2(k) = 0.0;
       PV(k) = 0.0;
     } else {
-      double fact = dk / lk;
+      double fact = dk * fast_rcp(lk);
       DD(k) = lk;
       DL(k) = fact;
       double tmp = DU(k);
@@ -318,8 +329,11 @@ __global__ void tri_inviter_kernel(int s, int m, const double* __restrict__ d, c
       PV(k) = 1.0;
     }
   }
-  for (int k = 0; k < s; ++k)
-    if (fabs(DD(k)) < eps_piv) DD(k) = (DD(k) < 0.0) ? -eps_piv : eps_piv;
+  for (int k = 0; k < s; ++k) {  // DD <- 1 / pivot (the solves multiply)
+    double p = DD(k);
+    if (fabs(p) < eps_piv) p = (p < 0.0) ? -eps_piv : eps_piv;
+    DD(k) = fast_rcp(p);
+  }
   if (!use_start) {
     uint32_t h = 0x9E3779B9u * (uint32_t)(i + 1) + 0x7F4A7C15u;
     for (int k = 0; k < s; ++k) {
@@ -345,7 +359,7 @@ __global__ void tri_inviter_kernel(int s, int m, const double* __restrict__ d, c
       double v = YY(k);
       if (k + 1 < s) v -= DU(k) * YY(k + 1);
       if (k + 2 < s) v -= DU2(k) * YY(k + 2);
-      v /= DD(k);
+      v *= DD(k);
       YY(k) = v;
       nrm = fmax(nrm, fabs(v));
     }

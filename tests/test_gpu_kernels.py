@@ -74,7 +74,7 @@ def test_philox_gauss_matches_oracle(api):
 
 
 @pytest.mark.parametrize("s,m", [(1, 1), (2, 2), (3, 1), (17, 17), (64, 20), (160, 60), (161, 161), (300, 100),
-                                 (500, 170)])
+                                 (500, 170), (640, 220), (641, 120)])
 def test_eigh_tridiagonal(api, s, m):
     rng = np.random.default_rng(1000 + s)
     M = rng.standard_normal((s, s))
@@ -107,3 +107,23 @@ def test_eigh_clustered_spectrum(api):
     assert np.abs(w - ref).max() <= 1e-12 * 100 * 5
     assert np.linalg.norm(V.T @ V - np.eye(m)) <= 1e-10
     assert np.linalg.norm(A @ V - V * w, axis=0).max() <= 1e-10 * 100
+
+
+@pytest.mark.parametrize("s", [12, 200])
+def test_eigh_repeated_eigenvalues(api, s):
+    """Exactly repeated eigenvalues: inverse iteration vectors of one eigenspace are not
+    orthogonal; the Newton-Schulz / clustered-MGS fallback must still return an orthonormal,
+    diagonalising basis."""
+    from workloads.generators import haar_q, planted
+    rng = np.random.default_rng(77 + s)
+    k = s // 4
+    lam = np.concatenate([np.full(k, 2.0), np.full(k, -1.0), np.full(k, 0.5), rng.uniform(-3, 3, s - 3 * k)])
+    A = planted(haar_q(rng, s), lam)
+    m = s // 2
+    w, V, npos = api.eigh(_cm(A), m)
+    w = w.cpu().numpy()
+    V = V.cpu().numpy()
+    ref = np.sort(lam)[::-1][:m]
+    assert np.abs(w - ref).max() <= 1e-12 * 3 * max(1, s / 20)
+    assert np.linalg.norm(V.T @ V - np.eye(m)) <= 1e-11 * max(1, s / 20)
+    assert np.linalg.norm(A @ V - V * w, axis=0).max() <= 1e-11 * 3 * max(1, s / 20)
