@@ -158,6 +158,11 @@ size_t psdproj_eigh_ws_elems(int s, int m);
 int psdproj_eigh(int s, const double* A, int lda, int m, double* w, double* V, int ldv, int* npos,
                  double* ws, void* stream);
 
+/* In-place Cholesky G = L L^T of the path's implicit Cholesky-QR (a6): G (t x t,
+ * ld, device) -> lower triangle L, upper triangle zeroed. Returns 0, or j + 1 when pivot j is
+ * <= 1e-12 * max diag(G) (R20; G is then left partially factored), or a negative error code. */
+int psdproj_cholesky(int t, double* G, int ld, void* stream);
+
 /* Raw Philox4x32-10 stream: out[4i+j] for counters (i, c1, c2, c3), key (k0, k1), device out. */
 int psdproj_philox_raw(int count, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0, uint32_t k1,
                        uint32_t* out, void* stream);

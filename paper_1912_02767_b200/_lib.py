@@ -20,7 +20,7 @@ EXPORTS = [
     "psdproj_project_host", "psdproj_project_batched", "psdproj_get_ritz", "psdproj_reset",
     "psdproj_destroy", "psdproj_last_error", "psdproj_dgemm", "psdproj_jacobi_ws_elems",
     "psdproj_jacobi", "psdproj_philox_raw", "psdproj_philox_gauss", "psdproj_eigh_ws_elems",
-    "psdproj_eigh",
+    "psdproj_eigh", "psdproj_cholesky",
 ]
 
 
@@ -86,6 +86,7 @@ def load(path=SO_PATH):
     L.psdproj_eigh_ws_elems.argtypes = [i, i]
     L.psdproj_eigh_ws_elems.restype = sz
     L.psdproj_eigh.argtypes = [i, vp, i, i, vp, vp, i, vp, vp, vp]
+    L.psdproj_cholesky.argtypes = [i, vp, i, vp]
     L.psdproj_philox_raw.argtypes = [i, u32, u32, u32, u32, u32, vp, vp]
     L.psdproj_philox_gauss.argtypes = [i, i, vp, i, u64, u32, u32, u32, vp]
     special = ("psdproj_default_params", "psdproj_workspace_bytes", "psdproj_last_error",

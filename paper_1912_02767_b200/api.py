@@ -197,6 +197,16 @@ def eigh(A, m=None, stream=None):
     return w[:m], V[:, :m], int(npos.item())
 
 
+def cholesky(G, stream=None):
+    """In-place Cholesky of the path (a6) on a column-major copy of G: (L, status)."""
+    L_ = _lib.load()
+    t = G.shape[0]
+    M = colmajor(t, t, device=G.device)
+    M.copy_(G)
+    rc = check(L_.psdproj_cholesky(t, _ptr(M), t, _stream_ptr(stream)), "psdproj_cholesky")
+    return M, rc
+
+
 def philox_raw(count, c1, c2, c3, k0, k1, device="cuda", stream=None):
     L = _lib.load()
     out = torch.empty(4 * count, dtype=torch.int32, device=device)

@@ -75,17 +75,20 @@ __host__ __device__ inline size_t chol_smem_doubles(int t, int CS) {
   return (size_t)chol_local_cols(t, CS) * t + (size_t)CHOL_NB * t + 16;
 }
 
+// Blocked Cholesky: panel b = [D; B] (rows j0.., CHOL_NB columns) is factored by its owner as
+// L_bb = chol(D) (every thread computes the 8 x 8 factor redundantly in registers) and
+// L_B = B L_bb^-T (row-parallel), so a panel costs one CTA barrier; one cluster barrier publishes
+// it; every CTA copies it (DSMEM) and applies the rank-CHOL_NB update to its own later columns.
 __global__ void __launch_bounds__(CLA_NT) cholesky_cluster_kernel(int t, double* __restrict__ G, int ld,
                                                                    double fail_rel, int* __restrict__ status) {
   extern __shared__ __align__(16) double sm[];
   __shared__ double red[33];
-  __shared__ int sh_bad;
   const int CS = (int)gridDim.x;
   const unsigned rank = cla_rank();
   const int ncl = chol_local_cols(t, CS);
   double* Al = sm;                      // ncl x t: local column lc = lb * NB + c <-> global (lb * CS + rank) * NB + c
   double* pl = Al + (size_t)ncl * t;    // NB x t: local copy of the current panel
-  double* xch = pl + (size_t)CHOL_NB * t;  // [0] max diag part, [1..2] fail flag by parity
+  double* xch = pl + (size_t)CHOL_NB * t;  // [0] max diag part, [1..2] status of panel by parity
   const int tid = threadIdx.x, NT = blockDim.x;
   const int warp = tid >> 5, lane = tid & 31, nw = NT >> 5;
   auto gcol = [&](int lc) { return ((lc / CHOL_NB) * CS + (int)rank) * CHOL_NB + (lc % CHOL_NB); };
@@ -122,33 +125,76 @@ __global__ void __launch_bounds__(CLA_NT) cholesky_cluster_kernel(int t, double*
   int fail = 0;
   for (int b = 0; b < nblk; ++b) {
     const int owner = b % CS, par = b & 1, j0 = b * CHOL_NB, jb = min(CHOL_NB, t - j0);
+    const int jn = j0 + jb;  // first column after the panel
     if ((int)rank == owner) {
-      double* P = Al + (size_t)(b / CS) * CHOL_NB * t;  // panel columns c = 0..jb-1, rows j0..t-1
-      if (tid == 0) sh_bad = 0;
-      for (int k = 0; k < jb; ++k) {
-        const int j = j0 + k;
-        __syncthreads();
-        const double dj = P[(size_t)k * t + j];
-        if (!(dj > floor_)) {
-          if (tid == 0) sh_bad = j + 1;
-          break;  // uniform: every thread read the same dj
-        }
-        const double ljj = sqrt(dj), inv = 1.0 / ljj;
-        double* pc = P + (size_t)k * t;
-        __syncthreads();
-        for (int i = j + tid; i < t; i += NT) pc[i] = (i == j) ? ljj : pc[i] * inv;
-        __syncthreads();
-        // rank-1 update of the remaining panel columns c > k, rows i >= j0 + c
-        for (int c = k + 1 + warp; c < jb; c += nw) {
-          double* qc = P + (size_t)c * t;
-          const double lg = pc[j0 + c];
-          for (int i = j0 + c + lane; i < t; i += 32) qc[i] -= pc[i] * lg;
+      double* P = Al + (size_t)(b / CS) * CHOL_NB * t;
+      // redundant 8 x 8 Cholesky of the diagonal block in registers
+      double Lb[CHOL_NB][CHOL_NB];
+#pragma unroll
+      for (int c = 0; c < CHOL_NB; ++c)
+#pragma unroll
+        for (int r = 0; r < CHOL_NB; ++r) Lb[r][c] = (r >= c && c < jb && r < jb) ? P[(size_t)c * t + j0 + r] : 0.0;
+      int f = 0;
+      double dinv[CHOL_NB];
+#pragma unroll
+      for (int c = 0; c < CHOL_NB; ++c) {
+        dinv[c] = 0.0;
+        if (c < jb && !f) {
+          double dcc = Lb[c][c];
+#pragma unroll
+          for (int k = 0; k < c; ++k) dcc = fma(-Lb[c][k], Lb[c][k], dcc);
+          if (!(dcc > floor_)) {
+            f = j0 + c + 1;
+          } else {
+            const double lcc = sqrt(dcc), inv = 1.0 / lcc;
+            Lb[c][c] = lcc;
+            dinv[c] = inv;
+#pragma unroll
+            for (int r = c + 1; r < CHOL_NB; ++r) {
+              if (r < jb) {
+                double v = Lb[r][c];
+#pragma unroll
+                for (int k = 0; k < c; ++k) v = fma(-Lb[r][k], Lb[c][k], v);
+                Lb[r][c] = v * inv;
+              }
+            }
+          }
         }
       }
-      __syncthreads();
-      if (tid == 0) xch[1 + par] = (double)sh_bad;
+      __syncthreads();  // every thread has read the diagonal block
+      if (!f) {
+        // diagonal block <- L_bb (lower), rows below <- B L_bb^-T (row-parallel forward substitution)
+        if (tid < CHOL_NB * CHOL_NB) {
+          const int r = tid % CHOL_NB, c = tid / CHOL_NB;
+          if (r < jb && c < jb && r >= c) {
+            double v = 0.0;
+#pragma unroll
+            for (int rr = 0; rr < CHOL_NB; ++rr)
+#pragma unroll
+              for (int cc = 0; cc < CHOL_NB; ++cc)
+                if (rr == r && cc == c) v = Lb[rr][cc];
+            P[(size_t)c * t + j0 + r] = v;
+          }
+        }
+        for (int i = jn + tid; i < t; i += NT) {
+          double x[CHOL_NB];
+#pragma unroll
+          for (int c = 0; c < CHOL_NB; ++c) x[c] = (c < jb) ? P[(size_t)c * t + i] : 0.0;
+#pragma unroll
+          for (int c = 0; c < CHOL_NB; ++c) {
+            double v = x[c];
+#pragma unroll
+            for (int k = 0; k < c; ++k) v = fma(-x[k], Lb[c][k], v);
+            x[c] = v * dinv[c];
+          }
+#pragma unroll
+          for (int c = 0; c < CHOL_NB; ++c)
+            if (c < jb) P[(size_t)c * t + i] = x[c];
+        }
+      }
+      if (tid == 0) xch[1 + par] = (double)f;
     }
-    cla_cluster_sync();  // the panel (in the owner's Al) and its status are visible
+    cla_cluster_sync();  // panel b factored and visible
     {
       const double f = *cla_remote(xch + 1 + par, (unsigned)owner);
       if (f != 0.0) {
@@ -156,29 +202,54 @@ __global__ void __launch_bounds__(CLA_NT) cholesky_cluster_kernel(int t, double*
         break;
       }
     }
-    const int jn = j0 + jb;  // first column after the panel
-    if (jn < t) {
+    if (jn >= t) break;
+    {
       const double* P = cla_remote(Al + (size_t)(b / CS) * CHOL_NB * t, (unsigned)owner);
-      for (int e = tid; e < jb * (t - jn); e += NT) {
-        int c = e / (t - jn), i = jn + (e - c * (t - jn));
+      const int len = t - jn, tot = jb * len;
+      int e = tid;
+      for (; e + 3 * NT < tot; e += 4 * NT) {
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          int ee = e + u * NT, c = ee / len, i = jn + (ee - c * len);
+          v[u] = P[(size_t)c * t + i];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          int ee = e + u * NT, c = ee / len, i = jn + (ee - c * len);
+          pl[(size_t)c * t + i] = v[u];
+        }
+      }
+      for (; e < tot; e += NT) {
+        int c = e / len, i = jn + (e - c * len);
         pl[(size_t)c * t + i] = P[(size_t)c * t + i];
       }
-      __syncthreads();
-      // own columns g >= jn: G[i][g] -= sum_c L[i][j0+c] L[g][j0+c], i >= g
-      for (int lc = warp; lc < ncl; lc += nw) {
-        const int g = gcol(lc);
-        if (g < jn || g >= t) continue;
-        double lgc[CHOL_NB];
+    }
+    __syncthreads();
+    // own columns g >= jn: G[i][g] -= sum_c L[i][j0+c] L[g][j0+c], i >= g (warp per column)
+    for (int lc = warp; lc < ncl; lc += nw) {
+      const int g = gcol(lc);
+      if (g < jn || g >= t) continue;
+      double lgc[CHOL_NB];
 #pragma unroll
-        for (int c = 0; c < CHOL_NB; ++c) lgc[c] = (c < jb) ? pl[(size_t)c * t + g] : 0.0;
-        double* col = Al + (size_t)lc * t;
-        for (int i = g + lane; i < t; i += 32) {
-          double acc = col[i];
+      for (int c = 0; c < CHOL_NB; ++c) lgc[c] = (c < jb) ? pl[(size_t)c * t + g] : 0.0;
+      double* col = Al + (size_t)lc * t;
+      int i = g + lane;
+      for (; i + 32 < t; i += 64) {
+        double a0 = col[i], a1 = col[i + 32];
 #pragma unroll
-          for (int c = 0; c < CHOL_NB; ++c)
-            if (c < jb) acc -= pl[(size_t)c * t + i] * lgc[c];
-          col[i] = acc;
+        for (int c = 0; c < CHOL_NB; ++c) {
+          a0 = fma(-pl[(size_t)c * t + i], lgc[c], a0);
+          a1 = fma(-pl[(size_t)c * t + i + 32], lgc[c], a1);
         }
+        col[i] = a0;
+        col[i + 32] = a1;
+      }
+      if (i < t) {
+        double a0 = col[i];
+#pragma unroll
+        for (int c = 0; c < CHOL_NB; ++c) a0 = fma(-pl[(size_t)c * t + i], lgc[c], a0);
+        col[i] = a0;
       }
     }
     __syncthreads();
@@ -213,11 +284,17 @@ __host__ __device__ inline size_t tri_smem_doubles(int s, int CS) {
 
 // PL = rows per lane (s <= 32 PL): the row vectors of a step (v', p' of the pending update and
 // v_j) are held in registers, so each own column costs PL independent smem loads and stores.
-template <int PL, int TNT>
+// GA = true (s too large for the cluster's shared memory): the own columns live in the global
+// scratch gA (L2-resident; CS * cdiv(s, CS) * s doubles + tail pad), everything else as above.
+__host__ __device__ inline size_t tri_smem_doubles_ga(int s, int CS) {
+  return 5 * (size_t)s + 3 * (size_t)cdiv(s, CS) + 2 * 32 + 16 + 1300;  // row overrun of PL = 40
+}
+template <int PL, int TNT, bool GA = false>
 __global__ void __launch_bounds__(TNT) tridiag_cluster_kernel(int s, const double* __restrict__ A, int lda,
                                                                   double* __restrict__ d, double* __restrict__ e,
                                                                   double* __restrict__ tau, double* __restrict__ Vh,
-                                                                  int ldv, long long* __restrict__ prof) {
+                                                                  int ldv, long long* __restrict__ prof,
+                                                                  double* __restrict__ gA) {
   extern __shared__ __align__(16) double sm[];
   __shared__ double Kbuf[2];
   __shared__ double wsum[2];
@@ -232,8 +309,8 @@ __global__ void __launch_bounds__(TNT) tridiag_cluster_kernel(int s, const doubl
   const int CS = (int)gridDim.x;
   const unsigned rank = cla_rank();
   const int ncl = cdiv(s, CS);
-  double* Al = sm;                      // ncl x s, own columns
-  double* vloc = Al + (size_t)ncl * s;  // 2 x s (parity): [tau_j at index j | v_j at j+1..s-1]
+  double* Al = GA ? gA + (size_t)rank * ncl * s : sm;  // ncl x s, own columns
+  double* vloc = GA ? sm : Al + (size_t)ncl * s;        // 2 x s (parity): [tau_j at index j | v_j at j+1..s-1]
   double* ploc = vloc + 2 * (size_t)s;  // 2 x s (parity): gathered p_j (all rows)
   double* pbuf = ploc + 2 * (size_t)s;  // own entries of p_j (global column index), read remotely
   double* wpart = pbuf + s;             // per-warp partials of p.v (32)
@@ -244,7 +321,11 @@ __global__ void __launch_bounds__(TNT) tridiag_cluster_kernel(int s, const doubl
   const int warp = tid >> 5, lane = tid & 31, nw = NT >> 5;
   // every row loop below reads whole 32-row groups unconditionally (rows >= s hit later arrays or
   // the 160-double tail pad; they are multiplied by zero and never stored), so smem starts zeroed
-  for (size_t q = (size_t)ncl * s + tid; q < tri_smem_doubles(s, CS); q += NT) sm[q] = 0.0;
+  if (GA) {
+    for (size_t q = tid; q < tri_smem_doubles_ga(s, CS); q += NT) sm[q] = 0.0;
+  } else {
+    for (size_t q = (size_t)ncl * s + tid; q < tri_smem_doubles(s, CS); q += NT) sm[q] = 0.0;
+  }
   for (int q = tid; q < ncl * s; q += NT) {
     int lc = q / s, i = q - lc * s, g = (int)rank + CS * lc;
     Al[q] = (g < s) ? 0.5 * (A[IDX(i, g, lda)] + A[IDX(g, i, lda)]) : 0.0;
@@ -525,26 +606,57 @@ __global__ void __launch_bounds__(256) backtransform_panel_kernel(int s, int m, 
 }
 
 // ------------------------------------------------------------------ helpers for the RR step
-// Li = L^-1 (t x t lower, ldl -> ldi), one warp per column j, column-oriented forward
-// substitution: x = e_j; for k >= j: x_k /= L_kk; x_{k+1:} -= x_k L_{k+1:,k} (coalesced column reads).
-__global__ void __launch_bounds__(256) trinv_cols_kernel(int t, const double* __restrict__ L, int ldl,
-                                                         double* __restrict__ Li, int ldi) {
-  extern __shared__ __align__(16) double xs[];  // (blockDim/32) x t
+// Li = L^-1 (t x t lower, ldl -> ldi): one warp per column j of the inverse (x = L^-1 e_j held in
+// registers, rows lane + 32 q), columns of L streamed through shared memory in panels of TI_KB
+// shared by the CTA's 8 warps: x_k /= L_kk; x_{k+1:} -= x_k L_{k+1:,k}.
+constexpr int TI_KB = 16;
+template <int PL>
+__global__ void __launch_bounds__(256) trinv_panel_kernel(int t, const double* __restrict__ L, int ldl,
+                                                          double* __restrict__ Li, int ldi) {
+  extern __shared__ __align__(16) double lp[];  // TI_KB x t
+  __shared__ double dinv[TI_KB];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int j = blockIdx.x * (blockDim.x >> 5) + w;
-  if (j >= t) return;
-  double* x = xs + (size_t)w * t;
-  for (int i = lane; i < t; i += 32) x[i] = (i == j) ? 1.0 : 0.0;
-  __syncwarp();
-  for (int k = j; k < t; ++k) {
-    const double xk = x[k] / __ldg(L + IDX(k, k, ldl));
-    __syncwarp();
-    if (lane == 0) x[k] = xk;
-    const double* lc = L + IDX(0, k, ldl);
-    for (int i = k + 1 + lane; i < t; i += 32) x[i] -= xk * __ldg(lc + i);
-    __syncwarp();
+  const int jbase = blockIdx.x * 8;
+  const int j = jbase + w;
+  double x[PL];
+#pragma unroll
+  for (int q = 0; q < PL; ++q) x[q] = (lane + 32 * q == j) ? 1.0 : 0.0;
+  for (int k0 = jbase; k0 < t; k0 += TI_KB) {
+    const int kb = min(TI_KB, t - k0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < kb * t; e += blockDim.x) {
+      const int c = e / t, i = e - c * t;
+      lp[(size_t)c * t + i] = (i > k0 + c) ? __ldg(L + IDX(i, k0 + c, ldl)) : 0.0;
+    }
+    if (threadIdx.x < kb) dinv[threadIdx.x] = 1.0 / __ldg(L + IDX(k0 + threadIdx.x, k0 + threadIdx.x, ldl));
+    __syncthreads();
+    if (j >= t) continue;
+    for (int c = 0; c < kb; ++c) {
+      const int k = k0 + c;
+      if (k < j) continue;
+      const int kq = k >> 5, kl = k & 31;
+      double xv = 0.0;
+#pragma unroll
+      for (int q = 0; q < PL; ++q)
+        if (q == kq) xv = x[q];
+      const double xk = __shfl_sync(0xffffffffu, xv, kl) * dinv[c];
+#pragma unroll
+      for (int q = 0; q < PL; ++q)
+        if (q == kq && lane == kl) x[q] = xk;
+      const double* lc = lp + (size_t)c * t;  // zero at rows <= k
+#pragma unroll
+      for (int q = 0; q < PL; ++q) {
+        const int i = lane + 32 * q;
+        if (i < t) x[q] = fma(-xk, lc[i], x[q]);
+      }
+    }
   }
-  for (int i = lane; i < t; i += 32) Li[IDX(i, j, ldi)] = (i >= j) ? x[i] : 0.0;
+  if (j >= t) return;
+#pragma unroll
+  for (int q = 0; q < PL; ++q) {
+    const int i = lane + 32 * q;
+    if (i < t) Li[IDX(i, j, ldi)] = x[q];
+  }
 }
 
 // Newton-Schulz step towards the polar factor: Z = 1.5 I - 0.5 M for M = Y^T Y (m x m), and

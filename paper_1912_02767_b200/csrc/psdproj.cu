@@ -249,6 +249,10 @@ static int cla_attrs() {
   static bool done = false;
   if (done) return 0;
   const int mx = CLA_SMEM_BYTES;
+  CK(cudaFuncSetAttribute(tridiag_cluster_kernel<24, 256, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  CK(cudaFuncSetAttribute(tridiag_cluster_kernel<24, 256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  CK(cudaFuncSetAttribute(tridiag_cluster_kernel<40, 256, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  CK(cudaFuncSetAttribute(tridiag_cluster_kernel<40, 256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   CK(cudaFuncSetAttribute(tridiag_cluster_kernel<4, 512>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   CK(cudaFuncSetAttribute(tridiag_cluster_kernel<4, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   CK(cudaFuncSetAttribute(tridiag_cluster_kernel<8, 512>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -259,7 +263,11 @@ static int cla_attrs() {
   CK(cudaFuncSetAttribute(tridiag_cluster_kernel<20, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   CK(cudaFuncSetAttribute(cholesky_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   CK(cudaFuncSetAttribute(cholesky_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-  CK(cudaFuncSetAttribute(trinv_cols_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  const int tmx = (int)(TI_KB * 32 * 40 * sizeof(double));
+  CK(cudaFuncSetAttribute(trinv_panel_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, tmx));
+  CK(cudaFuncSetAttribute(trinv_panel_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, tmx));
+  CK(cudaFuncSetAttribute(trinv_panel_kernel<24>, cudaFuncAttributeMaxDynamicSharedMemorySize, tmx));
+  CK(cudaFuncSetAttribute(trinv_panel_kernel<40>, cudaFuncAttributeMaxDynamicSharedMemorySize, tmx));
   const int bmx = (int)(BT_PB * 32 * BT_PER_LANE * sizeof(double));
   CK(cudaFuncSetAttribute(backtransform_panel_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, bmx));
   CK(cudaFuncSetAttribute(backtransform_panel_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, bmx));
@@ -284,8 +292,18 @@ static int cholesky_run(cudaStream_t st, int t, double* G, int ld, int* d_status
 // Li = L^-1 (lower triangular t x t)
 static int trinv_run(cudaStream_t st, int t, const double* L, int ldl, double* Li, int ldi) {
   TRY(cla_attrs());
-  const int wpb = 4;
-  trinv_cols_kernel<<<cdiv(t, wpb), 32 * wpb, (size_t)wpb * t * sizeof(double), st>>>(t, L, ldl, Li, ldi);
+  const size_t sm = (size_t)TI_KB * t * sizeof(double);
+  const int g = cdiv(t, 8);
+  if (t <= 32 * 8)
+    trinv_panel_kernel<8><<<g, 256, sm, st>>>(t, L, ldl, Li, ldi);
+  else if (t <= 32 * 16)
+    trinv_panel_kernel<16><<<g, 256, sm, st>>>(t, L, ldl, Li, ldi);
+  else if (t <= 32 * 24)
+    trinv_panel_kernel<24><<<g, 256, sm, st>>>(t, L, ldl, Li, ldi);
+  else if (t <= 32 * 40)
+    trinv_panel_kernel<40><<<g, 256, sm, st>>>(t, L, ldl, Li, ldi);
+  else
+    return set_err(PSDPROJ_E_CAPACITY, "trinv supports t <= 1280");
   CKL();
   return 0;
 }
@@ -322,28 +340,29 @@ static int eigh_top(cudaStream_t st, int s, const double* Hs, int ldh, int m, do
   static int tri_mode = -1;  // 0 auto, 1 force one-CTA
   if (tri_mode < 0) tri_mode = getenv("PSDPROJ_TRI_ONECTA") ? 1 : 0;
   int tcs = (tri_mode == 0 && s > 64) ? cla_cluster_size(s, tri_smem_doubles) : 0;
+  static long long* dprof = nullptr;
+  static int want_prof = getenv("PSDPROJ_TRI_PROF") ? 1 : 0;
+  if (want_prof && !dprof) CK(cudaMalloc(&dprof, 16 * 8 * sizeof(long long)));
+#define TRI_LAUNCH(PL, NTH, GA, CSZ, SMEM)                                                                         \
+  TRY(launch_cluster(tridiag_cluster_kernel<PL, NTH, GA>, CSZ, NTH, SMEM, st, s, Hs, ldh, w.td, w.te, w.ttau, w.Vh, \
+                     w.ldv, dprof, w.tG))
   if (tcs) {
-    static long long* dprof = nullptr;
-    static int want_prof = getenv("PSDPROJ_TRI_PROF") ? 1 : 0;
-    if (want_prof && !dprof) CK(cudaMalloc(&dprof, 16 * 8 * sizeof(long long)));
     const size_t tsm = tri_smem_doubles(s, tcs) * sizeof(double);
     if (s <= 32 * 4)
-      TRY(launch_cluster(tridiag_cluster_kernel<4, 512>, tcs, 512, tsm, st, s, Hs, ldh, w.td, w.te, w.ttau, w.Vh, w.ldv, dprof));
+      TRI_LAUNCH(4, 512, false, tcs, tsm);
     else if (s <= 32 * 8)
-      TRY(launch_cluster(tridiag_cluster_kernel<8, 512>, tcs, 512, tsm, st, s, Hs, ldh, w.td, w.te, w.ttau, w.Vh, w.ldv, dprof));
+      TRI_LAUNCH(8, 512, false, tcs, tsm);
     else if (s <= 32 * 14)
-      TRY(launch_cluster(tridiag_cluster_kernel<14, 256>, tcs, 256, tsm, st, s, Hs, ldh, w.td, w.te, w.ttau, w.Vh, w.ldv, dprof));
+      TRI_LAUNCH(14, 256, false, tcs, tsm);
     else
-      TRY(launch_cluster(tridiag_cluster_kernel<20, 256>, tcs, 256, tsm, st, s, Hs, ldh, w.td, w.te, w.ttau, w.Vh, w.ldv, dprof));
-    if (want_prof) {
-      long long h[128];
-      CK(cudaStreamSynchronize(st));
-      CK(cudaMemcpy(h, dprof, sizeof(h), cudaMemcpyDeviceToHost));
-      for (int r = 0; r < std::min(tcs, 3); ++r)
-        fprintf(stderr, "tri prof s=%d cs=%d rank %d: house %lld B1 %lld vcopy %lld fused %lld B2 %lld gatherK %lld sync %lld (cycles/step)\n",
-                s, tcs, r, h[r * 8 + 0] / (s - 2), h[r * 8 + 1] / (s - 2), h[r * 8 + 2] / (s - 2), h[r * 8 + 3] / (s - 2),
-                h[r * 8 + 4] / (s - 2), h[r * 8 + 5] / (s - 2), h[r * 8 + 6] / (s - 2));
-    }
+      TRI_LAUNCH(20, 256, false, tcs, tsm);
+  } else if (tri_mode == 0 && s > 64 && s <= 32 * TRI_BT_PER_LANE) {
+    // too large for shared memory: own columns in the L2-resident scratch tG (16-CTA cluster)
+    const size_t tsm = tri_smem_doubles_ga(s, 16) * sizeof(double);
+    if (s <= 32 * 24)
+      TRI_LAUNCH(24, 256, true, 16, tsm);
+    else
+      TRI_LAUNCH(40, 256, true, 16, tsm);
   } else {
     const size_t vecs = (size_t)s * 10;
     size_t dyn = ((s <= TRI_SMEM_MAX) ? (size_t)s * (s + 1) : 0) + vecs;
@@ -351,6 +370,16 @@ static int eigh_top(cudaStream_t st, int s, const double* Hs, int ldh, int m, do
     if (s > TRI_SMEM_MAX && dyn > 200 * 1024) return set_err(PSDPROJ_E_CAPACITY, "tridiag smem %zu for s=%d", dyn, s);
     tridiag_kernel<1024><<<1, 1024, dyn, st>>>(s, Hs, ldh, w.td, w.te, w.ttau, w.Vh, w.ldv, w.tG, w.ldg);
     CKL();
+  }
+#undef TRI_LAUNCH
+  if (want_prof && tcs) {
+    long long h[128];
+    CK(cudaStreamSynchronize(st));
+    CK(cudaMemcpy(h, dprof, sizeof(h), cudaMemcpyDeviceToHost));
+    for (int r = 0; r < std::min(tcs, 3); ++r)
+      fprintf(stderr, "tri prof s=%d cs=%d rank %d: house %lld B1 %lld vcopy %lld fused %lld B2 %lld gatherK %lld sync %lld (cycles/step)\n",
+              s, tcs, r, h[r * 8 + 0] / (s - 2), h[r * 8 + 1] / (s - 2), h[r * 8 + 2] / (s - 2), h[r * 8 + 3] / (s - 2),
+              h[r * 8 + 4] / (s - 2), h[r * 8 + 5] / (s - 2), h[r * 8 + 6] / (s - 2));
   }
   tri_prep_kernel<<<1, 1024, 0, st>>>(s, w.td, w.te, w.te2, w.tbounds);
   CKL();
@@ -500,7 +529,7 @@ static size_t carve(psdproj_ctx_s* c, int n, const psdproj_params& p, int m_max,
   c->te2 = cv.take<double>(vlen); c->tbounds = cv.take<double>(8); c->tnpos = cv.take<int>(8);
   c->tscr_elems = (size_t)6 * s_max * (size_t)(std::min(s_max, m_max + (s_max - 3 * m_max)) + 1);
   c->tscr = cv.take<double>(c->tscr_elems);
-  c->tG = cv.take<double>(s2);
+  c->tG = cv.take<double>(s2 + 16 * (size_t)s_max + 2048);  // also the GA tridiagonalisation scratch
   return cv.off + 256;
 }
 
@@ -1359,7 +1388,7 @@ extern "C" int psdproj_philox_gauss(int n, int q, double* out, int ld, uint64_t 
 
 extern "C" size_t psdproj_eigh_ws_elems(int s, int m) {
   size_t mm = (size_t)std::max(m, 1);
-  return (size_t)5 * s + 64 + (size_t)6 * s * mm + 2 * (size_t)s * s + 2 * mm * mm + (size_t)s * mm + 64;
+  return (size_t)5 * s + 64 + (size_t)6 * s * mm + 2 * (size_t)s * s + 16 * (size_t)s + 2048 + 2 * mm * mm + (size_t)s * mm + 64;
 }
 
 extern "C" int psdproj_eigh(int s, const double* A, int lda, int m, double* w, double* V, int ldv, int* npos,
@@ -1379,7 +1408,7 @@ extern "C" int psdproj_eigh(int s, const double* A, int lda, int m, double* w, d
   e.tscr_elems = (size_t)6 * s * mm;
   e.tG = e.tscr + e.tscr_elems;
   e.ldg = s;
-  e.Vh = e.tG + (size_t)s * s;
+  e.Vh = e.tG + (size_t)s * s + 16 * (size_t)s + 2048;
   e.ldv = s;
   e.nsM = e.Vh + (size_t)s * s;
   e.nsZ = e.nsM + mm * mm;
@@ -1393,4 +1422,18 @@ extern "C" int psdproj_eigh(int s, const double* A, int lda, int m, double* w, d
     CK(cudaStreamSynchronize(st));
   }
   return 0;
+}
+
+extern "C" int psdproj_cholesky(int t, double* G, int ld, void* stream) {
+  if (t <= 0 || ld < t || !G) return set_err(PSDPROJ_E_INVALID, "invalid cholesky args");
+  cudaStream_t st = (cudaStream_t)stream;
+  int* d_status = nullptr;
+  CK(cudaMallocAsync(&d_status, sizeof(int), st));
+  CK(cudaMemsetAsync(d_status, 0, sizeof(int), st));
+  int rc = cholesky_run(st, t, G, ld, d_status);
+  int h = 0;
+  if (rc == 0) CK(cudaMemcpyAsync(&h, d_status, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaFreeAsync(d_status, st));
+  CK(cudaStreamSynchronize(st));
+  return rc < 0 ? rc : h;
 }

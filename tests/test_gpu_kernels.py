@@ -74,7 +74,7 @@ def test_philox_gauss_matches_oracle(api):
 
 
 @pytest.mark.parametrize("s,m", [(1, 1), (2, 2), (3, 1), (17, 17), (64, 20), (160, 60), (161, 161), (300, 100),
-                                 (500, 170), (640, 220), (641, 120)])
+                                 (500, 170), (640, 220), (641, 120), (800, 260), (1100, 300)])
 def test_eigh_tridiagonal(api, s, m):
     rng = np.random.default_rng(1000 + s)
     M = rng.standard_normal((s, s))
@@ -127,3 +127,26 @@ def test_eigh_repeated_eigenvalues(api, s):
     assert np.abs(w - ref).max() <= 1e-12 * 3 * max(1, s / 20)
     assert np.linalg.norm(V.T @ V - np.eye(m)) <= 1e-11 * max(1, s / 20)
     assert np.linalg.norm(A @ V - V * w, axis=0).max() <= 1e-11 * 3 * max(1, s / 20)
+
+
+@pytest.mark.parametrize("t", [1, 5, 8, 9, 64, 150, 301, 520])
+def test_cholesky_cluster(api, t):
+    """a6 Cholesky (cluster kernel for t <= ~580, one CTA above) vs LAPACK on an SPD Gram matrix."""
+    rng = np.random.default_rng(300 + t)
+    M = rng.standard_normal((t + 20, t))
+    G = M.T @ M
+    L, rc = api.cholesky(_cm(G))
+    assert rc == 0
+    L = L.cpu().numpy()
+    ref = np.linalg.cholesky(G)
+    assert np.abs(np.triu(L, 1)).max() == 0.0
+    assert np.linalg.norm(L - ref) <= 1e-12 * np.linalg.norm(ref) * max(1, t / 10)
+
+
+def test_cholesky_breakdown(api):
+    """Rank-deficient Gram (two equal columns): the failing pivot is reported (R20)."""
+    rng = np.random.default_rng(9)
+    M = rng.standard_normal((40, 30))
+    M[:, 17] = M[:, 3]
+    L, rc = api.cholesky(_cm(M.T @ M))
+    assert rc == 18
