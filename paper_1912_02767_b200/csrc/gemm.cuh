@@ -211,3 +211,121 @@ __global__ void splitk_reduce_kernel(int M, int N, int splits, double alpha, con
 }
 
 }  // namespace psd
+
+namespace psd {
+
+// ---------------------------------------------------------------- k-paired DMMA GEMM
+// Same contract as dgemm_kernel. Shared tiles store k permuted in pairs (k, k+4) of every 8-block
+// adjacent, so one LDS.128 feeds the fragments of two consecutive m8n8k4 MMAs:
+//   element (o, k) of a BO x 16 tile -> s[(8 (k / 8) / 2 + (k % 4)) * P + 2 o + (k % 8) / 4]
+// with pitch P = 2 BO + 4 (doubles; 2 BO + 4 = 4 mod 16 keeps the 8 lanes of each LDS.128 phase on
+// distinct bank groups). Global -> shared by 8-byte cp.async (the permutation breaks 16-byte runs).
+template <int BO, int THREADS, bool OUTER_CONTIG>
+__device__ __forceinline__ void load_tile_kp(double* sm, const double* __restrict__ g, int ld, int o0, int k0, int O,
+                                             int K, int tid) {
+  constexpr int P = 2 * BO + 4;
+  constexpr int CH = BO * 16;
+#pragma unroll
+  for (int c = tid; c < CH; c += THREADS) {
+    int o, k;
+    if (OUTER_CONTIG) {  // (o, k) at g[o + k ld]: o fastest across threads
+      k = c / BO;
+      o = c % BO;
+    } else {  // (o, k) at g[k + o ld]: k fastest
+      o = c / 16;
+      k = c % 16;
+    }
+    const int go = o0 + o, gk = k0 + k;
+    const bool valid = go < O && gk < K;
+    const double* src = g + (valid ? (OUTER_CONTIG ? IDX(go, gk, ld) : IDX(gk, go, ld)) : 0);
+    const int kp = (k >> 3) * 4 + (k & 3), h = (k >> 2) & 1;
+    cp_async_8(sm + kp * P + 2 * o + h, src, valid ? 8 : 0);
+  }
+}
+
+template <int OPA, int OPB, int BM, int BN, int STAGES>
+__global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32, (BM * BN >= 8192) ? 2 : 3)
+    dgemm_kp_kernel(int M, int N, int K, double alpha, const double* __restrict__ A, int lda,
+                    const double* __restrict__ B, int ldb, double beta, double* __restrict__ C, int ldc,
+                    double* __restrict__ partial, int ktiles_per_split) {
+  constexpr int WM = 32, WN = 32, BK = 16;
+  constexpr int WARPS_M = BM / WM, THREADS = (BM / WM) * (BN / WN) * 32;
+  constexpr int MI = WM / 8, NI = WN / 8;
+  constexpr int PA = 2 * BM + 4, PB = 2 * BN + 4;
+  constexpr int A_ELEMS = 8 * PA, B_ELEMS = 8 * PB, STAGE = A_ELEMS + B_ELEMS;
+  extern __shared__ __align__(16) double smem[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp % WARPS_M, wn = warp / WARPS_M;
+  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  const int KT = cdiv(K, BK);
+  const int kt0 = blockIdx.z * ktiles_per_split;
+  const int nkt = max(0, min(KT, kt0 + ktiles_per_split) - kt0);
+  double acc[MI][NI][2];
+#pragma unroll
+  for (int i = 0; i < MI; ++i)
+#pragma unroll
+    for (int j = 0; j < NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  auto issue = [&](int s, int kt) {
+    double* sa = smem + (size_t)s * STAGE;
+    load_tile_kp<BM, THREADS, OPA == OP_N>(sa, A, lda, m0, kt * BK, M, K, tid);
+    load_tile_kp<BN, THREADS, OPB == OP_T>(sa + A_ELEMS, B, ldb, n0, kt * BK, N, K, tid);
+  };
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nkt) issue(s, kt0 + s);
+    cp_async_commit();
+  }
+  const int fr = lane >> 2, fk = lane & 3;
+  for (int it = 0; it < nkt; ++it) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      const int nx = it + STAGES - 1;
+      if (nx < nkt) issue(nx % STAGES, kt0 + nx);
+      cp_async_commit();
+    }
+    const double* sa = smem + (size_t)(it % STAGES) * STAGE;
+    const double* sb = sa + A_ELEMS;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      double2 af[MI], bf[NI];
+#pragma unroll
+      for (int i = 0; i < MI; ++i)
+        af[i] = *reinterpret_cast<const double2*>(sa + (q * 4 + fk) * PA + 2 * (wm * WM + i * 8 + fr));
+#pragma unroll
+      for (int j = 0; j < NI; ++j)
+        bf[j] = *reinterpret_cast<const double2*>(sb + (q * 4 + fk) * PB + 2 * (wn * WN + j * 8 + fr));
+#pragma unroll
+      for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < NI; ++j) dmma_884(acc[i][j], af[i].x, bf[j].x);
+#pragma unroll
+      for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < NI; ++j) dmma_884(acc[i][j], af[i].y, bf[j].y);
+    }
+  }
+  cp_async_wait<0>();
+#pragma unroll
+  for (int i = 0; i < MI; ++i) {
+    const int row = m0 + wm * WM + i * 8 + fr;
+    if (row >= M) continue;
+#pragma unroll
+    for (int j = 0; j < NI; ++j) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int col = n0 + wn * WN + j * 8 + fk * 2 + h;
+        if (col >= N) continue;
+        const double v = acc[i][j][h];
+        if (partial) {
+          partial[(size_t)blockIdx.z * M * N + IDX(row, col, M)] = v;
+        } else {
+          double* c = C + IDX(row, col, ldc);
+          *c = (beta == 0.0) ? alpha * v : alpha * v + beta * (*c);
+        }
+      }
+    }
+  }
+}
+
+}  // namespace psd

@@ -104,16 +104,62 @@ int gemm_launch(cudaStream_t st, int M, int N, int K, double alpha, const double
 }
 }  // namespace
 
+template <int OA, int OB, int BM, int BN, int ST>
+static int gemm_kp_launch(cudaStream_t st, int M, int N, int K, double alpha, const double* A, int lda,
+                          const double* B, int ldb, double beta, double* C, int ldc, double* part, size_t part_elems) {
+  constexpr int THREADS = (BM / 32) * (BN / 32) * 32;
+  constexpr size_t SMEM = (size_t)ST * 8 * ((2 * BM + 4) + (2 * BN + 4)) * sizeof(double);
+  auto kern = dgemm_kp_kernel<OA, OB, BM, BN, ST>;
+  static bool attr = false;
+  static int per_sm = 1;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, SMEM));
+    per_sm = std::max(per_sm, 1);
+    attr = true;
+  }
+  const int KT = cdiv(std::max(K, 1), 16);
+  const int tiles = cdiv(M, BM) * cdiv(N, BN);
+  const int slots = sms() * per_sm;
+  int splits = 1;
+  if (part && tiles < slots && KT >= 8) {
+    splits = std::min(std::max(1, slots / tiles), KT / 4);
+    splits = std::max(1, std::min(splits, 32));
+    while (splits > 1 && (size_t)splits * M * N > part_elems) --splits;
+  }
+  const int ktps = cdiv(KT, splits);
+  splits = cdiv(KT, ktps);
+  dim3 grid(cdiv(M, BM), cdiv(N, BN), splits);
+  kern<<<grid, THREADS, SMEM, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits > 1 ? part : nullptr, ktps);
+  CKL();
+  if (splits > 1) {
+    splitk_reduce_kernel<<<grid1d((size_t)M * N), 256, 0, st>>>(M, N, splits, alpha, part, beta, C, ldc);
+    CKL();
+  }
+  return 0;
+}
+
 static int dgemm(cudaStream_t st, int opA, int opB, int M, int N, int K, double alpha, const double* A, int lda,
                  const double* B, int ldb, double beta, double* C, int ldc, double* part, size_t part_elems) {
   if (M <= 0 || N <= 0) return 0;
-  if (K <= 0) {
-    // C = beta C
-    if (beta == 0.0) {
-      CK(cudaMemset2DAsync(C, (size_t)ldc * 8, 0, (size_t)M * 8, N, st));
-      return 0;
-    }
-    // C = alpha*0 + beta*C via a zero-K split-free launch
+  if (K <= 0 && beta == 0.0) {
+    CK(cudaMemset2DAsync(C, (size_t)ldc * 8, 0, (size_t)M * 8, N, st));
+    return 0;
+  }
+  static int mode = -1;  // 0: k-paired kernel (default), 1: first-cut kernel
+  if (mode < 0) mode = (getenv("PSDPROJ_GEMM") && std::string(getenv("PSDPROJ_GEMM")) == "old") ? 1 : 0;
+  if (mode == 0) {
+    static int tile = -1;
+    if (tile < 0) tile = getenv("PSDPROJ_GEMM_TILE") ? atoi(getenv("PSDPROJ_GEMM_TILE")) : 64;
+    const bool big = tile == 128 && M >= 1024 && N >= 48;
+#define GK(OA, OB)                                                                                              \
+  return big ? gemm_kp_launch<OA, OB, 128, 64, 4>(st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, part, part_elems) \
+             : gemm_kp_launch<OA, OB, 64, 64, 4>(st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, part, part_elems)
+    if (opA == OP_N && opB == OP_N) GK(OP_N, OP_N);
+    if (opA == OP_T && opB == OP_N) GK(OP_T, OP_N);
+    if (opA == OP_N && opB == OP_T) GK(OP_N, OP_T);
+    GK(OP_T, OP_T);
+#undef GK
   }
   bool vec = (lda % 2 == 0) && (ldb % 2 == 0) && (((uintptr_t)A & 15) == 0) && (((uintptr_t)B & 15) == 0);
   int KT = cdiv(std::max(K, 1), GBK);
