@@ -242,7 +242,7 @@ def main():
     total = 1 + W + K
     mats = gen_matrices(cfg, total, dev)
     torch.cuda.synchronize()
-    prm = api.default_params(max_iter=args.max_iter, profile=1, seed=1912 + rank, ctx_id=rank)
+    prm = api.default_params(max_iter=args.max_iter, profile=3, seed=1912 + rank, ctx_id=rank)
     ctx = api.Context(cfg.n, params=prm, device=dev)
     out = torch.empty_like(mats[0])
     st = torch.cuda.current_stream()
@@ -358,6 +358,9 @@ def main():
             "roofline": roof,
             "step_roofline": {"frac": step_frac, "t_roof_ms": t_roof * 1e3 / K, "flops": flops / K,
                               "bytes": byts / K, "definition": "max(bytes/HBM, flops/P64) / step time"},
+            "phase_ms_per_step": {nm: round(sum(i["phase_ms"][k] for i in infos) / K, 3) for k, nm in enumerate(
+                ["a3_block_multiply", "w_p_projection", "gram_pencil", "cholesky_pencil", "rr_eigensolve",
+                 "rotation", "residual_norms", "host_locking_assembly"])},
             "iters_per_projection": {"mean": statistics.mean(iters), "min": min(iters), "max": max(iters),
                                      "cold": infos_warm[0]["iters"]},
             "status": [i["status"] for i in infos],

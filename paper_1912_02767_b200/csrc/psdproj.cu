@@ -97,19 +97,19 @@ int gemm_launch(cudaStream_t st, int M, int N, int K, double alpha, const double
                                                 splits > 1 ? part : nullptr, ktps);
   CKL();
   if (splits > 1) {
-    splitk_reduce_kernel<<<grid1d((size_t)M * N), 256, 0, st>>>(M, N, splits, alpha, part, beta, C, ldc);
+    splitk_reduce_kernel<<<dim3(cdiv(M, 256), N), 256, 0, st>>>(M, N, splits, alpha, part, beta, C, ldc);
     CKL();
   }
   return 0;
 }
 }  // namespace
 
-template <int OA, int OB, int BM, int BN, int ST>
+template <int OA, int OB, int BM, int BN, int ST, int TAG = 0>
 static int gemm_kp_launch(cudaStream_t st, int M, int N, int K, double alpha, const double* A, int lda,
                           const double* B, int ldb, double beta, double* C, int ldc, double* part, size_t part_elems) {
   constexpr int THREADS = (BM / 32) * (BN / 32) * 32;
   constexpr size_t SMEM = (size_t)ST * 8 * ((2 * BM + 4) + (2 * BN + 4)) * sizeof(double);
-  auto kern = dgemm_kp_kernel<OA, OB, BM, BN, ST>;
+  auto kern = dgemm_kp_kernel<OA, OB, BM, BN, ST, TAG>;
   static bool attr = false;
   static int per_sm = 1;
   if (!attr) {
@@ -133,7 +133,7 @@ static int gemm_kp_launch(cudaStream_t st, int M, int N, int K, double alpha, co
   kern<<<grid, THREADS, SMEM, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits > 1 ? part : nullptr, ktps);
   CKL();
   if (splits > 1) {
-    splitk_reduce_kernel<<<grid1d((size_t)M * N), 256, 0, st>>>(M, N, splits, alpha, part, beta, C, ldc);
+    splitk_reduce_kernel<<<dim3(cdiv(M, 256), N), 256, 0, st>>>(M, N, splits, alpha, part, beta, C, ldc);
     CKL();
   }
   return 0;
@@ -718,7 +718,11 @@ struct Run {
       }
       CK(cudaEventRecord(c->ev[2 * nev], st));
     }
-    TRY(dgemm(st, OP_N, OP_N, n, k, n, sgn, A, lda, Z, ldz, 0.0, Y, ldy, c->part, c->part_elems));
+    {
+      int rc_ = gemm_kp_launch<OP_N, OP_N, 64, 64, 4, 1>(st, n, k, n, sgn, A, lda, Z, ldz, 0.0, Y, ldy, c->part,
+                                                         c->part_elems);
+      if (rc_ < 0) return rc_;
+    }
     if (prof) {
       CK(cudaEventRecord(c->ev[2 * nev + 1], st));
       nev++;
@@ -1074,40 +1078,34 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
     int offW = mU, offE = mU + a, offP = mU + a + qe;
     int s = offP + ap;
     if (s > c->s_max) return set_err(PSDPROJ_E_CAPACITY, "RR basis %d > s_max %d", s, c->s_max);
-    // W = R_J (+ pending expansion E)
+    // W = R_J (+ pending expansion E) and P_J sit contiguously in S: [W E P] at offW; both are
+    // projected against the locked block and X_U in one pass (one Gram + one update GEMM each)
     TRY(run.mark(1));
     TRY(run.gather(n, a, c->S + (size_t)offW * ld, ld, c->R, ld, Jorig));
     TRY(run.copy_cols(n, qe, c->S + (size_t)offE * ld, ld, c->E, ld));
     int aw = a + qe;
     double* W = c->S + (size_t)offW * ld;
-    if (hard && nL > 0 && aw > 0) {
-      TRY(run.gemm(OP_T, OP_N, nL, aw, n, 1.0, c->XL, ld, W, ld, 0.0, c->Y, ldm));
-      TRY(run.gemm(OP_N, OP_N, n, aw, nL, -1.0, c->XL, ld, c->Y, ldm, 1.0, W, ld));
-    }
-    if (aw > 0) {  // W <- W - X_U (X_U^T W): the pencil's X-block of G becomes [I 0]
-      TRY(run.gemm(OP_T, OP_N, mU, aw, n, 1.0, c->S, ld, W, ld, 0.0, c->Y, ldm));
-      TRY(run.gemm(OP_N, OP_N, n, aw, mU, -1.0, c->S, ld, c->Y, ldm, 1.0, W, ld));
-    }
-    TRY(run.normalize(n, aw, W, ld, nullptr, 0));
-    TRY(run.mark(0));
-    TRY(run.amul(sgn, A, lda, W, ld, aw, c->BS + (size_t)offW * ld, ld));
-    TRY(run.mark(1));
-    // P_J, B P_J
+    double* P = c->S + (size_t)offP * ld;
+    double* BP = c->BS + (size_t)offP * ld;
     if (ap > 0) {
-      double* P = c->S + (size_t)offP * ld;
-      double* BP = c->BS + (size_t)offP * ld;
       TRY(run.gather(n, ap, P, ld, c->Pb, ld, PJ));
       TRY(run.gather(n, ap, BP, ld, c->BPb, ld, PJ));
-      if (hard && nL > 0) {
-        TRY(run.gemm(OP_T, OP_N, nL, ap, n, 1.0, c->XL, ld, P, ld, 0.0, c->Y, ldm));
-        TRY(run.gemm(OP_N, OP_N, n, ap, nL, -1.0, c->XL, ld, c->Y, ldm, 1.0, P, ld));
-        TRY(run.gemm(OP_N, OP_N, n, ap, nL, -1.0, c->BXL, ld, c->Y, ldm, 1.0, BP, ld));
-      }
-      TRY(run.gemm(OP_T, OP_N, mU, ap, n, 1.0, c->S, ld, P, ld, 0.0, c->Y, ldm));
-      TRY(run.gemm(OP_N, OP_N, n, ap, mU, -1.0, c->S, ld, c->Y, ldm, 1.0, P, ld));
-      TRY(run.gemm(OP_N, OP_N, n, ap, mU, -1.0, c->BS, ld, c->Y, ldm, 1.0, BP, ld));
-      TRY(run.normalize(n, ap, P, ld, BP, ld));
     }
+    const int wp = aw + ap;
+    if (hard && nL > 0 && wp > 0) {
+      TRY(run.gemm(OP_T, OP_N, nL, wp, n, 1.0, c->XL, ld, W, ld, 0.0, c->Y, ldm));
+      TRY(run.gemm(OP_N, OP_N, n, wp, nL, -1.0, c->XL, ld, c->Y, ldm, 1.0, W, ld));
+      if (ap > 0) TRY(run.gemm(OP_N, OP_N, n, ap, nL, -1.0, c->BXL, ld, c->Y + (size_t)aw * ldm, ldm, 1.0, BP, ld));
+    }
+    if (wp > 0) {  // [W P] <- [W P] - X_U (X_U^T [W P]): the pencil's X-block of G becomes [I 0]
+      TRY(run.gemm(OP_T, OP_N, mU, wp, n, 1.0, c->S, ld, W, ld, 0.0, c->Y, ldm));
+      TRY(run.gemm(OP_N, OP_N, n, wp, mU, -1.0, c->S, ld, c->Y, ldm, 1.0, W, ld));
+      if (ap > 0) TRY(run.gemm(OP_N, OP_N, n, ap, mU, -1.0, c->BS, ld, c->Y + (size_t)aw * ldm, ldm, 1.0, BP, ld));
+    }
+    TRY(run.normalize(n, aw, W, ld, nullptr, 0));
+    if (ap > 0) TRY(run.normalize(n, ap, P, ld, BP, ld));
+    TRY(run.mark(0));
+    TRY(run.amul(sgn, A, lda, W, ld, aw, c->BS + (size_t)offW * ld, ld));
     // ---- line 6: Rayleigh-Ritz on span(X, R, P) via the pencil (S^T BS, S^T S)
     // only the direction block of G is needed (X^T X = I, X^T [W P] = 0 by construction)
     TRY(run.mark(2));
