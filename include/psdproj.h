@@ -92,6 +92,7 @@ typedef struct {
   int amul_launches;/* number of timed block-multiply launches                                 */
   int last_pos, last_neg; /* sign counts fed to the next call's side rule                      */
   int launches;     /* kernels this call launched (all of them libpsdproj's own)               */
+  int dropped;      /* basis directions dropped at a failing Cholesky pivot (R41)              */
   double phase_ms[8]; /* profile & 2: device time per phase: 0 block multiply, 1 W/P projection,
                          2 Gram/pencil, 3 Cholesky + L^-1 H L^-T, 4 RR eigensolve, 5 rotation,
                          6 residual norms, 7 host round trips / locking / assembly            */
@@ -116,8 +117,11 @@ int psdproj_project(psdproj_ctx ctx, const double* A, int lda, double* Pi, int l
 int psdproj_project_host(psdproj_ctx ctx, const double* A_host, int lda, double* Pi_host, int ldpi,
                          double tol, void* stream, psdproj_info* info);
 
-/* Batched: count independent contexts (one per cone block, possibly different n), issued in
- * order on one stream. Per-item status in infos[i].status; returns the worst status. */
+/* Batched: count independent contexts (one per cone block, possibly different n). The blocks are
+ * driven by up to PSDPROJ_BATCH_THREADS (env, default 8) host threads, each on its own stream
+ * forked from and joined back to `stream` (the latency-bound iterations of different blocks
+ * overlap on the GPU). Distinct ctxs are required. Per-item status in infos[i].status; returns
+ * the worst status (or the first negative error code). */
 int psdproj_project_batched(psdproj_ctx* ctxs, int count, const double* const* A, const int* lda,
                             double* const* Pi, const int* ldpi, const double* tol, void* stream,
                             psdproj_info* infos);

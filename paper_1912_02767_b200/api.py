@@ -10,7 +10,7 @@ import ctypes
 import torch
 
 from . import _lib
-from ._lib import Info, Params, check
+from ._lib import Info, Params, PsdprojError, check
 
 __all__ = ["Context", "default_params", "project_batched", "dgemm", "jacobi", "philox_raw",
            "philox_gauss", "workspace_bytes", "colmajor"]

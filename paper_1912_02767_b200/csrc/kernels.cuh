@@ -681,6 +681,36 @@ __global__ void count_pos_kernel(int s, const double* __restrict__ w, int* __res
 
 __global__ void set_int_kernel(int* p, int v) { *p = v; }
 
+// swap columns i and j of an n-row column-major matrix
+__global__ void swap_cols_kernel(int n, double* __restrict__ X, int ld, int i, int j) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    double a = X[IDX(r, i, ld)];
+    X[IDX(r, i, ld)] = X[IDX(r, j, ld)];
+    X[IDX(r, j, ld)] = a;
+  }
+}
+
+// symmetric permutation of the s x s matrix M: swap rows i, j and columns i, j (one thread per
+// index r handles M[r][i] <-> M[r][j] and then the mirrored entries; the 2 x 2 block is done by r = i)
+__global__ void swap_sym_kernel(int s, double* __restrict__ M, int ld, int i, int j) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < s; r += gridDim.x * blockDim.x) {
+    if (r == i || r == j) continue;
+    double a = M[IDX(r, i, ld)], b = M[IDX(r, j, ld)];
+    M[IDX(r, i, ld)] = b;
+    M[IDX(r, j, ld)] = a;
+    double c = M[IDX(i, r, ld)], d = M[IDX(j, r, ld)];
+    M[IDX(i, r, ld)] = d;
+    M[IDX(j, r, ld)] = c;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    double ii = M[IDX(i, i, ld)], jj = M[IDX(j, j, ld)], ij = M[IDX(i, j, ld)], ji = M[IDX(j, i, ld)];
+    M[IDX(i, i, ld)] = jj;
+    M[IDX(j, j, ld)] = ii;
+    M[IDX(i, j, ld)] = ji;
+    M[IDX(j, i, ld)] = ij;
+  }
+}
+
 __global__ void fill_identity_kernel(int k, double* __restrict__ M, int ld) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < k) M[IDX(i, i, ld)] = 1.0;

@@ -21,6 +21,7 @@
 #include <cstring>
 #include <numeric>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "psdproj.h"
@@ -1118,6 +1119,26 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
       sU = s - ap;  // drop P and retry (R20)
       rc = run.rr(sU, mU, mU, c->d_thU, std::min(mU + qe, sU));
     }
+    // R41: still rank deficient -> drop the direction at the failing pivot (greedy rank-revealing
+    // Cholesky; the oracle's Householder fallback drops the same near-dependent columns)
+    while (rc > 0 && sU > mU) {
+      const int col = rc - 1;  // failing column of the basis (index in S)
+      if (col < mU || col >= sU) return set_err(PSDPROJ_E_DEGENERATE, "Cholesky-QR failed at pivot %d (s=%d)", rc, sU);
+      const int last = sU - 1;
+      if (col != last) {
+        swap_cols_kernel<<<grid1d((size_t)n), 256, 0, st>>>(n, c->S, ld, col, last);
+        CKL();
+        swap_cols_kernel<<<grid1d((size_t)n), 256, 0, st>>>(n, c->BS, ld, col, last);
+        CKL();
+        swap_sym_kernel<<<grid1d((size_t)sU), 256, 0, st>>>(sU, c->G, ldm, col, last);
+        CKL();
+        swap_sym_kernel<<<grid1d((size_t)sU), 256, 0, st>>>(sU, c->Hm, ldm, col, last);
+        CKL();
+      }
+      --sU;
+      info->dropped++;
+      rc = run.rr(sU, mU, mU, c->d_thU, std::min(mU + qe, sU));
+    }
     if (rc > 0) return set_err(PSDPROJ_E_DEGENERATE, "Cholesky-QR failed at pivot %d (s=%d)", rc, sU);
     TRY(rc);
     int mUn = std::min(mU + qe, sU);
@@ -1352,12 +1373,69 @@ extern "C" int psdproj_project_batched(psdproj_ctx* ctxs, int count, const doubl
                                        psdproj_info* infos) {
   if (count < 0 || (count > 0 && (!ctxs || !A || !lda || !Pi || !ldpi || !tol || !infos)))
     return set_err(PSDPROJ_E_INVALID, "invalid batched arguments");
-  int worst = PSDPROJ_OK;
-  for (int i = 0; i < count; ++i) {
-    int rc = psdproj_project(ctxs[i], A[i], lda[i], Pi[i], ldpi[i], tol[i], stream, &infos[i]);
-    if (rc < 0) return rc;
-    worst = std::max(worst, rc);
+  if (count == 0) return PSDPROJ_OK;
+  // Independent blocks are driven by up to PSDPROJ_BATCH_THREADS host threads (default 8), each on
+  // its own stream forked from / joined back to the caller's stream, so the latency-bound
+  // per-iteration work of different blocks overlaps on the GPU.
+  int nth = 8;
+  if (const char* e = getenv("PSDPROJ_BATCH_THREADS")) nth = std::max(1, atoi(e));
+  nth = std::min(nth, count);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (nth == 1) {
+    int worst = PSDPROJ_OK;
+    for (int i = 0; i < count; ++i) {
+      int rc = psdproj_project(ctxs[i], A[i], lda[i], Pi[i], ldpi[i], tol[i], stream, &infos[i]);
+      if (rc < 0) return rc;
+      worst = std::max(worst, rc);
+    }
+    return worst;
   }
+  std::vector<cudaStream_t> ss(nth);
+  std::vector<cudaEvent_t> evs(nth + 1);
+  for (int t = 0; t < nth; ++t) {
+    CK(cudaStreamCreateWithFlags(&ss[t], cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&evs[t], cudaEventDisableTiming));
+  }
+  CK(cudaEventCreateWithFlags(&evs[nth], cudaEventDisableTiming));
+  CK(cudaEventRecord(evs[nth], st));
+  for (int t = 0; t < nth; ++t) CK(cudaStreamWaitEvent(ss[t], evs[nth], 0));
+  std::vector<int> rcs(nth, PSDPROJ_OK);
+  std::vector<std::string> errs(nth);
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  std::vector<std::thread> th;
+  for (int t = 0; t < nth; ++t) {
+    th.emplace_back([&, t]() {
+      cudaSetDevice(dev);
+      int worst = PSDPROJ_OK;
+      for (int i = t; i < count; i += nth) {
+        int rc = psdproj_project(ctxs[i], A[i], lda[i], Pi[i], ldpi[i], tol[i], ss[t], &infos[i]);
+        if (rc < 0) {
+          worst = rc;
+          errs[t] = g_err;
+          break;
+        }
+        worst = std::max(worst, rc);
+      }
+      rcs[t] = worst;
+    });
+  }
+  for (auto& x : th) x.join();
+  int worst = PSDPROJ_OK;
+  for (int t = 0; t < nth; ++t) {
+    CK(cudaEventRecord(evs[t], ss[t]));
+    CK(cudaStreamWaitEvent(st, evs[t], 0));
+  }
+  for (int t = 0; t < nth; ++t) {
+    if (rcs[t] < 0 && worst >= 0) {
+      worst = rcs[t];
+      g_err = errs[t];
+    } else if (worst >= 0) {
+      worst = std::max(worst, rcs[t]);
+    }
+  }
+  for (int t = 0; t <= nth; ++t) cudaEventDestroy(evs[t]);
+  for (int t = 0; t < nth; ++t) cudaStreamDestroy(ss[t]);
   return worst;
 }
 

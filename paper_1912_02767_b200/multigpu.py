@@ -1,0 +1,145 @@
+"""Batch sharding of independent cone blocks across GPUs (BASELINE configs[3]).
+
+The paper projects every PSD block of a block-split SDP independently;
+a batch of independent blocks shards with no data-path collective: each rank owns a fixed subset
+of blocks (and their warm-start contexts) for every ADMM round, and only per-round scalars
+(device time, iteration counts, worst status) cross ranks. One process per GPU; the process
+group is torch.distributed (NCCL on the box, gloo in the CPU tests) and is used only for those
+scalars and for the final gather of statistics.
+
+Host logic only: the projections themselves run through api.project_batched (libpsdproj.so).
+"""
+import heapq
+import time
+
+import numpy as np
+
+
+def block_cost(n, npos):
+    """Relative cost of one warm projection of an n x n block with npos positive eigenvalues:
+    LOBPCG on the smaller side costs ~ n^2 (p + guard) per iteration; a block with
+    min(p, n - p) >= n/3 takes the DIRECT eigensolver path (~ n^3)."""
+    p = min(npos, n - npos)
+    if 3 * p >= n:
+        return float(n) ** 3 / 8.0
+    return float(n) ** 2 * (p + 16)
+
+
+def lpt_partition(costs, world):
+    """Longest-processing-time-first assignment of blocks to ranks. Deterministic: blocks in
+    order of decreasing cost (ties by index), each to the least-loaded rank (ties by rank).
+    Returns (list of block-index lists per rank, per-rank load)."""
+    order = sorted(range(len(costs)), key=lambda i: (-costs[i], i))
+    heap = [(0.0, r) for r in range(world)]
+    heapq.heapify(heap)
+    parts = [[] for _ in range(world)]
+    for i in order:
+        load, r = heapq.heappop(heap)
+        parts[r].append(i)
+        heapq.heappush(heap, (load + costs[i], r))
+    loads = [0.0] * world
+    for r, p in enumerate(parts):
+        loads[r] = sum(costs[i] for i in p)
+        p.sort()
+    return parts, loads
+
+
+def lpt_bound(costs, world):
+    """Graham's bound for LPT: makespan <= (4/3 - 1/(3 world)) OPT, OPT >= max(mean, max cost)."""
+    opt_lb = max(sum(costs) / world, max(costs) if costs else 0.0)
+    return (4.0 / 3.0 - 1.0 / (3.0 * world)) * opt_lb
+
+
+class C4Shard:
+    """The blocks of BASELINE configs[3] (C4) owned by one rank: device matrices, one psdproj
+    context per block (warm state across rounds), and the round-to-round drift."""
+
+    def __init__(self, cfg, block_ids, device, seed=1912, max_iter=500):
+        import torch
+
+        from . import api
+        from workloads.generators import planted
+
+        self.cfg = cfg
+        self.ids = list(block_ids)
+        self.device = device
+        self.mats, self.ctxs, self.outs = [], [], []
+        for i in self.ids:
+            Q, lam = cfg.block(i)
+            A = torch.from_numpy(planted(Q, lam)).to(device)
+            self.mats.append(A)
+            self.outs.append(torch.empty_like(A))
+            prm = api.default_params(max_iter=max_iter, seed=seed, ctx_id=i)
+            self.ctxs.append(api.Context(cfg.sizes[i], params=prm, device=device))
+        self.round = 0
+
+    def drift(self):
+        """A_{r+1} = A_r + 1e-3 sym(G) per block (R32); inputs generated outside timed regions."""
+        import torch
+
+        for k, i in enumerate(self.ids):
+            self.mats[k] += torch.from_numpy(self.cfg.drift(i, self.round)).to(self.device)
+        self.round += 1
+
+    def project(self, tol=None):
+        from . import api
+
+        tol = self.cfg.tol if tol is None else tol
+        _, infos = api.project_batched(self.ctxs, self.mats, [tol] * len(self.ids), outs=self.outs)
+        return infos
+
+    def close(self):
+        for c in self.ctxs:
+            c.close()
+
+
+def shard_c4(cfg, rank, world):
+    costs = [block_cost(n, p) for n, p in zip(cfg.sizes, cfg.npos)]
+    parts, loads = lpt_partition(costs, world)
+    return parts[rank], loads
+
+
+def run_c4(cfg, rank, world, dist, device, rounds, warmup, tol=None):
+    """Sharded C4 rounds on this rank; returns (device ms of the timed rounds, max over ranks),
+    projections done by all ranks, and the per-rank mean LOBPCG iterations."""
+    import torch
+
+    ids, _ = shard_c4(cfg, rank, world)
+    sh = C4Shard(cfg, ids, device)
+    st = torch.cuda.current_stream()
+    for _ in range(warmup):
+        sh.project(tol)
+        sh.drift()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    iters, worst = [], 0
+    ms = 0.0
+    for _ in range(rounds):
+        torch.cuda.synchronize()
+        ev0.record(st)
+        infos = sh.project(tol)
+        ev1.record(st)
+        torch.cuda.synchronize()
+        ms += ev0.elapsed_time(ev1)
+        iters += [i["iters"] for i in infos]
+        worst = max([worst] + [i["status"] for i in infos])
+        sh.drift()  # the next round's inputs, outside the timed region
+    if dist is not None:
+        dist.barrier()
+    t = torch.tensor([ms, float(len(ids) * rounds), float(worst)], dtype=torch.float64, device=device)
+    if dist is not None:
+        mx = t.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = t.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        ms_max, proj, worst = float(mx[0]), float(sm[1]), int(mx[2])
+    else:
+        ms_max, proj = ms, float(len(ids) * rounds)
+    sh.close()
+    return ms_max, proj, (float(np.mean(iters)) if iters else 0.0), worst
+
+
+def wall():
+    return time.perf_counter()

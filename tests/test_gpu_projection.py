@@ -41,3 +41,147 @@ def test_planted_parity(api, n, p, side):
         err = np.linalg.norm(Pi.cpu().numpy() - Pstar)
         assert err / np.linalg.norm(A) <= 1e-9, (call, err, info)
         assert info["err_bound"] >= err - 1e-12 * np.linalg.norm(A)
+
+
+# ---------------------------------------------------------------- edge cases
+@pytest.mark.parametrize("case", ["n1_pos", "n1_neg", "n2_diag", "zero", "minus_identity", "psd", "rank1"])
+def test_edge_cases(api, case):
+    rng = np.random.default_rng(11)
+    if case == "n1_pos":
+        A, expect = np.array([[2.5]]), np.array([[2.5]])
+    elif case == "n1_neg":
+        A, expect = np.array([[-3.0]]), np.zeros((1, 1))
+    elif case == "n2_diag":
+        A, expect = np.diag([1.0, -1.0]), np.diag([1.0, 0.0])
+    elif case == "zero":
+        A = np.zeros((40, 40))
+        expect = A.copy()
+    elif case == "minus_identity":
+        A, expect = -np.eye(50), np.zeros((50, 50))
+    elif case == "psd":
+        M = rng.standard_normal((30, 8))
+        A = M @ M.T
+        expect = A.copy()
+    else:
+        v = rng.standard_normal(64)
+        A = np.outer(v, v) - 0.5 * np.eye(64)
+        expect = project_exact(A)
+    n = A.shape[0]
+    ctx = api.Context(n, seed=5)
+    for call in range(2):  # cold, then warm
+        Pi, info = ctx.project(_dev(A), 1e-10)
+        err = np.linalg.norm(Pi.cpu().numpy() - expect)
+        assert info["status"] in (0, 1), info
+        assert err <= 1e-9 * max(1.0, np.linalg.norm(A)), (case, call, err, info)
+        assert info["err_bound"] >= err - 1e-12
+
+
+def test_nonfinite_input_is_rejected(api):
+    A = np.eye(20)
+    A[3, 7] = A[7, 3] = np.nan
+    ctx = api.Context(20)
+    with pytest.raises(api.PsdprojError if hasattr(api, "PsdprojError") else Exception) as ei:
+        ctx.project(_dev(A), 1e-8)
+    assert "-2" in str(ei.value) or "nan" in str(ei.value).lower()
+
+
+def test_direct_path_mixed_spectrum(api):
+    """Half positive: the one-third rule takes the DIRECT eigensolver."""
+    rng = np.random.default_rng(4)
+    n = 180
+    lam = rng.uniform(-1, 1, n)
+    A = planted(haar_q(rng, n), lam)
+    ctx = api.Context(n, seed=2)
+    ctx.project(_dev(A), 1e-10)      # cold call learns the counts
+    Pi, info = ctx.project(_dev(A), 1e-10)
+    assert info["side"] == 2
+    Pstar = project_exact(A)
+    assert np.linalg.norm(Pi.cpu().numpy() - Pstar) <= 1e-11 * np.linalg.norm(A)
+
+
+def test_host_io_matches_device(api):
+    cfg = C1()
+    seq = drift_sequence(cfg, steps=2)
+    _, A0, _ = next(seq)
+    _, A1, _ = next(seq)
+    dctx = api.Context(cfg.n, params=api.default_params(seed=9))
+    hctx = api.Context(cfg.n, params=api.default_params(seed=9, host_io=1))
+    for A in (A0, A1):
+        Pd, _ = dctx.project(_dev(A), 1e-10)
+        Ph, info = hctx.project_host(torch.from_numpy(A.copy()), 1e-10)
+        assert np.array_equal(Pd.cpu().numpy(), Ph.numpy())
+
+
+def test_determinism_bitwise(api):
+    """Fixed-order reductions (R25): same inputs and seed -> bitwise identical Pi and info."""
+    rng = np.random.default_rng(8)
+    lam = np.concatenate([rng.uniform(0.1, 3, 15), rng.uniform(-3, -0.1, 285)])
+    A = planted(haar_q(rng, 300), lam)
+    outs = []
+    for _ in range(2):
+        ctx = api.Context(300, seed=21)
+        Pi, info = ctx.project(_dev(A), 1e-9)
+        outs.append((Pi.cpu().numpy(), info["iters"], info["err_bound"]))
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert outs[0][1:] == outs[1][1:]
+
+
+def test_c4_batched_parity(api):
+    """BASELINE configs[3] blocks through psdproj_project_batched (threaded, one stream per worker):
+    every block matches the oracle's exact projection and its bound dominates the error."""
+    from workloads.generators import C4
+    cfg = C4(24)
+    ids = list(range(24))
+    mats = [planted(*cfg.block(i)) for i in ids]
+    ctxs = [api.Context(cfg.sizes[i], params=api.default_params(seed=3, ctx_id=i)) for i in ids]
+    for rnd in range(2):
+        outs, infos = api.project_batched(ctxs, [_dev(A) for A in mats], [1e-10] * len(ids))
+        for k, i in enumerate(ids):
+            Pe = project_exact(mats[k])
+            err = np.linalg.norm(outs[k].cpu().numpy() - Pe)
+            nA = np.linalg.norm(mats[k])
+            assert infos[k]["status"] in (0, 1), (i, infos[k])
+            assert err / nA <= 1e-9, (rnd, i, cfg.sizes[i], err / nA, infos[k]["side"])
+            assert infos[k]["err_bound"] >= err - 1e-12 * nA
+        mats = [A + cfg.drift(i, rnd) for A, i in zip(mats, ids)]
+
+
+def test_c3r_reduced_sequence(api):
+    """C3-R at n = 1000 (configs[2] spectrum; closed-form Pi*_t = Q_t max(L, 0) Q_t^T): the
+    returned bound dominates the true error up to the positive eigenvalues the block missed
+    (Theorem 3's perp term, ignored by the paper's bound)."""
+    from workloads.generators import C3R, rotation_sequence
+    cfg = C3R(1000)
+    ctx = api.Context(cfg.n, params=api.default_params(seed=4, max_iter=150))
+    for t, A, Q, lam in rotation_sequence(cfg, steps=3):
+        Pi, info = ctx.project(_dev(A), cfg.tol)
+        Pstar = (Q * np.maximum(lam, 0)) @ Q.T
+        err = np.linalg.norm(Pi.cpu().numpy() - Pstar)
+        pos = np.sort(lam[lam > 0])[::-1]
+        missed = np.sqrt(np.sum(pos[info["npos"]:] ** 2)) if info["npos"] < pos.size else 0.0
+        assert info["npos"] <= pos.size                       # interlacing (PAPER.md:381)
+        assert err <= info["err_bound"] + missed + 1e-9, (t, err, info["err_bound"], missed, info["npos"])
+        assert err / np.linalg.norm(A) <= 1e-4
+
+
+def test_full_size_sampled_entries(api):
+    """BASELINE's full size n = 4000 (the bench workload), one warm C3-R call in the bench's launch
+    configuration: sampled entries of Pi against the closed form, within the Frobenius bound."""
+    from workloads.generators import C3R, rotation_sequence
+    cfg = C3R(4000)
+    ctx = api.Context(cfg.n, params=api.default_params(seed=1912, max_iter=60, profile=3))
+    rng = np.random.default_rng(0)
+    for t, A, Q, lam in rotation_sequence(cfg, steps=2, device="cuda"):
+        Pi, info = ctx.project(A.contiguous(), cfg.tol)
+        if t == 0:
+            continue
+        i = rng.integers(0, cfg.n, 400)
+        j = rng.integers(0, cfg.n, 400)
+        lp = torch.clamp(lam, min=0)
+        ref = ((Q[i] * lp) * Q[j]).sum(dim=1).cpu().numpy()
+        got = Pi[i, j].cpu().numpy()
+        lamc = lam.cpu().numpy()
+        pos = np.sort(lamc[lamc > 0])[::-1]
+        missed = np.sqrt(np.sum(pos[info["npos"]:] ** 2)) if info["npos"] < pos.size else 0.0
+        assert np.abs(got - ref).max() <= info["err_bound"] + missed + 1e-9
+        assert info["launches"] > 0
