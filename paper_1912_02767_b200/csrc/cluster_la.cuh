@@ -271,24 +271,26 @@ __global__ void __launch_bounds__(CLA_NT) cholesky_cluster_kernel(int t, double*
 // applied lazily, fused with the matrix-vector product of step j (one pass over the own columns
 // per step), except for column j, which the owner's warp 0 updates eagerly before forming the
 // Householder vector of step j. Step j:
-//   owner(j), warp 0:  column j <- step j-1 update; Householder vector v_j, tau_j -> vloc[par]
+//   owner(j), warp 0: column j <- step j-1 update; Householder v_j, tau_j; v_j[i] is stored into
+//                     CTA (i % CS)'s vloc (DSMEM stores), tau_j into every CTA's vloc[j]
 //   B1 (cluster barrier)
-//   all:  v_j, tau_j <- owner's vloc[par] (DSMEM)
-//         for own g > j: A[:, g] -= v' a'_g + p' v'_g (step j-1: a' = p'_g - 2 K' v'_g);
-//                        p_g = tau_j A[:, g] . v_j; per-warp partials of p . v_j
+//   all:  v_j <- gather of the interleaved pieces (DSMEM), so no CTA's port serves the broadcast
+//         rows split over the threads: for own columns g > j, A[r, g] -= v'_r a'_g + p'_r v'_g
+//         (step j-1, a' = p'_g - 2 K' v'_g) and partial dots A[r, g] v_j[r]; column sums -> p_g
 //   B2
-//   all:  ploc[par] <- p (DSMEM gather); warp 0: K_j = tau_j / 2 * sum(partials)
+//   all:  p_j <- gather (DSMEM); K_j = tau_j / 2 * sum of the CTAs' partials of p.v_j
+// (Column sums are reduced in a fixed order: results are deterministic.)
+constexpr int TRI_CB = 8;  // own columns processed per batch (independent reduction chains)
 __host__ __device__ inline size_t tri_smem_doubles(int s, int CS) {
-  return (size_t)cdiv(s, CS) * s + 5 * (size_t)s + 3 * (size_t)cdiv(s, CS) + 2 * 32 + 16 + 160;
+  return (size_t)cdiv(s, CS) * s + 5 * (size_t)s + 3 * (size_t)cdiv(s, CS) + 16 * (size_t)(cdiv(s, CS) + TRI_CB) + 2 * 32 +
+         16;
+}
+// GA = true (s too large for the cluster's shared memory): the own columns live in the global
+// scratch gA (L2-resident; CS * cdiv(s, CS) * s doubles), everything else as above.
+__host__ __device__ inline size_t tri_smem_doubles_ga(int s, int CS) {
+  return 5 * (size_t)s + 3 * (size_t)cdiv(s, CS) + 16 * (size_t)(cdiv(s, CS) + TRI_CB) + 2 * 32 + 16 + 1300;
 }
 
-// PL = rows per lane (s <= 32 PL): the row vectors of a step (v', p' of the pending update and
-// v_j) are held in registers, so each own column costs PL independent smem loads and stores.
-// GA = true (s too large for the cluster's shared memory): the own columns live in the global
-// scratch gA (L2-resident; CS * cdiv(s, CS) * s doubles + tail pad), everything else as above.
-__host__ __device__ inline size_t tri_smem_doubles_ga(int s, int CS) {
-  return 5 * (size_t)s + 3 * (size_t)cdiv(s, CS) + 2 * 32 + 16 + 1300;  // row overrun of PL = 40
-}
 template <int PL, int TNT, bool GA = false>
 __global__ void __launch_bounds__(TNT) tridiag_cluster_kernel(int s, const double* __restrict__ A, int lda,
                                                                   double* __restrict__ d, double* __restrict__ e,
@@ -297,7 +299,6 @@ __global__ void __launch_bounds__(TNT) tridiag_cluster_kernel(int s, const doubl
                                                                   double* __restrict__ gA) {
   extern __shared__ __align__(16) double sm[];
   __shared__ double Kbuf[2];
-  __shared__ double wsum[2];
   long long pt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long tprev = 0;
 #define TRI_T(k)                  \
@@ -311,16 +312,14 @@ __global__ void __launch_bounds__(TNT) tridiag_cluster_kernel(int s, const doubl
   const int ncl = cdiv(s, CS);
   double* Al = GA ? gA + (size_t)rank * ncl * s : sm;  // ncl x s, own columns
   double* vloc = GA ? sm : Al + (size_t)ncl * s;        // 2 x s (parity): [tau_j at index j | v_j at j+1..s-1]
-  double* ploc = vloc + 2 * (size_t)s;  // 2 x s (parity): gathered p_j (all rows)
-  double* pbuf = ploc + 2 * (size_t)s;  // own entries of p_j (global column index), read remotely
-  double* wpart = pbuf + s;             // per-warp partials of p.v (32)
-  double* dl = wpart + 64;              // d, e, tau of own columns (local column index); written out at the end
+  double* ploc = vloc + 2 * (size_t)s;                  // 2 x s (parity): gathered p_j (all rows)
+  double* pbuf = ploc + 2 * (size_t)s;                  // own entries of p_j (global column index), read remotely
+  double* wpart = pbuf + s;                             // 2 x 32: per-warp partials of p.v (parity)
+  double* dl = wpart + 64;                              // d, e, tau of own columns (written out at the end)
   double* el = dl + ncl;
   double* tl = el + ncl;
   const int tid = threadIdx.x, NT = blockDim.x;
   const int warp = tid >> 5, lane = tid & 31, nw = NT >> 5;
-  // every row loop below reads whole 32-row groups unconditionally (rows >= s hit later arrays or
-  // the 160-double tail pad; they are multiplied by zero and never stored), so smem starts zeroed
   if (GA) {
     for (size_t q = tid; q < tri_smem_doubles_ga(s, CS); q += NT) sm[q] = 0.0;
   } else {
@@ -331,6 +330,7 @@ __global__ void __launch_bounds__(TNT) tridiag_cluster_kernel(int s, const doubl
     Al[q] = (g < s) ? 0.5 * (A[IDX(i, g, lda)] + A[IDX(g, i, lda)]) : 0.0;
   }
   __syncthreads();
+  cla_cluster_sync();  // every CTA is running before the first DSMEM store
   if (prof && threadIdx.x == 0) tprev = clock64();
   for (int j = 0; j + 2 < s; ++j) {
     const int owner = j % CS, par = j & 1, pp = par ^ 1;
@@ -384,79 +384,79 @@ __global__ void __launch_bounds__(TNT) tridiag_cluster_kernel(int s, const doubl
         dl[j / CS] = dj;
         el[j / CS] = beta;
         tl[j / CS] = tj;
-        vb[j] = tj;
       }
+      if (lane < CS) *cla_remote(vb + j, (unsigned)lane) = tj;
 #pragma unroll
-      for (int q = 0; q < PL; ++q) {  // v_j -> broadcast buffer and (reflector storage) column j
+      for (int q = 0; q < PL; ++q) {  // v_j -> its interleaved holders, and (reflector storage) column j
         const int i = j + lane + 32 * q;
         if (i > j && i < s) {
           const double v = (i == j + 1) ? 1.0 : x[q] * scale;
-          vb[i] = v;
+          *cla_remote(vb + i, (unsigned)(i & (CS - 1))) = v;
           col[i] = v;
         }
       }
     }
     TRI_T(0);
-    cla_cluster_sync();  // B1: v_j, tau_j visible; step j-1 finished everywhere
+    cla_cluster_sync();  // B1: v_j pieces and tau_j visible; step j-1 finished everywhere
     TRI_T(1);
     double* vj = vloc + (size_t)par * s;
-    if ((int)rank != owner) {
-      const double* ov = cla_remote(vj, (unsigned)owner);
-      int i = j + tid;
+    {
+      int i = j + 1 + tid;
       for (; i + NT < s; i += 2 * NT) {
-        const double a = ov[i], b = ov[i + NT];
+        const int r0 = i & (CS - 1), r1 = (i + NT) & (CS - 1);
+        const double a = (r0 == (int)rank) ? vj[i] : *cla_remote(vj + i, (unsigned)r0);
+        const double b = (r1 == (int)rank) ? vj[i + NT] : *cla_remote(vj + i + NT, (unsigned)r1);
         vj[i] = a;
         vj[i + NT] = b;
       }
-      if (i < s) vj[i] = ov[i];
+      if (i < s) {
+        const int r0 = i & (CS - 1);
+        if (r0 != (int)rank) vj[i] = *cla_remote(vj + i, (unsigned)r0);
+      }
     }
     __syncthreads();
     TRI_T(2);
     const double tj = vj[j];
     const double Kp = pend ? Kbuf[pp] : 0.0;
-    // row vectors in registers: rows i = j + 1 + lane + 32 q (rows >= s read finite padding, masked)
-    double rv[PL], rp[PL], rj[PL];
+    // column per warp, rows i = j + 1 + lane + 32 q (rows >= s read finite padding and are masked):
+    // v_j in registers, v' and p' of the pending update re-read per column
+    double rj[PL];
+    const double* vpr = vloc + (size_t)pp * s + j + 1 + lane;
+    const double* pqr = ploc + (size_t)pp * s + j + 1 + lane;
     {
-      const double* vp = vloc + (size_t)pp * s + j + 1 + lane;
-      const double* pq = ploc + (size_t)pp * s + j + 1 + lane;
       const double* vv = vj + j + 1 + lane;
-      const double pm = pend ? 1.0 : 0.0;
 #pragma unroll
-      for (int q = 0; q < PL; ++q) {
-        const bool ok = j + 1 + lane + 32 * q < s;
-        rv[q] = ok ? pm * vp[32 * q] : 0.0;
-        rp[q] = ok ? pm * pq[32 * q] : 0.0;
-        rj[q] = ok ? vv[32 * q] : 0.0;
-      }
+      for (int q = 0; q < PL; ++q) rj[q] = (j + 1 + lane + 32 * q < s) ? vv[32 * q] : 0.0;
     }
     const int lc0 = (j + 1 > (int)rank) ? (j + 1 - (int)rank + CS - 1) / CS : 0;
     double part = 0.0;
     for (int lc = lc0 + warp; lc < ncl; lc += nw) {
       const int g = (int)rank + CS * lc;
       if (g >= s) break;
-      double* col = Al + (size_t)lc * s;
-      double bg = 0.0, ag = 0.0;
-      if (pend) {
-        bg = vloc[(size_t)pp * s + g];
-        ag = ploc[(size_t)pp * s + g] - 2.0 * Kp * bg;
-      }
-      double x[PL];
-      double* cp = col + j + 1 + lane;
-#pragma unroll
-      for (int q = 0; q < PL; ++q) x[q] = cp[32 * q];
+      double* cp = Al + (size_t)lc * s + j + 1 + lane;
       double a0 = 0.0, a1 = 0.0;
-#pragma unroll
-      for (int q = 0; q < PL; ++q) {
-        x[q] = fma(-rv[q], ag, fma(-rp[q], bg, x[q]));
-        if (q & 1)
-          a1 = fma(x[q], rj[q], a1);
-        else
-          a0 = fma(x[q], rj[q], a0);
-      }
       if (pend) {
+        const double bg = vloc[(size_t)pp * s + g];
+        const double ag = ploc[(size_t)pp * s + g] - 2.0 * Kp * bg;
+        double x[PL];
 #pragma unroll
-        for (int q = 0; q < PL; ++q)
+        for (int q = 0; q < PL; ++q) x[q] = fma(-vpr[32 * q], ag, fma(-pqr[32 * q], bg, cp[32 * q]));
+#pragma unroll
+        for (int q = 0; q < PL; ++q) {
+          if (q & 1)
+            a1 = fma(x[q], rj[q], a1);
+          else
+            a0 = fma(x[q], rj[q], a0);
           if (j + 1 + lane + 32 * q < s) cp[32 * q] = x[q];
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < PL; ++q) {
+          if (q & 1)
+            a1 = fma(cp[32 * q], rj[q], a1);
+          else
+            a0 = fma(cp[32 * q], rj[q], a0);
+        }
       }
       double acc = a0 + a1;
 #pragma unroll
@@ -465,16 +465,9 @@ __global__ void __launch_bounds__(TNT) tridiag_cluster_kernel(int s, const doubl
       if (lane == 0) pbuf[g] = acc;
       part = fma(acc, vj[g], part);
     }
-    if (lane == 0) wpart[warp] = part;
-    __syncthreads();
-    if (warp == 0) {
-      double pv = (lane < nw) ? wpart[lane] : 0.0;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) pv += __shfl_xor_sync(0xffffffffu, pv, o);
-      if (lane == 0) wsum[par] = pv;
-    }
+    if (lane == 0) wpart[par * 32 + warp] = part;
     TRI_T(3);
-    cla_cluster_sync();  // B2: p_j entries and per-CTA partial sums visible
+    cla_cluster_sync();  // B2: p_j entries and partials visible
     TRI_T(4);
     double* pj = ploc + (size_t)par * s;
     {
@@ -488,7 +481,8 @@ __global__ void __launch_bounds__(TNT) tridiag_cluster_kernel(int s, const doubl
       if (i < s) pj[i] = *cla_remote(pbuf + i, (unsigned)(i & (CS - 1)));
     }
     if (warp == nw - 1) {
-      double pv = (lane < CS) ? *cla_remote(wsum + par, (unsigned)lane) : 0.0;
+      double pv = 0.0;
+      for (int q = lane; q < nw * CS; q += 32) pv += *cla_remote(wpart + par * 32 + (q % nw), (unsigned)(q / nw));
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) pv += __shfl_xor_sync(0xffffffffu, pv, o);
       if (lane == 0) Kbuf[par] = 0.5 * tj * pv;

@@ -424,7 +424,7 @@ static int eigh_top(cudaStream_t st, int s, const double* Hs, int ldh, int m, do
     CK(cudaStreamSynchronize(st));
     CK(cudaMemcpy(h, dprof, sizeof(h), cudaMemcpyDeviceToHost));
     for (int r = 0; r < std::min(tcs, 3); ++r)
-      fprintf(stderr, "tri prof s=%d cs=%d rank %d: house %lld B1 %lld vcopy %lld fused %lld B2 %lld gatherK %lld sync %lld (cycles/step)\n",
+      fprintf(stderr, "tri prof s=%d cs=%d rank %d: house %lld B1 %lld vgather %lld cols %lld B2 %lld gatherK %lld sync %lld (cycles/step)\n",
               s, tcs, r, h[r * 8 + 0] / (s - 2), h[r * 8 + 1] / (s - 2), h[r * 8 + 2] / (s - 2), h[r * 8 + 3] / (s - 2),
               h[r * 8 + 4] / (s - 2), h[r * 8 + 5] / (s - 2), h[r * 8 + 6] / (s - 2));
   }
