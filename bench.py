@@ -390,8 +390,9 @@ def main():
             "step_roofline": {"frac": step_frac, "t_roof_ms": t_roof * 1e3 / K, "flops": flops / K,
                               "bytes": byts / K, "definition": "max(bytes/HBM, flops/P64) / step time"},
             "phase_ms_per_step": {nm: round(sum(i["phase_ms"][k] for i in infos) / K, 3) for k, nm in enumerate(
-                ["a3_block_multiply", "w_p_projection", "gram_pencil", "cholesky_pencil", "rr_eigensolve",
-                 "rotation", "residual_norms", "host_locking_assembly"])},
+                ["a3_block_multiply", "w_p_projection", "gram_pencil", "cholesky_pencil", "rr_tridiagonal",
+                 "rotation", "residual_norms", "host_locking_assembly", "rr_bisection", "rr_inverse_iteration",
+                 "rr_back_transform", "rr_reorth_and_coeffs"])},
             "iters_per_projection": {"mean": statistics.mean(iters), "min": min(iters), "max": max(iters),
                                      "cold": infos_warm[0]["iters"]},
             "status": [i["status"] for i in infos],

@@ -93,9 +93,11 @@ typedef struct {
   int last_pos, last_neg; /* sign counts fed to the next call's side rule                      */
   int launches;     /* kernels this call launched (all of them libpsdproj's own)               */
   int dropped;      /* basis directions dropped at a failing Cholesky pivot (R41)              */
-  double phase_ms[8]; /* profile & 2: device time per phase: 0 block multiply, 1 W/P projection,
-                         2 Gram/pencil, 3 Cholesky + L^-1 H L^-T, 4 RR eigensolve, 5 rotation,
-                         6 residual norms, 7 host round trips / locking / assembly            */
+  double phase_ms[12]; /* profile & 2: device time per phase: 0 block multiply, 1 W/P projection,
+                         2 Gram/pencil, 3 Cholesky + L^-1 H L^-T, 4 RR tridiagonalisation,
+                         5 rotation, 6 residual norms, 7 host round trips / locking / assembly,
+                         8 RR bisection, 9 RR inverse iteration, 10 RR back-transformation,
+                         11 RR re-orthonormalisation + C' = L^-T Y                          */
 } psdproj_info;
 
 /* Fill *p with the defaults documented above. */

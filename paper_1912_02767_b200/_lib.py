@@ -43,7 +43,7 @@ class Info(ctypes.Structure):
         ("flops", ctypes.c_double), ("bytes", ctypes.c_double), ("amul_flops", ctypes.c_double),
         ("amul_bytes", ctypes.c_double), ("amul_ms", ctypes.c_double), ("amul_launches", ctypes.c_int),
         ("last_pos", ctypes.c_int), ("last_neg", ctypes.c_int), ("launches", ctypes.c_int),
-        ("dropped", ctypes.c_int), ("phase_ms", ctypes.c_double * 8),
+        ("dropped", ctypes.c_int), ("phase_ms", ctypes.c_double * 12),
     ]
 
     def as_dict(self):

@@ -21,6 +21,7 @@
 #include <cooperative_groups.h>
 
 #include "common.cuh"
+#include "gemm.cuh"  // cp.async helpers
 
 namespace psd {
 
@@ -79,16 +80,22 @@ __host__ __device__ inline size_t chol_smem_doubles(int t, int CS) {
 // L_bb = chol(D) (every thread computes the 8 x 8 factor redundantly in registers) and
 // L_B = B L_bb^-T (row-parallel), so a panel costs one CTA barrier; one cluster barrier publishes
 // it; every CTA copies it (DSMEM) and applies the rank-CHOL_NB update to its own later columns.
+// GA = true (t too large for shared memory): the own columns live in the L2-resident global scratch
+// gA (CS * chol_local_cols(t, CS) * t doubles); panels are still exchanged through DSMEM.
+__host__ __device__ inline size_t chol_smem_doubles_ga(int t, int CS) { return (size_t)CHOL_NB * t + 16; }
+template <bool GA = false>
 __global__ void __launch_bounds__(CLA_NT) cholesky_cluster_kernel(int t, double* __restrict__ G, int ld,
-                                                                   double fail_rel, int* __restrict__ status) {
+                                                                   double fail_rel, int* __restrict__ status,
+                                                                   double* __restrict__ gA) {
   extern __shared__ __align__(16) double sm[];
   __shared__ double red[33];
+  __shared__ double xchs[4];
   const int CS = (int)gridDim.x;
   const unsigned rank = cla_rank();
   const int ncl = chol_local_cols(t, CS);
-  double* Al = sm;                      // ncl x t: local column lc = lb * NB + c <-> global (lb * CS + rank) * NB + c
-  double* pl = Al + (size_t)ncl * t;    // NB x t: local copy of the current panel
-  double* xch = pl + (size_t)CHOL_NB * t;  // [0] max diag part, [1..2] status of panel by parity
+  double* Al = GA ? gA + (size_t)rank * ncl * t : sm;  // ncl x t: local column lc = lb * NB + c <-> global (lb * CS + rank) * NB + c
+  double* pl = GA ? sm : Al + (size_t)ncl * t;          // NB x t: local copy of the current panel
+  double* xch = xchs;                      // [0] max diag part, [1..2] status of panel by parity
   const int tid = threadIdx.x, NT = blockDim.x;
   const int warp = tid >> 5, lane = tid & 31, nw = NT >> 5;
   auto gcol = [&](int lc) { return ((lc / CHOL_NB) * CS + (int)rank) * CHOL_NB + (lc % CHOL_NB); };
@@ -204,7 +211,8 @@ __global__ void __launch_bounds__(CLA_NT) cholesky_cluster_kernel(int t, double*
     }
     if (jn >= t) break;
     {
-      const double* P = cla_remote(Al + (size_t)(b / CS) * CHOL_NB * t, (unsigned)owner);
+      const double* P = GA ? gA + ((size_t)owner * ncl + (size_t)(b / CS) * CHOL_NB) * t
+                           : cla_remote(Al + (size_t)(b / CS) * CHOL_NB * t, (unsigned)owner);
       const int len = t - jn, tot = jb * len;
       int e = tid;
       for (; e + 3 * NT < tot; e += 4 * NT) {
@@ -296,7 +304,7 @@ __global__ void __launch_bounds__(TNT) tridiag_cluster_kernel(int s, const doubl
                                                                   double* __restrict__ d, double* __restrict__ e,
                                                                   double* __restrict__ tau, double* __restrict__ Vh,
                                                                   int ldv, long long* __restrict__ prof,
-                                                                  double* __restrict__ gA) {
+                                                                  double* __restrict__ gA, int dbg) {
   extern __shared__ __align__(16) double sm[];
   __shared__ double Kbuf[2];
   long long pt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -430,7 +438,7 @@ __global__ void __launch_bounds__(TNT) tridiag_cluster_kernel(int s, const doubl
     }
     const int lc0 = (j + 1 > (int)rank) ? (j + 1 - (int)rank + CS - 1) / CS : 0;
     double part = 0.0;
-    for (int lc = lc0 + warp; lc < ncl; lc += nw) {
+    for (int lc = lc0 + warp; lc < ncl && !(dbg & 1); lc += nw) {
       const int g = (int)rank + CS * lc;
       if (g >= s) break;
       double* cp = Al + (size_t)lc * s + j + 1 + lane;
@@ -547,9 +555,11 @@ constexpr int BT_PER_LANE = 40;  // s <= 1280
 template <int PL>
 __global__ void __launch_bounds__(256) backtransform_panel_kernel(int s, int m, const double* __restrict__ Vh, int ldv,
                                                                   const double* __restrict__ tau,
-                                                                  double* __restrict__ y, int ldy) {
-  extern __shared__ __align__(16) double pv[];  // BT_PB x s
-  __shared__ double ptau[BT_PB];
+                                                                  double* __restrict__ y, int ldy, int PB) {
+  // two panel buffers (PB <= BT_PB reflectors x s each): panel k+1 streams in with cp.async while
+  // panel k is applied
+  extern __shared__ __align__(16) double pv[];
+  __shared__ double ptau[2][BT_PB];
   const int lane = threadIdx.x & 31;
   const int col = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const bool active = col < m;
@@ -560,36 +570,58 @@ __global__ void __launch_bounds__(256) backtransform_panel_kernel(int s, int m, 
     int k = lane + 32 * q;
     r[q] = (active && k < s) ? yc[k] : 0.0;
   }
-  const int nref = s - 2;  // reflectors 0 .. s-3
-  for (int hi = nref - 1; hi >= 0; hi -= BT_PB) {
-    const int lo = max(0, hi - BT_PB + 1);
-    __syncthreads();
-    for (int q = threadIdx.x; q < (hi - lo + 1) * s; q += blockDim.x) {
-      int c = q / s, i = q - c * s, j = lo + c;
-      pv[(size_t)c * s + i] = (i > j) ? __ldg(Vh + IDX(i, j, ldv)) : 0.0;
+  const int nref = s - 2;  // reflectors 0 .. s-3, applied from the last one down
+  const int npan = cdiv(max(nref, 0), PB);
+  auto issue = [&](int pnl, int buf) {
+    const int hi = nref - 1 - pnl * PB, lo = max(0, hi - PB + 1);
+    double* dst = pv + (size_t)buf * PB * s;
+    for (int c = 0; c <= hi - lo; ++c) {
+      const int j = lo + c;
+      for (int i = threadIdx.x; i < s; i += blockDim.x)
+        cp_async_8(dst + (size_t)c * s + i, Vh + IDX(i, j, ldv), (i > j) ? 8 : 0);  // zero-fill rows <= j
     }
-    if (threadIdx.x < hi - lo + 1) ptau[threadIdx.x] = __ldg(tau + lo + threadIdx.x);
+    if (threadIdx.x <= hi - lo) ptau[buf][threadIdx.x] = __ldg(tau + lo + threadIdx.x);
+    cp_async_commit();
+  };
+  if (npan > 0) issue(0, 0);
+  for (int pnl = 0; pnl < npan; ++pnl) {
+    const int buf = pnl & 1;
+    if (pnl + 1 < npan) {
+      issue(pnl + 1, buf ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
     __syncthreads();
-    if (!active) continue;
-    for (int j = hi; j >= lo; --j) {
-      const double tj = ptau[j - lo];
-      if (tj == 0.0) continue;
-      const double* v = pv + (size_t)(j - lo) * s;
-      double acc = 0.0;
+    const int hi = nref - 1 - pnl * PB, lo = max(0, hi - PB + 1);
+    if (active) {
+      for (int j = hi; j >= lo; --j) {
+        const double tj = ptau[buf][j - lo];
+        if (tj == 0.0) continue;
+        const double* v = pv + (size_t)buf * PB * s + (size_t)(j - lo) * s;
+        double a0 = 0.0, a1 = 0.0;
 #pragma unroll
-      for (int q = 0; q < PL; ++q) {
-        int k = lane + 32 * q;
-        if (k < s) acc = fma(v[k], r[q], acc);
-      }
+        for (int q = 0; q < PL; ++q) {
+          int k = lane + 32 * q;
+          if (k < s) {
+            if (q & 1)
+              a1 = fma(v[k], r[q], a1);
+            else
+              a0 = fma(v[k], r[q], a0);
+          }
+        }
+        double acc = a0 + a1;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      acc *= tj;
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        acc *= tj;
 #pragma unroll
-      for (int q = 0; q < PL; ++q) {
-        int k = lane + 32 * q;
-        if (k < s) r[q] = fma(-acc, v[k], r[q]);
+        for (int q = 0; q < PL; ++q) {
+          int k = lane + 32 * q;
+          if (k < s) r[q] = fma(-acc, v[k], r[q]);
+        }
       }
     }
+    __syncthreads();  // buffer `buf` is refilled by the next issue
   }
   if (!active) return;
 #pragma unroll
@@ -650,6 +682,146 @@ __global__ void __launch_bounds__(256) trinv_panel_kernel(int t, const double* _
   for (int q = 0; q < PL; ++q) {
     const int i = lane + 32 * q;
     if (i < t) Li[IDX(i, j, ldi)] = x[q];
+  }
+}
+
+// Blocked back-transformation with the compact WY form (LAPACK dlarft/dlarfb): the reflectors of
+// panel p (columns lo..hi, hi - lo + 1 <= WY_PB) satisfy H_lo ... H_hi = I - V T V^T with T upper
+// triangular. larft_kernel builds every panel's T in parallel (one CTA per panel); the apply kernel
+// walks the panels from the last to the first, Y <- (I - V T V^T) Y: per panel and column, WY_PB
+// independent dot products (one interleaved warp reduction) instead of WY_PB dependent ones.
+constexpr int WY_PB = 16;
+__global__ void __launch_bounds__(256) larft_kernel(int s, const double* __restrict__ Vh, int ldv,
+                                                    const double* __restrict__ tau, double* __restrict__ Tb) {
+  __shared__ double G[WY_PB][WY_PB + 1];
+  __shared__ double T[WY_PB][WY_PB + 1];
+  const int nref = s - 2;
+  const int p = blockIdx.x;
+  const int lo = p * WY_PB, kb = min(WY_PB, nref - lo);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  // Gram of the panel columns (upper triangle incl. diagonal), v_c zero at rows <= lo + c
+  for (int pr = warp; pr < kb * kb; pr += nw) {
+    const int a = pr % kb, b = pr / kb;
+    if (a > b) continue;
+    const int j0 = lo + b;  // column b is nonzero from row j0 + 1
+    double acc = 0.0;
+    for (int i = j0 + 1 + lane; i < s; i += 32) acc = fma(__ldg(Vh + IDX(i, lo + a, ldv)), __ldg(Vh + IDX(i, j0, ldv)), acc);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) G[a][b] = acc;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {  // T(0:i-1, i) = T(0:i-1, 0:i-1) (-tau_i G(0:i-1, i)), one lane per row
+    const int r = lane;
+    for (int i = 0; i < kb; ++i) {
+      const double ti = __ldg(tau + lo + i);
+      T[r < WY_PB ? r : 0][i] = 0.0;
+      __syncwarp();
+      // w_r <- sum_{c = r..i-1} T[r][c] (-tau_i G[c][i])
+      double acc = 0.0;
+      for (int c = r; c < i; ++c) acc = fma(T[r][c], -ti * G[c][i], acc);
+      __syncwarp();
+      if (r < i) T[r][i] = acc;
+      if (r == i) T[r][i] = ti;
+      __syncwarp();
+    }
+    for (int e = lane; e < WY_PB * WY_PB; e += 32) {
+      const int a = e % WY_PB, b = e / WY_PB;
+      Tb[(size_t)p * WY_PB * WY_PB + e] = (a < kb && b < kb && a <= b) ? T[a][b] : 0.0;
+    }
+  }
+}
+
+template <int PL>
+__global__ void __launch_bounds__(256) backtransform_wy_kernel(int s, int m, const double* __restrict__ Vh, int ldv,
+                                                               const double* __restrict__ Tb,
+                                                               double* __restrict__ y, int ldy) {
+  // two panel buffers (WY_PB x 32 PL each, rows >= s zero) + T, streamed with cp.async
+  extern __shared__ __align__(16) double pv[];
+  const int LDP = 32 * PL;
+  double* Ts = pv + (size_t)2 * WY_PB * LDP;  // 2 x WY_PB x WY_PB
+  double* wsm = Ts + 2 * WY_PB * WY_PB;       // per warp: 32 WY_PB partials + w + z
+  const int lane = threadIdx.x & 31;
+  const int col = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const bool active = col < m;
+  double* yc = y + (size_t)(active ? col : 0) * ldy;
+  double r[PL];
+#pragma unroll
+  for (int q = 0; q < PL; ++q) {
+    const int k = lane + 32 * q;
+    r[q] = (active && k < s) ? yc[k] : 0.0;
+  }
+  const int nref = s - 2;
+  const int npan = cdiv(max(nref, 0), WY_PB);
+  auto issue = [&](int pnl, int buf) {
+    const int lo = pnl * WY_PB, kb = min(WY_PB, nref - lo);
+    double* dst = pv + (size_t)buf * WY_PB * LDP;
+    for (int e = threadIdx.x; e < WY_PB * LDP; e += blockDim.x) {
+      const int c = e / LDP, i = e - c * LDP, j = lo + c;
+      const bool ok = c < kb && i > j && i < s;
+      cp_async_8(dst + e, ok ? Vh + IDX(i, j, ldv) : Vh, ok ? 8 : 0);
+    }
+    for (int e = threadIdx.x; e < WY_PB * WY_PB; e += blockDim.x)
+      cp_async_8(Ts + (size_t)buf * WY_PB * WY_PB + e, Tb + (size_t)pnl * WY_PB * WY_PB + e, 8);
+    cp_async_commit();
+  };
+  if (npan > 0) issue(npan - 1, (npan - 1) & 1);
+  for (int pnl = npan - 1; pnl >= 0; --pnl) {
+    const int buf = pnl & 1;
+    if (pnl > 0) {
+      issue(pnl - 1, buf ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    if (active) {
+      const double* V = pv + (size_t)buf * WY_PB * LDP;
+      const double* T = Ts + (size_t)buf * WY_PB * WY_PB;
+      double* wp = wsm + (size_t)(threadIdx.x >> 5) * (32 * (WY_PB + 1) + 2 * WY_PB);  // [lane][c] partials (ld 17), w, z
+      // lane partials of w_c = v_c . y (c loop kept rolled: bounded registers)
+#pragma unroll 1
+      for (int c = 0; c < WY_PB; ++c) {
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+        for (int q = 0; q < PL; ++q) {
+          const double vv = V[(size_t)c * LDP + lane + 32 * q];
+          if (q & 1)
+            a1 = fma(vv, r[q], a1);
+          else
+            a0 = fma(vv, r[q], a0);
+        }
+        wp[lane * (WY_PB + 1) + c] = a0 + a1;
+      }
+      __syncwarp();
+      if (lane < WY_PB) {  // w_c = sum over lanes (fixed order)
+        double acc = 0.0;
+#pragma unroll 8
+        for (int l = 0; l < 32; ++l) acc += wp[l * (WY_PB + 1) + lane];
+        wp[32 * (WY_PB + 1) + lane] = acc;
+      }
+      __syncwarp();
+      if (lane < WY_PB) {  // z = T w (T upper triangular, column-major)
+        double acc = 0.0;
+        for (int bcol = lane; bcol < WY_PB; ++bcol) acc = fma(T[lane + bcol * WY_PB], wp[32 * (WY_PB + 1) + bcol], acc);
+        wp[32 * (WY_PB + 1) + WY_PB + lane] = acc;
+      }
+      __syncwarp();
+#pragma unroll 1
+      for (int c = 0; c < WY_PB; ++c) {
+        const double zc = wp[32 * (WY_PB + 1) + WY_PB + c];
+#pragma unroll
+        for (int q = 0; q < PL; ++q) r[q] = fma(-V[(size_t)c * LDP + lane + 32 * q], zc, r[q]);
+      }
+      __syncwarp();
+    }
+    __syncthreads();  // buffer `buf` is refilled by the next issue
+  }
+  if (!active) return;
+#pragma unroll
+  for (int q = 0; q < PL; ++q) {
+    const int k = lane + 32 * q;
+    if (k < s) yc[k] = r[q];
   }
 }
 

@@ -308,14 +308,19 @@ static int cla_attrs() {
   CK(cudaFuncSetAttribute(tridiag_cluster_kernel<14, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   CK(cudaFuncSetAttribute(tridiag_cluster_kernel<20, 256>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   CK(cudaFuncSetAttribute(tridiag_cluster_kernel<20, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-  CK(cudaFuncSetAttribute(cholesky_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-  CK(cudaFuncSetAttribute(cholesky_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  CK(cudaFuncSetAttribute(cholesky_cluster_kernel<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  CK(cudaFuncSetAttribute(cholesky_cluster_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  CK(cudaFuncSetAttribute(cholesky_cluster_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  CK(cudaFuncSetAttribute(cholesky_cluster_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   const int tmx = (int)(TI_KB * 32 * 40 * sizeof(double));
   CK(cudaFuncSetAttribute(trinv_panel_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, tmx));
   CK(cudaFuncSetAttribute(trinv_panel_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, tmx));
   CK(cudaFuncSetAttribute(trinv_panel_kernel<24>, cudaFuncAttributeMaxDynamicSharedMemorySize, tmx));
   CK(cudaFuncSetAttribute(trinv_panel_kernel<40>, cudaFuncAttributeMaxDynamicSharedMemorySize, tmx));
-  const int bmx = (int)(BT_PB * 32 * BT_PER_LANE * sizeof(double));
+  const int bmx = CLA_SMEM_BYTES;
+  CK(cudaFuncSetAttribute(backtransform_wy_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, bmx));
+  CK(cudaFuncSetAttribute(backtransform_wy_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, bmx));
+  CK(cudaFuncSetAttribute(backtransform_wy_kernel<20>, cudaFuncAttributeMaxDynamicSharedMemorySize, bmx));
   CK(cudaFuncSetAttribute(backtransform_panel_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, bmx));
   CK(cudaFuncSetAttribute(backtransform_panel_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, bmx));
   CK(cudaFuncSetAttribute(backtransform_panel_kernel<24>, cudaFuncAttributeMaxDynamicSharedMemorySize, bmx));
@@ -325,11 +330,16 @@ static int cla_attrs() {
 }
 
 // L = chol(G) in place (t x t, ld); status = failing pivot + 1 or 0 (a6, R20)
-static int cholesky_run(cudaStream_t st, int t, double* G, int ld, int* d_status) {
+static int cholesky_run(cudaStream_t st, int t, double* G, int ld, int* d_status, double* gscratch = nullptr,
+                        size_t gscratch_elems = 0) {
   TRY(cla_attrs());
   if (int cs = cla_cluster_size(t, chol_smem_doubles)) {
-    return launch_cluster(cholesky_cluster_kernel, cs, CLA_NT, chol_smem_doubles(t, cs) * sizeof(double), st, t, G, ld,
-                          1e-12, d_status);
+    return launch_cluster(cholesky_cluster_kernel<false>, cs, CLA_NT, chol_smem_doubles(t, cs) * sizeof(double), st, t,
+                          G, ld, 1e-12, d_status, (double*)nullptr);
+  }
+  if (gscratch && (size_t)16 * chol_local_cols(t, 16) * t <= gscratch_elems && t <= 4096) {
+    return launch_cluster(cholesky_cluster_kernel<true>, 16, CLA_NT, chol_smem_doubles_ga(t, 16) * sizeof(double), st,
+                          t, G, ld, 1e-12, d_status, gscratch);
   }
   cholesky_kernel<1024><<<1, 1024, 0, st>>>(t, G, ld, 1e-12, d_status);
   CKL();
@@ -370,6 +380,9 @@ struct EighScratch {
   double *nsM, *nsZ, *nsY;  // m x m, m x m, s x m (ld = ldv)
   unsigned long long* dev;   // NS deviation (double bits)
   size_t tscr_elems;
+  void* mark_obj = nullptr;  // optional phase marker (profile bit 1): mark_fn(mark_obj, phase)
+  int (*mark_fn)(void*, int) = nullptr;
+  int mark(int ph) const { return mark_fn ? mark_fn(mark_obj, ph) : 0; }
 };
 
 static int eigh_top(cudaStream_t st, int s, const double* Hs, int ldh, int m, double* lam, double* Yv, int ldy,
@@ -389,10 +402,11 @@ static int eigh_top(cudaStream_t st, int s, const double* Hs, int ldh, int m, do
   int tcs = (tri_mode == 0 && s > 64) ? cla_cluster_size(s, tri_smem_doubles) : 0;
   static long long* dprof = nullptr;
   static int want_prof = getenv("PSDPROJ_TRI_PROF") ? 1 : 0;
+  static int tri_dbg = getenv("PSDPROJ_TRI_DBG") ? atoi(getenv("PSDPROJ_TRI_DBG")) : 0;  // timing experiments only
   if (want_prof && !dprof) CK(cudaMalloc(&dprof, 16 * 8 * sizeof(long long)));
 #define TRI_LAUNCH(PL, NTH, GA, CSZ, SMEM)                                                                         \
   TRY(launch_cluster(tridiag_cluster_kernel<PL, NTH, GA>, CSZ, NTH, SMEM, st, s, Hs, ldh, w.td, w.te, w.ttau, w.Vh, \
-                     w.ldv, dprof, w.tG))
+                     w.ldv, dprof, w.tG, tri_dbg))
   if (tcs) {
     const size_t tsm = tri_smem_doubles(s, tcs) * sizeof(double);
     if (s <= 32 * 4)
@@ -428,11 +442,13 @@ static int eigh_top(cudaStream_t st, int s, const double* Hs, int ldh, int m, do
               s, tcs, r, h[r * 8 + 0] / (s - 2), h[r * 8 + 1] / (s - 2), h[r * 8 + 2] / (s - 2), h[r * 8 + 3] / (s - 2),
               h[r * 8 + 4] / (s - 2), h[r * 8 + 5] / (s - 2), h[r * 8 + 6] / (s - 2));
   }
+  TRY(w.mark(8));
   tri_prep_kernel<<<1, 1024, 0, st>>>(s, w.td, w.te, w.te2, w.tbounds);
   CKL();
-  tri_bisect_kernel<<<cdiv(m + 1, 8), 256, (size_t)2 * s * sizeof(double), st>>>(s, m, w.td, w.te2, w.tbounds, lam, npos);
+  tri_bisect_kernel<<<cdiv(m + 1, 2), 64, (size_t)2 * s * sizeof(double), st>>>(s, m, w.td, w.te2, w.tbounds, lam, npos);
   CKL();
   if (m <= 0) return 0;
+  TRY(w.mark(9));
   // inverse iteration: vectors per CTA so that 6 s doubles each fit in shared memory
   int vpb = (int)std::min<size_t>(64, (220 * 1024) / ((size_t)6 * s * sizeof(double)));
   int smem_ok = vpb >= 1;
@@ -448,22 +464,45 @@ static int eigh_top(cudaStream_t st, int s, const double* Hs, int ldh, int m, do
       CKL();
     }
   } else {
-    tri_inviter_kernel<<<cdiv(m, vpb), vpb, ism, st>>>(s, m, w.td, w.te, lam, w.tbounds, Yv, ldy, w.tscr, 3, 0,
+    tri_inviter_kernel<<<cdiv(m, vpb), vpb, ism, st>>>(s, m, w.td, w.te, lam, w.tbounds, Yv, ldy, w.tscr, 2, 0,
                                                        smem_ok);
     CKL();
   }
+  TRY(w.mark(10));
   if (s > 2) {
-    const size_t bsm = (size_t)BT_PB * s * sizeof(double);
+    static int bt_mode = -1;  // 0: compact-WY (default for s <= 768), 1: reflector-by-reflector panels
+    if (bt_mode < 0) bt_mode = getenv("PSDPROJ_BT_SIMPLE") ? 1 : 0;
+    const int npan = cdiv(s - 2, WY_PB);
+    if (bt_mode == 0 && s <= 32 * 20) {
+      double* Tb = w.tG;  // free after the tridiagonalisation
+      larft_kernel<<<npan, 256, 0, st>>>(s, w.Vh, w.ldv, w.ttau, Tb);
+      CKL();
+#define BT_WY(PL)                                                                                              \
+  backtransform_wy_kernel<PL><<<cdiv(m, 8), 256, ((size_t)2 * WY_PB * 32 * PL + 2 * WY_PB * WY_PB + 8 * (32 * (WY_PB + 1) + 2 * WY_PB)) * sizeof(double), \
+                                st>>>(s, m, w.Vh, w.ldv, Tb, Yv, ldy)
+      if (s <= 32 * 8)
+        BT_WY(8);
+      else if (s <= 32 * 16)
+        BT_WY(16);
+      else
+        BT_WY(20);
+#undef BT_WY
+      CKL();
+    } else {
+    const int pb = (int)std::max<size_t>(1, std::min<size_t>(BT_PB, (size_t)CLA_SMEM_BYTES / (2 * (size_t)s * sizeof(double))));
+    const size_t bsm = (size_t)2 * pb * s * sizeof(double);
     if (s <= 32 * 8)
-      backtransform_panel_kernel<8><<<cdiv(m, 8), 256, bsm, st>>>(s, m, w.Vh, w.ldv, w.ttau, Yv, ldy);
+      backtransform_panel_kernel<8><<<cdiv(m, 8), 256, bsm, st>>>(s, m, w.Vh, w.ldv, w.ttau, Yv, ldy, pb);
     else if (s <= 32 * 16)
-      backtransform_panel_kernel<16><<<cdiv(m, 8), 256, bsm, st>>>(s, m, w.Vh, w.ldv, w.ttau, Yv, ldy);
+      backtransform_panel_kernel<16><<<cdiv(m, 8), 256, bsm, st>>>(s, m, w.Vh, w.ldv, w.ttau, Yv, ldy, pb);
     else if (s <= 32 * 24)
-      backtransform_panel_kernel<24><<<cdiv(m, 8), 256, bsm, st>>>(s, m, w.Vh, w.ldv, w.ttau, Yv, ldy);
+      backtransform_panel_kernel<24><<<cdiv(m, 8), 256, bsm, st>>>(s, m, w.Vh, w.ldv, w.ttau, Yv, ldy, pb);
     else
-      backtransform_panel_kernel<BT_PER_LANE><<<cdiv(m, 8), 256, bsm, st>>>(s, m, w.Vh, w.ldv, w.ttau, Yv, ldy);
+      backtransform_panel_kernel<BT_PER_LANE><<<cdiv(m, 8), 256, bsm, st>>>(s, m, w.Vh, w.ldv, w.ttau, Yv, ldy, pb);
+    }
     CKL();
   }
+  TRY(w.mark(11));
   if (!mgs) {
     // two Newton-Schulz steps; dev records max|Y^T Y - I| before the second step
     for (int it = 0; it < 2; ++it) {
@@ -762,6 +801,8 @@ struct Run {
     w.nsM = c->G; w.nsZ = c->Hm; w.nsY = c->Gc;
     w.dev = reinterpret_cast<unsigned long long*>(c->d_scal + 16);
     w.tscr_elems = c->tscr_elems;
+    w.mark_obj = this;
+    w.mark_fn = [](void* o, int ph) { return static_cast<Run*>(o)->mark(ph); };
     return w;
   }
   int tri_eig(int s, const double* Hs, int ldh, int m, double* lam, double* Yv, int ldy, int* npos, bool mgs) {
@@ -786,7 +827,7 @@ struct Run {
     CK(cudaMemsetAsync(c->d_status, 0, sizeof(int), st));
     if (t > 0) {
       TRY(copy_cols(t, t, c->Gc, ldm, c->G + kx + (size_t)kx * ldm, ldm));
-      TRY(cholesky_run(st, t, c->Gc, ldm, c->d_status));
+      TRY(cholesky_run(st, t, c->Gc, ldm, c->d_status, c->tG, (size_t)c->s_max * c->s_max + 16 * (size_t)c->s_max + 2048));
       TRY(trinv_run(st, t, c->Gc, ldm, c->Li + kx + (size_t)kx * ldm, ldm));
     }
     // Hh = L^-1 H L^-T
@@ -1552,10 +1593,14 @@ extern "C" int psdproj_cholesky(int t, double* G, int ld, void* stream) {
   int* d_status = nullptr;
   CK(cudaMallocAsync(&d_status, sizeof(int), st));
   CK(cudaMemsetAsync(d_status, 0, sizeof(int), st));
-  int rc = cholesky_run(st, t, G, ld, d_status);
+  const size_t gel = (size_t)16 * chol_local_cols(t, 16) * t;
+  double* gs = nullptr;
+  CK(cudaMallocAsync(&gs, gel * sizeof(double), st));
+  int rc = cholesky_run(st, t, G, ld, d_status, gs, gel);
   int h = 0;
   if (rc == 0) CK(cudaMemcpyAsync(&h, d_status, sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaFreeAsync(d_status, st));
+  CK(cudaFreeAsync(gs, st));
   CK(cudaStreamSynchronize(st));
   return rc < 0 ? rc : h;
 }

@@ -343,31 +343,40 @@ __global__ void tri_inviter_kernel(int s, int m, const double* __restrict__ d, c
   } else {
     for (int k = 0; k < s; ++k) YY(k) = yi[k];
   }
+  // iterations without separate scaling passes: the previous iteration's 1/max scale is applied as
+  // the forward sweep reads each entry, and the last backward sweep accumulates ||y||^2
+  double sc = 1.0, n2 = 0.0;
   for (int it = 0; it < iters; ++it) {
+    const bool last = it + 1 == iters;
+    double y0 = YY(0) * sc;
     for (int k = 0; k + 1 < s; ++k) {  // dgttrs forward (L with interchanges)
+      const double y1 = YY(k + 1) * sc;
       if (PV(k) == 0.0) {
-        YY(k + 1) -= DL(k) * YY(k);
+        YY(k) = y0;
+        y0 = y1 - DL(k) * y0;
       } else {
-        double tmp = YY(k);
-        double y1 = YY(k + 1);
         YY(k) = y1;
-        YY(k + 1) = tmp - DL(k) * y1;
+        y0 = y0 - DL(k) * y1;
       }
     }
+    YY(s - 1) = y0;
     double nrm = 0.0;
+    double b1 = 0.0, b2 = 0.0;  // YY(k + 1), YY(k + 2) of the back substitution
     for (int k = s - 1; k >= 0; --k) {  // back substitution with U
       double v = YY(k);
-      if (k + 1 < s) v -= DU(k) * YY(k + 1);
-      if (k + 2 < s) v -= DU2(k) * YY(k + 2);
+      if (k + 1 < s) v -= DU(k) * b1;
+      if (k + 2 < s) v -= DU2(k) * b2;
       v *= DD(k);
       YY(k) = v;
-      nrm = fmax(nrm, fabs(v));
+      b2 = b1;
+      b1 = v;
+      if (last)
+        n2 = fma(v, v, n2);
+      else
+        nrm = fmax(nrm, fabs(v));
     }
-    double sc = (nrm > 0.0) ? 1.0 / nrm : 1.0;
-    for (int k = 0; k < s; ++k) YY(k) *= sc;
+    sc = (nrm > 0.0) ? 1.0 / nrm : 1.0;
   }
-  double n2 = 0.0;
-  for (int k = 0; k < s; ++k) n2 += YY(k) * YY(k);
   double inv = (n2 > 0.0) ? rsqrt(n2) : 0.0;
   for (int k = 0; k < s; ++k) yi[k] = YY(k) * inv;
 #undef DD

@@ -129,7 +129,7 @@ def test_eigh_repeated_eigenvalues(api, s):
     assert np.linalg.norm(A @ V - V * w, axis=0).max() <= 1e-11 * 3 * max(1, s / 20)
 
 
-@pytest.mark.parametrize("t", [1, 5, 8, 9, 64, 150, 301, 520])
+@pytest.mark.parametrize("t", [1, 5, 8, 9, 64, 150, 301, 520, 700, 1100])
 def test_cholesky_cluster(api, t):
     """a6 Cholesky (cluster kernel for t <= ~580, one CTA above) vs LAPACK on an SPD Gram matrix."""
     rng = np.random.default_rng(300 + t)
