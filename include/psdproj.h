@@ -119,6 +119,20 @@ int psdproj_project(psdproj_ctx ctx, const double* A, int lda, double* Pi, int l
 int psdproj_project_host(psdproj_ctx ctx, const double* A_host, int lda, double* Pi_host, int ldpi,
                          double tol, void* stream, psdproj_info* info);
 
+/* ---- row-sharded mode (one matrix over the GPUs of a node) ----
+ * Every rank holds the contiguous row block [row0, row0 + nrows) of A (nrows x n, lda >= nrows)
+ * and receives the same rows of Pi; rank r's block must start where rank r-1's ends. Per LOBPCG
+ * iteration the library all-gathers the new directions W (for the block multiply A_local W),
+ * all-reduces the Gram partials and column sums of squares (NCCL, on the call's stream), and
+ * runs the small dense Rayleigh-Ritz step replicated (identical inputs -> identical decisions on
+ * every rank). Pi_local = W_local W^T (W = V diag(sqrt(theta+)), gathered). The exact
+ * eigensolver (DIRECT) is not available: such calls return PSDPROJ_E_CAPACITY.
+ * NCCL is loaded at run time (dlopen libnccl.so.2 or PSDPROJ_NCCL_LIB). */
+int psdproj_get_nccl_uid(void* uid_out /* 128 bytes, host */);
+size_t psdproj_workspace_bytes_sharded(int n, int nrows_max, int nranks, const psdproj_params* p);
+int psdproj_create_sharded(int n, int row0, int nrows, const void* nccl_uid, int rank, int nranks,
+                           const psdproj_params* p, void* ws, size_t ws_bytes, psdproj_ctx* out);
+
 /* Batched: count independent contexts (one per cone block, possibly different n). The blocks are
  * driven by up to PSDPROJ_BATCH_THREADS (env, default 8) host threads, each on its own stream
  * forked from and joined back to `stream` (the latency-bound iterations of different blocks

@@ -20,7 +20,8 @@ EXPORTS = [
     "psdproj_project_host", "psdproj_project_batched", "psdproj_get_ritz", "psdproj_reset",
     "psdproj_destroy", "psdproj_last_error", "psdproj_dgemm", "psdproj_jacobi_ws_elems",
     "psdproj_jacobi", "psdproj_philox_raw", "psdproj_philox_gauss", "psdproj_eigh_ws_elems",
-    "psdproj_eigh", "psdproj_cholesky",
+    "psdproj_eigh", "psdproj_cholesky", "psdproj_get_nccl_uid", "psdproj_workspace_bytes_sharded",
+    "psdproj_create_sharded",
 ]
 
 
@@ -87,10 +88,14 @@ def load(path=SO_PATH):
     L.psdproj_eigh_ws_elems.restype = sz
     L.psdproj_eigh.argtypes = [i, vp, i, i, vp, vp, i, vp, vp, vp]
     L.psdproj_cholesky.argtypes = [i, vp, i, vp]
+    L.psdproj_get_nccl_uid.argtypes = [vp]
+    L.psdproj_workspace_bytes_sharded.argtypes = [i, i, i, P(Params)]
+    L.psdproj_workspace_bytes_sharded.restype = sz
+    L.psdproj_create_sharded.argtypes = [i, i, i, vp, i, i, P(Params), vp, sz, P(vp)]
     L.psdproj_philox_raw.argtypes = [i, u32, u32, u32, u32, u32, vp, vp]
     L.psdproj_philox_gauss.argtypes = [i, i, vp, i, u64, u32, u32, u32, vp]
     special = ("psdproj_default_params", "psdproj_workspace_bytes", "psdproj_last_error",
-               "psdproj_jacobi_ws_elems", "psdproj_eigh_ws_elems")
+               "psdproj_jacobi_ws_elems", "psdproj_eigh_ws_elems", "psdproj_workspace_bytes_sharded")
     for name in EXPORTS:
         if name not in special:
             getattr(L, name).restype = ctypes.c_int

@@ -12,8 +12,8 @@ import torch
 from . import _lib
 from ._lib import Info, Params, PsdprojError, check
 
-__all__ = ["Context", "default_params", "project_batched", "dgemm", "jacobi", "philox_raw",
-           "philox_gauss", "workspace_bytes", "colmajor"]
+__all__ = ["Context", "ShardedContext", "default_params", "project_batched", "dgemm", "jacobi", "philox_raw",
+           "philox_gauss", "workspace_bytes", "colmajor", "colmajor_copy", "nccl_uid", "row_blocks"]
 
 
 def _stream_ptr(stream):
@@ -139,6 +139,79 @@ class Context:
     @property
     def handle(self):
         return self._h
+
+
+def nccl_uid():
+    """128-byte NCCL unique id for psdproj_create_sharded (rank 0 creates it, then broadcasts)."""
+    buf = ctypes.create_string_buffer(128)
+    check(_lib.load().psdproj_get_nccl_uid(buf), "psdproj_get_nccl_uid")
+    return buf.raw
+
+
+def row_blocks(n, world):
+    """Contiguous, balanced row blocks (offset, rows) of the row-sharded mode, rank order."""
+    base, extra = divmod(n, world)
+    out, off = [], 0
+    for r in range(world):
+        rows = base + (1 if r < extra else 0)
+        out.append((off, rows))
+        off += rows
+    return out
+
+
+def colmajor_copy(M):
+    """Column-major (stride(0) == 1) copy of a 2-D float64 tensor."""
+    out = colmajor(M.shape[0], M.shape[1], device=M.device)
+    out.copy_(M)
+    return out
+
+
+class ShardedContext:
+    """psdproj_create_sharded: rank `rank` of `world` holds rows [row0, row0 + nrows) of every
+    n x n input (a column-major nrows x n block) and gets the same rows of Pi. All ranks call
+    project() collectively (NCCL inside the library, on the current stream)."""
+
+    def __init__(self, n, row0, nrows, uid, rank, world, params=None, device="cuda", nrows_max=None, **kw):
+        L = _lib.load()
+        self.n, self.row0, self.nrows = n, row0, nrows
+        self.params = params if params is not None else default_params(**kw)
+        nrmax = nrows_max or max(r for _, r in row_blocks(n, world))
+        nbytes = int(L.psdproj_workspace_bytes_sharded(n, nrmax, world, ctypes.byref(self.params)))
+        self.ws = torch.empty(nbytes + 256, dtype=torch.uint8, device=device)
+        base = self.ws.data_ptr()
+        off = (-base) % 256
+        self._h = ctypes.c_void_p()
+        ub = ctypes.create_string_buffer(bytes(uid), 128)
+        check(L.psdproj_create_sharded(n, row0, nrows, ub, rank, world, ctypes.byref(self.params),
+                                       ctypes.c_void_p(base + off), nbytes, ctypes.byref(self._h)),
+              "psdproj_create_sharded")
+
+    def project(self, A_local, tol, out=None, stream=None):
+        L = _lib.load()
+        if A_local.shape != (self.nrows, self.n) or not A_local.is_cuda:
+            raise ValueError(f"A_local must be a CUDA ({self.nrows}, {self.n}) float64 tensor")
+        lda = _ld_colmajor(A_local)
+        if out is None:
+            out = colmajor(self.nrows, self.n, device=A_local.device)
+        info = Info()
+        rc = L.psdproj_project(self._h, _ptr(A_local), lda, _ptr(out), _ld_colmajor(out), float(tol),
+                               _stream_ptr(stream), ctypes.byref(info))
+        check(rc, "psdproj_project (sharded)")
+        return out, info.as_dict()
+
+    def reset(self):
+        check(_lib.load().psdproj_reset(self._h), "psdproj_reset")
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            _lib.load().psdproj_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def project_batched(ctxs, As, tols, outs=None, stream=None):

@@ -45,7 +45,7 @@ template <int NT>
 __global__ void __launch_bounds__(NT) resid_norm_kernel(int n, const double* __restrict__ X, int ldx,
                                                         const double* __restrict__ BX, int ldb,
                                                         const double* __restrict__ theta, double* __restrict__ R,
-                                                        int ldr, double* __restrict__ rnorm) {
+                                                        int ldr, double* __restrict__ rnorm, int squared = 0) {
   __shared__ double red[32];
   int j = blockIdx.x;
   double th = theta[j];
@@ -56,12 +56,12 @@ __global__ void __launch_bounds__(NT) resid_norm_kernel(int n, const double* __r
     acc += v * v;
   }
   acc = block_sum<NT>(acc, red);
-  if (threadIdx.x == 0) rnorm[j] = sqrt(acc);
+  if (threadIdx.x == 0) rnorm[j] = squared ? acc : sqrt(acc);
 }
 
 template <int NT>
 __global__ void __launch_bounds__(NT) colnorm_kernel(int n, const double* __restrict__ Z, int ld,
-                                                     double* __restrict__ out) {
+                                                     double* __restrict__ out, int squared = 0) {
   __shared__ double red[32];
   int j = blockIdx.x;
   double acc = 0.0;
@@ -70,7 +70,42 @@ __global__ void __launch_bounds__(NT) colnorm_kernel(int n, const double* __rest
     acc += v * v;
   }
   acc = block_sum<NT>(acc, red);
-  if (threadIdx.x == 0) out[j] = sqrt(acc);
+  if (threadIdx.x == 0) out[j] = squared ? acc : sqrt(acc);
+}
+
+__global__ void i2d_kernel(const int* __restrict__ f, double* __restrict__ d) {
+  if (threadIdx.x == 0) d[0] = (double)f[0];
+}
+__global__ void d2i_kernel(const double* __restrict__ d, int* __restrict__ f) {
+  if (threadIdx.x == 0) f[0] = d[0] != 0.0 ? 1 : 0;
+}
+
+__global__ void sqrt_inplace_kernel(int k, double* __restrict__ v) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < k; i += gridDim.x * blockDim.x) v[i] = sqrt(v[i]);
+}
+
+// row-sharded mode: Z_full (n x k, ldf) <- rank-major packed all-gather buffer (rank r's block is
+// rows[r] x k with ld nrmax at offset r * nrmax * k; its rows start at global row offs[r])
+__global__ void unpack_rows_kernel(int nranks, int nrmax, int k, const int* __restrict__ rows,
+                                   const int* __restrict__ offs, const double* __restrict__ pack,
+                                   double* __restrict__ full, int ldf) {
+  const size_t per = (size_t)nrmax * k, total = per * nranks;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+    const int r = (int)(e / per);
+    const size_t w = e - (size_t)r * per;
+    const int i = (int)(w % nrmax), j = (int)(w / nrmax);
+    if (i < rows[r]) full[IDX(offs[r] + i, j, ldf)] = pack[e];
+  }
+}
+
+// packed (ld = nrmax) copy of a local row block (the all-gather send buffer); rows >= nl zeroed
+__global__ void pack_rows_kernel(int nl, int nrmax, int k, const double* __restrict__ src, int lds,
+                                 double* __restrict__ dst) {
+  const size_t total = (size_t)nrmax * k;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e % nrmax), j = (int)(e / nrmax);
+    dst[e] = (i < nl) ? src[IDX(i, j, lds)] : 0.0;
+  }
 }
 
 // Z[:, j] /= norm[j] (and Z2 likewise when given); zero norms leave the column unchanged.
@@ -148,6 +183,32 @@ __global__ void philox_gauss_kernel(int n, int q, double* __restrict__ dst, int 
     int64_t l0 = 2 * h, l1 = 2 * h + 1;
     dst[IDX(l0 % n, l0 / n, ld)] = rad * cv;
     if (l1 < total) dst[IDX(l1 % n, l1 / n, ld)] = rad * sv;
+  }
+}
+
+__global__ void philox_gauss_rows_kernel(int nl, int row0, int n, int q, double* __restrict__ dst, int ld,
+                                         uint64_t seed, uint32_t stream, uint32_t ctx, uint32_t tag) {
+  const int64_t total = (int64_t)nl * q;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e % nl), j = (int)(e / nl);
+    const int64_t l = (int64_t)(row0 + i) + (int64_t)j * n;
+    uint32_t c[4] = {(uint32_t)(l >> 1), stream, ctx, tag};
+    philox10(c, (uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32));
+    const double u1 = u53(c[0], c[1]), u2 = u53(c[2], c[3]);
+    const double rad = sqrt(-2.0 * log(u1));
+    double sv, cv;
+    sincospi(2.0 * u2, &sv, &cv);
+    dst[IDX(i, j, ld)] = (l & 1) ? rad * sv : rad * cv;
+  }
+}
+
+// W[:, j] = V[:, j] * sqrt(w[j]) (w > 0): Pi = W W^T is exactly symmetric entry by entry
+__global__ void scale_sqrt_cols_kernel(int n, int cols, double* __restrict__ dst, int ldd,
+                                       const double* __restrict__ src, int lds, const double* __restrict__ w) {
+  size_t total = (size_t)n * cols;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+    int i = (int)(e % n), j = (int)(e / n);
+    dst[IDX(i, j, ldd)] = src[IDX(i, j, lds)] * sqrt(w[j]);
   }
 }
 
@@ -730,23 +791,24 @@ __global__ void symmetrize_kernel(int n, double* __restrict__ P, int ld) {
 }
 
 // non-finite scan (E_NONFINITE, R-first pass): flag[0] |= 1 if any entry is inf/nan
-__global__ void nonfinite_kernel(int n, const double* __restrict__ A, int lda, int* __restrict__ flag) {
-  int64_t total = (int64_t)n * n;
+// rows x cols block (rows = n, cols = n unsharded; the local row block in the row-sharded mode)
+__global__ void nonfinite_kernel(int rows, int cols, const double* __restrict__ A, int lda, int* __restrict__ flag) {
+  int64_t total = (int64_t)rows * cols;
   int bad = 0;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    int i = (int)(e % n), j = (int)(e / n);
+    int i = (int)(e % rows), j = (int)(e / rows);
     if (!isfinite(A[IDX(i, j, lda)])) bad = 1;
   }
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
 }
 
 // Frobenius norm partials: out[block] = sum of squares of its slice (second pass on host order)
-__global__ void fro_partial_kernel(int n, const double* __restrict__ A, int lda, double* __restrict__ out) {
+__global__ void fro_partial_kernel(int rows, int cols, const double* __restrict__ A, int lda, double* __restrict__ out) {
   __shared__ double red[32];
-  int64_t total = (int64_t)n * n;
+  int64_t total = (int64_t)rows * cols;
   double acc = 0.0;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    int i = (int)(e % n), j = (int)(e / n);
+    int i = (int)(e % rows), j = (int)(e / rows);
     double v = A[IDX(i, j, lda)];
     acc += v * v;
   }

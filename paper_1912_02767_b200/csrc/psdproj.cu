@@ -12,6 +12,8 @@
 // expansion (line 8, R8-R11), stopping rule with guard (R12), Theorem-3 bound
 // (R14-R16, R36), side rule (R17-R18).
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -63,6 +65,43 @@ static thread_local long long g_launches = 0;  // kernels issued by this thread 
   } while (0)
 
 static inline int rup(int x, int a) { return (x + a - 1) / a * a; }
+
+// ------------------------------------------------------------------ NCCL (row-sharded mode, §8.e)
+// Loaded on first use with dlopen (the library in the process -- torch's -- or PSDPROJ_NCCL_LIB), so
+// libpsdproj.so has no link-time NCCL dependency and the single-GPU path never touches it.
+struct NcclApi {
+  bool tried = false, ok = false;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  const char* (*getErrorString)(ncclResult_t) = nullptr;
+};
+static NcclApi g_nccl;
+static int nccl_load() {
+  if (g_nccl.tried) return g_nccl.ok ? 0 : set_err(PSDPROJ_E_NCCL, "NCCL library not available");
+  g_nccl.tried = true;
+  void* h = nullptr;
+  if (const char* e = getenv("PSDPROJ_NCCL_LIB")) h = dlopen(e, RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return set_err(PSDPROJ_E_NCCL, "dlopen(libnccl.so.2) failed: %s", dlerror());
+  g_nccl.getUniqueId = (decltype(g_nccl.getUniqueId))dlsym(h, "ncclGetUniqueId");
+  g_nccl.commInitRank = (decltype(g_nccl.commInitRank))dlsym(h, "ncclCommInitRank");
+  g_nccl.allReduce = (decltype(g_nccl.allReduce))dlsym(h, "ncclAllReduce");
+  g_nccl.allGather = (decltype(g_nccl.allGather))dlsym(h, "ncclAllGather");
+  g_nccl.commDestroy = (decltype(g_nccl.commDestroy))dlsym(h, "ncclCommDestroy");
+  g_nccl.getErrorString = (decltype(g_nccl.getErrorString))dlsym(h, "ncclGetErrorString");
+  g_nccl.ok = g_nccl.getUniqueId && g_nccl.commInitRank && g_nccl.allReduce && g_nccl.allGather &&
+              g_nccl.commDestroy && g_nccl.getErrorString;
+  return g_nccl.ok ? 0 : set_err(PSDPROJ_E_NCCL, "NCCL symbols missing");
+}
+#define NK(x)                                                                                                  \
+  do {                                                                                                         \
+    ncclResult_t r_ = (x);                                                                                     \
+    if (r_ != ncclSuccess) return set_err(PSDPROJ_E_NCCL, "%s:%d %s: %s", __FILE__, __LINE__, #x,             \
+                                          g_nccl.getErrorString ? g_nccl.getErrorString(r_) : "nccl error"); \
+  } while (0)
 static int g_sms = 0;
 static int sms() {
   if (!g_sms) {
@@ -522,6 +561,14 @@ static int eigh_top(cudaStream_t st, int s, const double* Hs, int ldh, int m, do
 // ------------------------------------------------------------------ context
 struct psdproj_ctx_s {
   int n = 0, ld = 0;
+  // row-sharded mode (§8.e): this rank holds rows [row0, row0 + nr) of every n-sized block; the
+  // tall-skinny buffers have nr rows (ld = rup(nr, 8)); Gram / norm partials are all-reduced, the
+  // block multiply gathers Z. Unsharded: nr = n, row0 = 0, nranks = 1.
+  bool sharded = false;
+  int rank = 0, nranks = 1, row0 = 0, nr = 0, nrmax = 0, ldn = 0;
+  ncclComm_t comm = nullptr;
+  int *d_rows = nullptr, *d_offs = nullptr;
+  double *zsend = nullptr, *zpack = nullptr, *zfull = nullptr, *gbuf = nullptr;
   psdproj_params prm{};
   int m0 = 0, q = 0, m_max = 0, s_max = 0, NJ = 0, tcols = 0;
   // device (carved from the caller's workspace)
@@ -570,7 +617,7 @@ struct Carver {
 };
 
 static void resolve(int n, const psdproj_params* in, psdproj_params& p, int& m0, int& q, int& m_max, int& s_max,
-                    int& NJ, int& tcols) {
+                    int& NJ, int& tcols, bool sharded = false) {
   if (in)
     p = *in;
   else
@@ -581,15 +628,16 @@ static void resolve(int n, const psdproj_params* in, psdproj_params& p, int& m0,
   m_max = p.m_max > 0 ? std::min(p.m_max, n) : std::min(n, (n + 2) / 3 + 1);
   m_max = std::max(m_max, std::min(n, m0));
   s_max = 3 * m_max + q;
-  NJ = std::max(s_max, n);
+  NJ = sharded ? s_max : std::max(s_max, n);  // the sharded mode has no DIRECT path
   NJ += NJ & 1;
-  tcols = std::max(s_max, n);
+  tcols = sharded ? s_max : std::max(s_max, n);
 }
 
 static size_t carve(psdproj_ctx_s* c, int n, const psdproj_params& p, int m_max, int s_max, int NJ, int tcols,
-                    char* base, size_t cap, bool dry) {
+                    char* base, size_t cap, bool dry, int nl = -1, int nranks = 1, int nrmax = 0) {
   Carver cv{base, 0, cap, dry};
-  int ld = rup(std::max(n, 1), 8);
+  if (nl < 0) nl = n;
+  int ld = rup(std::max(nl, 1), 8);
   size_t nS = (size_t)ld * s_max, nM = (size_t)ld * m_max, nT = (size_t)ld * tcols, s2 = (size_t)s_max * s_max;
   c->S = cv.take<double>(nS); c->BS = cv.take<double>(nS);
   c->S2 = cv.take<double>(nS); c->BS2 = cv.take<double>(nS);
@@ -616,6 +664,16 @@ static size_t carve(psdproj_ctx_s* c, int n, const psdproj_params& p, int m_max,
   c->tscr_elems = (size_t)6 * s_max * (size_t)(std::min(s_max, m_max + (s_max - 3 * m_max)) + 1);
   c->tscr = cv.take<double>(c->tscr_elems);
   c->tG = cv.take<double>(s2 + 16 * (size_t)s_max + 2048);  // also the GA tridiagonalisation scratch
+  if (nranks > 1 || nl != n || nrmax > 0) {  // row-sharded buffers
+    const int ldn = rup(n, 8);
+    const size_t nz = (size_t)std::max(nrmax, 1) * s_max;
+    c->zsend = cv.take<double>(nz);
+    c->zpack = cv.take<double>(nz * nranks);
+    c->zfull = cv.take<double>((size_t)ldn * s_max);
+    c->gbuf = cv.take<double>(s2);
+    c->d_rows = cv.take<int>(nranks + 8);
+    c->d_offs = cv.take<int>(nranks + 8);
+  }
   return cv.off + 256;
 }
 
@@ -655,6 +713,8 @@ extern "C" int psdproj_create(int n, const psdproj_params* in, void* ws, size_t 
   auto* c = new psdproj_ctx_s();
   c->n = n;
   c->ld = rup(n, 8);
+  c->ldn = c->ld;
+  c->nr = n;
   c->prm = p;
   c->m0 = m0; c->q = q; c->m_max = m_max; c->s_max = s_max; c->NJ = NJ; c->tcols = tcols;
   carve(c, n, p, m_max, s_max, NJ, tcols, (char*)ws, ws_bytes, false);
@@ -669,8 +729,99 @@ extern "C" int psdproj_create(int n, const psdproj_params* in, void* ws, size_t 
   return PSDPROJ_OK;
 }
 
+extern "C" int psdproj_get_nccl_uid(void* uid_out) {
+  if (!uid_out) return set_err(PSDPROJ_E_INVALID, "uid_out NULL");
+  TRY(nccl_load());
+  ncclUniqueId id;
+  NK(g_nccl.getUniqueId(&id));
+  std::memcpy(uid_out, &id, sizeof(id));
+  return PSDPROJ_OK;
+}
+
+extern "C" size_t psdproj_workspace_bytes_sharded(int n, int nrows_max, int nranks, const psdproj_params* in) {
+  if (n <= 0 || nrows_max <= 0 || nranks <= 0) return 0;
+  psdproj_params p;
+  int m0, q, m_max, s_max, NJ, tcols;
+  resolve(n, in, p, m0, q, m_max, s_max, NJ, tcols, true);
+  psdproj_ctx_s tmp;
+  return carve(&tmp, n, p, m_max, s_max, NJ, tcols, nullptr, 0, true, nrows_max, nranks, nrows_max);
+}
+
+extern "C" int psdproj_create_sharded(int n, int row0, int nrows, const void* nccl_uid, int rank, int nranks,
+                                      const psdproj_params* in, void* ws, size_t ws_bytes, psdproj_ctx* out) {
+  if (!out) return set_err(PSDPROJ_E_INVALID, "out is NULL");
+  *out = nullptr;
+  if (n <= 0 || nrows <= 0 || row0 < 0 || row0 + nrows > n || nranks <= 0 || rank < 0 || rank >= nranks || !nccl_uid)
+    return set_err(PSDPROJ_E_INVALID, "invalid sharded arguments (n=%d row0=%d nrows=%d rank=%d/%d)", n, row0, nrows,
+                   rank, nranks);
+  if (!ws || ((uintptr_t)ws & 255)) return set_err(PSDPROJ_E_WORKSPACE, "workspace NULL or not 256-byte aligned");
+  psdproj_params p;
+  int m0, q, m_max, s_max, NJ, tcols;
+  resolve(n, in, p, m0, q, m_max, s_max, NJ, tcols, true);
+  if (p.side == PSDPROJ_SIDE_DIRECT || p.host_io) return set_err(PSDPROJ_E_INVALID, "sharded mode: no DIRECT side / host_io");
+  TRY(nccl_load());
+  ncclComm_t comm;
+  ncclUniqueId id;
+  std::memcpy(&id, nccl_uid, sizeof(id));
+  NK(g_nccl.commInitRank(&comm, nranks, id, rank));
+  // every rank's row block (all-gather of (row0, nrows) through the new communicator)
+  int* dv = nullptr;
+  CK(cudaMalloc(&dv, sizeof(int) * 2 * (nranks + 1)));
+  int mine[2] = {row0, nrows};
+  CK(cudaMemcpy(dv, mine, sizeof(mine), cudaMemcpyHostToDevice));
+  NK(g_nccl.allGather(dv, dv + 2, 2, ncclInt32, comm, 0));
+  std::vector<int> all(2 * nranks);
+  CK(cudaMemcpy(all.data(), dv + 2, sizeof(int) * 2 * nranks, cudaMemcpyDeviceToHost));
+  CK(cudaFree(dv));
+  std::vector<int> offs(nranks), rows(nranks);
+  int nrmax = 0, covered = 0;
+  for (int r = 0; r < nranks; ++r) {
+    offs[r] = all[2 * r];
+    rows[r] = all[2 * r + 1];
+    nrmax = std::max(nrmax, rows[r]);
+    if (offs[r] != covered) {
+      g_nccl.commDestroy(comm);
+      return set_err(PSDPROJ_E_INVALID, "row blocks must be contiguous and ordered by rank");
+    }
+    covered += rows[r];
+  }
+  if (covered != n) {
+    g_nccl.commDestroy(comm);
+    return set_err(PSDPROJ_E_INVALID, "row blocks cover %d of %d rows", covered, n);
+  }
+  psdproj_ctx_s tmp;
+  size_t need = carve(&tmp, n, p, m_max, s_max, NJ, tcols, nullptr, 0, true, nrows, nranks, nrmax);
+  if (ws_bytes < need) {
+    g_nccl.commDestroy(comm);
+    return set_err(PSDPROJ_E_WORKSPACE, "workspace %zu < needed %zu", ws_bytes, need);
+  }
+  auto* c = new psdproj_ctx_s();
+  c->n = n;
+  c->ld = rup(nrows, 8);
+  c->ldn = rup(n, 8);
+  c->prm = p;
+  c->m0 = m0; c->q = q; c->m_max = m_max; c->s_max = s_max; c->NJ = NJ; c->tcols = tcols;
+  c->sharded = true;
+  c->rank = rank; c->nranks = nranks; c->row0 = row0; c->nr = nrows; c->nrmax = nrmax;
+  c->comm = comm;
+  carve(c, n, p, m_max, s_max, NJ, tcols, (char*)ws, ws_bytes, false, nrows, nranks, nrmax);
+  CK(cudaMemcpy(c->d_rows, rows.data(), sizeof(int) * nranks, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(c->d_offs, offs.data(), sizeof(int) * nranks, cudaMemcpyHostToDevice));
+  c->h_d_len = (size_t)4 * (std::max(s_max, n) + 64);
+  c->h_i_len = (size_t)8 * (std::max(s_max, n) + 64);
+  if (cudaMallocHost(&c->h_d, c->h_d_len * sizeof(double)) != cudaSuccess ||
+      cudaMallocHost(&c->h_i, c->h_i_len * sizeof(int)) != cudaSuccess) {
+    g_nccl.commDestroy(comm);
+    delete c;
+    return set_err(PSDPROJ_E_CUDA, "cudaMallocHost failed");
+  }
+  *out = c;
+  return PSDPROJ_OK;
+}
+
 extern "C" int psdproj_destroy(psdproj_ctx c) {
   if (!c) return PSDPROJ_OK;
+  if (c->comm && g_nccl.ok) g_nccl.commDestroy(c->comm);
   if (c->h_d) cudaFreeHost(c->h_d);
   if (c->h_i) cudaFreeHost(c->h_i);
   for (auto e : c->ev) cudaEventDestroy(e);
@@ -739,16 +890,49 @@ struct Run {
     }
     return dgemm(st, oa, ob, M, N, K, al, A, lda, B, ldb, be, C, ldc, c->part, c->part_elems);
   }
-  // block multiply (a3): Y = sgn * A * Z, the hot kernel; optionally timed with events
+  // row-sharded mode: sum over ranks (in place, on the call's stream); no-op otherwise
+  int allreduce(double* buf, size_t count) {
+    if (!c->sharded || count == 0) return 0;
+    NK(g_nccl.allReduce(buf, buf, count, ncclFloat64, ncclSum, c->comm, st));
+    return 0;
+  }
+  // Gram C = A^T B (M x N) over the rows of tall-skinny blocks: local rows, then summed over ranks
+  int gram(int M, int N, const double* A, int lda, const double* B, int ldb, double* C, int ldc) {
+    if (M <= 0 || N <= 0) return 0;
+    if (!c->sharded) return gemm(OP_T, OP_N, M, N, c->nr, 1.0, A, lda, B, ldb, 0.0, C, ldc);
+    TRY(gemm(OP_T, OP_N, M, N, c->nr, 1.0, A, lda, B, ldb, 0.0, c->gbuf, M));
+    TRY(allreduce(c->gbuf, (size_t)M * N));
+    CK(cudaMemcpy2DAsync(C, (size_t)ldc * 8, c->gbuf, (size_t)M * 8, (size_t)M * 8, N, cudaMemcpyDeviceToDevice, st));
+    return 0;
+  }
+  // all n rows of a tall-skinny block (k columns) into c->zfull (ld c->ldn): pack, all-gather, unpack
+  int gather_full(const double* Zl, int ldz, int k) {
+    if (k <= 0) return 0;
+    const size_t per = (size_t)c->nrmax * k;
+    pack_rows_kernel<<<grid1d(per), 256, 0, st>>>(c->nr, c->nrmax, k, Zl, ldz, c->zsend);
+    CKL();
+    NK(g_nccl.allGather(c->zsend, c->zpack, per, ncclFloat64, c->comm, st));
+    unpack_rows_kernel<<<grid1d(per * c->nranks), 256, 0, st>>>(c->nranks, c->nrmax, k, c->d_rows, c->d_offs, c->zpack,
+                                                                 c->zfull, c->ldn);
+    CKL();
+    return 0;
+  }
+  // block multiply (a3): Y = sgn * A * Z, the hot kernel; optionally timed with events. Sharded:
+  // Y (local rows) = sgn * A_local (nr x n) * Z_full, Z_full all-gathered from the ranks' rows.
   int amul(double sgn, const double* A, int lda, const double* Z, int ldz, int k, double* Y, int ldy) {
     if (k <= 0) return 0;
-    int n = c->n;
+    int n = c->n, nl = c->nr;
     info->a_passes++;
     info->a_cols += k;
-    info->amul_flops += 2.0 * n * (double)n * k;
-    info->amul_bytes += 8.0 * n * (double)n;
-    info->flops += 2.0 * n * (double)n * k;
-    info->bytes += 8.0 * n * (double)n + 16.0 * n * (double)k;
+    info->amul_flops += 2.0 * nl * (double)n * k;
+    info->amul_bytes += 8.0 * nl * (double)n;
+    info->flops += 2.0 * nl * (double)n * k;
+    info->bytes += 8.0 * nl * (double)n + 16.0 * n * (double)k;
+    if (c->sharded) {
+      TRY(gather_full(Z, ldz, k));
+      Z = c->zfull;
+      ldz = c->ldn;
+    }
     bool prof = c->prm.profile & 1;
     if (prof) {
       while ((int)c->ev.size() < 2 * (nev + 1)) {
@@ -759,7 +943,7 @@ struct Run {
       CK(cudaEventRecord(c->ev[2 * nev], st));
     }
     {
-      int rc_ = gemm_kp_launch<OP_N, OP_N, 64, 64, 4, 1>(st, n, k, n, sgn, A, lda, Z, ldz, 0.0, Y, ldy, c->part,
+      int rc_ = gemm_kp_launch<OP_N, OP_N, 64, 64, 4, 1>(st, nl, k, n, sgn, A, lda, Z, ldz, 0.0, Y, ldy, c->part,
                                                          c->part_elems);
       if (rc_ < 0) return rc_;
     }
@@ -767,6 +951,20 @@ struct Run {
       CK(cudaEventRecord(c->ev[2 * nev + 1], st));
       nev++;
     }
+    return 0;
+  }
+  // N(0,1) rows [row0, row0 + nr) of the global n x q Philox block (R11)
+  int philox(int q, double* dst, int ldd, uint32_t tag) {
+    if (q <= 0) return 0;
+    if (!c->sharded) {
+      philox_gauss_kernel<<<grid1d(((size_t)c->n * q + 1) / 2), 256, 0, st>>>(c->n, q, dst, ldd, c->prm.seed,
+                                                                           (uint32_t)c->calls, c->prm.ctx_id, tag);
+    } else {
+      philox_gauss_rows_kernel<<<grid1d((size_t)c->nr * q), 256, 0, st>>>(c->nr, c->row0, c->n, q, dst, ldd,
+                                                                          c->prm.seed, (uint32_t)c->calls,
+                                                                          c->prm.ctx_id, tag);
+    }
+    CKL();
     return 0;
   }
   int gather(int n, int cols, double* dst, int ldd, const double* src, int lds, const std::vector<int>& idx) {
@@ -787,8 +985,13 @@ struct Run {
   }
   int normalize(int n, int cols, double* Z, int ldz, double* Z2, int ldz2) {
     if (cols <= 0) return 0;
-    colnorm_kernel<256><<<cols, 256, 0, st>>>(n, Z, ldz, c->d_norm);
+    colnorm_kernel<256><<<cols, 256, 0, st>>>(n, Z, ldz, c->d_norm, c->sharded ? 1 : 0);
     CKL();
+    if (c->sharded) {
+      TRY(allreduce(c->d_norm, cols));
+      sqrt_inplace_kernel<<<cdiv(cols, 256), 256, 0, st>>>(cols, c->d_norm);
+      CKL();
+    }
     scale_cols_kernel<<<grid1d((size_t)n * cols), 256, 0, st>>>(n, cols, Z, ldz, Z2, ldz2, c->d_norm);
     CKL();
     return 0;
@@ -995,6 +1198,7 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
   psdproj_info* info = run.info;
   cudaStream_t st = run.st;
   const int n = c->n, ld = c->ld, ldm = c->s_max;
+  const int nl = c->nr;  // rows of the tall-skinny blocks held here (n unless row-sharded)
   const double sgn = side == PSDPROJ_SIDE_POS ? 1.0 : -1.0;
   const bool hard = c->prm.locking == PSDPROJ_LOCK_HARD;
   const int g = c->prm.guard;
@@ -1007,22 +1211,20 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
   if (m > c->m_max) return set_err(PSDPROJ_E_CAPACITY, "block %d > m_max %d", m, c->m_max);
   // ---- start block X0 in S[:, :m] and B X0 in BS
   if (cold) {
-    philox_gauss_kernel<<<grid1d(((size_t)n * m + 1) / 2), 256, 0, st>>>(n, m, c->S, ld, c->prm.seed,
-                                                                         (uint32_t)c->calls, c->prm.ctx_id, 0u);
-    CKL();
+    TRY(run.philox(m, c->S, ld, 0u));
   } else {
-    TRY(run.copy_cols(n, m, c->S, ld, c->Xw, ld));
+    TRY(run.copy_cols(nl, m, c->S, ld, c->Xw, ld));
   }
   TRY(run.amul(sgn, A, lda, c->S, ld, m, c->BS, ld));
   // ---- Alg. 3 line 2: Rayleigh-Ritz on span(X0): G = X0^T X0 (I when warm), H = X0^T B X0
-  if (cold) TRY(run.gemm(OP_T, OP_N, m, m, n, 1.0, c->S, ld, c->S, ld, 0.0, c->G, ldm));
-  TRY(run.gemm(OP_T, OP_N, m, m, n, 1.0, c->S, ld, c->BS, ld, 0.0, c->Hm, ldm));
+  if (cold) TRY(run.gram(m, m, c->S, ld, c->S, ld, c->G, ldm));
+  TRY(run.gram(m, m, c->S, ld, c->BS, ld, c->Hm, ldm));
   int rc = run.rr(m, cold ? 0 : m, 0, c->d_thU, m);
   if (rc > 0) return set_err(PSDPROJ_E_DEGENERATE, "start block rank deficient");
   TRY(rc);
   std::vector<double> thU(c->h_d, c->h_d + m);  // all m values (the initial RR keeps m of m)
-  TRY(run.gemm(OP_N, OP_N, n, m, m, 1.0, c->S, ld, c->Cp, ldm, 0.0, c->S2, ld));
-  TRY(run.gemm(OP_N, OP_N, n, m, m, 1.0, c->BS, ld, c->Cp, ldm, 0.0, c->BS2, ld));
+  TRY(run.gemm(OP_N, OP_N, nl, m, m, 1.0, c->S, ld, c->Cp, ldm, 0.0, c->S2, ld));
+  TRY(run.gemm(OP_N, OP_N, nl, m, m, 1.0, c->BS, ld, c->Cp, ldm, 0.0, c->BS2, ld));
   std::swap(c->S, c->S2);
   std::swap(c->BS, c->BS2);
   CK(cudaMemcpyAsync(c->d_thU, c->d_ths, sizeof(double) * m, cudaMemcpyDeviceToDevice, st));
@@ -1035,8 +1237,13 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
   for (;;) {
     // ---- line 5: R = B X - X Theta, r_i = ||R_i|| (unlocked columns)
     TRY(run.mark(6));
-    resid_norm_kernel<256><<<mU, 256, 0, st>>>(n, c->S, ld, c->BS, ld, c->d_thU, c->R, ld, c->d_r);
+    resid_norm_kernel<256><<<mU, 256, 0, st>>>(nl, c->S, ld, c->BS, ld, c->d_thU, c->R, ld, c->d_r, c->sharded ? 1 : 0);
     CKL();
+    if (c->sharded) {  // column sums of squares over the ranks' rows
+      TRY(run.allreduce(c->d_r, mU));
+      sqrt_inplace_kernel<<<cdiv(mU, 256), 256, 0, st>>>(mU, c->d_r);
+      CKL();
+    }
     CK(cudaMemcpyAsync(c->h_d, c->d_r, sizeof(double) * mU, cudaMemcpyDeviceToHost, st));
     TRY(run.sync());
     rU.assign(c->h_d, c->h_d + mU);
@@ -1073,8 +1280,8 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
         keep.push_back(j);
     }
     if (!lock.empty()) {
-      TRY(run.gather(n, (int)lock.size(), c->XL + (size_t)nL * ld, ld, c->S, ld, lock));
-      TRY(run.gather(n, (int)lock.size(), c->BXL + (size_t)nL * ld, ld, c->BS, ld, lock));
+      TRY(run.gather(nl, (int)lock.size(), c->XL + (size_t)nL * ld, ld, c->S, ld, lock));
+      TRY(run.gather(nl, (int)lock.size(), c->BXL + (size_t)nL * ld, ld, c->BS, ld, lock));
       for (int j : lock) {
         thL.push_back(thU[j]);
         rL.push_back(rU[j]);
@@ -1082,14 +1289,14 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
       nL += (int)lock.size();
       // compact U (X, BX, P, BP, theta)
       int nk = (int)keep.size();
-      TRY(run.gather(n, nk, c->T, ld, c->S, ld, keep));
-      TRY(run.copy_cols(n, nk, c->S, ld, c->T, ld));
-      TRY(run.gather(n, nk, c->T, ld, c->BS, ld, keep));
-      TRY(run.copy_cols(n, nk, c->BS, ld, c->T, ld));
-      TRY(run.gather(n, nk, c->T, ld, c->Pb, ld, keep));
-      TRY(run.copy_cols(n, nk, c->Pb, ld, c->T, ld));
-      TRY(run.gather(n, nk, c->T, ld, c->BPb, ld, keep));
-      TRY(run.copy_cols(n, nk, c->BPb, ld, c->T, ld));
+      TRY(run.gather(nl, nk, c->T, ld, c->S, ld, keep));
+      TRY(run.copy_cols(nl, nk, c->S, ld, c->T, ld));
+      TRY(run.gather(nl, nk, c->T, ld, c->BS, ld, keep));
+      TRY(run.copy_cols(nl, nk, c->BS, ld, c->T, ld));
+      TRY(run.gather(nl, nk, c->T, ld, c->Pb, ld, keep));
+      TRY(run.copy_cols(nl, nk, c->Pb, ld, c->T, ld));
+      TRY(run.gather(nl, nk, c->T, ld, c->BPb, ld, keep));
+      TRY(run.copy_cols(nl, nk, c->BPb, ld, c->T, ld));
       std::vector<double> th2, r2;
       std::vector<char> hp2;
       for (int j : keep) {
@@ -1123,29 +1330,29 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
     // W = R_J (+ pending expansion E) and P_J sit contiguously in S: [W E P] at offW; both are
     // projected against the locked block and X_U in one pass (one Gram + one update GEMM each)
     TRY(run.mark(1));
-    TRY(run.gather(n, a, c->S + (size_t)offW * ld, ld, c->R, ld, Jorig));
-    TRY(run.copy_cols(n, qe, c->S + (size_t)offE * ld, ld, c->E, ld));
+    TRY(run.gather(nl, a, c->S + (size_t)offW * ld, ld, c->R, ld, Jorig));
+    TRY(run.copy_cols(nl, qe, c->S + (size_t)offE * ld, ld, c->E, ld));
     int aw = a + qe;
     double* W = c->S + (size_t)offW * ld;
     double* P = c->S + (size_t)offP * ld;
     double* BP = c->BS + (size_t)offP * ld;
     if (ap > 0) {
-      TRY(run.gather(n, ap, P, ld, c->Pb, ld, PJ));
-      TRY(run.gather(n, ap, BP, ld, c->BPb, ld, PJ));
+      TRY(run.gather(nl, ap, P, ld, c->Pb, ld, PJ));
+      TRY(run.gather(nl, ap, BP, ld, c->BPb, ld, PJ));
     }
     const int wp = aw + ap;
     if (hard && nL > 0 && wp > 0) {
-      TRY(run.gemm(OP_T, OP_N, nL, wp, n, 1.0, c->XL, ld, W, ld, 0.0, c->Y, ldm));
-      TRY(run.gemm(OP_N, OP_N, n, wp, nL, -1.0, c->XL, ld, c->Y, ldm, 1.0, W, ld));
-      if (ap > 0) TRY(run.gemm(OP_N, OP_N, n, ap, nL, -1.0, c->BXL, ld, c->Y + (size_t)aw * ldm, ldm, 1.0, BP, ld));
+      TRY(run.gram(nL, wp, c->XL, ld, W, ld, c->Y, ldm));
+      TRY(run.gemm(OP_N, OP_N, nl, wp, nL, -1.0, c->XL, ld, c->Y, ldm, 1.0, W, ld));
+      if (ap > 0) TRY(run.gemm(OP_N, OP_N, nl, ap, nL, -1.0, c->BXL, ld, c->Y + (size_t)aw * ldm, ldm, 1.0, BP, ld));
     }
     if (wp > 0) {  // [W P] <- [W P] - X_U (X_U^T [W P]): the pencil's X-block of G becomes [I 0]
-      TRY(run.gemm(OP_T, OP_N, mU, wp, n, 1.0, c->S, ld, W, ld, 0.0, c->Y, ldm));
-      TRY(run.gemm(OP_N, OP_N, n, wp, mU, -1.0, c->S, ld, c->Y, ldm, 1.0, W, ld));
-      if (ap > 0) TRY(run.gemm(OP_N, OP_N, n, ap, mU, -1.0, c->BS, ld, c->Y + (size_t)aw * ldm, ldm, 1.0, BP, ld));
+      TRY(run.gram(mU, wp, c->S, ld, W, ld, c->Y, ldm));
+      TRY(run.gemm(OP_N, OP_N, nl, wp, mU, -1.0, c->S, ld, c->Y, ldm, 1.0, W, ld));
+      if (ap > 0) TRY(run.gemm(OP_N, OP_N, nl, ap, mU, -1.0, c->BS, ld, c->Y + (size_t)aw * ldm, ldm, 1.0, BP, ld));
     }
-    TRY(run.normalize(n, aw, W, ld, nullptr, 0));
-    if (ap > 0) TRY(run.normalize(n, ap, P, ld, BP, ld));
+    TRY(run.normalize(nl, aw, W, ld, nullptr, 0));
+    if (ap > 0) TRY(run.normalize(nl, ap, P, ld, BP, ld));
     TRY(run.mark(0));
     TRY(run.amul(sgn, A, lda, W, ld, aw, c->BS + (size_t)offW * ld, ld));
     // ---- line 6: Rayleigh-Ritz on span(X, R, P) via the pencil (S^T BS, S^T S)
@@ -1153,7 +1360,7 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
     TRY(run.mark(2));
     TRY(run.gemm(OP_T, OP_N, s - mU, s - mU, n, 1.0, c->S + (size_t)mU * ld, ld, c->S + (size_t)mU * ld, ld, 0.0,
                  c->G + mU + (size_t)mU * ldm, ldm));
-    TRY(run.gemm(OP_T, OP_N, s, s, n, 1.0, c->S, ld, c->BS, ld, 0.0, c->Hm, ldm));
+    TRY(run.gram(s, s, c->S, ld, c->BS, ld, c->Hm, ldm));
     int sU = s;
     rc = run.rr(s, mU, mU, c->d_thU, std::min(mU + qe, s));
     if (rc > 0 && ap > 0) {
@@ -1167,9 +1374,9 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
       if (col < mU || col >= sU) return set_err(PSDPROJ_E_DEGENERATE, "Cholesky-QR failed at pivot %d (s=%d)", rc, sU);
       const int last = sU - 1;
       if (col != last) {
-        swap_cols_kernel<<<grid1d((size_t)n), 256, 0, st>>>(n, c->S, ld, col, last);
+        swap_cols_kernel<<<grid1d((size_t)nl), 256, 0, st>>>(nl, c->S, ld, col, last);
         CKL();
-        swap_cols_kernel<<<grid1d((size_t)n), 256, 0, st>>>(n, c->BS, ld, col, last);
+        swap_cols_kernel<<<grid1d((size_t)nl), 256, 0, st>>>(nl, c->BS, ld, col, last);
         CKL();
         swap_sym_kernel<<<grid1d((size_t)sU), 256, 0, st>>>(sU, c->G, ldm, col, last);
         CKL();
@@ -1187,10 +1394,10 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
     const int rr_npos = run.rr_npos;
     // ---- rotation (a8): X <- S C', BX <- BS C', P <- S_[R P] C'_[R P], BP likewise
     TRY(run.mark(5));
-    TRY(run.gemm(OP_N, OP_N, n, mUn, sU, 1.0, c->S, ld, c->Cp, ldm, 0.0, c->S2, ld));
-    TRY(run.gemm(OP_N, OP_N, n, mUn, sU, 1.0, c->BS, ld, c->Cp, ldm, 0.0, c->BS2, ld));
-    TRY(run.gemm(OP_N, OP_N, n, mUn, sU - mU, 1.0, c->S + (size_t)mU * ld, ld, c->Cp + mU, ldm, 0.0, c->Pb, ld));
-    TRY(run.gemm(OP_N, OP_N, n, mUn, sU - mU, 1.0, c->BS + (size_t)mU * ld, ld, c->Cp + mU, ldm, 0.0, c->BPb, ld));
+    TRY(run.gemm(OP_N, OP_N, nl, mUn, sU, 1.0, c->S, ld, c->Cp, ldm, 0.0, c->S2, ld));
+    TRY(run.gemm(OP_N, OP_N, nl, mUn, sU, 1.0, c->BS, ld, c->Cp, ldm, 0.0, c->BS2, ld));
+    TRY(run.gemm(OP_N, OP_N, nl, mUn, sU - mU, 1.0, c->S + (size_t)mU * ld, ld, c->Cp + mU, ldm, 0.0, c->Pb, ld));
+    TRY(run.gemm(OP_N, OP_N, nl, mUn, sU - mU, 1.0, c->BS + (size_t)mU * ld, ld, c->Cp + mU, ldm, 0.0, c->BPb, ld));
     std::swap(c->S, c->S2);
     std::swap(c->BS, c->BS2);
     CK(cudaMemcpyAsync(c->d_thU, c->d_ths, sizeof(double) * mUn, cudaMemcpyDeviceToDevice, st));
@@ -1207,19 +1414,18 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
     if (p_rr >= mt - g + 1 && mt < n) {
       int qq = std::min(c->q, n - mt);
       if (mt + qq > c->m_max) {  // R18: the block reached the exact-eig regime (m_max = ceil(n/3)+1)
+        if (c->sharded) return set_err(PSDPROJ_E_CAPACITY, "block %d exceeds m_max %d (no DIRECT in sharded mode)", mt + qq, c->m_max);
         abort_direct = true;
         return PSDPROJ_OK;
       }
-      philox_gauss_kernel<<<grid1d(((size_t)n * qq + 1) / 2), 256, 0, st>>>(
-          n, qq, c->E, ld, c->prm.seed, (uint32_t)c->calls, c->prm.ctx_id, (uint32_t)k);
-      CKL();
+      TRY(run.philox(qq, c->E, ld, (uint32_t)k));
       for (int pass = 0; pass < 2; ++pass) {
         if (nL > 0) {
-          TRY(run.gemm(OP_T, OP_N, nL, qq, n, 1.0, c->XL, ld, c->E, ld, 0.0, c->Y, ldm));
-          TRY(run.gemm(OP_N, OP_N, n, qq, nL, -1.0, c->XL, ld, c->Y, ldm, 1.0, c->E, ld));
+          TRY(run.gram(nL, qq, c->XL, ld, c->E, ld, c->Y, ldm));
+          TRY(run.gemm(OP_N, OP_N, nl, qq, nL, -1.0, c->XL, ld, c->Y, ldm, 1.0, c->E, ld));
         }
-        TRY(run.gemm(OP_T, OP_N, mU, qq, n, 1.0, c->S, ld, c->E, ld, 0.0, c->Y, ldm));
-        TRY(run.gemm(OP_N, OP_N, n, qq, mU, -1.0, c->S, ld, c->Y, ldm, 1.0, c->E, ld));
+        TRY(run.gram(mU, qq, c->S, ld, c->E, ld, c->Y, ldm));
+        TRY(run.gemm(OP_N, OP_N, nl, qq, mU, -1.0, c->S, ld, c->Y, ldm, 1.0, c->E, ld));
       }
       qe = qq;
       info->expansions++;
@@ -1240,15 +1446,15 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
   int p = (int)wts.size();
   double* V = c->T;
   double* BV = c->T2;
-  TRY(run.gather(n, (int)lpos.size(), V, ld, c->XL, ld, lpos));
-  TRY(run.gather(n, (int)upos.size(), V + (size_t)lpos.size() * ld, ld, c->S, ld, upos));
+  TRY(run.gather(nl, (int)lpos.size(), V, ld, c->XL, ld, lpos));
+  TRY(run.gather(nl, (int)upos.size(), V + (size_t)lpos.size() * ld, ld, c->S, ld, upos));
   for (int j = 0; j < p; ++j) c->h_d[j] = wts[j];
   CK(cudaMemcpyAsync(c->d_w, c->h_d, sizeof(double) * std::max(p, 1), cudaMemcpyHostToDevice, st));
   double lock_def = 0.0;
   if (hard && nL > 0 && p > 0) {
-    TRY(run.gather(n, (int)lpos.size(), BV, ld, c->BXL, ld, lpos));
-    TRY(run.gather(n, (int)upos.size(), BV + (size_t)lpos.size() * ld, ld, c->BS, ld, upos));
-    TRY(run.gemm(OP_T, OP_N, p, p, n, 1.0, V, ld, BV, ld, 0.0, c->Y, ldm));
+    TRY(run.gather(nl, (int)lpos.size(), BV, ld, c->BXL, ld, lpos));
+    TRY(run.gather(nl, (int)upos.size(), BV + (size_t)lpos.size() * ld, ld, c->BS, ld, upos));
+    TRY(run.gram(p, p, V, ld, BV, ld, c->Y, ldm));
     offdiag_fro_kernel<1024><<<1, 1024, 0, st>>>(p, c->Y, ldm, c->d_w, c->d_scal + 8);
     CKL();
     CK(cudaMemcpyAsync(c->h_d + c->h_d_len - 8, c->d_scal + 8, sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -1263,16 +1469,23 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
   info->npos = p;
   // ---- a11: Pi = V Theta+ V^T (side +) or A + V Theta+ V^T (side -, pairs of -A)
   if (sgn < 0 && Pi != A) {
-    CK(cudaMemcpy2DAsync(Pi, (size_t)ldpi * 8, A, (size_t)lda * 8, (size_t)n * 8, n, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpy2DAsync(Pi, (size_t)ldpi * 8, A, (size_t)lda * 8, (size_t)nl * 8, n, cudaMemcpyDeviceToDevice, st));
   }
-  if (p > 0) {
+  if (p > 0 && !c->sharded) {
     scale_copy_cols_kernel<<<grid1d((size_t)n * p), 256, 0, st>>>(n, p, c->E, ld, V, ld, c->d_w);
     CKL();
     TRY(run.gemm(OP_N, OP_T, n, n, p, 1.0, c->E, ld, V, ld, sgn < 0 ? 1.0 : 0.0, Pi, ldpi));
     symmetrize_kernel<<<grid1d((size_t)n * n), 256, 0, st>>>(n, Pi, ldpi);
     CKL();
+  } else if (p > 0) {
+    // row-sharded: Pi_local = W_local W^T with W = V diag(sqrt(theta+)) (each entry a sum of identical
+    // products in the same order on both sides of the diagonal), W gathered from the ranks
+    scale_sqrt_cols_kernel<<<grid1d((size_t)nl * p), 256, 0, st>>>(nl, p, c->E, ld, V, ld, c->d_w);
+    CKL();
+    TRY(run.gather_full(c->E, ld, p));
+    TRY(run.gemm(OP_N, OP_T, nl, n, p, 1.0, c->E, ld, c->zfull, c->ldn, sgn < 0 ? 1.0 : 0.0, Pi, ldpi));
   } else if (sgn > 0) {
-    CK(cudaMemset2DAsync(Pi, (size_t)ldpi * 8, 0, (size_t)n * 8, n, st));
+    CK(cudaMemset2DAsync(Pi, (size_t)ldpi * 8, 0, (size_t)nl * 8, n, st));
   }
   // ---- a12: warm block for the next call: all columns by theta desc, first p + extra
   struct Col { double th; int src; int j; };
@@ -1288,12 +1501,12 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
     if (cols[i].src == 0) { li.push_back(cols[i].j); pos_l.push_back(i); }
     else { ui.push_back(cols[i].j); pos_u.push_back(i); }
   }
-  TRY(run.gather(n, (int)li.size(), c->T2, ld, c->XL, ld, li));
-  TRY(run.gather(n, (int)ui.size(), c->T2 + (size_t)li.size() * ld, ld, c->S, ld, ui));
+  TRY(run.gather(nl, (int)li.size(), c->T2, ld, c->XL, ld, li));
+  TRY(run.gather(nl, (int)ui.size(), c->T2 + (size_t)li.size() * ld, ld, c->S, ld, ui));
   std::vector<int> perm(keepn);  // Xw[:, pos] = T2[:, staged index]
   for (size_t i = 0; i < pos_l.size(); ++i) perm[pos_l[i]] = (int)i;
   for (size_t i = 0; i < pos_u.size(); ++i) perm[pos_u[i]] = (int)(li.size() + i);
-  TRY(run.gather(n, keepn, c->Xw, ld, c->T2, ld, perm));
+  TRY(run.gather(nl, keepn, c->Xw, ld, c->T2, ld, perm));
   c->m_warm = keepn;
   c->th_warm.clear();
   for (int i = 0; i < keepn; ++i) c->th_warm.push_back(cols[i].th);
@@ -1313,12 +1526,22 @@ static int project_impl(psdproj_ctx c, const double* A, int lda, double* Pi, int
                         psdproj_info* info) {
   int n = c->n;
   // first pass: non-finite check and ||A||_F (deterministic partials, host sums in order)
-  int nb = std::min(sms() * 2, std::max(1, (int)(((size_t)n * n + 255) / 256)));
+  const int nl = c->nr;
+  int nb = c->sharded ? sms() * 2 : std::min(sms() * 2, std::max(1, (int)(((size_t)nl * n + 255) / 256)));
   CK(cudaMemsetAsync(c->d_status + 8, 0, sizeof(int), st));
-  nonfinite_kernel<<<nb, 256, 0, st>>>(n, A, lda, c->d_status + 8);
+  nonfinite_kernel<<<nb, 256, 0, st>>>(nl, n, A, lda, c->d_status + 8);
   CKL();
-  fro_partial_kernel<<<nb, 256, 0, st>>>(n, A, lda, c->T2);
+  fro_partial_kernel<<<nb, 256, 0, st>>>(nl, n, A, lda, c->T2);
   CKL();
+  if (c->sharded) {  // every rank needs the global ||A||_F and the non-finite flag
+    int* flag = c->d_status + 8;
+    double* fl = c->T2 + nb;
+    i2d_kernel<<<1, 32, 0, st>>>(flag, fl);
+    CKL();
+    NK(g_nccl.allReduce(c->T2, c->T2, (size_t)nb + 1, ncclFloat64, ncclSum, c->comm, st));
+    d2i_kernel<<<1, 32, 0, st>>>(fl, flag);
+    CKL();
+  }
   CK(cudaMemcpyAsync(c->h_d, c->T2, sizeof(double) * nb, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(c->h_i + c->h_i_len - 32, c->d_status + 8, sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -1336,6 +1559,8 @@ static int project_impl(psdproj_ctx c, const double* A, int lda, double* Pi, int
     int mstart = (c->warm && c->block_side == mode) ? c->m_warm : c->m0;
     if (3 * mstart >= n) mode = PSDPROJ_SIDE_DIRECT;  // R18
   }
+  if (mode == PSDPROJ_SIDE_DIRECT && c->sharded)
+    return set_err(PSDPROJ_E_CAPACITY, "the one-third rule selects the exact eigensolver (PAPER.md:505), which the row-sharded mode does not provide");
   int rc;
   if (mode == PSDPROJ_SIDE_DIRECT) {
     rc = direct_path(run, A, lda, Pi, ldpi);
@@ -1382,7 +1607,7 @@ extern "C" int psdproj_project(psdproj_ctx c, const double* A, int lda, double* 
   std::memset(info, 0, sizeof(*info));
   if (!c) return info->status = set_err(PSDPROJ_E_INVALID, "ctx NULL");
   if (c->poisoned) return info->status = set_err(PSDPROJ_E_CUDA, "context poisoned by an earlier CUDA error");
-  if (!A || !Pi || lda < c->n || ldpi < c->n || !(tol > 0.0) || !std::isfinite(tol))
+  if (!A || !Pi || lda < c->nr || ldpi < c->nr || !(tol > 0.0) || !std::isfinite(tol))
     return info->status = set_err(PSDPROJ_E_INVALID, "invalid arguments (lda=%d ldpi=%d tol=%g)", lda, ldpi, tol);
   if ((const void*)Pi == (const void*)A && lda != ldpi)
     return info->status = set_err(PSDPROJ_E_INVALID, "aliased Pi needs ldpi == lda");
@@ -1397,7 +1622,7 @@ extern "C" int psdproj_project_host(psdproj_ctx c, const double* A_host, int lda
   psdproj_info local;
   if (!info) info = &local;
   std::memset(info, 0, sizeof(*info));
-  if (!c || !c->stage) return info->status = set_err(PSDPROJ_E_INVALID, "ctx NULL or created without host_io");
+  if (!c || !c->stage || c->sharded) return info->status = set_err(PSDPROJ_E_INVALID, "ctx NULL, sharded, or created without host_io");
   if (!A_host || !Pi_host || lda < c->n || ldpi < c->n) return info->status = set_err(PSDPROJ_E_INVALID, "invalid arguments");
   cudaStream_t st = (cudaStream_t)stream;
   int n = c->n, ld = c->ld;
@@ -1487,8 +1712,8 @@ extern "C" int psdproj_get_ritz(psdproj_ctx c, double* vals_host, int cap, doubl
   if (vals_host)
     for (int i = 0; i < k; ++i) vals_host[i] = c->th_warm[i];
   if (vecs_dev && k > 0) {
-    if (ldv < c->n) return set_err(PSDPROJ_E_INVALID, "ldv < n");
-    CK(cudaMemcpy2D(vecs_dev, (size_t)ldv * 8, c->Xw, (size_t)c->ld * 8, (size_t)c->n * 8, k, cudaMemcpyDeviceToDevice));
+    if (ldv < c->nr) return set_err(PSDPROJ_E_INVALID, "ldv < rows held by this context");
+    CK(cudaMemcpy2D(vecs_dev, (size_t)ldv * 8, c->Xw, (size_t)c->ld * 8, (size_t)c->nr * 8, k, cudaMemcpyDeviceToDevice));
   }
   return k;
 }

@@ -185,3 +185,23 @@ def test_full_size_sampled_entries(api):
         missed = np.sqrt(np.sum(pos[info["npos"]:] ** 2)) if info["npos"] < pos.size else 0.0
         assert np.abs(got - ref).max() <= info["err_bound"] + missed + 1e-9
         assert info["launches"] > 0
+
+
+def test_row_sharded_single_rank_matches_unsharded(api):
+    """Row-sharded mode (§8.e) with one rank: NCCL all-gathers / all-reduces on a 1-rank
+    communicator; same iterates as the unsharded context, Pi = W W^T exactly symmetric, and the
+    projection matches the oracle."""
+    cfg = C1()
+    uid = api.nccl_uid()
+    sh = api.ShardedContext(cfg.n, 0, cfg.n, uid, 0, 1, params=api.default_params(seed=13))
+    un = api.Context(cfg.n, params=api.default_params(seed=13))
+    for t, A, _ in drift_sequence(cfg, steps=3):
+        Ad = _dev(A)
+        Ps, info_s = sh.project(api.colmajor_copy(Ad), 1e-10)
+        Pu, info_u = un.project(Ad, 1e-10)
+        Ps = Ps.cpu().numpy()
+        assert info_s["iters"] == info_u["iters"] and info_s["npos"] == info_u["npos"]
+        assert np.array_equal(Ps, Ps.T)
+        assert np.linalg.norm(Ps - Pu.cpu().numpy()) <= 1e-12 * np.linalg.norm(A)
+        assert np.linalg.norm(Ps - project_exact(A)) / np.linalg.norm(A) <= 1e-9
+    sh.close()

@@ -79,3 +79,59 @@ def test_gloo_world2_sharding():
     assert not set(got[0]) & set(got[1])
     assert mx[0] == 11.0 and sm[1] == 512.0 and mx[2] == 1.0
     assert max(loads) / min(loads) < 1.01   # 512 blocks balance to well under 1%
+
+
+# ---------------------------------------------------------------- row-sharded single matrix (§8.e)
+def test_row_blocks_partition():
+    from paper_1912_02767_b200.api import row_blocks
+    for n, world in ((4000, 8), (4001, 3), (7, 4), (5, 5)):
+        blocks = row_blocks(n, world)
+        assert blocks[0][0] == 0 and sum(r for _, r in blocks) == n
+        assert all(blocks[k + 1][0] == blocks[k][0] + blocks[k][1] for k in range(world - 1))
+        assert max(r for _, r in blocks) - min(r for _, r in blocks) <= 1
+
+
+def _gram_worker(rank, world, port, out):
+    """Host reference of the sharded math the library runs over NCCL: every Gram S^T (B S) is the
+    sum of the row-block partials, the column norms are sums of squares, and the gathered block
+    multiply A_local Z_full equals the row block of A Z."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1912_02767_b200.api import row_blocks
+    rng = np.random.default_rng(0)
+    n, s = 97, 11
+    M = rng.standard_normal((n, n))
+    A = (M + M.T) / 2
+    S = rng.standard_normal((n, s))
+    r0, nr = row_blocks(n, world)[rank]
+    Sl = S[r0:r0 + nr]
+    # all-gather of the local rows (rank order) -> full S; A_local S_full = rows of A S
+    parts = [None] * world
+    dist.all_gather_object(parts, Sl)
+    Sfull = np.vstack(parts)
+    Yl = A[r0:r0 + nr] @ Sfull
+    G = torch.from_numpy(Sl.T @ Yl)
+    dist.all_reduce(G)
+    cn = torch.from_numpy((Sl ** 2).sum(axis=0))
+    dist.all_reduce(cn)
+    if rank == 0:
+        out.put((G.numpy(), np.sqrt(cn.numpy()), S.T @ (A @ S), np.linalg.norm(S, axis=0)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_sharded_gram_identity():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gram_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    G, cn, Gref, cnref = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert np.abs(G - Gref).max() <= 1e-12 * np.abs(Gref).max()
+    assert np.abs(cn - cnref).max() <= 1e-13 * cnref.max()
