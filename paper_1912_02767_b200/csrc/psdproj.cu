@@ -192,9 +192,12 @@ static int dgemm(cudaStream_t st, int opA, int opB, int M, int N, int K, double 
     static int tile = -1;
     if (tile < 0) tile = getenv("PSDPROJ_GEMM_TILE") ? atoi(getenv("PSDPROJ_GEMM_TILE")) : 64;
     const bool big = tile == 128 && M >= 1024 && N >= 48;
-#define GK(OA, OB)                                                                                              \
-  return big ? gemm_kp_launch<OA, OB, 128, 64, 4>(st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, part, part_elems) \
-             : gemm_kp_launch<OA, OB, 64, 64, 4>(st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, part, part_elems)
+    // narrow tiles when a 64-wide last column tile would be at most half used (N mod 64 in 1..32)
+    const bool narrow = !big && N <= 96 && (N % 64) != 0 && (N % 64) <= 32;
+#define GK(OA, OB)                                                                                                     \
+  return big      ? gemm_kp_launch<OA, OB, 128, 64, 4>(st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, part, part_elems) \
+         : narrow ? gemm_kp_launch<OA, OB, 64, 32, 4>(st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, part, part_elems)  \
+                  : gemm_kp_launch<OA, OB, 64, 64, 4>(st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, part, part_elems)
     if (opA == OP_N && opB == OP_N) GK(OP_N, OP_N);
     if (opA == OP_T && opB == OP_N) GK(OP_T, OP_N);
     if (opA == OP_N && opB == OP_T) GK(OP_N, OP_T);
@@ -943,8 +946,11 @@ struct Run {
       CK(cudaEventRecord(c->ev[2 * nev], st));
     }
     {
-      int rc_ = gemm_kp_launch<OP_N, OP_N, 64, 64, 4, 1>(st, nl, k, n, sgn, A, lda, Z, ldz, 0.0, Y, ldy, c->part,
-                                                         c->part_elems);
+      const bool narrow = k <= 96 && (k % 64) != 0 && (k % 64) <= 32;
+      int rc_ = narrow ? gemm_kp_launch<OP_N, OP_N, 64, 32, 4, 1>(st, nl, k, n, sgn, A, lda, Z, ldz, 0.0, Y, ldy,
+                                                                  c->part, c->part_elems)
+                       : gemm_kp_launch<OP_N, OP_N, 64, 64, 4, 1>(st, nl, k, n, sgn, A, lda, Z, ldz, 0.0, Y, ldy,
+                                                                  c->part, c->part_elems);
       if (rc_ < 0) return rc_;
     }
     if (prof) {

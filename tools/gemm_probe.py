@@ -10,7 +10,7 @@ import torch
 from paper_1912_02767_b200 import api
 
 n = 4000
-shapes = [("a3 NN", 0, 0, n, k, n) for k in (16, 32, 64, 128, 150, 200, 300)] + [
+shapes = [("a3 NN", 0, 0, n, k, n) for k in (16, 32, 64, 87, 100, 128, 150, 200, 300)] + [
     ("gram TN", 1, 0, 400, 400, n), ("gram TN", 1, 0, 200, 200, n), ("rot NN", 0, 0, n, 200, 400),
     ("rot NN", 0, 0, n, 130, 330), ("orth NN", 0, 0, n, 110, 130), ("Pi NT", 0, 1, n, n, 200)]
 ws = torch.empty(1 << 25, dtype=torch.float64, device="cuda")
