@@ -243,9 +243,12 @@ __global__ void tri_bisect_kernel(int s, int m, const double* __restrict__ dg, c
   }
   const int k = s - 1 - ks;  // ascending index: count(lo) <= k < count(hi)
   double lo = bounds[0], hi = bounds[1];
+  // absolute accuracy u ||T|| suffices: the Rayleigh-Ritz values enter absolute residual tests, and
+  // bisection to a relative tolerance near zero would add rounds for no gain (dstebz's ABSTOL)
+  const double atol = 4.0 * PSD_U * fmax(fabs(lo), fabs(hi));
   for (int it = 0; it < 64; ++it) {
     double w = hi - lo;
-    if (w <= 2.0 * PSD_U * fmax(fabs(lo), fabs(hi)) + 4.0 * pivmin) break;
+    if (w <= fmax(2.0 * PSD_U * fmax(fabs(lo), fabs(hi)), atol) + 4.0 * pivmin) break;
     double x = lo + w * (double)(lane + 1) / 33.0;
     int c = sturm_count(s, d, e2, x, pivmin);
     unsigned below = __ballot_sync(0xffffffffu, c <= k);  // x still at or below the target
