@@ -164,6 +164,26 @@ def sum_over_ranks(dist, v):
     return float(t.item())
 
 
+PHASES = ["a3_block_multiply", "w_p_projection", "gram_pencil", "cholesky_pencil", "rr_tridiagonal", "rotation",
+          "residual_norms", "host_locking_assembly", "rr_bisection", "rr_inverse_iteration", "rr_back_transform",
+          "rr_reorth_and_coeffs"]
+
+
+def dominant_phase(infos, K, ms_step):
+    """The phase that dominates a step (library profile bit 1, CUDA events on the launching stream).
+    At n = 4000 it is the Rayleigh-Ritz tridiagonalisation: latency-bound (two cluster barriers and
+    two DSMEM round trips per Householder step), so its roof is the barrier/DSMEM floor measured by
+    tools/micro/cluster_bench.cu (profiles/cluster_bench_r01.txt), not HBM or FP64."""
+    tot = [sum(i["phase_ms"][k] for i in infos) / K for k in range(len(PHASES))]
+    k = max(range(len(PHASES)), key=lambda j: tot[j])
+    out = {"phase": PHASES[k], "ms_per_step": round(tot[k], 3), "share": round(tot[k] / ms_step, 4)}
+    if PHASES[k] == "rr_tridiagonal":
+        out.update({"bound": "latency", "kernel": "tridiag_cluster_kernel (16-CTA cluster, DSMEM)",
+                    "floor_note": "per Householder step >= 2 x (cluster barrier ~560 cyc + DSMEM round trip ~600 cyc) "
+                                  "= ~2.3k cycles; measured ~8k cycles/step at s = 400 (PSDPROJ_TRI_PROF)"})
+    return out
+
+
 def cpu_baseline(cfg, tol, args, gpu_iters):
     """The oracle as it stands (oracle/lobpcg.py) on a bounded sample of the same workload:
     one warm projection of step 1 started from the exact top block of step 0 (planted Q),
@@ -457,6 +477,7 @@ def main():
                 ["a3_block_multiply", "w_p_projection", "gram_pencil", "cholesky_pencil", "rr_tridiagonal",
                  "rotation", "residual_norms", "host_locking_assembly", "rr_bisection", "rr_inverse_iteration",
                  "rr_back_transform", "rr_reorth_and_coeffs"])},
+            "dominant_phase": dominant_phase(infos, K, ms / K),
             "iters_per_projection": {"mean": statistics.mean(iters), "min": min(iters), "max": max(iters),
                                      "cold": infos_warm[0]["iters"]},
             "status": [i["status"] for i in infos],
