@@ -36,7 +36,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c3r", choices=["c3r", "c1", "c2", "c3", "c4"])
+    ap.add_argument("--workload", default="c3r", choices=["c3r", "c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--c4-blocks", type=int, default=512)
     ap.add_argument("--shard", action="store_true",
                     help="row-shard the single matrix across the ranks (NCCL inside libpsdproj; strong scaling)")
@@ -275,6 +275,45 @@ def run_c4_bench(args, rank, world, local, dist):
         dist.destroy_process_group()
 
 
+def run_c5_bench(args, rank, world, local, dist):
+    """BASELINE configs[4] (f1): approximate ADMM (Alg. 1) on the MaxCut SDP of an Erdos-Renyi
+    graph, n = 2000, p = 0.01, +-1 weights, to primal/dual residual 1e-4 (R33); one warm LOBPCG
+    projection of the 2000 x 2000 block per ADMM iteration with tolerance 10/k^1.01.
+    One step = one ADMM iteration; the whole solve is timed (device events around the loop)."""
+    import torch
+    from paper_1912_02767_b200.admm import MaxCutADMM
+    from workloads.generators import maxcut_graph
+    n = args.n or 2000
+    L = maxcut_graph(n=n, p_edge=0.01, seed=501)
+    solver = MaxCutADMM(L, device=f"cuda:{local}")
+    for _ in range(max(args.warmup, 0)):
+        solver.step()
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    k0 = solver.k
+    out = solver.solve(eps=1e-4, max_iter=args.max_iter if args.max_iter != 500 else 5000)
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    its = solver.k - k0
+    if rank == 0:
+        infos = solver.infos
+        line = {"metric": "MaxCut SDP approximate-ADMM iterations/sec (one warm LOBPCG projection each), n=2000",
+                "value": its / (ms / 1e3), "unit": "ADMM iterations/s", "n_gpus": 1, "steps": its,
+                "warmup": args.warmup, "ms_per_step": ms / max(its, 1), "higher_is_better": True,
+                "scaling": "none", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": f"C5 MaxCut SDP, ER n={n}, p=0.01, +-1 weights (configs[4]), eps 1e-4",
+                           "rho": solver.rho, "sigma": solver.sigma, "alpha": solver.alpha},
+                "solve_s": ms / 1e3, "admm_iters": out["iters"], "r_prim": out["r_prim"], "r_dual": out["r_dual"],
+                "objective": out["objective"],
+                "lobpcg_iters_per_admm_iter": sum(i["iters"] for i in infos) / max(len(infos), 1),
+                "sides": sorted(set(i["side"] for i in infos)), "cold_calls": sum(i["cold"] for i in infos)}
+        print(json.dumps(line), flush=True)
+    solver.close()
+
+
 def run_sharded_bench(args, rank, world, local, dist):
     """One C3-R matrix row-sharded over the ranks: rank r holds a contiguous row block
     of every input; per iteration the library all-gathers W and all-reduces the Gram partials.
@@ -347,6 +386,9 @@ def main():
     rank, world, local, dist = dist_setup(args)
     if args.workload == "c4":
         run_c4_bench(args, rank, world, local, dist)
+        return
+    if args.workload == "c5":
+        run_c5_bench(args, rank, world, local, dist)
         return
     if args.shard:
         run_sharded_bench(args, rank, world, local, dist)

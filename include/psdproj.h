@@ -155,6 +155,21 @@ int psdproj_destroy(psdproj_ctx ctx);
 /* Thread-local message of the last error ("" if none). */
 const char* psdproj_last_error(void);
 
+/* ---- f1: approximate ADMM (Alg. 1) for the MaxCut SDP (BASELINE configs[4]) ----
+ * min <Q, X> s.t. diag(X) = 1, X in S+, as A x = z, z in C = {1}^n x S+ with A = [D; I], P = 0.
+ * step1: the elementwise KKT solve of line 3 (A^T A is diagonal), the relaxation of line 4, and the
+ * projection input V = alpha X~ + (1 - alpha) Zp + Yp / rho of line 5 (Zh = the relaxed z-hat,
+ * zeh its diagonal part). The caller projects V with psdproj_project (Zp <- Pi(V), tolerance
+ * 10/k^1.01). step2: the dual update of line 6 and the residual maxima
+ * res_host[0..2] = (max|X - Zp|, max|diag X - 1|, max|Q + Yp + Diag(ye)|) (host, synchronous).
+ * All matrices n x n, column-major, ld, device; ye, zeh length n, device. Reading R43. */
+int psdproj_admm_maxcut_step1(int n, double* X, const double* Zp, const double* Yp, const double* ye,
+                              const double* Q, int ld, double sigma, double rho, double alpha, double* Zh,
+                              double* V, double* zeh, void* stream);
+int psdproj_admm_maxcut_step2(int n, const double* X, const double* Zp, const double* Zh, double* Yp, double* ye,
+                              const double* zeh, const double* Q, int ld, double rho, double* res_host,
+                              void* stream);
+
 /* ---- kernel-level entry points (tests and benchmarks call the same kernels the path uses) ---- */
 
 /* C = alpha op(A) op(B) + beta C, column-major, opA/opB: 0 = N, 1 = T. ws: device scratch of

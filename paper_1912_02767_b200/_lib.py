@@ -21,7 +21,7 @@ EXPORTS = [
     "psdproj_destroy", "psdproj_last_error", "psdproj_dgemm", "psdproj_jacobi_ws_elems",
     "psdproj_jacobi", "psdproj_philox_raw", "psdproj_philox_gauss", "psdproj_eigh_ws_elems",
     "psdproj_eigh", "psdproj_cholesky", "psdproj_get_nccl_uid", "psdproj_workspace_bytes_sharded",
-    "psdproj_create_sharded",
+    "psdproj_create_sharded", "psdproj_admm_maxcut_step1", "psdproj_admm_maxcut_step2",
 ]
 
 
@@ -89,6 +89,8 @@ def load(path=SO_PATH):
     L.psdproj_eigh.argtypes = [i, vp, i, i, vp, vp, i, vp, vp, vp]
     L.psdproj_cholesky.argtypes = [i, vp, i, vp]
     L.psdproj_get_nccl_uid.argtypes = [vp]
+    L.psdproj_admm_maxcut_step1.argtypes = [i, vp, vp, vp, vp, vp, i, d, d, d, vp, vp, vp, vp]
+    L.psdproj_admm_maxcut_step2.argtypes = [i, vp, vp, vp, vp, vp, vp, vp, i, d, P(d), vp]
     L.psdproj_workspace_bytes_sharded.argtypes = [i, i, i, P(Params)]
     L.psdproj_workspace_bytes_sharded.restype = sz
     L.psdproj_create_sharded.argtypes = [i, i, i, vp, i, i, P(Params), vp, sz, P(vp)]

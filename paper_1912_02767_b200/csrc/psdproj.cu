@@ -484,6 +484,13 @@ static int eigh_top(cudaStream_t st, int s, const double* Hs, int ldh, int m, do
               s, tcs, r, h[r * 8 + 0] / (s - 2), h[r * 8 + 1] / (s - 2), h[r * 8 + 2] / (s - 2), h[r * 8 + 3] / (s - 2),
               h[r * 8 + 4] / (s - 2), h[r * 8 + 5] / (s - 2), h[r * 8 + 6] / (s - 2));
   }
+  static int dbg_eigh = getenv("PSDPROJ_DEBUG_EIGH") ? 1 : 0;
+  if (dbg_eigh) {
+    double hb[4] = {0, 0, 0, 0};
+    cudaError_t e0 = cudaStreamSynchronize(st);
+    cudaMemcpy(hb, w.td, sizeof(double) * std::min(s, 4), cudaMemcpyDeviceToHost);
+    fprintf(stderr, "eigh s=%d m=%d mgs=%d tcs=%d sync=%s d0=%g\n", s, m, (int)mgs, tcs, cudaGetErrorString(e0), hb[0]);
+  }
   TRY(w.mark(8));
   tri_prep_kernel<<<1, 1024, 0, st>>>(s, w.td, w.te, w.te2, w.tbounds);
   CKL();
@@ -1330,6 +1337,28 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
     }
     int a = (int)Jorig.size();
     int ap = (int)PJ.size();
+    if (mU + a + qe + ap == 0) {
+      // every column is locked and no direction is left, but the guard test (R12) is not met: the
+      // block has no non-positive column -- draw the expansion block now (Alg. 3 line 8, R8)
+      const int mt = nL;
+      if (mt >= n) {
+        status = PSDPROJ_OK;
+        break;
+      }
+      const int qq = std::min(c->q, n - mt);
+      if (mt + qq > c->m_max) {
+        if (c->sharded) return set_err(PSDPROJ_E_CAPACITY, "block %d exceeds m_max %d", mt + qq, c->m_max);
+        abort_direct = true;
+        return PSDPROJ_OK;
+      }
+      TRY(run.philox(qq, c->E, ld, (uint32_t)(k + 1) | 0x80000000u));
+      for (int pass = 0; pass < 2 && nL > 0; ++pass) {
+        TRY(run.gram(nL, qq, c->XL, ld, c->E, ld, c->Y, ldm));
+        TRY(run.gemm(OP_N, OP_N, nl, qq, nL, -1.0, c->XL, ld, c->Y, ldm, 1.0, c->E, ld));
+      }
+      qe = qq;
+      info->expansions++;
+    }
     int offW = mU, offE = mU + a, offP = mU + a + qe;
     int s = offP + ap;
     if (s > c->s_max) return set_err(PSDPROJ_E_CAPACITY, "RR basis %d > s_max %d", s, c->s_max);
@@ -1834,4 +1863,33 @@ extern "C" int psdproj_cholesky(int t, double* G, int ld, void* stream) {
   CK(cudaFreeAsync(gs, st));
   CK(cudaStreamSynchronize(st));
   return rc < 0 ? rc : h;
+}
+
+// ------------------------------------------------------------------ f1: approximate ADMM (MaxCut SDP)
+extern "C" int psdproj_admm_maxcut_step1(int n, double* X, const double* Zp, const double* Yp, const double* ye,
+                                         const double* Q, int ld, double sigma, double rho, double alpha, double* Zh,
+                                         double* V, double* zeh, void* stream) {
+  if (n <= 0 || ld < n || !X || !Zp || !Yp || !ye || !Q || !Zh || !V || !zeh || !(rho > 0.0) || !(sigma >= 0.0) ||
+      !(alpha > 0.0 && alpha < 2.0))
+    return set_err(PSDPROJ_E_INVALID, "invalid admm step1 arguments");
+  admm_maxcut_step1_kernel<<<grid1d((size_t)n * n), 256, 0, (cudaStream_t)stream>>>(n, X, Zp, Yp, ye, Q, sigma, rho,
+                                                                                     alpha, Zh, V, zeh, ld);
+  CKL();
+  return 0;
+}
+
+extern "C" int psdproj_admm_maxcut_step2(int n, const double* X, const double* Zp, const double* Zh, double* Yp,
+                                         double* ye, const double* zeh, const double* Q, int ld, double rho,
+                                         double* res_host, void* stream) {
+  if (n <= 0 || ld < n || !X || !Zp || !Zh || !Yp || !ye || !zeh || !Q || !res_host || !(rho > 0.0))
+    return set_err(PSDPROJ_E_INVALID, "invalid admm step2 arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  static thread_local unsigned long long* dres = nullptr;
+  if (!dres) CK(cudaMalloc(&dres, 4 * sizeof(unsigned long long)));
+  CK(cudaMemsetAsync(dres, 0, 3 * sizeof(unsigned long long), st));
+  admm_maxcut_step2_kernel<<<grid1d((size_t)n * n), 256, 0, st>>>(n, X, Zp, Zh, Yp, ye, zeh, Q, rho, ld, dres);
+  CKL();
+  CK(cudaMemcpyAsync(res_host, dres, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return 0;
 }

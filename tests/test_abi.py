@@ -14,7 +14,7 @@ HDR = os.path.join(ROOT, "include", "psdproj.h")
 def declared_functions():
     txt = open(HDR).read()
     txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
-    return sorted(set(re.findall(r"\b(psdproj_[a-z_]+)\s*\(", txt)))
+    return sorted(set(re.findall(r"\b(psdproj_[a-z0-9_]+)\s*\(", txt)))
 
 
 @pytest.fixture(scope="module")
