@@ -65,6 +65,7 @@ static thread_local long long g_launches = 0;  // kernels issued by this thread 
   } while (0)
 
 static inline int rup(int x, int a) { return (x + a - 1) / a * a; }
+constexpr int EIG_MAX = 2048;  // largest dense eigenproblem of the RR / DIRECT eigensolver
 
 // ------------------------------------------------------------------ NCCL (row-sharded mode, §8.e)
 // Loaded on first use with dlopen (the library in the process -- torch's -- or PSDPROJ_NCCL_LIB), so
@@ -367,6 +368,9 @@ static int cla_attrs() {
   CK(cudaFuncSetAttribute(backtransform_panel_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, bmx));
   CK(cudaFuncSetAttribute(backtransform_panel_kernel<24>, cudaFuncAttributeMaxDynamicSharedMemorySize, bmx));
   CK(cudaFuncSetAttribute(backtransform_panel_kernel<BT_PER_LANE>, cudaFuncAttributeMaxDynamicSharedMemorySize, bmx));
+  CK(cudaFuncSetAttribute(backtransform_panel_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, bmx));
+  CK(cudaFuncSetAttribute(tridiag_cluster_kernel<64, 256, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  CK(cudaFuncSetAttribute(tridiag_cluster_kernel<64, 256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   done = true;
   return 0;
 }
@@ -438,7 +442,7 @@ static int eigh_top(cudaStream_t st, int s, const double* Hs, int ldh, int m, do
     CK(cudaFuncSetAttribute(tri_bisect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     attr = true;
   }
-  if (s > 32 * TRI_BT_PER_LANE) return set_err(PSDPROJ_E_CAPACITY, "eigensolver supports s <= %d", 32 * TRI_BT_PER_LANE);
+  if (s > EIG_MAX) return set_err(PSDPROJ_E_CAPACITY, "eigensolver supports s <= %d", EIG_MAX);
   static int tri_mode = -1;  // 0 auto, 1 force one-CTA
   if (tri_mode < 0) tri_mode = getenv("PSDPROJ_TRI_ONECTA") ? 1 : 0;
   int tcs = (tri_mode == 0 && s > 64) ? cla_cluster_size(s, tri_smem_doubles) : 0;
@@ -459,13 +463,15 @@ static int eigh_top(cudaStream_t st, int s, const double* Hs, int ldh, int m, do
       TRI_LAUNCH(14, 256, false, tcs, tsm);
     else
       TRI_LAUNCH(20, 256, false, tcs, tsm);
-  } else if (tri_mode == 0 && s > 64 && s <= 32 * TRI_BT_PER_LANE) {
+  } else if (tri_mode == 0 && s > 64 && s <= EIG_MAX) {
     // too large for shared memory: own columns in the L2-resident scratch tG (16-CTA cluster)
     const size_t tsm = tri_smem_doubles_ga(s, 16) * sizeof(double);
     if (s <= 32 * 24)
       TRI_LAUNCH(24, 256, true, 16, tsm);
-    else
+    else if (s <= 32 * 40)
       TRI_LAUNCH(40, 256, true, 16, tsm);
+    else
+      TRI_LAUNCH(64, 256, true, 16, tsm);
   } else {
     const size_t vecs = (size_t)s * 10;
     size_t dyn = ((s <= TRI_SMEM_MAX) ? (size_t)s * (s + 1) : 0) + vecs;
@@ -546,8 +552,10 @@ static int eigh_top(cudaStream_t st, int s, const double* Hs, int ldh, int m, do
       backtransform_panel_kernel<16><<<cdiv(m, 8), 256, bsm, st>>>(s, m, w.Vh, w.ldv, w.ttau, Yv, ldy, pb);
     else if (s <= 32 * 24)
       backtransform_panel_kernel<24><<<cdiv(m, 8), 256, bsm, st>>>(s, m, w.Vh, w.ldv, w.ttau, Yv, ldy, pb);
-    else
+    else if (s <= 32 * BT_PER_LANE)
       backtransform_panel_kernel<BT_PER_LANE><<<cdiv(m, 8), 256, bsm, st>>>(s, m, w.Vh, w.ldv, w.ttau, Yv, ldy, pb);
+    else
+      backtransform_panel_kernel<64><<<cdiv(m, 8), 256, bsm, st>>>(s, m, w.Vh, w.ldv, w.ttau, Yv, ldy, pb);
     }
     CKL();
   }
@@ -637,6 +645,8 @@ static void resolve(int n, const psdproj_params* in, psdproj_params& p, int& m0,
   // default capacity n/3: a wider block is the exact-eig regime anyway (R18)
   m_max = p.m_max > 0 ? std::min(p.m_max, n) : std::min(n, (n + 2) / 3 + 1);
   m_max = std::max(m_max, std::min(n, m0));
+  m_max = std::max(1, std::min(m_max, (EIG_MAX - q) / 3));  // the RR basis (<= 3 m + q) must fit the eigensolver
+  m0 = std::min(m0, m_max);
   s_max = 3 * m_max + q;
   NJ = sharded ? s_max : std::max(s_max, n);  // the sharded mode has no DIRECT path
   NJ += NJ & 1;
@@ -1129,7 +1139,7 @@ static int direct_path(Run& run, const double* A, int lda, double* Pi, int ldpi)
   double* V = c->T;
   static int dmode = -1;  // 1: Jacobi for DIRECT (PSDPROJ_RR=jacobi)
   if (dmode < 0) dmode = (getenv("PSDPROJ_RR") && std::string(getenv("PSDPROJ_RR")) == "jacobi") ? 1 : 0;
-  if (dmode == 0 && n <= 32 * TRI_BT_PER_LANE) {
+  if (dmode == 0 && n <= EIG_MAX) {
     // tridiagonal eigensolver, all n pairs, descending; order = identity
     TRY(run.tri_eig(n, A, lda, n, c->d_ths, V, ld, c->tnpos, false));
     CK(cudaMemcpyAsync(c->h_d + c->h_d_len - 16, c->d_scal + 16, sizeof(double), cudaMemcpyDeviceToHost, st));

@@ -74,7 +74,7 @@ def test_philox_gauss_matches_oracle(api):
 
 
 @pytest.mark.parametrize("s,m", [(1, 1), (2, 2), (3, 1), (17, 17), (64, 20), (160, 60), (161, 161), (300, 100),
-                                 (500, 170), (640, 220), (641, 120), (800, 260), (1100, 300)])
+                                 (500, 170), (640, 220), (641, 120), (800, 260), (1100, 300), (2000, 200)])
 def test_eigh_tridiagonal(api, s, m):
     rng = np.random.default_rng(1000 + s)
     M = rng.standard_normal((s, s))

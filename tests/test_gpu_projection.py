@@ -44,7 +44,8 @@ def test_planted_parity(api, n, p, side):
 
 
 # ---------------------------------------------------------------- edge cases
-@pytest.mark.parametrize("case", ["n1_pos", "n1_neg", "n2_diag", "zero", "minus_identity", "psd", "rank1"])
+@pytest.mark.parametrize("case", ["n1_pos", "n1_neg", "n2_diag", "zero", "minus_identity", "psd", "rank1",
+                                  "n4_one_pos", "k4_laplacian"])
 def test_edge_cases(api, case):
     rng = np.random.default_rng(11)
     if case == "n1_pos":
@@ -62,6 +63,14 @@ def test_edge_cases(api, case):
         M = rng.standard_normal((30, 8))
         A = M @ M.T
         expect = A.copy()
+    elif case == "n4_one_pos":  # cold block of one column locks at once with no guard column (R8)
+        Q = np.linalg.qr(rng.standard_normal((4, 4)))[0]
+        A = (Q * np.array([3.0, -1.0, -2.0, -3.0])) @ Q.T
+        A = 0.5 * (A + A.T)
+        expect = project_exact(A)
+    elif case == "k4_laplacian":  # repeated eigenvalues {0, 4, 4, 4} shifted: {-1, 3, 3, 3}
+        A = 4.0 * np.eye(4) - np.ones((4, 4)) - np.eye(4)
+        expect = project_exact(A)
     else:
         v = rng.standard_normal(64)
         A = np.outer(v, v) - 0.5 * np.eye(64)
