@@ -214,3 +214,37 @@ def test_row_sharded_single_rank_matches_unsharded(api):
         assert np.linalg.norm(Ps - Pu.cpu().numpy()) <= 1e-12 * np.linalg.norm(A)
         assert np.linalg.norm(Ps - project_exact(A)) / np.linalg.norm(A) <= 1e-9
     sh.close()
+
+
+@pytest.mark.parametrize("locking", [1, 2])
+def test_locking_modes_parity(api, locking):
+    """Soft (BLOPEX active mask) and hard locking (R35) reach the same projection."""
+    rng = np.random.default_rng(21)
+    n, p = 240, 14
+    lam = np.concatenate([rng.uniform(0.2, 4, p), rng.uniform(-4, -0.2, n - p)])
+    Q = haar_q(rng, n)
+    A = planted(Q, lam)
+    Pstar = (Q * np.maximum(lam, 0)) @ Q.T
+    ctx = api.Context(n, params=api.default_params(seed=5, locking=locking))
+    Pi, info = ctx.project(_dev(A), 1e-10)
+    err = np.linalg.norm(Pi.cpu().numpy() - Pstar)
+    assert info["status"] == 0, info
+    assert err / np.linalg.norm(A) <= 1e-9
+    assert info["err_bound"] >= err - 1e-12 * np.linalg.norm(A)
+    if locking == 1:
+        assert info["locked"] == 0
+
+
+def test_random_expansion_path(api):
+    """A cold block narrower than the positive eigenspace saturates and is widened by random
+    Philox columns (Alg. 3 line 8; R8-R11) until a guard appears."""
+    rng = np.random.default_rng(22)
+    n, p = 300, 40
+    lam = np.concatenate([rng.uniform(0.5, 5, p), rng.uniform(-5, -0.5, n - p)])
+    Q = haar_q(rng, n)
+    A = planted(Q, lam)
+    Pstar = (Q * np.maximum(lam, 0)) @ Q.T
+    ctx = api.Context(n, params=api.default_params(seed=6, m0=8, expand_q=12, side=1))
+    Pi, info = ctx.project(_dev(A), 1e-10)
+    assert info["expansions"] >= 1 and info["npos"] == p, info
+    assert np.linalg.norm(Pi.cpu().numpy() - Pstar) / np.linalg.norm(A) <= 1e-9
