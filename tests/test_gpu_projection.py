@@ -248,3 +248,20 @@ def test_random_expansion_path(api):
     Pi, info = ctx.project(_dev(A), 1e-10)
     assert info["expansions"] >= 1 and info["npos"] == p, info
     assert np.linalg.norm(Pi.cpu().numpy() - Pstar) / np.linalg.norm(A) <= 1e-9
+
+
+@pytest.mark.parametrize("n,p", [(13, 3), (77, 9), (129, 100), (333, 21), (517, 60)])
+def test_odd_sizes_parity(api, n, p):
+    """Ragged orders (ld rounding, partial tiles in every kernel) on both sides of the one-third rule."""
+    rng = np.random.default_rng(n + p)
+    lam = np.concatenate([rng.uniform(0.05, 3, p), rng.uniform(-3, -0.05, n - p)])
+    Q = haar_q(rng, n)
+    A = planted(Q, lam)
+    Pstar = (Q * np.maximum(lam, 0)) @ Q.T
+    ctx = api.Context(n, seed=8)
+    for call in range(3):
+        Pi, info = ctx.project(_dev(A), 1e-10)
+        err = np.linalg.norm(Pi.cpu().numpy() - Pstar)
+        assert info["status"] in (0, 1)
+        assert err / np.linalg.norm(A) <= 1e-9, (call, err, info["side"], info["iters"])
+        assert info["err_bound"] >= err - 1e-12 * np.linalg.norm(A)
