@@ -299,6 +299,70 @@ __host__ __device__ inline size_t tri_smem_doubles_ga(int s, int CS) {
   return 5 * (size_t)s + 3 * (size_t)cdiv(s, CS) + 16 * (size_t)(cdiv(s, CS) + TRI_CB) + 2 * 32 + 16 + 1300;
 }
 
+// Fused loop of one tridiagonalisation step on the CTA's own columns g > j (column per warp, rows
+// i = j + 1 + lane + 32 q for q < Q; rows >= s read finite padding, masked by v_j = 0 and by the
+// store predicate). Q <= 20: v', p', v_j in registers; larger Q re-reads v', p' per column.
+template <int Q>
+__device__ __forceinline__ double tri_fused_cols(int j, int s, int CS, unsigned rank, int ncl, int warp, int nw,
+                                                 int lane, bool pend, double Kp, double tj, double* __restrict__ Al,
+                                                 const double* __restrict__ vprow, const double* __restrict__ pprow,
+                                                 const double* __restrict__ vj, double* __restrict__ pbuf, int dbg) {
+  constexpr bool REG = Q <= 20;
+  const int i0 = j + 1 + lane;
+  double rj[Q], rv[REG ? Q : 1], rp[REG ? Q : 1];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const bool ok = i0 + 32 * q < s;
+    rj[q] = ok ? vj[i0 + 32 * q] : 0.0;
+    if (REG) {
+      rv[REG ? q : 0] = (ok && pend) ? vprow[i0 + 32 * q] : 0.0;
+      rp[REG ? q : 0] = (ok && pend) ? pprow[i0 + 32 * q] : 0.0;
+    }
+  }
+  const int lc0 = (j + 1 > (int)rank) ? (j + 1 - (int)rank + CS - 1) / CS : 0;
+  double part = 0.0;
+  for (int lc = lc0 + warp; lc < ncl && !(dbg & 1); lc += nw) {
+    const int g = (int)rank + CS * lc;
+    if (g >= s) break;
+    double* cp = Al + (size_t)lc * s + i0;
+    double a0 = 0.0, a1 = 0.0;
+    if (pend) {
+      const double bg = vprow[g];
+      const double ag = pprow[g] - 2.0 * Kp * bg;
+      double x[Q];
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const double vq = REG ? rv[REG ? q : 0] : vprow[i0 + 32 * q];
+        const double pq = REG ? rp[REG ? q : 0] : pprow[i0 + 32 * q];
+        x[q] = fma(-vq, ag, fma(-pq, bg, cp[32 * q]));
+      }
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        if (q & 1)
+          a1 = fma(x[q], rj[q], a1);
+        else
+          a0 = fma(x[q], rj[q], a0);
+        if (i0 + 32 * q < s) cp[32 * q] = x[q];
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        if (q & 1)
+          a1 = fma(cp[32 * q], rj[q], a1);
+        else
+          a0 = fma(cp[32 * q], rj[q], a0);
+      }
+    }
+    double acc = a0 + a1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    acc *= tj;
+    if (lane == 0) pbuf[g] = acc;
+    part = fma(acc, vj[g], part);
+  }
+  return part;
+}
+
 template <int PL, int TNT, bool GA = false>
 __global__ void __launch_bounds__(TNT) tridiag_cluster_kernel(int s, const double* __restrict__ A, int lda,
                                                                   double* __restrict__ d, double* __restrict__ e,
@@ -426,53 +490,26 @@ __global__ void __launch_bounds__(TNT) tridiag_cluster_kernel(int s, const doubl
     TRI_T(2);
     const double tj = vj[j];
     const double Kp = pend ? Kbuf[pp] : 0.0;
-    // column per warp, rows i = j + 1 + lane + 32 q (rows >= s read finite padding and are masked):
-    // v_j in registers, v' and p' of the pending update re-read per column
-    double rj[PL];
-    const double* vpr = vloc + (size_t)pp * s + j + 1 + lane;
-    const double* pqr = ploc + (size_t)pp * s + j + 1 + lane;
-    {
-      const double* vv = vj + j + 1 + lane;
-#pragma unroll
-      for (int q = 0; q < PL; ++q) rj[q] = (j + 1 + lane + 32 * q < s) ? vv[32 * q] : 0.0;
-    }
-    const int lc0 = (j + 1 > (int)rank) ? (j + 1 - (int)rank + CS - 1) / CS : 0;
-    double part = 0.0;
-    for (int lc = lc0 + warp; lc < ncl && !(dbg & 1); lc += nw) {
-      const int g = (int)rank + CS * lc;
-      if (g >= s) break;
-      double* cp = Al + (size_t)lc * s + j + 1 + lane;
-      double a0 = 0.0, a1 = 0.0;
-      if (pend) {
-        const double bg = vloc[(size_t)pp * s + g];
-        const double ag = ploc[(size_t)pp * s + g] - 2.0 * Kp * bg;
-        double x[PL];
-#pragma unroll
-        for (int q = 0; q < PL; ++q) x[q] = fma(-vpr[32 * q], ag, fma(-pqr[32 * q], bg, cp[32 * q]));
-#pragma unroll
-        for (int q = 0; q < PL; ++q) {
-          if (q & 1)
-            a1 = fma(x[q], rj[q], a1);
-          else
-            a0 = fma(x[q], rj[q], a0);
-          if (j + 1 + lane + 32 * q < s) cp[32 * q] = x[q];
-        }
-      } else {
-#pragma unroll
-        for (int q = 0; q < PL; ++q) {
-          if (q & 1)
-            a1 = fma(cp[32 * q], rj[q], a1);
-          else
-            a0 = fma(cp[32 * q], rj[q], a0);
-        }
-      }
-      double acc = a0 + a1;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      acc *= tj;
-      if (lane == 0) pbuf[g] = acc;
-      part = fma(acc, vj[g], part);
-    }
+    // fused pending update (step j-1) + p_g = tau_j A[:, g] . v_j over the own columns g > j; the
+    // row loop length is dispatched on the trailing size (no work on rows past s)
+    const int nq = (s - j - 1 + 31) >> 5;
+    const double* vprow = vloc + (size_t)pp * s;
+    const double* pprow = ploc + (size_t)pp * s;
+    double part;
+#define TRI_COLS(QQ) tri_fused_cols<QQ>(j, s, CS, rank, ncl, warp, nw, lane, pend, Kp, tj, Al, vprow, pprow, vj, pbuf, dbg)
+    if (nq <= 2)
+      part = TRI_COLS((PL < 2 ? PL : 2));
+    else if (nq <= 4)
+      part = TRI_COLS((PL < 4 ? PL : 4));
+    else if (nq <= 8)
+      part = TRI_COLS((PL < 8 ? PL : 8));
+    else if (nq <= 14)
+      part = TRI_COLS((PL < 14 ? PL : 14));
+    else if (nq <= 20)
+      part = TRI_COLS((PL < 20 ? PL : 20));
+    else
+      part = TRI_COLS(PL);
+#undef TRI_COLS
     if (lane == 0) wpart[par * 32 + warp] = part;
     TRI_T(3);
     cla_cluster_sync();  // B2: p_j entries and partials visible
