@@ -299,6 +299,69 @@ __host__ __device__ inline size_t tri_smem_doubles_ga(int s, int CS) {
   return 5 * (size_t)s + 3 * (size_t)cdiv(s, CS) + 16 * (size_t)(cdiv(s, CS) + TRI_CB) + 2 * 32 + 16 + 1300;
 }
 
+// Householder vector of step j by the owner's warp 0 (rows i = j + lane + 32 q, q < Q): eager
+// update of column j with step j-1, sigma, (tau, beta), v_j pushed to its interleaved holders
+// (DSMEM stores; tau_j to every CTA) and kept in column j as reflector storage. No global stores:
+// a release barrier would wait for them to reach L2.
+template <int Q>
+__device__ __forceinline__ void tri_house(int j, int s, int CS, double* __restrict__ col,
+                                          const double* __restrict__ vp, const double* __restrict__ pq, double Kq,
+                                          bool pend, double* __restrict__ vb, double* __restrict__ dj_out,
+                                          double* __restrict__ e_out, double* __restrict__ t_out) {
+  const int lane = threadIdx.x & 31;
+  double ag = 0.0, bg = 0.0;
+  if (pend) {
+    bg = vp[j];
+    ag = pq[j] - 2.0 * Kq * bg;
+  }
+  double x[Q];
+  const double* cp = col + j + lane;
+#pragma unroll
+  for (int q = 0; q < Q; ++q) x[q] = cp[32 * q];
+  if (pend) {
+#pragma unroll
+    for (int q = 0; q < Q; ++q) x[q] = fma(-vp[j + lane + 32 * q], ag, fma(-pq[j + lane + 32 * q], bg, x[q]));
+  }
+  double acc = 0.0;
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const int i = j + lane + 32 * q;
+    const double xs = (i >= j + 2 && i < s) ? x[q] : 0.0;
+    acc = fma(xs, xs, acc);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  const double sigma = acc;
+  const double alpha = __shfl_sync(0xffffffffu, x[0], 1);  // row j + 1 sits in lane 1, slot 0
+  const double dj = __shfl_sync(0xffffffffu, x[0], 0);
+  double tj, beta, scale;
+  if (sigma == 0.0) {
+    tj = 0.0;
+    beta = alpha;
+    scale = 0.0;
+  } else {
+    const double mu = sqrt(fma(alpha, alpha, sigma));
+    beta = (alpha <= 0.0) ? mu : -mu;
+    tj = (beta - alpha) / beta;
+    scale = 1.0 / (alpha - beta);
+  }
+  if (lane == 0) {
+    *dj_out = dj;
+    *e_out = beta;
+    *t_out = tj;
+  }
+  if (lane < CS) *cla_remote(vb + j, (unsigned)lane) = tj;
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const int i = j + lane + 32 * q;
+    if (i > j && i < s) {
+      const double v = (i == j + 1) ? 1.0 : x[q] * scale;
+      *cla_remote(vb + i, (unsigned)(i & (CS - 1))) = v;
+      col[i] = v;
+    }
+  }
+}
+
 // Fused loop of one tridiagonalisation step on the CTA's own columns g > j (column per warp, rows
 // i = j + 1 + lane + 32 q for q < Q; rows >= s read finite padding, masked by v_j = 0 and by the
 // store predicate). Q <= 20: v', p', v_j in registers; larger Q re-reads v', p' per column.
@@ -408,65 +471,23 @@ __global__ void __launch_bounds__(TNT) tridiag_cluster_kernel(int s, const doubl
     const int owner = j % CS, par = j & 1, pp = par ^ 1;
     const bool pend = j > 0;  // step j-1's update is pending on columns > j
     if ((int)rank == owner && warp == 0) {
-      // eager update of column j with step j-1 (rows >= j) fused with sigma = sum_{i >= j+2} x_i^2
+      const int nqh = (s - j + 31) >> 5;  // rows j..s-1
       double* col = Al + (size_t)(j / CS) * s;
-      const double* vp = vloc + (size_t)pp * s;
-      const double* pq = ploc + (size_t)pp * s;
-      double ag = 0.0, bg = 0.0;
-      if (pend) {
-        bg = vp[j];
-        ag = pq[j] - 2.0 * Kbuf[pp] * bg;
-      }
-      double x[PL];
-      const double* cp = col + j + lane;
-#pragma unroll
-      for (int q = 0; q < PL; ++q) x[q] = cp[32 * q];
-      if (pend) {
-        const double* vpp = vp + j + lane;
-        const double* pqq = pq + j + lane;
-#pragma unroll
-        for (int q = 0; q < PL; ++q) x[q] = fma(-vpp[32 * q], ag, fma(-pqq[32 * q], bg, x[q]));
-      }
-      double acc = 0.0;
-#pragma unroll
-      for (int q = 0; q < PL; ++q) {
-        const int i = j + lane + 32 * q;
-        const double xs = (i >= j + 2 && i < s) ? x[q] : 0.0;
-        acc = fma(xs, xs, acc);
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      const double sigma = acc;
-      const double alpha = __shfl_sync(0xffffffffu, x[0], 1);  // row j + 1 sits in lane 1, slot 0
-      const double dj = __shfl_sync(0xffffffffu, x[0], 0);
-      double tj, beta, scale;
-      if (sigma == 0.0) {
-        tj = 0.0;
-        beta = alpha;
-        scale = 0.0;
-      } else {
-        const double mu = sqrt(fma(alpha, alpha, sigma));
-        beta = (alpha <= 0.0) ? mu : -mu;
-        tj = (beta - alpha) / beta;
-        scale = 1.0 / (alpha - beta);
-      }
-      // no global stores inside the loop: a release barrier would wait for them to reach L2
-      double* vb = vloc + (size_t)par * s;
-      if (lane == 0) {
-        dl[j / CS] = dj;
-        el[j / CS] = beta;
-        tl[j / CS] = tj;
-      }
-      if (lane < CS) *cla_remote(vb + j, (unsigned)lane) = tj;
-#pragma unroll
-      for (int q = 0; q < PL; ++q) {  // v_j -> its interleaved holders, and (reflector storage) column j
-        const int i = j + lane + 32 * q;
-        if (i > j && i < s) {
-          const double v = (i == j + 1) ? 1.0 : x[q] * scale;
-          *cla_remote(vb + i, (unsigned)(i & (CS - 1))) = v;
-          col[i] = v;
-        }
-      }
+#define TRI_HOUSE(QQ) tri_house<QQ>(j, s, CS, col, vloc + (size_t)pp * s, ploc + (size_t)pp * s, Kbuf[pp], pend, \
+                                    vloc + (size_t)par * s, dl + j / CS, el + j / CS, tl + j / CS)
+      if (nqh <= 2)
+        TRI_HOUSE((PL < 2 ? PL : 2));
+      else if (nqh <= 4)
+        TRI_HOUSE((PL < 4 ? PL : 4));
+      else if (nqh <= 8)
+        TRI_HOUSE((PL < 8 ? PL : 8));
+      else if (nqh <= 14)
+        TRI_HOUSE((PL < 14 ? PL : 14));
+      else if (nqh <= 20)
+        TRI_HOUSE((PL < 20 ? PL : 20));
+      else
+        TRI_HOUSE(PL);
+#undef TRI_HOUSE
     }
     TRI_T(0);
     cla_cluster_sync();  // B1: v_j pieces and tau_j visible; step j-1 finished everywhere
