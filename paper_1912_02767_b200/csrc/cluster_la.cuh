@@ -83,10 +83,17 @@ __host__ __device__ inline size_t chol_smem_doubles(int t, int CS) {
 // GA = true (t too large for shared memory): the own columns live in the L2-resident global scratch
 // gA (CS * chol_local_cols(t, CS) * t doubles); panels are still exchanged through DSMEM.
 __host__ __device__ inline size_t chol_smem_doubles_ga(int t, int CS) { return (size_t)CHOL_NB * t + 16; }
-template <bool GA = false>
+// INV = true (shared-memory variant only): the triangular inverse X = L^-1 is formed alongside
+// (right-looking forward substitution on the identity: X_b <- L_bb^-1 X_b, X_{>b} -= L_{>b,b} X_b,
+// each CTA on its own columns with the panel it already holds) and written to Linv (ldi).
+__host__ __device__ inline size_t chol_inv_smem_doubles(int t, int CS) {
+  return 2 * (size_t)chol_local_cols(t, CS) * t + (size_t)CHOL_NB * t + 16;
+}
+template <bool GA = false, bool INV = false>
 __global__ void __launch_bounds__(CLA_NT) cholesky_cluster_kernel(int t, double* __restrict__ G, int ld,
                                                                    double fail_rel, int* __restrict__ status,
-                                                                   double* __restrict__ gA) {
+                                                                   double* __restrict__ gA,
+                                                                   double* __restrict__ Linv, int ldi) {
   extern __shared__ __align__(16) double sm[];
   __shared__ double red[33];
   __shared__ double xchs[4];
@@ -94,7 +101,8 @@ __global__ void __launch_bounds__(CLA_NT) cholesky_cluster_kernel(int t, double*
   const unsigned rank = cla_rank();
   const int ncl = chol_local_cols(t, CS);
   double* Al = GA ? gA + (size_t)rank * ncl * t : sm;  // ncl x t: local column lc = lb * NB + c <-> global (lb * CS + rank) * NB + c
-  double* pl = GA ? sm : Al + (size_t)ncl * t;          // NB x t: local copy of the current panel
+  double* Xl = (INV && !GA) ? sm + (size_t)ncl * t : nullptr;  // ncl x t: own columns of L^-1
+  double* pl = GA ? sm : sm + (size_t)(INV ? 2 : 1) * ncl * t;   // NB x t: local copy of the current panel
   double* xch = xchs;                      // [0] max diag part, [1..2] status of panel by parity
   const int tid = threadIdx.x, NT = blockDim.x;
   const int warp = tid >> 5, lane = tid & 31, nw = NT >> 5;
@@ -102,6 +110,7 @@ __global__ void __launch_bounds__(CLA_NT) cholesky_cluster_kernel(int t, double*
   for (int e = tid; e < ncl * t; e += NT) {
     int lc = e / t, i = e - lc * t, g = gcol(lc);
     Al[e] = (g < t) ? G[IDX(i, g, ld)] : 0.0;
+    if (INV) Xl[e] = (i == g) ? 1.0 : 0.0;
   }
   __syncthreads();
   double mx = 0.0;
@@ -209,31 +218,68 @@ __global__ void __launch_bounds__(CLA_NT) cholesky_cluster_kernel(int t, double*
         break;
       }
     }
-    if (jn >= t) break;
+    if (jn >= t && !INV) break;
+    const int cr0 = INV ? j0 : jn;  // first panel row copied (the diagonal block too when forming L^-1)
     {
       const double* P = GA ? gA + ((size_t)owner * ncl + (size_t)(b / CS) * CHOL_NB) * t
                            : cla_remote(Al + (size_t)(b / CS) * CHOL_NB * t, (unsigned)owner);
-      const int len = t - jn, tot = jb * len;
+      const int len = t - cr0, tot = jb * len;
       int e = tid;
       for (; e + 3 * NT < tot; e += 4 * NT) {
         double v[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          int ee = e + u * NT, c = ee / len, i = jn + (ee - c * len);
+          int ee = e + u * NT, c = ee / len, i = cr0 + (ee - c * len);
           v[u] = P[(size_t)c * t + i];
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          int ee = e + u * NT, c = ee / len, i = jn + (ee - c * len);
+          int ee = e + u * NT, c = ee / len, i = cr0 + (ee - c * len);
           pl[(size_t)c * t + i] = v[u];
         }
       }
       for (; e < tot; e += NT) {
-        int c = e / len, i = jn + (e - c * len);
+        int c = e / len, i = cr0 + (e - c * len);
         pl[(size_t)c * t + i] = P[(size_t)c * t + i];
       }
     }
     __syncthreads();
+    if (INV) {
+      // own columns g < jn of X: X[j0:jn, g] <- L_bb^-1 X[j0:jn, g]; X[jn:, g] -= L[jn:, j0:jn] X[j0:jn, g]
+      for (int lc = warp; lc < ncl; lc += nw) {
+        const int g = gcol(lc);
+        if (g >= jn || g >= t) continue;
+        double* xc = Xl + (size_t)lc * t;
+        double xb[CHOL_NB];
+#pragma unroll
+        for (int c = 0; c < CHOL_NB; ++c) xb[c] = (c < jb) ? xc[j0 + c] : 0.0;
+#pragma unroll
+        for (int c = 0; c < CHOL_NB; ++c) {
+          if (c < jb) {
+            double v = xb[c];
+#pragma unroll
+            for (int k = 0; k < c; ++k) v = fma(-pl[(size_t)k * t + j0 + c], xb[k], v);
+            xb[c] = v / pl[(size_t)c * t + j0 + c];
+          }
+        }
+        __syncwarp();
+        if (lane < jb) {
+          double v = 0.0;
+#pragma unroll
+          for (int c = 0; c < CHOL_NB; ++c)
+            if (c == lane) v = xb[c];
+          xc[j0 + lane] = v;
+        }
+        for (int i = jn + lane; i < t; i += 32) {
+          double a = xc[i];
+#pragma unroll
+          for (int c = 0; c < CHOL_NB; ++c)
+            if (c < jb) a = fma(-pl[(size_t)c * t + i], xb[c], a);
+          xc[i] = a;
+        }
+      }
+      if (jn >= t) break;
+    }
     // own columns g >= jn: G[i][g] -= sum_c L[i][j0+c] L[g][j0+c], i >= g (warp per column)
     for (int lc = warp; lc < ncl; lc += nw) {
       const int g = gcol(lc);
@@ -264,9 +310,13 @@ __global__ void __launch_bounds__(CLA_NT) cholesky_cluster_kernel(int t, double*
   }
   if (rank == 0 && tid == 0) *status = fail;
   if (!fail) {
+    __syncthreads();
     for (int e = tid; e < ncl * t; e += NT) {
       int lc = e / t, i = e - lc * t, g = gcol(lc);
-      if (g < t) G[IDX(i, g, ld)] = (i >= g) ? Al[e] : 0.0;
+      if (g < t) {
+        G[IDX(i, g, ld)] = (i >= g) ? Al[e] : 0.0;
+        if (INV) Linv[IDX(i, g, ldi)] = (i >= g) ? Xl[e] : 0.0;
+      }
     }
   }
   cla_cluster_sync();  // no CTA leaves while its shared memory may still be read

@@ -351,10 +351,12 @@ static int cla_attrs() {
   CK(cudaFuncSetAttribute(tridiag_cluster_kernel<14, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   CK(cudaFuncSetAttribute(tridiag_cluster_kernel<20, 256>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   CK(cudaFuncSetAttribute(tridiag_cluster_kernel<20, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-  CK(cudaFuncSetAttribute(cholesky_cluster_kernel<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-  CK(cudaFuncSetAttribute(cholesky_cluster_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-  CK(cudaFuncSetAttribute(cholesky_cluster_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-  CK(cudaFuncSetAttribute(cholesky_cluster_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  CK(cudaFuncSetAttribute(cholesky_cluster_kernel<false, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  CK(cudaFuncSetAttribute(cholesky_cluster_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  CK(cudaFuncSetAttribute(cholesky_cluster_kernel<false, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  CK(cudaFuncSetAttribute(cholesky_cluster_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  CK(cudaFuncSetAttribute(cholesky_cluster_kernel<true, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  CK(cudaFuncSetAttribute(cholesky_cluster_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   const int tmx = (int)(TI_KB * 32 * 40 * sizeof(double));
   CK(cudaFuncSetAttribute(trinv_panel_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, tmx));
   CK(cudaFuncSetAttribute(trinv_panel_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, tmx));
@@ -376,20 +378,33 @@ static int cla_attrs() {
 }
 
 // L = chol(G) in place (t x t, ld); status = failing pivot + 1 or 0 (a6, R20)
+// L = chol(G) in place; with Linv != nullptr also L^-1 (fused when it fits in shared memory, else a
+// separate panel-streamed inverse). Returns 0 or a negative error.
+static int trinv_run(cudaStream_t st, int t, const double* L, int ldl, double* Li, int ldi);
 static int cholesky_run(cudaStream_t st, int t, double* G, int ld, int* d_status, double* gscratch = nullptr,
-                        size_t gscratch_elems = 0) {
+                        size_t gscratch_elems = 0, double* Linv = nullptr, int ldi = 0) {
   TRY(cla_attrs());
+  static int fuse = getenv("PSDPROJ_CHOL_NOFUSE") ? 0 : 1;
+  if (Linv && fuse) {
+    if (int cs = cla_cluster_size(t, chol_inv_smem_doubles)) {
+      return launch_cluster(cholesky_cluster_kernel<false, true>, cs, CLA_NT,
+                            chol_inv_smem_doubles(t, cs) * sizeof(double), st, t, G, ld, 1e-12, d_status,
+                            (double*)nullptr, Linv, ldi);
+    }
+  }
   if (int cs = cla_cluster_size(t, chol_smem_doubles)) {
-    return launch_cluster(cholesky_cluster_kernel<false>, cs, CLA_NT, chol_smem_doubles(t, cs) * sizeof(double), st, t,
-                          G, ld, 1e-12, d_status, (double*)nullptr);
+    TRY(launch_cluster(cholesky_cluster_kernel<false, false>, cs, CLA_NT, chol_smem_doubles(t, cs) * sizeof(double),
+                       st, t, G, ld, 1e-12, d_status, (double*)nullptr, (double*)nullptr, 0));
+    return Linv ? trinv_run(st, t, G, ld, Linv, ldi) : 0;
   }
   if (gscratch && (size_t)16 * chol_local_cols(t, 16) * t <= gscratch_elems && t <= 4096) {
-    return launch_cluster(cholesky_cluster_kernel<true>, 16, CLA_NT, chol_smem_doubles_ga(t, 16) * sizeof(double), st,
-                          t, G, ld, 1e-12, d_status, gscratch);
+    TRY(launch_cluster(cholesky_cluster_kernel<true, false>, 16, CLA_NT, chol_smem_doubles_ga(t, 16) * sizeof(double),
+                       st, t, G, ld, 1e-12, d_status, gscratch, (double*)nullptr, 0));
+    return Linv ? trinv_run(st, t, G, ld, Linv, ldi) : 0;
   }
   cholesky_kernel<1024><<<1, 1024, 0, st>>>(t, G, ld, 1e-12, d_status);
   CKL();
-  return 0;
+  return Linv ? trinv_run(st, t, G, ld, Linv, ldi) : 0;
 }
 
 // Li = L^-1 (lower triangular t x t)
@@ -1053,8 +1068,8 @@ struct Run {
     CK(cudaMemsetAsync(c->d_status, 0, sizeof(int), st));
     if (t > 0) {
       TRY(copy_cols(t, t, c->Gc, ldm, c->G + kx + (size_t)kx * ldm, ldm));
-      TRY(cholesky_run(st, t, c->Gc, ldm, c->d_status, c->tG, (size_t)c->s_max * c->s_max + 16 * (size_t)c->s_max + 2048));
-      TRY(trinv_run(st, t, c->Gc, ldm, c->Li + kx + (size_t)kx * ldm, ldm));
+      TRY(cholesky_run(st, t, c->Gc, ldm, c->d_status, c->tG, (size_t)c->s_max * c->s_max + 16 * (size_t)c->s_max + 2048,
+                       c->Li + kx + (size_t)kx * ldm, ldm));
     }
     // Hh = L^-1 H L^-T
     TRY(dgemm(st, OP_N, OP_N, s, s, s, 1.0, c->Li, ldm, c->Hm, ldm, 0.0, c->Y, ldm, c->part, c->part_elems));
