@@ -230,6 +230,29 @@ __global__ void insert_known_kernel(int s, int kxG, int kxH, double* __restrict_
   }
 }
 
+// One pass preparing the Rayleigh-Ritz pencil: insert_known_kernel's work, Li = [I 0; 0 0] (the
+// Cholesky writes the L^-1 block), Gc = the direction block of G (the Cholesky input), status = 0.
+__global__ void rr_prep_kernel(int s, int kxG, int kxH, double* __restrict__ G, double* __restrict__ H, int ld,
+                               const double* __restrict__ theta, double* __restrict__ Li, double* __restrict__ Gc,
+                               int* __restrict__ status) {
+  int total = s * s;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *status = 0;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    int i = e % s, j = e / s;
+    Li[IDX(i, j, ld)] = (i == j && i < kxG) ? 1.0 : 0.0;
+    if (i > j) continue;
+    double g = (j < kxG) ? ((i == j) ? 1.0 : 0.0)
+                         : (i < kxG ? 0.0 : 0.5 * (G[IDX(i, j, ld)] + G[IDX(j, i, ld)]));
+    double h = (j < kxH) ? ((i == j) ? theta[i] : 0.0) : 0.5 * (H[IDX(i, j, ld)] + H[IDX(j, i, ld)]);
+    G[IDX(i, j, ld)] = g; G[IDX(j, i, ld)] = g;
+    H[IDX(i, j, ld)] = h; H[IDX(j, i, ld)] = h;
+    if (i >= kxG) {
+      Gc[IDX(i - kxG, j - kxG, ld)] = g;
+      Gc[IDX(j - kxG, i - kxG, ld)] = g;
+    }
+  }
+}
+
 // ---------------------------------------------------------------- a6 Cholesky (one CTA)
 // In place on the lower triangle of G (s x s, ld). Fails (status = j+1) when a pivot is
 // <= fail_rel * max diag(G) (R20). Upper triangle is zeroed on success.

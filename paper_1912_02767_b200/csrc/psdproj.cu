@@ -1056,18 +1056,13 @@ struct Run {
     info->rr_max = std::max(info->rr_max, s);
     info->flops += 9.0 * s * (double)s * s + s * (double)s * s / 3.0 + 2.0 * s * (double)s * s;
     TRY(mark(3));
-    insert_known_kernel<<<grid1d((size_t)s * s), 256, 0, st>>>(s, kxG, kxH, c->G, c->Hm, ldm, d_theta_known);
-    CKL();
-    // G = [I 0; 0 D]: factor only the direction block D = L22 L22^T (size t = s - kxG)
+    // G = [I 0; 0 D]: factor only the direction block D = L22 L22^T (size t = s - kxG); one pass
+    // inserts the known blocks, sets Li = [I 0; 0 0], copies D to Gc and clears the status
     const int kx = kxG, t = s - kxG;
-    CK(cudaMemset2DAsync(c->Li, (size_t)ldm * 8, 0, (size_t)s * 8, s, st));
-    if (kx > 0) {
-      fill_identity_kernel<<<cdiv(kx, 256), 256, 0, st>>>(kx, c->Li, ldm);
-      CKL();
-    }
-    CK(cudaMemsetAsync(c->d_status, 0, sizeof(int), st));
+    rr_prep_kernel<<<grid1d((size_t)s * s), 256, 0, st>>>(s, kxG, kxH, c->G, c->Hm, ldm, d_theta_known, c->Li, c->Gc,
+                                                          c->d_status);
+    CKL();
     if (t > 0) {
-      TRY(copy_cols(t, t, c->Gc, ldm, c->G + kx + (size_t)kx * ldm, ldm));
       TRY(cholesky_run(st, t, c->Gc, ldm, c->d_status, c->tG, (size_t)c->s_max * c->s_max + 16 * (size_t)c->s_max + 2048,
                        c->Li + kx + (size_t)kx * ldm, ldm));
     }
