@@ -232,23 +232,29 @@ __global__ void insert_known_kernel(int s, int kxG, int kxH, double* __restrict_
 
 // One pass preparing the Rayleigh-Ritz pencil: insert_known_kernel's work, Li = [I 0; 0 0] (the
 // Cholesky writes the L^-1 block), Gc = the direction block of G (the Cholesky input), status = 0.
+// parts: bit 0 = the G side (G known blocks, Li, Gc, status), bit 1 = the H side (H known blocks).
 __global__ void rr_prep_kernel(int s, int kxG, int kxH, double* __restrict__ G, double* __restrict__ H, int ld,
                                const double* __restrict__ theta, double* __restrict__ Li, double* __restrict__ Gc,
-                               int* __restrict__ status) {
+                               int* __restrict__ status, int parts) {
   int total = s * s;
-  if (blockIdx.x == 0 && threadIdx.x == 0) *status = 0;
+  const bool gs = parts & 1, hs = parts & 2;
+  if (gs && blockIdx.x == 0 && threadIdx.x == 0) *status = 0;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
     int i = e % s, j = e / s;
-    Li[IDX(i, j, ld)] = (i == j && i < kxG) ? 1.0 : 0.0;
+    if (gs) Li[IDX(i, j, ld)] = (i == j && i < kxG) ? 1.0 : 0.0;
     if (i > j) continue;
-    double g = (j < kxG) ? ((i == j) ? 1.0 : 0.0)
-                         : (i < kxG ? 0.0 : 0.5 * (G[IDX(i, j, ld)] + G[IDX(j, i, ld)]));
-    double h = (j < kxH) ? ((i == j) ? theta[i] : 0.0) : 0.5 * (H[IDX(i, j, ld)] + H[IDX(j, i, ld)]);
-    G[IDX(i, j, ld)] = g; G[IDX(j, i, ld)] = g;
-    H[IDX(i, j, ld)] = h; H[IDX(j, i, ld)] = h;
-    if (i >= kxG) {
-      Gc[IDX(i - kxG, j - kxG, ld)] = g;
-      Gc[IDX(j - kxG, i - kxG, ld)] = g;
+    if (gs) {
+      double g = (j < kxG) ? ((i == j) ? 1.0 : 0.0)
+                           : (i < kxG ? 0.0 : 0.5 * (G[IDX(i, j, ld)] + G[IDX(j, i, ld)]));
+      G[IDX(i, j, ld)] = g; G[IDX(j, i, ld)] = g;
+      if (i >= kxG) {
+        Gc[IDX(i - kxG, j - kxG, ld)] = g;
+        Gc[IDX(j - kxG, i - kxG, ld)] = g;
+      }
+    }
+    if (hs) {
+      double h = (j < kxH) ? ((i == j) ? theta[i] : 0.0) : 0.5 * (H[IDX(i, j, ld)] + H[IDX(j, i, ld)]);
+      H[IDX(i, j, ld)] = h; H[IDX(j, i, ld)] = h;
     }
   }
 }

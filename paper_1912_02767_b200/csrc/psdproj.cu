@@ -634,6 +634,10 @@ struct psdproj_ctx_s {
   bool poisoned = false;
   std::vector<cudaEvent_t> ev;
   std::vector<cudaEvent_t> pev;  // phase-timing events (profile & 2)
+  // side stream: the direction-block Gram and its Cholesky run there, overlapping the block multiply
+  cudaStream_t st2 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  double* part2 = nullptr;
 };
 
 struct Carver {
@@ -688,6 +692,7 @@ static size_t carve(psdproj_ctx_s* c, int n, const psdproj_params& p, int m_max,
   c->jM = cv.take<double>(nj); c->jM2 = cv.take<double>(nj); c->jQ = cv.take<double>(nj);
   c->part_elems = 2 * std::max(s2, nM);
   c->part = cv.take<double>(c->part_elems);
+  c->part2 = cv.take<double>(c->part_elems);
   int vlen = std::max(s_max, n) + 8;
   c->d_thU = cv.take<double>(vlen); c->d_r = cv.take<double>(vlen); c->d_norm = cv.take<double>(vlen);
   c->d_w = cv.take<double>(vlen); c->d_ths = cv.take<double>(vlen); c->d_scal = cv.take<double>(64);
@@ -861,6 +866,9 @@ extern "C" int psdproj_destroy(psdproj_ctx c) {
   if (c->h_i) cudaFreeHost(c->h_i);
   for (auto e : c->ev) cudaEventDestroy(e);
   for (auto e : c->pev) cudaEventDestroy(e);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->st2) cudaStreamDestroy(c->st2);
   delete c;
   return PSDPROJ_OK;
 }
@@ -883,6 +891,7 @@ struct Run {
   psdproj_ctx_s* c;
   cudaStream_t st;
   psdproj_info* info;
+  double* part = nullptr;  // split-K partials of this Run's stream (c->part, or c->part2 on the side stream)
   int ihost = 0;  // next free int slot in the pinned buffer (per iteration)
   int rr_npos = 0;  // positive Ritz values among all s of the last Rayleigh-Ritz (expansion test)
   int nev = 0;
@@ -923,7 +932,7 @@ struct Run {
       info->flops += 2.0 * M * N * (double)K;
       info->bytes += 8.0 * ((double)M * K + (double)K * N + (double)M * N);
     }
-    return dgemm(st, oa, ob, M, N, K, al, A, lda, B, ldb, be, C, ldc, c->part, c->part_elems);
+    return dgemm(st, oa, ob, M, N, K, al, A, lda, B, ldb, be, C, ldc, part ? part : c->part, c->part_elems);
   }
   // row-sharded mode: sum over ranks (in place, on the call's stream); no-op otherwise
   int allreduce(double* buf, size_t count) {
@@ -1051,21 +1060,34 @@ struct Run {
   }
   // Rayleigh-Ritz on the pencil (H, G) in c->G / c->Hm (s x s, ld s_max):
   // returns 0 (ok), >0 (Cholesky failed at that pivot), <0 error. Outputs Cp (s x mU), theta desc in h_d[0..s).
-  int rr(int s, int kxG, int kxH, const double* d_theta_known, int mU) {
-    int ldm = c->s_max;
-    info->rr_max = std::max(info->rr_max, s);
-    info->flops += 9.0 * s * (double)s * s + s * (double)s * s / 3.0 + 2.0 * s * (double)s * s;
-    TRY(mark(3));
-    // G = [I 0; 0 D]: factor only the direction block D = L22 L22^T (size t = s - kxG); one pass
-    // inserts the known blocks, sets Li = [I 0; 0 0], copies D to Gc and clears the status
-    const int kx = kxG, t = s - kxG;
-    rr_prep_kernel<<<grid1d((size_t)s * s), 256, 0, st>>>(s, kxG, kxH, c->G, c->Hm, ldm, d_theta_known, c->Li, c->Gc,
-                                                          c->d_status);
+  // G side of the pencil: known blocks of G, Li = [I 0; 0 0], Cholesky (+ L^-1) of the direction
+  // block D (size s - kxG). May run on the side stream (stream_, part_ of a Run bound to it).
+  int rr_factor(int s, int kxG) {
+    const int ldm = c->s_max, kx = kxG, t = s - kxG;
+    rr_prep_kernel<<<grid1d((size_t)s * s), 256, 0, st>>>(s, kxG, 0, c->G, c->Hm, ldm, nullptr, c->Li, c->Gc,
+                                                          c->d_status, 1);
     CKL();
     if (t > 0) {
       TRY(cholesky_run(st, t, c->Gc, ldm, c->d_status, c->tG, (size_t)c->s_max * c->s_max + 16 * (size_t)c->s_max + 2048,
                        c->Li + kx + (size_t)kx * ldm, ldm));
     }
+    return 0;
+  }
+  int rr(int s, int kxG, int kxH, const double* d_theta_known, int mU, bool prefactored = false) {
+    int ldm = c->s_max;
+    info->rr_max = std::max(info->rr_max, s);
+    info->flops += 9.0 * s * (double)s * s + s * (double)s * s / 3.0 + 2.0 * s * (double)s * s;
+    TRY(mark(3));
+    // G = [I 0; 0 D]: factor only the direction block D = L22 L22^T (size t = s - kxG)
+    const int kx = kxG;
+    if (prefactored) {
+      CK(cudaStreamWaitEvent(st, c->ev_join, 0));
+    } else {
+      TRY(rr_factor(s, kxG));
+    }
+    rr_prep_kernel<<<grid1d((size_t)s * s), 256, 0, st>>>(s, kxG, kxH, c->G, c->Hm, ldm, d_theta_known, c->Li, c->Gc,
+                                                          c->d_status, 2);
+    CKL();
     // Hh = L^-1 H L^-T
     TRY(dgemm(st, OP_N, OP_N, s, s, s, 1.0, c->Li, ldm, c->Hm, ldm, 0.0, c->Y, ldm, c->part, c->part_elems));
     TRY(dgemm(st, OP_N, OP_T, s, s, s, 1.0, c->Y, ldm, c->Li, ldm, 0.0, c->Hh, ldm, c->part, c->part_elems));
@@ -1408,16 +1430,35 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
     }
     TRY(run.normalize(nl, aw, W, ld, nullptr, 0));
     if (ap > 0) TRY(run.normalize(nl, ap, P, ld, BP, ld));
+    // ---- line 6: Rayleigh-Ritz on span(X, R, P) via the pencil (S^T BS, S^T S). Only the direction
+    // block of G is needed (X^T X = I, X^T [W P] = 0 by construction); it does not depend on B W, so
+    // its Gram and Cholesky run on the side stream, overlapping the block multiply (unsharded mode)
+    static int ovl_env = getenv("PSDPROJ_NO_OVERLAP") ? 0 : 1;
+    const bool ovl = ovl_env && !c->sharded && s > mU;
+    if (ovl) {
+      if (!c->st2) {
+        CK(cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+      }
+      CK(cudaEventRecord(c->ev_fork, st));
+      CK(cudaStreamWaitEvent(c->st2, c->ev_fork, 0));
+      Run r2{c, c->st2, info};
+      r2.part = c->part2;
+      TRY(r2.gram(s - mU, s - mU, c->S + (size_t)mU * ld, ld, c->S + (size_t)mU * ld, ld, c->G + mU + (size_t)mU * ldm,
+                  ldm));
+      TRY(r2.rr_factor(s, mU));
+      CK(cudaEventRecord(c->ev_join, c->st2));
+    }
     TRY(run.mark(0));
     TRY(run.amul(sgn, A, lda, W, ld, aw, c->BS + (size_t)offW * ld, ld));
-    // ---- line 6: Rayleigh-Ritz on span(X, R, P) via the pencil (S^T BS, S^T S)
-    // only the direction block of G is needed (X^T X = I, X^T [W P] = 0 by construction)
     TRY(run.mark(2));
-    TRY(run.gemm(OP_T, OP_N, s - mU, s - mU, n, 1.0, c->S + (size_t)mU * ld, ld, c->S + (size_t)mU * ld, ld, 0.0,
-                 c->G + mU + (size_t)mU * ldm, ldm));
+    if (!ovl)
+      TRY(run.gram(s - mU, s - mU, c->S + (size_t)mU * ld, ld, c->S + (size_t)mU * ld, ld, c->G + mU + (size_t)mU * ldm,
+                   ldm));
     TRY(run.gram(s, s, c->S, ld, c->BS, ld, c->Hm, ldm));
     int sU = s;
-    rc = run.rr(s, mU, mU, c->d_thU, std::min(mU + qe, s));
+    rc = run.rr(s, mU, mU, c->d_thU, std::min(mU + qe, s), ovl);
     if (rc > 0 && ap > 0) {
       sU = s - ap;  // drop P and retry (R20)
       rc = run.rr(sU, mU, mU, c->d_thU, std::min(mU + qe, sU));
