@@ -171,16 +171,17 @@ PHASES = ["a3_block_multiply", "w_p_projection", "gram_pencil", "cholesky_pencil
 
 def dominant_phase(infos, K, ms_step):
     """The phase that dominates a step (library profile bit 1, CUDA events on the launching stream).
-    At n = 4000 it is the Rayleigh-Ritz tridiagonalisation: latency-bound (two cluster barriers and
-    two DSMEM round trips per Householder step), so its roof is the barrier/DSMEM floor measured by
-    tools/micro/cluster_bench.cu (profiles/cluster_bench_r01.txt), not HBM or FP64."""
+    At n = 4000 it is the Rayleigh-Ritz tridiagonalisation: latency-bound (three one-way DSMEM
+    pushes per Householder step), so its roof is the push-hop floor measured by
+    tools/micro/push_bench2.cu (profiles/push_bench_r01.txt), not HBM or FP64."""
     tot = [sum(i["phase_ms"][k] for i in infos) / K for k in range(len(PHASES))]
     k = max(range(len(PHASES)), key=lambda j: tot[j])
     out = {"phase": PHASES[k], "ms_per_step": round(tot[k], 3), "share": round(tot[k] / ms_step, 4)}
     if PHASES[k] == "rr_tridiagonal":
-        out.update({"bound": "latency", "kernel": "tridiag_cluster_kernel (16-CTA cluster, DSMEM)",
-                    "floor_note": "per Householder step >= 2 x (cluster barrier ~560 cyc + DSMEM round trip ~600 cyc) "
-                                  "= ~2.3k cycles; measured ~8k cycles/step at s = 400 (PSDPROJ_TRI_PROF)"})
+        out.update({"bound": "latency", "kernel": "tridiag_reg_kernel (16-CTA cluster, registers, st.async pushes)",
+                    "floor_note": "per Householder step >= 3 st.async hops (~0.9k cycles each, push_bench2) + the "
+                                  "owner's Householder scalars = ~3.5k cycles; measured ~4.2k (s = 200) to ~5.8k "
+                                  "(s = 400) cycles/step (PSDPROJ_TRI_PROF)"})
     return out
 
 

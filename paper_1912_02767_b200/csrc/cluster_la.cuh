@@ -357,7 +357,8 @@ template <int Q>
 __device__ __forceinline__ void tri_house(int j, int s, int CS, double* __restrict__ col,
                                           const double* __restrict__ vp, const double* __restrict__ pq, double Kq,
                                           bool pend, double* __restrict__ vb, double* __restrict__ dj_out,
-                                          double* __restrict__ e_out, double* __restrict__ t_out) {
+                                          double* __restrict__ e_out, double* __restrict__ t_out,
+                                          double* __restrict__ vout) {
   const int lane = threadIdx.x & 31;
   double ag = 0.0, bg = 0.0;
   if (pend) {
@@ -407,7 +408,7 @@ __device__ __forceinline__ void tri_house(int j, int s, int CS, double* __restri
     if (i > j && i < s) {
       const double v = (i == j + 1) ? 1.0 : x[q] * scale;
       *cla_remote(vb + i, (unsigned)(i & (CS - 1))) = v;
-      col[i] = v;
+      vout[i] = v;
     }
   }
 }
@@ -524,7 +525,7 @@ __global__ void __launch_bounds__(TNT) tridiag_cluster_kernel(int s, const doubl
       const int nqh = (s - j + 31) >> 5;  // rows j..s-1
       double* col = Al + (size_t)(j / CS) * s;
 #define TRI_HOUSE(QQ) tri_house<QQ>(j, s, CS, col, vloc + (size_t)pp * s, ploc + (size_t)pp * s, Kbuf[pp], pend, \
-                                    vloc + (size_t)par * s, dl + j / CS, el + j / CS, tl + j / CS)
+                                    vloc + (size_t)par * s, dl + j / CS, el + j / CS, tl + j / CS, col)
       if (nqh <= 2)
         TRI_HOUSE((PL < 2 ? PL : 2));
       else if (nqh <= 4)
@@ -653,6 +654,403 @@ __global__ void __launch_bounds__(TNT) tridiag_cluster_kernel(int s, const doubl
     }
   }
   cla_cluster_sync();  // no CTA leaves while its shared memory may still be read
+}
+
+// ---- push-style DSMEM exchange: st.async into the receiver's shared memory, completing on the
+// receiver's mbarrier (one hop, no cluster barrier; tools/micro/push_bench.cu: ~570 cycles for a
+// one-double broadcast hop against ~1.6k for barrier.cluster + remote load)
+__device__ __forceinline__ uint32_t cla_smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint32_t cla_mapa(uint32_t a, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cla_mbar_init(uint64_t* b, int cnt) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(cla_smem_u32(b)), "r"(cnt) : "memory");
+}
+// the local arrival of a phase, announcing the bytes the phase will receive
+__device__ __forceinline__ void cla_mbar_arm(uint64_t* b, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(cla_smem_u32(b)), "r"(tx)
+               : "memory");
+}
+__device__ __forceinline__ void cla_mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nCLA_WAIT_%=: mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra CLA_WAIT_%=;\n}\n" ::"r"(cla_smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void cla_st_async(uint32_t raddr, double v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(raddr),
+               "l"(__double_as_longlong(v)), "r"(rbar)
+               : "memory");
+}
+
+// Register-resident, push-exchanged tridiagonalisation (s <= 64 KR, cdiv(s, CS) <= TRI_TCG CR):
+// the own columns live in registers, so a step moves no matrix bytes through shared memory, and
+// the exchanges of a step are one-way st.async pushes completing on the receiver's mbarrier
+// instead of cluster barriers + remote loads (tools/micro/push_bench*.cu: ~0.9k cycles per hop
+// against ~1.6k for barrier.cluster + remote load).
+// Thread t: column group cg = t / 64 (two warps), rows r = t % 64 + 64 k (k < KR), own local
+// columns lc = cg + TRI_TCG c (c < CR). Step j (parity buffers par = j & 1, mbarrier phase j >> 1):
+//   U1  owner(j): the threads of column j apply the pending update (step j-1) to it, copy it to
+//       colb and reduce sigma = ||A[j+2:, j]||^2; Householder scalars; v_j[i] pushed to holder
+//       i % CS (holder-major thread mapping: a warp targets at most two CTAs), tau_j to every
+//       CTA (hbar); v_j kept in refl for the output
+//   U2  all: the pending update on the other own columns (overlaps the flight of v_j)
+//   F   every CTA: wait hbar, push its held rows of v_j to every CTA (vbar); wait vbar
+//   D   all: acc[c] = sum_r a[r][c] v_j[r] (rows > j); column sums by an in-warp transpose
+//       reduction + the group's two warps; p_g = tau_j sum for own g > j pushed to every CTA's
+//       ploc[par][g], the CTA's part of p.v_j to wpart[par][rank] (pbar, warp w serving
+//       destinations w, w + 8); wait pbar; K_j = tau_j / 2 sum(wpart)
+// Three hops per column (owner -> holders -> all, p all-gather): the step is latency-bound at
+// ~4-6k cycles (s = 200..450) against ~7-8k for tridiag_cluster_kernel.
+// Buffer reuse is ordered by the data dependencies: nothing is written into a parity-par buffer
+// for step j + 2 before every CTA has pushed p_{j+1}, i.e. finished reading step j's buffers.
+// Each CTA re-arms a barrier for step j + 2 right after observing its step-j phase (by then no
+// step-(j+2) bytes can have arrived), so no phase ever sees bytes before its expect_tx.
+constexpr int TRI_TCG = 4;
+__host__ __device__ inline size_t tri_reg_smem_doubles(int s, int CS) {
+  return (size_t)cdiv(s, CS) * s + 4 * (size_t)s + 3 * (size_t)cdiv(s, CS) + (s + 256) + 2 * 8 * 32 + 64 + 16;
+}
+template <int N>
+__device__ __forceinline__ double tri_xreduce(double (&v)[N], int lane) {
+  // transpose reduction: after log2 N halving levels lane holds column c(lane) summed over the
+  // lanes that agree with it in bits 4 .. 5 - log2 N; the remaining levels sum those lanes
+#pragma unroll
+  for (int h = N / 2, o = 16; h >= 1; h >>= 1, o >>= 1) {
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < h; ++i) {
+      const double send = up ? v[i] : v[i + h];
+      const double keep = up ? v[i + h] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  double r = v[0];
+#pragma unroll
+  for (int o = 16 / N; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+  return r;
+}
+template <int N>
+__device__ __forceinline__ int tri_xreduce_col(int lane) {
+  int c = 0;
+#pragma unroll
+  for (int h = N / 2, o = 16; h >= 1; h >>= 1, o >>= 1)
+    if (lane & o) c += h;
+  return c;
+}
+__host__ __device__ constexpr int tri_pow2_ceil(int n) { return n <= 1 ? 1 : 2 * tri_pow2_ceil((n + 1) / 2); }
+__device__ __forceinline__ int tri_held_first(int j, int h, int CS) { return j + 1 + ((h - j - 1) & (CS - 1)); }
+__device__ __forceinline__ uint32_t tri_tx_h(int j, int s, int h, int CS) {
+  const int f = tri_held_first(j, h, CS);
+  return 8u * (uint32_t)(1 + (f < s ? (s - 1 - f) / CS + 1 : 0));
+}
+
+template <int KR, int CR>
+__global__ void __launch_bounds__(256, 1) tridiag_reg_kernel(int s, const double* __restrict__ A, int lda,
+                                                             double* __restrict__ d, double* __restrict__ e,
+                                                             double* __restrict__ tau, double* __restrict__ Vh, int ldv,
+                                                             long long* __restrict__ prof, int dbg) {
+  constexpr int NT = 256, RG = 64, TCG = TRI_TCG, CRP = tri_pow2_ceil(CR);
+  static_assert(RG * TCG == NT, "thread layout");
+  static_assert(CRP <= 32, "columns per thread");
+  extern __shared__ __align__(16) double sm[];
+  __shared__ __align__(8) uint64_t hbar[2], vbar[2], pbar[2];
+  __shared__ double hsm[18];
+  long long pt[8] = {0, 0, 0, 0, 0, 0, 0, 0}, po[4] = {0, 0, 0, 0};
+  long long tprev = 0;
+#define TRI_O(k)                                                          \
+  if (prof && threadIdx.x == 0) {                                         \
+    long long tn;                                                         \
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(tn)::"memory");          \
+    po[k] += tn - tprev;                                                  \
+    tprev = tn;                                                           \
+  }
+#define TRI_T(k)                                                          \
+  if (prof && threadIdx.x == 0) {                                         \
+    long long tn;                                                         \
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(tn)::"memory");          \
+    pt[k] += tn - tprev;                                                  \
+    tprev = tn;                                                           \
+  }
+  const int CS = (int)gridDim.x, lcs = __ffs(CS) - 1;  // CS in {4, 8, 16}
+  const int TPD = NT / CS, ltpd = __ffs(TPD) - 1;      // threads per holder / destination
+  const unsigned rank = cla_rank();
+  const int ncl = cdiv(s, CS);  // <= 32: a holder has at most 2 TPD rows
+  double* refl = sm;                      // ncl x s: reflectors of the own columns
+  double* vloc = refl + (size_t)ncl * s;  // 2 x s (parity): [tau_j at index j | v_j at j+1..s-1]
+  double* ploc = vloc + 2 * (size_t)s;    // 2 x s (parity): p_j (pushed by the column owners)
+  double* colb = ploc + 2 * (size_t)s;    // column j for the owner's Householder step (s + 256: tail pad)
+  double* wred = colb + s + 256;          // 2 x 8 warps x 32: per-warp column partials (parity)
+  double* wpart = wred + 2 * 8 * 32;      // 2 x 32 (parity): every CTA's part of p.v_j, by rank
+  double* dl = wpart + 64;
+  double* el = dl + ncl;
+  double* tl = el + ncl;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int cg = tid / RG, rg = tid % RG;
+  for (size_t q = tid; q < tri_reg_smem_doubles(s, CS); q += NT) sm[q] = 0.0;
+  double a[KR][CR];
+#pragma unroll
+  for (int c = 0; c < CR; ++c) {
+    const int g = (int)rank + CS * (cg + TCG * c);
+#pragma unroll
+    for (int k = 0; k < KR; ++k) {
+      const int r = rg + RG * k;
+      a[k][c] = (g < s && r < s) ? 0.5 * (A[IDX(r, g, lda)] + A[IDX(g, r, lda)]) : 0.0;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int b = 0; b < 2; ++b) {
+      cla_mbar_init(&hbar[b], 1);
+      cla_mbar_init(&vbar[b], 1);
+      cla_mbar_init(&pbar[b], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int jj = 0; jj < 2 && jj + 2 < s; ++jj) {
+      cla_mbar_arm(&hbar[jj], tri_tx_h(jj, s, (int)rank, CS));
+      cla_mbar_arm(&vbar[jj], 8u * (uint32_t)(s - jj - 1));
+      cla_mbar_arm(&pbar[jj], 8u * (uint32_t)(s - jj - 1 + CS));
+    }
+  }
+  __syncthreads();
+  cla_cluster_sync();  // every CTA's barriers are initialised and armed before the first push
+  if (prof && threadIdx.x == 0) tprev = clock64();
+  double Kp = 0.0;  // K_{j-1}
+  for (int j = 0; j + 2 < s; ++j) {
+    const int owner = j & (CS - 1), par = j & 1, pp = par ^ 1;
+    const uint32_t ph = (uint32_t)(j >> 1) & 1u;
+    const bool pend = j > 0;
+    const bool rearm = tid == 0 && j + 4 < s;  // step j + 2 exists
+    double* vj = vloc + (size_t)par * s;
+    const double* vp = vloc + (size_t)pp * s;
+    const double* pq = ploc + (size_t)pp * s;
+    // ---- U: the pending update of step j-1 (rows >= j), column j first on its owner
+    double rv[KR], rp[KR], ag[CR], bg[CR];
+#pragma unroll
+    for (int k = 0; k < KR; ++k) {
+      const int r = rg + RG * k;
+      const bool ok = pend && r >= j && r < s;
+      rv[k] = ok ? vp[r] : 0.0;
+      rp[k] = ok ? pq[r] : 0.0;
+    }
+#pragma unroll
+    for (int c = 0; c < CR; ++c) {
+      const int g = (int)rank + CS * (cg + TCG * c);
+      const bool act = pend && g >= j && g < s;
+      const int gi = act ? g : 0;
+      bg[c] = act ? vp[gi] : 0.0;
+      ag[c] = act ? pq[gi] - 2.0 * Kp * bg[c] : 0.0;
+    }
+    if ((int)rank == owner) {
+      // column j = local column lj: group lj % TCG (two warps), slot lj / TCG. Its threads update
+      // it, copy it to colb and form the partial sums of sigma = ||A[j+2:, j]||^2.
+      const int lj = j >> lcs, cgj = lj & (TCG - 1), cj = lj >> 2;
+      if (cg == cgj) {
+        double sg = 0.0;
+#pragma unroll
+        for (int c = 0; c < CR; ++c) {
+          if (c == cj) {
+#pragma unroll
+            for (int k = 0; k < KR; ++k) {
+              const int r = rg + RG * k;
+              const double x = fma(-rv[k], ag[c], fma(-rp[k], bg[c], a[k][c]));
+              a[k][c] = x;
+              if (r >= j && r < s) {
+                colb[r] = x;
+                if (r >= j + 2) sg = fma(x, x, sg);
+                if (r == j) hsm[16] = x;
+                if (r == j + 1) hsm[17] = x;
+              }
+            }
+            ag[c] = 0.0;  // done: the U2 pass below must not apply it again
+            bg[c] = 0.0;
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sg += __shfl_xor_sync(0xffffffffu, sg, o);
+        if (lane == 0) hsm[warp & 1] = sg;
+      }
+      TRI_O(0);
+      __syncthreads();
+      TRI_O(1);
+      // Householder vector (LAPACK dlarfg, beta = -sign(alpha) ||(alpha, x)||): 1/mu from rsqrt,
+      // 1/(alpha - beta) from a refined reciprocal (the owner's critical path)
+      const double sigma = hsm[0] + hsm[1];
+      const double dj = hsm[16], alpha = hsm[17];
+      double tj, beta, scale;
+      if (sigma == 0.0) {
+        tj = 0.0;
+        beta = alpha;
+        scale = 0.0;
+      } else {
+        const double ss = fma(alpha, alpha, sigma);
+        const double rr = rsqrt(ss);
+        const double mu = ss * rr;
+        beta = (alpha <= 0.0) ? mu : -mu;
+        tj = fma(alpha, (alpha <= 0.0) ? -rr : rr, 1.0);  // (beta - alpha) / beta
+        const double dd = alpha - beta;
+        double rc;
+        asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rc) : "d"(dd));
+        double ee = fma(-dd, rc, 1.0);
+        rc = fma(rc, ee, rc);
+        ee = fma(-dd, rc, 1.0);
+        scale = fma(rc, ee, rc);
+      }
+      TRI_O(2);
+      if (tid == 0) {
+        dl[lj] = dj;
+        el[lj] = beta;
+        tl[lj] = tj;
+      }
+      // v_j pushed holder-major: thread t serves holder t / TPD, rows i0 + CS (t % TPD + TPD q)
+      const int hh = tid >> ltpd, mm = tid & (TPD - 1);
+      const int i0 = j + ((hh - j) & (CS - 1));
+      const uint32_t vb0 = cla_smem_u32(vj), hb0 = cla_smem_u32(&hbar[par]);
+      if (mm == 0) cla_st_async(cla_mapa(vb0 + 8u * (uint32_t)j, (uint32_t)hh), tj, cla_mapa(hb0, (uint32_t)hh));
+      double* vout = refl + (size_t)lj * s;
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int i = i0 + CS * (mm + TPD * q);
+        if (i > j && i < s) {
+          const double v = (i == j + 1) ? 1.0 : colb[i] * scale;
+          cla_st_async(cla_mapa(vb0 + 8u * (uint32_t)i, (uint32_t)hh), v, cla_mapa(hb0, (uint32_t)hh));
+          vout[i] = v;
+        }
+      }
+      if (prof && tid == 0) pt[7] += 1;
+    }
+    TRI_T(0);
+    // U2: the other own columns (overlaps the flight of v_j)
+#pragma unroll
+    for (int k = 0; k < KR; ++k) {
+      if (pend && RG * k < s && RG * k + RG - 1 >= j) {
+#pragma unroll
+        for (int c = 0; c < CR; ++c) a[k][c] = fma(-rv[k], ag[c], fma(-rp[k], bg[c], a[k][c]));
+      }
+    }
+    TRI_T(5);
+    cla_mbar_wait(&hbar[par], ph);  // tau_j and the held rows of v_j
+    if (rearm) cla_mbar_arm(&hbar[par], tri_tx_h(j + 2, s, (int)rank, CS));
+    TRI_T(1);
+    {
+      // the held rows (i = f + CS m) to every CTA: thread t serves destination t / TPD, rows
+      // m = t % TPD + TPD q
+      const int f = tri_held_first(j, (int)rank, CS);
+      const uint32_t v0 = cla_smem_u32(vj), b0 = cla_smem_u32(&vbar[par]);
+      const int dst = tid >> ltpd, mm = tid & (TPD - 1);
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int i = f + CS * (mm + TPD * q);
+        if (i < s) cla_st_async(cla_mapa(v0 + 8u * (uint32_t)i, (uint32_t)dst), vj[i], cla_mapa(b0, (uint32_t)dst));
+      }
+    }
+    cla_mbar_wait(&vbar[par], ph);  // all rows of v_j
+    if (rearm) cla_mbar_arm(&vbar[par], 8u * (uint32_t)(s - j - 3));
+    TRI_T(2);
+    // ---- D: column sums of A[:, g] v_j (rows > j) for the own columns
+    const double tj = vj[j];
+    double rj[KR], acc[CRP];
+#pragma unroll
+    for (int k = 0; k < KR; ++k) {
+      const int r = rg + RG * k;
+      rj[k] = (r > j && r < s) ? vj[r] : 0.0;
+    }
+#pragma unroll
+    for (int c = 0; c < CRP; ++c) acc[c] = 0.0;
+#pragma unroll
+    for (int k = 0; k < KR; ++k) {
+      if (RG * k < s && RG * k + RG - 1 > j) {
+#pragma unroll
+        for (int c = 0; c < CR; ++c) acc[c] = fma(a[k][c], rj[k], acc[c]);
+      }
+    }
+    double* wr = wred + par * 256;
+    {
+      const double w = tri_xreduce<CRP>(acc, lane);
+      if ((lane & (32 / CRP - 1)) == 0) wr[warp * 32 + tri_xreduce_col<CRP>(lane)] = w;
+    }
+    TRI_T(6);
+    __syncthreads();
+    {
+      // p_g of the own columns (lane = local column), pushed by every warp to destinations
+      // warp, warp + 8
+      double part = 0.0, pg = 0.0;
+      const int lc = lane, g = (int)rank + CS * lc;
+      const bool act = lc < ncl && g > j && g < s;
+      if (act) {
+        const int cgl = lc % TCG, c = lc / TCG;
+        pg = tj * (wr[(2 * cgl) * 32 + c] + wr[(2 * cgl + 1) * 32 + c]);
+        part = pg * vj[g];
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      const uint32_t b0 = cla_smem_u32(&pbar[par]);
+      const uint32_t p0 = cla_smem_u32(ploc + (size_t)par * s + g);
+      const uint32_t w0 = cla_smem_u32(wpart + par * 32 + rank);
+      for (int dst = warp; dst < CS; dst += 8) {
+        if (act) cla_st_async(cla_mapa(p0, (uint32_t)dst), pg, cla_mapa(b0, (uint32_t)dst));
+        if (lane == 0) cla_st_async(cla_mapa(w0, (uint32_t)dst), part, cla_mapa(b0, (uint32_t)dst));
+      }
+    }
+    TRI_T(3);
+    cla_mbar_wait(&pbar[par], ph);  // p_j and the CTAs' parts of p.v_j
+    if (rearm) cla_mbar_arm(&pbar[par], 8u * (uint32_t)(s - j - 3 + CS));
+    {
+      double k0 = 0.0, k1 = 0.0;
+      for (int q = 0; q < CS; q += 2) {
+        k0 += wpart[par * 32 + q];
+        k1 += wpart[par * 32 + q + 1];
+      }
+      Kp = 0.5 * tj * (k0 + k1);
+    }
+    TRI_T(4);
+  }
+  if (prof && threadIdx.x == 0)
+    for (int k = 0; k < 8; ++k) prof[rank * 8 + k] = pt[k];
+  if (prof && threadIdx.x == 0)
+    for (int k = 0; k < 4; ++k) prof[128 + rank * 4 + k] = po[k];
+#undef TRI_T
+#undef TRI_O
+  // the last pending update (step s-3) on the trailing 2 x 2, then d, e of the last two columns
+  if (s >= 3) {
+    const int pl = (s - 3) & 1;
+    const double* vp = vloc + (size_t)pl * s;
+    const double* pq = ploc + (size_t)pl * s;
+#pragma unroll
+    for (int c = 0; c < CR; ++c) {
+      const int g = (int)rank + CS * (cg + TCG * c);
+      if (g >= s - 2 && g < s) {
+        const double bg = vp[g], ag = pq[g] - 2.0 * Kp * bg;
+#pragma unroll
+        for (int k = 0; k < KR; ++k) {
+          const int r = rg + RG * k;
+          if (r >= g && r < s) {
+            const double x = a[k][c] - (vp[r] * ag + pq[r] * bg);
+            if (r == g)
+              d[g] = x;
+            else
+              e[g] = x;  // (s-1, s-2)
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (int q = tid; q < ncl * s; q += NT) {
+    int lc = q / s, i = q - lc * s, g = (int)rank + CS * lc;
+    if (g + 2 < s && i > g) Vh[IDX(i, g, ldv)] = refl[q];
+  }
+  for (int lc = tid; lc < ncl; lc += NT) {
+    int g = (int)rank + CS * lc;
+    if (g + 2 < s) {
+      d[g] = dl[lc];
+      e[g] = el[lc];
+      tau[g] = tl[lc];
+    }
+  }
+  cla_cluster_sync();  // no CTA leaves while a push to it may be in flight
 }
 
 // Back-transformation Y <- Q Y, Q = H_0 H_1 ... H_{s-3} (apply H_{s-3} first): one warp per

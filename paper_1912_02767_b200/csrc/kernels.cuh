@@ -238,7 +238,11 @@ __global__ void rr_prep_kernel(int s, int kxG, int kxH, double* __restrict__ G, 
                                int* __restrict__ status, int parts) {
   int total = s * s;
   const bool gs = parts & 1, hs = parts & 2;
-  if (gs && blockIdx.x == 0 && threadIdx.x == 0) *status = 0;
+  if (gs && blockIdx.x == 0 && threadIdx.x == 0) {
+    *status = 0;
+    *(unsigned long long*)(status + 16) = 0ull;  // linv_growth_kernel's key and block counter
+    status[20] = 0;
+  }
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
     int i = e % s, j = e / s;
     if (gs) Li[IDX(i, j, ld)] = (i == j && i < kxG) ? 1.0 : 0.0;
@@ -256,6 +260,50 @@ __global__ void rr_prep_kernel(int s, int kxG, int kxH, double* __restrict__ G, 
       double h = (j < kxH) ? ((i == j) ? theta[i] : 0.0) : 0.5 * (H[IDX(i, j, ld)] + H[IDX(j, i, ld)]);
       H[IDX(i, j, ld)] = h; H[IDX(j, i, ld)] = h;
     }
+  }
+}
+
+// Cholesky-QR conditioning guard (reading R44): the pivot rule (R20) bounds 1 / L_jj but not the
+// growth of the triangular inverse; a direction block whose L^-1 has an entry with
+// |L^-1_ij|^2 > thresh (unit-norm directions: cond(G) >~ thresh, the caller passes 1e8) is treated
+// like a failing pivot at row i, the direction nearly dependent on the ones before it, so the
+// caller drops it (R41).
+// Only sets *status when the Cholesky succeeded. Key / counter live at status[16..20] (reset by
+// rr_prep_kernel); the last block to finish decides.
+__global__ void linv_growth_kernel(int t, const double* __restrict__ Li, int ld, double thresh, int* status) {
+  __shared__ unsigned long long wk[32];
+  __shared__ bool last;
+  unsigned long long* key = (unsigned long long*)(status + 16);
+  unsigned* counter = (unsigned*)(status + 20);
+  unsigned long long best = 0;
+  const size_t total = (size_t)t * t;
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e % t), j = (int)(e / t);
+    if (i >= j) {
+      const float v = (float)fabs(Li[IDX(i, j, ld)]);
+      const unsigned long long k = ((unsigned long long)__float_as_uint(v) << 32) | (unsigned)i;
+      best = k > best ? k : best;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long y = __shfl_xor_sync(0xffffffffu, best, o);
+    best = y > best ? y : best;
+  }
+  if ((threadIdx.x & 31) == 0) wk[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) best = wk[w] > best ? wk[w] : best;
+    atomicMax(key, best);
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    const unsigned long long k = atomicAdd(key, 0ull);
+    const double v = (double)__uint_as_float((unsigned)(k >> 32));
+    if (*status == 0 && !(v * v <= thresh)) *status = (int)(k & 0xffffffffu) + 1;
   }
 }
 
@@ -777,27 +825,6 @@ __global__ void swap_cols_kernel(int n, double* __restrict__ X, int ld, int i, i
     double a = X[IDX(r, i, ld)];
     X[IDX(r, i, ld)] = X[IDX(r, j, ld)];
     X[IDX(r, j, ld)] = a;
-  }
-}
-
-// symmetric permutation of the s x s matrix M: swap rows i, j and columns i, j (one thread per
-// index r handles M[r][i] <-> M[r][j] and then the mirrored entries; the 2 x 2 block is done by r = i)
-__global__ void swap_sym_kernel(int s, double* __restrict__ M, int ld, int i, int j) {
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < s; r += gridDim.x * blockDim.x) {
-    if (r == i || r == j) continue;
-    double a = M[IDX(r, i, ld)], b = M[IDX(r, j, ld)];
-    M[IDX(r, i, ld)] = b;
-    M[IDX(r, j, ld)] = a;
-    double c = M[IDX(i, r, ld)], d = M[IDX(j, r, ld)];
-    M[IDX(i, r, ld)] = d;
-    M[IDX(j, r, ld)] = c;
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    double ii = M[IDX(i, i, ld)], jj = M[IDX(j, j, ld)], ij = M[IDX(i, j, ld)], ji = M[IDX(j, i, ld)];
-    M[IDX(i, i, ld)] = jj;
-    M[IDX(j, j, ld)] = ii;
-    M[IDX(i, j, ld)] = ji;
-    M[IDX(j, i, ld)] = ij;
   }
 }
 

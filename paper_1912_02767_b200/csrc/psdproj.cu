@@ -373,6 +373,15 @@ static int cla_attrs() {
   CK(cudaFuncSetAttribute(backtransform_panel_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, bmx));
   CK(cudaFuncSetAttribute(tridiag_cluster_kernel<64, 256, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   CK(cudaFuncSetAttribute(tridiag_cluster_kernel<64, 256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+#define TRI_REG_ATTR(KR, CR)                                                                                          \
+  CK(cudaFuncSetAttribute(tridiag_reg_kernel<KR, CR>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)); \
+  CK(cudaFuncSetAttribute(tridiag_reg_kernel<KR, CR>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  TRI_REG_ATTR(3, 5)
+  TRI_REG_ATTR(4, 4)
+  TRI_REG_ATTR(6, 6)
+  TRI_REG_ATTR(7, 7)
+  TRI_REG_ATTR(8, 8)
+#undef TRI_REG_ATTR
   done = true;
   return 0;
 }
@@ -385,24 +394,25 @@ static int cholesky_run(cudaStream_t st, int t, double* G, int ld, int* d_status
                         size_t gscratch_elems = 0, double* Linv = nullptr, int ldi = 0) {
   TRY(cla_attrs());
   static int fuse = getenv("PSDPROJ_CHOL_NOFUSE") ? 0 : 1;
+  const double frel = 1e-12;  // R20
   if (Linv && fuse) {
     if (int cs = cla_cluster_size(t, chol_inv_smem_doubles)) {
       return launch_cluster(cholesky_cluster_kernel<false, true>, cs, CLA_NT,
-                            chol_inv_smem_doubles(t, cs) * sizeof(double), st, t, G, ld, 1e-12, d_status,
+                            chol_inv_smem_doubles(t, cs) * sizeof(double), st, t, G, ld, frel, d_status,
                             (double*)nullptr, Linv, ldi);
     }
   }
   if (int cs = cla_cluster_size(t, chol_smem_doubles)) {
     TRY(launch_cluster(cholesky_cluster_kernel<false, false>, cs, CLA_NT, chol_smem_doubles(t, cs) * sizeof(double),
-                       st, t, G, ld, 1e-12, d_status, (double*)nullptr, (double*)nullptr, 0));
+                       st, t, G, ld, frel, d_status, (double*)nullptr, (double*)nullptr, 0));
     return Linv ? trinv_run(st, t, G, ld, Linv, ldi) : 0;
   }
   if (gscratch && (size_t)16 * chol_local_cols(t, 16) * t <= gscratch_elems && t <= 4096) {
     TRY(launch_cluster(cholesky_cluster_kernel<true, false>, 16, CLA_NT, chol_smem_doubles_ga(t, 16) * sizeof(double),
-                       st, t, G, ld, 1e-12, d_status, gscratch, (double*)nullptr, 0));
+                       st, t, G, ld, frel, d_status, gscratch, (double*)nullptr, 0));
     return Linv ? trinv_run(st, t, G, ld, Linv, ldi) : 0;
   }
-  cholesky_kernel<1024><<<1, 1024, 0, st>>>(t, G, ld, 1e-12, d_status);
+  cholesky_kernel<1024><<<1, 1024, 0, st>>>(t, G, ld, frel, d_status);
   CKL();
   return Linv ? trinv_run(st, t, G, ld, Linv, ldi) : 0;
 }
@@ -464,11 +474,96 @@ static int eigh_top(cudaStream_t st, int s, const double* Hs, int ldh, int m, do
   static long long* dprof = nullptr;
   static int want_prof = getenv("PSDPROJ_TRI_PROF") ? 1 : 0;
   static int tri_dbg = getenv("PSDPROJ_TRI_DBG") ? atoi(getenv("PSDPROJ_TRI_DBG")) : 0;  // timing experiments only
-  if (want_prof && !dprof) CK(cudaMalloc(&dprof, 16 * 8 * sizeof(long long)));
+  if (want_prof && !dprof) CK(cudaMalloc(&dprof, 16 * 12 * sizeof(long long)));
+  if (want_prof) CK(cudaMemsetAsync(dprof, 0, 16 * 12 * sizeof(long long), st));
 #define TRI_LAUNCH(PL, NTH, GA, CSZ, SMEM)                                                                         \
   TRY(launch_cluster(tridiag_cluster_kernel<PL, NTH, GA>, CSZ, NTH, SMEM, st, s, Hs, ldh, w.td, w.te, w.ttau, w.Vh, \
                      w.ldv, dprof, w.tG, tri_dbg))
-  if (tcs) {
+  static int tri_reg = getenv("PSDPROJ_TRI_NOREG") ? 0 : 1;
+  const int kr = cdiv(s, 64), cr = tcs ? cdiv(cdiv(s, tcs), TRI_TCG) : 99;
+  if (tcs && tri_reg && kr <= 8 && cr <= 8 &&
+      tri_reg_smem_doubles(s, tcs) * sizeof(double) <= (size_t)CLA_SMEM_BYTES) {
+    const size_t tsm = tri_reg_smem_doubles(s, tcs) * sizeof(double);
+#define TRI_REG(KR, CR) \
+  TRY(launch_cluster(tridiag_reg_kernel<KR, CR>, tcs, 256, tsm, st, s, Hs, ldh, w.td, w.te, w.ttau, w.Vh, w.ldv, dprof, tri_dbg))
+    if (kr <= 3 && cr <= 5)
+      TRI_REG(3, 5);
+    else if (kr <= 4 && cr <= 4)
+      TRI_REG(4, 4);
+    else if (kr <= 6 && cr <= 6)
+      TRI_REG(6, 6);
+    else if (kr <= 7 && cr <= 7)
+      TRI_REG(7, 7);
+    else
+      TRI_REG(8, 8);
+#undef TRI_REG
+    static int verify = getenv("PSDPROJ_TRI_VERIFY") ? 1 : 0;  // debugging: compare with the smem kernel
+    if (verify) {
+      static double* vb = nullptr;
+      if (!vb) CK(cudaMalloc(&vb, sizeof(double) * ((size_t)2 * EIG_MAX * EIG_MAX + 4 * EIG_MAX)));
+      double *vd = vb, *ve = vb + EIG_MAX, *vt = vb + 2 * EIG_MAX, *vV = vb + 4 * EIG_MAX;
+      const size_t tsm2 = tri_smem_doubles(s, tcs) * sizeof(double);
+      if (s <= 32 * 8)
+        TRY(launch_cluster(tridiag_cluster_kernel<8, 512>, tcs, 512, tsm2, st, s, Hs, ldh, vd, ve, vt, vV, w.ldv,
+                           (long long*)nullptr, w.tG, 0));
+      else if (s <= 32 * 14)
+        TRY(launch_cluster(tridiag_cluster_kernel<14, 256>, tcs, 256, tsm2, st, s, Hs, ldh, vd, ve, vt, vV, w.ldv,
+                           (long long*)nullptr, w.tG, 0));
+      else
+        TRY(launch_cluster(tridiag_cluster_kernel<20, 256>, tcs, 256, tsm2, st, s, Hs, ldh, vd, ve, vt, vV, w.ldv,
+                           (long long*)nullptr, w.tG, 0));
+      CK(cudaStreamSynchronize(st));
+      std::vector<double> a1(2 * s), a2(2 * s);
+      CK(cudaMemcpy(a1.data(), w.td, s * sizeof(double), cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(a1.data() + s, w.te, (s - 1) * sizeof(double), cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(a2.data(), vd, s * sizeof(double), cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(a2.data() + s, ve, (s - 1) * sizeof(double), cudaMemcpyDeviceToHost));
+      double mx = 0, df = 0;
+      int at = -1;
+      for (int i = 0; i < 2 * s - 1; ++i) {
+        mx = std::max(mx, std::fabs(a2[i]));
+        const double dd = std::fabs(std::fabs(a1[i]) - std::fabs(a2[i]));
+        if (!(dd <= df)) { df = dd; at = i; }
+      }
+      {
+        // reflectors: tau and Vh columns 0..s-3 (rows below the diagonal)
+        std::vector<double> t1(s), t2(s), V1((size_t)s * w.ldv), V2((size_t)s * w.ldv);
+        CK(cudaMemcpy(t1.data(), w.ttau, (s - 2) * sizeof(double), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(t2.data(), vt, (s - 2) * sizeof(double), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(V1.data(), w.Vh, (size_t)s * w.ldv * sizeof(double), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(V2.data(), vV, (size_t)s * w.ldv * sizeof(double), cudaMemcpyDeviceToHost));
+        double dt = 0, dv = 0;
+        int atv = -1;
+        for (int g = 0; g + 2 < s; ++g) {
+          dt = std::max(dt, std::fabs(t1[g] - t2[g]));
+          for (int i = g + 1; i < s; ++i) {
+            const double dd = std::fabs(V1[(size_t)g * w.ldv + i] - V2[(size_t)g * w.ldv + i]);
+            if (!(dd <= dv)) { dv = dd; atv = g; }
+          }
+        }
+        if (!(dt <= 1e-9) || !(dv <= 1e-9)) {
+          fprintf(stderr, "TRI_VERIFY s=%d cs=%d: tau diff %g, Vh diff %g (column %d)\n", s, tcs, dt, dv, atv);
+          df = 1.0;
+          mx = 0.0;
+        }
+      }
+      if (!(df <= 1e-10 * mx)) {
+        static int nb = 0;
+        fprintf(stderr, "TRI_VERIFY s=%d cs=%d: max |d,e| diff %g at %d (scale %g)\n", s, tcs, df, at, mx);
+        if (nb < 3) {
+          std::vector<double> H((size_t)s * s);
+          CK(cudaMemcpy2D(H.data(), s * sizeof(double), Hs, (size_t)ldh * sizeof(double), s * sizeof(double), s,
+                          cudaMemcpyDeviceToHost));
+          char fn[128];
+          snprintf(fn, sizeof fn, "gpurun_out/tri_bad_%d.bin", nb++);
+          if (FILE* f = fopen(fn, "wb")) {
+            fwrite(H.data(), sizeof(double), H.size(), f);
+            fclose(f);
+          }
+        }
+      }
+    }
+  } else if (tcs) {
     const size_t tsm = tri_smem_doubles(s, tcs) * sizeof(double);
     if (s <= 32 * 4)
       TRI_LAUNCH(4, 512, false, tcs, tsm);
@@ -497,13 +592,18 @@ static int eigh_top(cudaStream_t st, int s, const double* Hs, int ldh, int m, do
   }
 #undef TRI_LAUNCH
   if (want_prof && tcs) {
-    long long h[128];
+    long long h[192];
     CK(cudaStreamSynchronize(st));
     CK(cudaMemcpy(h, dprof, sizeof(h), cudaMemcpyDeviceToHost));
     for (int r = 0; r < std::min(tcs, 3); ++r)
-      fprintf(stderr, "tri prof s=%d cs=%d rank %d: house %lld B1 %lld vgather %lld cols %lld B2 %lld gatherK %lld sync %lld (cycles/step)\n",
+      fprintf(stderr, "tri prof s=%d cs=%d rank %d: house %lld B1 %lld vgather %lld cols %lld B2 %lld U2 %lld D %lld (cycles/step) owner-steps %lld house/owner-step %lld\n",
               s, tcs, r, h[r * 8 + 0] / (s - 2), h[r * 8 + 1] / (s - 2), h[r * 8 + 2] / (s - 2), h[r * 8 + 3] / (s - 2),
-              h[r * 8 + 4] / (s - 2), h[r * 8 + 5] / (s - 2), h[r * 8 + 6] / (s - 2));
+              h[r * 8 + 4] / (s - 2), h[r * 8 + 5] / (s - 2), h[r * 8 + 6] / (s - 2), h[r * 8 + 7],
+              h[r * 8 + 7] ? h[r * 8 + 0] / h[r * 8 + 7] : 0);
+    for (int r = 0; r < std::min(tcs, 3); ++r)
+      if (h[r * 8 + 7])
+        fprintf(stderr, "   owner-step: U1 %lld syncthreads %lld scalars %lld (cycles)\n", h[128 + r * 4] / h[r * 8 + 7],
+                h[128 + r * 4 + 1] / h[r * 8 + 7], h[128 + r * 4 + 2] / h[r * 8 + 7]);
   }
   static int dbg_eigh = getenv("PSDPROJ_DEBUG_EIGH") ? 1 : 0;
   if (dbg_eigh) {
@@ -1070,6 +1170,15 @@ struct Run {
     if (t > 0) {
       TRY(cholesky_run(st, t, c->Gc, ldm, c->d_status, c->tG, (size_t)c->s_max * c->s_max + 16 * (size_t)c->s_max + 2048,
                        c->Li + kx + (size_t)kx * ldm, ldm));
+      // R44: reject a direction block with max |L^-1|^2 > 1e8 (unit-norm directions: cond(G) >~ 1e8).
+      // Cholesky-QR leaves the new block orthonormal only to ~u cond(G), and the pencil takes
+      // X^T X = I for granted in the next step; the pivot rule (R20) alone admits cond(G) ~ 1e12
+      static double gmax = getenv("PSDPROJ_LINV_MAX") ? atof(getenv("PSDPROJ_LINV_MAX")) : 1e8;
+      if (gmax > 0) {
+        linv_growth_kernel<<<std::min(296, cdiv(t * t, 256)), 256, 0, st>>>(
+            t, c->Li + kx + (size_t)kx * ldm, ldm, gmax, c->d_status);
+        CKL();
+      }
     }
     return 0;
   }
@@ -1271,10 +1380,22 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
     TRY(run.copy_cols(nl, m, c->S, ld, c->Xw, ld));
   }
   TRY(run.amul(sgn, A, lda, c->S, ld, m, c->BS, ld));
-  // ---- Alg. 3 line 2: Rayleigh-Ritz on span(X0): G = X0^T X0 (I when warm), H = X0^T B X0
-  if (cold) TRY(run.gram(m, m, c->S, ld, c->S, ld, c->G, ldm));
+  // ---- Alg. 3 line 2: Rayleigh-Ritz on span(X0): G = X0^T X0, H = X0^T B X0 (G is formed for a warm
+  // block too: it is the previous call's block, orthonormal only up to that call's drift)
+  TRY(run.gram(m, m, c->S, ld, c->S, ld, c->G, ldm));
   TRY(run.gram(m, m, c->S, ld, c->BS, ld, c->Hm, ldm));
-  int rc = run.rr(m, cold ? 0 : m, 0, c->d_thU, m);
+  int rc = run.rr(m, 0, 0, c->d_thU, m);
+  if (rc > 0 && !cold) {
+    // the warm block lost rank (e.g. the previous input was 0): cold start (R28)
+    cold = true;
+    info->cold = 1;
+    m = c->m0;
+    TRY(run.philox(m, c->S, ld, 0u));
+    TRY(run.amul(sgn, A, lda, c->S, ld, m, c->BS, ld));
+    TRY(run.gram(m, m, c->S, ld, c->S, ld, c->G, ldm));
+    TRY(run.gram(m, m, c->S, ld, c->BS, ld, c->Hm, ldm));
+    rc = run.rr(m, 0, 0, c->d_thU, m);
+  }
   if (rc > 0) return set_err(PSDPROJ_E_DEGENERATE, "start block rank deficient");
   TRY(rc);
   std::vector<double> thU(c->h_d, c->h_d + m);  // all m values (the initial RR keeps m of m)
@@ -1289,7 +1410,46 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
   std::vector<char> hasP(m, 0);
   int status = PSDPROJ_NOT_CONVERGED;
   int k = 0;
+  static int restart = getenv("PSDPROJ_RESTART") ? atoi(getenv("PSDPROJ_RESTART")) : 100;
   for (;;) {
+    // R47: restart every `restart` iterations -- X_U re-orthonormalised (against X_L, then by the
+    // Cholesky-QR of the start-block RR), B X_U recomputed, Rayleigh-Ritz on span(X_U), P dropped.
+    // The pencil takes X_U^T X_U = I and B X_U from the rotation; both drift (by ~u cond(G) and
+    // ~u ||C'|| per step) on long runs that never meet the stopping rule.
+    if (restart > 0 && k > 0 && k % restart == 0 && mU > 0) {
+      TRY(run.mark(0));
+      if (hard && nL > 0) {
+        TRY(run.gram(nL, mU, c->XL, ld, c->S, ld, c->Y, ldm));
+        TRY(run.gemm(OP_N, OP_N, nl, mU, nL, -1.0, c->XL, ld, c->Y, ldm, 1.0, c->S, ld));
+      }
+      TRY(run.amul(sgn, A, lda, c->S, ld, mU, c->BS, ld));
+      int rr0;
+      for (;;) {
+        TRY(run.gram(mU, mU, c->S, ld, c->S, ld, c->G, ldm));
+        TRY(run.gram(mU, mU, c->S, ld, c->BS, ld, c->Hm, ldm));
+        rr0 = run.rr(mU, 0, 0, c->d_thU, mU);
+        if (rr0 <= 0 || mU <= 1) break;
+        // a column that became dependent on the others (duplicated direction): drop it (R41)
+        const int col = rr0 - 1, last = mU - 1;
+        if (col != last) {
+          swap_cols_kernel<<<grid1d((size_t)nl), 256, 0, st>>>(nl, c->S, ld, col, last);
+          CKL();
+          swap_cols_kernel<<<grid1d((size_t)nl), 256, 0, st>>>(nl, c->BS, ld, col, last);
+          CKL();
+        }
+        --mU;
+        info->dropped++;
+      }
+      if (rr0 > 0) return set_err(PSDPROJ_E_DEGENERATE, "restart block rank deficient");
+      TRY(rr0);
+      thU.assign(c->h_d, c->h_d + mU);
+      TRY(run.gemm(OP_N, OP_N, nl, mU, mU, 1.0, c->S, ld, c->Cp, ldm, 0.0, c->S2, ld));
+      TRY(run.gemm(OP_N, OP_N, nl, mU, mU, 1.0, c->BS, ld, c->Cp, ldm, 0.0, c->BS2, ld));
+      std::swap(c->S, c->S2);
+      std::swap(c->BS, c->BS2);
+      CK(cudaMemcpyAsync(c->d_thU, c->d_ths, sizeof(double) * mU, cudaMemcpyDeviceToDevice, st));
+      hasP.assign(mU, 0);
+    }
     // ---- line 5: R = B X - X Theta, r_i = ||R_i|| (unlocked columns)
     TRY(run.mark(6));
     resid_norm_kernel<256><<<mU, 256, 0, st>>>(nl, c->S, ld, c->BS, ld, c->d_thU, c->R, ld, c->d_r, c->sharded ? 1 : 0);
@@ -1302,6 +1462,17 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
     CK(cudaMemcpyAsync(c->h_d, c->d_r, sizeof(double) * mU, cudaMemcpyDeviceToHost, st));
     TRY(run.sync());
     rU.assign(c->h_d, c->h_d + mU);
+    const int trace = getenv("PSDPROJ_TRACE") ? 1 : 0;  // debugging: per-iteration state on stderr
+    if (trace) {
+      double tmx = -INFINITY, tmn = INFINITY, rmx = 0;
+      for (int j = 0; j < mU; ++j) {
+        tmx = std::max(tmx, thU[j]);
+        tmn = std::min(tmn, thU[j]);
+        rmx = std::max(rmx, rU[j]);
+      }
+      fprintf(stderr, "trace k=%d mU=%d nL=%d qe=%d theta[%g, %g] rmax %g tol %g dropped %d\n", k, mU, nL, qe, tmn, tmx,
+              rmx, tol, info->dropped);
+    }
     // ---- stopping rule (R12)
     int npos = nL;
     bool conv_pos = true;
@@ -1418,10 +1589,16 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
       TRY(run.gather(nl, ap, BP, ld, c->BPb, ld, PJ));
     }
     const int wp = aw + ap;
-    if (hard && nL > 0 && wp > 0) {
-      TRY(run.gram(nL, wp, c->XL, ld, W, ld, c->Y, ldm));
-      TRY(run.gemm(OP_N, OP_N, nl, wp, nL, -1.0, c->XL, ld, c->Y, ldm, 1.0, W, ld));
-      if (ap > 0) TRY(run.gemm(OP_N, OP_N, nl, ap, nL, -1.0, c->BXL, ld, c->Y + (size_t)aw * ldm, ldm, 1.0, BP, ld));
+    if (hard && nL > 0 && mU + wp > 0) {
+      // [X_U W P] <- [X_U W P] - X_L (X_L^T [X_U W P]) (B-images of X_U and P alike). X_U is
+      // re-projected every iteration: it inherits the rotation's O(u ||C'||) component along X_L,
+      // which otherwise compounds over a long run until active columns duplicate locked ones (R46)
+      const int cols = mU + wp;
+      TRY(run.gram(nL, cols, c->XL, ld, c->S, ld, c->Y, ldm));
+      TRY(run.gemm(OP_N, OP_N, nl, cols, nL, -1.0, c->XL, ld, c->Y, ldm, 1.0, c->S, ld));
+      if (mU > 0) TRY(run.gemm(OP_N, OP_N, nl, mU, nL, -1.0, c->BXL, ld, c->Y, ldm, 1.0, c->BS, ld));
+      if (ap > 0)
+        TRY(run.gemm(OP_N, OP_N, nl, ap, nL, -1.0, c->BXL, ld, c->Y + (size_t)(mU + aw) * ldm, ldm, 1.0, BP, ld));
     }
     if (wp > 0) {  // [W P] <- [W P] - X_U (X_U^T [W P]): the pencil's X-block of G becomes [I 0]
       TRY(run.gram(mU, wp, c->S, ld, W, ld, c->Y, ldm));
@@ -1459,8 +1636,16 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
     TRY(run.gram(s, s, c->S, ld, c->BS, ld, c->Hm, ldm));
     int sU = s;
     rc = run.rr(s, mU, mU, c->d_thU, std::min(mU + qe, s), ovl);
+    // a failed attempt still ran the eigensolver, which uses G / Hm as scratch: a retry forms the
+    // pencil again from S, BS
+    auto regram = [&](int sr) -> int {
+      TRY(run.gram(sr - mU, sr - mU, c->S + (size_t)mU * ld, ld, c->S + (size_t)mU * ld, ld,
+                   c->G + mU + (size_t)mU * ldm, ldm));
+      return run.gram(sr, sr, c->S, ld, c->BS, ld, c->Hm, ldm);
+    };
     if (rc > 0 && ap > 0) {
       sU = s - ap;  // drop P and retry (R20)
+      TRY(regram(sU));
       rc = run.rr(sU, mU, mU, c->d_thU, std::min(mU + qe, sU));
     }
     // R41: still rank deficient -> drop the direction at the failing pivot (greedy rank-revealing
@@ -1474,13 +1659,10 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
         CKL();
         swap_cols_kernel<<<grid1d((size_t)nl), 256, 0, st>>>(nl, c->BS, ld, col, last);
         CKL();
-        swap_sym_kernel<<<grid1d((size_t)sU), 256, 0, st>>>(sU, c->G, ldm, col, last);
-        CKL();
-        swap_sym_kernel<<<grid1d((size_t)sU), 256, 0, st>>>(sU, c->Hm, ldm, col, last);
-        CKL();
       }
       --sU;
       info->dropped++;
+      TRY(regram(sU));
       rc = run.rr(sU, mU, mU, c->d_thU, std::min(mU + qe, sU));
     }
     if (rc > 0) return set_err(PSDPROJ_E_DEGENERATE, "Cholesky-QR failed at pivot %d (s=%d)", rc, sU);
@@ -1496,6 +1678,25 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
     TRY(run.gemm(OP_N, OP_N, nl, mUn, sU - mU, 1.0, c->BS + (size_t)mU * ld, ld, c->Cp + mU, ldm, 0.0, c->BPb, ld));
     std::swap(c->S, c->S2);
     std::swap(c->BS, c->BS2);
+    if (getenv("PSDPROJ_TRACE")) {  // debugging: orthonormality of the new block
+      std::vector<double> hY((size_t)ldm * std::max(mUn, 1));
+      TRY(run.gram(mUn, mUn, c->S, ld, c->S, ld, c->Y, ldm));
+      TRY(run.sync());
+      CK(cudaMemcpy(hY.data(), c->Y, sizeof(double) * (size_t)ldm * mUn, cudaMemcpyDeviceToHost));
+      double oU = 0;
+      for (int j = 0; j < mUn; ++j)
+        for (int i = 0; i < mUn; ++i) oU = std::max(oU, std::fabs(hY[(size_t)j * ldm + i] - (i == j)));
+      double oL = 0;
+      if (nL > 0) {
+        TRY(run.gram(nL, mUn, c->XL, ld, c->S, ld, c->Y, ldm));
+        TRY(run.sync());
+        CK(cudaMemcpy(hY.data(), c->Y, sizeof(double) * (size_t)ldm * mUn, cudaMemcpyDeviceToHost));
+        for (int j = 0; j < mUn; ++j)
+          for (int i = 0; i < nL; ++i) oL = std::max(oL, std::fabs(hY[(size_t)j * ldm + i]));
+      }
+      fprintf(stderr, "   rotation: s=%d mUn=%d |XU'XU-I| %g |XL'XU| %g  theta %g..%g\n", sU, mUn, oU, oL,
+              ths.empty() ? 0.0 : ths.back(), ths.empty() ? 0.0 : ths.front());
+    }
     CK(cudaMemcpyAsync(c->d_thU, c->d_ths, sizeof(double) * mUn, cudaMemcpyDeviceToDevice, st));
     thU.assign(ths.begin(), ths.begin() + mUn);
     rU.assign(mUn, INFINITY);

@@ -73,8 +73,10 @@ def test_philox_gauss_matches_oracle(api):
     assert np.abs(got - ref).max() < 1e-13
 
 
-@pytest.mark.parametrize("s,m", [(1, 1), (2, 2), (3, 1), (17, 17), (64, 20), (160, 60), (161, 161), (300, 100),
-                                 (500, 170), (640, 220), (641, 120), (800, 260), (1100, 300), (2000, 200)])
+@pytest.mark.parametrize("s,m", [(1, 1), (2, 2), (3, 1), (17, 17), (64, 20), (65, 65), (100, 33), (129, 129),
+                                 (160, 60), (161, 161), (193, 64), (256, 90), (257, 257), (300, 100), (385, 128),
+                                 (449, 150), (500, 170), (512, 512), (513, 171), (640, 220), (641, 120), (800, 260),
+                                 (1100, 300), (2000, 200)])
 def test_eigh_tridiagonal(api, s, m):
     rng = np.random.default_rng(1000 + s)
     M = rng.standard_normal((s, s))

@@ -16,4 +16,4 @@ for k, A in enumerate(mats):
     print(json.dumps({"n": n, "k": k, "ms": round(dt*1e3, 2), "iters": inf["iters"], "status": inf["status"], "npos": inf["npos"],
           "rr_max": inf["rr_max"], "a_cols/it": round(inf["a_cols"]/max(1,inf["iters"]),1), "amul_ms": round(inf["amul_ms"],2),
           "amul_TF": round(inf["amul_flops"]/max(inf["amul_ms"],1e-9)/1e9, 2), "locked": inf["locked"], "launches": inf["launches"],
-          "bound": inf["err_bound"], "m": inf["m"], "phase_ms": [round(x, 2) for x in inf["phase_ms"]]}), flush=True)
+          "bound": inf["err_bound"], "m": inf["m"], "dropped": inf["dropped"], "phase_ms": [round(x, 2) for x in inf["phase_ms"]]}), flush=True)
