@@ -688,30 +688,29 @@ __device__ __forceinline__ void cla_st_async(uint32_t raddr, double v, uint32_t 
 
 // Register-resident, push-exchanged tridiagonalisation (s <= 64 KR, cdiv(s, CS) <= TRI_TCG CR):
 // the own columns live in registers, so a step moves no matrix bytes through shared memory, and
-// the exchanges of a step are one-way st.async pushes completing on the receiver's mbarrier
-// instead of cluster barriers + remote loads (tools/micro/push_bench*.cu: ~0.9k cycles per hop
+// the exchanges of a step are one-way pushes completing on the receiver's mbarrier instead of
+// cluster barriers + remote loads (tools/micro/push_bench*.cu: ~0.9k cycles per st.async hop
 // against ~1.6k for barrier.cluster + remote load).
 // Thread t: column group cg = t / 64 (two warps), rows r = t % 64 + 64 k (k < KR), own local
 // columns lc = cg + TRI_TCG c (c < CR). Step j (parity buffers par = j & 1, mbarrier phase j >> 1):
 //   U1  owner(j): the threads of column j apply the pending update (step j-1) to it, copy it to
-//       colb and reduce sigma = ||A[j+2:, j]||^2; Householder scalars; v_j[i] pushed to holder
-//       i % CS (holder-major thread mapping: a warp targets at most two CTAs), tau_j to every
-//       CTA (hbar); v_j kept in refl for the output
+//       colb and reduce sigma = ||A[j+2:, j]||^2; Householder scalars; v_j written to the
+//       reflector store (tau_j at row j) and sent by one bulk copy (cp.async.bulk
+//       shared::cta -> shared::cluster) per CTA, completing on each CTA's vbar
 //   U2  all: the pending update on the other own columns (overlaps the flight of v_j)
-//   F   every CTA: wait hbar, push its held rows of v_j to every CTA (vbar); wait vbar
-//   D   all: acc[c] = sum_r a[r][c] v_j[r] (rows > j); column sums by an in-warp transpose
-//       reduction + the group's two warps; p_g = tau_j sum for own g > j pushed to every CTA's
-//       ploc[par][g], the CTA's part of p.v_j to wpart[par][rank] (pbar, warp w serving
-//       destinations w, w + 8); wait pbar; K_j = tau_j / 2 sum(wpart)
-// Three hops per column (owner -> holders -> all, p all-gather): the step is latency-bound at
-// ~4-6k cycles (s = 200..450) against ~7-8k for tridiag_cluster_kernel.
+//   D   all: wait vbar; acc[c] = sum_r a[r][c] v_j[r] (rows > j); column sums by an in-warp
+//       transpose reduction + the group's two warps; p_g = tau_j sum for own g > j st.async'ed to
+//       every CTA's ploc[par][g], the CTA's part of p.v_j to wpart[par][rank] (pbar, warp w
+//       serving destinations w, w + 8); wait pbar; K_j = tau_j / 2 sum(wpart)
+// Two hops per column (the owner's broadcast, the p all-gather): the step is latency-bound.
 // Buffer reuse is ordered by the data dependencies: nothing is written into a parity-par buffer
 // for step j + 2 before every CTA has pushed p_{j+1}, i.e. finished reading step j's buffers.
 // Each CTA re-arms a barrier for step j + 2 right after observing its step-j phase (by then no
 // step-(j+2) bytes can have arrived), so no phase ever sees bytes before its expect_tx.
 constexpr int TRI_TCG = 4;
 __host__ __device__ inline size_t tri_reg_smem_doubles(int s, int CS) {
-  return (size_t)cdiv(s, CS) * s + 4 * (size_t)s + 3 * (size_t)cdiv(s, CS) + (s + 256) + 2 * 8 * 32 + 64 + 16;
+  const size_t sr = (size_t)((s + 1) & ~1);
+  return (size_t)cdiv(s, CS) * sr + 4 * sr + 3 * (size_t)cdiv(s, CS) + (s + 256) + 2 * 8 * 32 + 64 + 16;
 }
 template <int N>
 __device__ __forceinline__ double tri_xreduce(double (&v)[N], int lane) {
@@ -741,11 +740,6 @@ __device__ __forceinline__ int tri_xreduce_col(int lane) {
   return c;
 }
 __host__ __device__ constexpr int tri_pow2_ceil(int n) { return n <= 1 ? 1 : 2 * tri_pow2_ceil((n + 1) / 2); }
-__device__ __forceinline__ int tri_held_first(int j, int h, int CS) { return j + 1 + ((h - j - 1) & (CS - 1)); }
-__device__ __forceinline__ uint32_t tri_tx_h(int j, int s, int h, int CS) {
-  const int f = tri_held_first(j, h, CS);
-  return 8u * (uint32_t)(1 + (f < s ? (s - 1 - f) / CS + 1 : 0));
-}
 
 template <int KR, int CR>
 __global__ void __launch_bounds__(256, 1) tridiag_reg_kernel(int s, const double* __restrict__ A, int lda,
@@ -756,7 +750,7 @@ __global__ void __launch_bounds__(256, 1) tridiag_reg_kernel(int s, const double
   static_assert(RG * TCG == NT, "thread layout");
   static_assert(CRP <= 32, "columns per thread");
   extern __shared__ __align__(16) double sm[];
-  __shared__ __align__(8) uint64_t hbar[2], vbar[2], pbar[2];
+  __shared__ __align__(8) uint64_t vbar[2], pbar[2];
   __shared__ double hsm[18];
   long long pt[8] = {0, 0, 0, 0, 0, 0, 0, 0}, po[4] = {0, 0, 0, 0};
   long long tprev = 0;
@@ -775,13 +769,13 @@ __global__ void __launch_bounds__(256, 1) tridiag_reg_kernel(int s, const double
     tprev = tn;                                                           \
   }
   const int CS = (int)gridDim.x, lcs = __ffs(CS) - 1;  // CS in {4, 8, 16}
-  const int TPD = NT / CS, ltpd = __ffs(TPD) - 1;      // threads per holder / destination
   const unsigned rank = cla_rank();
-  const int ncl = cdiv(s, CS);  // <= 32: a holder has at most 2 TPD rows
-  double* refl = sm;                      // ncl x s: reflectors of the own columns
-  double* vloc = refl + (size_t)ncl * s;  // 2 x s (parity): [tau_j at index j | v_j at j+1..s-1]
-  double* ploc = vloc + 2 * (size_t)s;    // 2 x s (parity): p_j (pushed by the column owners)
-  double* colb = ploc + 2 * (size_t)s;    // column j for the owner's Householder step (s + 256: tail pad)
+  const int ncl = cdiv(s, CS);  // <= 32 (one lane per own column in the p push)
+  const int sr = (s + 1) & ~1;             // even row stride: 16-byte aligned bulk copies
+  double* refl = sm;                       // ncl x sr: reflectors of the own columns (tau_j at row j)
+  double* vloc = refl + (size_t)ncl * sr;  // 2 x sr (parity): [tau_j at index j | v_j at j+1..s-1]
+  double* ploc = vloc + 2 * (size_t)sr;    // 2 x sr (parity): p_j (pushed by the column owners)
+  double* colb = ploc + 2 * (size_t)sr;    // column j for the owner's Householder step (s + 256: tail pad)
   double* wred = colb + s + 256;          // 2 x 8 warps x 32: per-warp column partials (parity)
   double* wpart = wred + 2 * 8 * 32;      // 2 x 32 (parity): every CTA's part of p.v_j, by rank
   double* dl = wpart + 64;
@@ -803,14 +797,12 @@ __global__ void __launch_bounds__(256, 1) tridiag_reg_kernel(int s, const double
   __syncthreads();
   if (tid == 0) {
     for (int b = 0; b < 2; ++b) {
-      cla_mbar_init(&hbar[b], 1);
       cla_mbar_init(&vbar[b], 1);
       cla_mbar_init(&pbar[b], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int jj = 0; jj < 2 && jj + 2 < s; ++jj) {
-      cla_mbar_arm(&hbar[jj], tri_tx_h(jj, s, (int)rank, CS));
-      cla_mbar_arm(&vbar[jj], 8u * (uint32_t)(s - jj - 1));
+      cla_mbar_arm(&vbar[jj], 8u * (uint32_t)(sr - (jj & ~1)));
       cla_mbar_arm(&pbar[jj], 8u * (uint32_t)(s - jj - 1 + CS));
     }
   }
@@ -823,9 +815,9 @@ __global__ void __launch_bounds__(256, 1) tridiag_reg_kernel(int s, const double
     const uint32_t ph = (uint32_t)(j >> 1) & 1u;
     const bool pend = j > 0;
     const bool rearm = tid == 0 && j + 4 < s;  // step j + 2 exists
-    double* vj = vloc + (size_t)par * s;
-    const double* vp = vloc + (size_t)pp * s;
-    const double* pq = ploc + (size_t)pp * s;
+    double* vj = vloc + (size_t)par * sr;
+    const double* vp = vloc + (size_t)pp * sr;
+    const double* pq = ploc + (size_t)pp * sr;
     // ---- U: the pending update of step j-1 (rows >= j), column j first on its owner
     double rv[KR], rp[KR], ag[CR], bg[CR];
 #pragma unroll
@@ -904,20 +896,20 @@ __global__ void __launch_bounds__(256, 1) tridiag_reg_kernel(int s, const double
         el[lj] = beta;
         tl[lj] = tj;
       }
-      // v_j pushed holder-major: thread t serves holder t / TPD, rows i0 + CS (t % TPD + TPD q)
-      const int hh = tid >> ltpd, mm = tid & (TPD - 1);
-      const int i0 = j + ((hh - j) & (CS - 1));
-      const uint32_t vb0 = cla_smem_u32(vj), hb0 = cla_smem_u32(&hbar[par]);
-      if (mm == 0) cla_st_async(cla_mapa(vb0 + 8u * (uint32_t)j, (uint32_t)hh), tj, cla_mapa(hb0, (uint32_t)hh));
-      double* vout = refl + (size_t)lj * s;
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const int i = i0 + CS * (mm + TPD * q);
-        if (i > j && i < s) {
-          const double v = (i == j + 1) ? 1.0 : colb[i] * scale;
-          cla_st_async(cla_mapa(vb0 + 8u * (uint32_t)i, (uint32_t)hh), v, cla_mapa(hb0, (uint32_t)hh));
-          vout[i] = v;
-        }
+      // v_j (rows > j) into the reflector store with tau_j at row j, then one bulk copy per CTA of
+      // rows [j & ~1, sr) (row j - 1, when copied, is dead at the receivers) completing on its vbar
+      double* vout = refl + (size_t)lj * sr;
+      for (int i = j + 1 + tid; i < s; i += NT) vout[i] = (i == j + 1) ? 1.0 : colb[i] * scale;
+      if (tid == 0) vout[j] = tj;
+      __syncthreads();
+      if (tid < CS) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        const int i0 = j & ~1;
+        asm volatile(
+            "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                cla_mapa(cla_smem_u32(vj + i0), (uint32_t)tid)),
+            "r"(cla_smem_u32(vout + i0)), "r"(8u * (uint32_t)(sr - i0)), "r"(cla_mapa(cla_smem_u32(&vbar[par]), (uint32_t)tid))
+            : "memory");
       }
       if (prof && tid == 0) pt[7] += 1;
     }
@@ -931,23 +923,9 @@ __global__ void __launch_bounds__(256, 1) tridiag_reg_kernel(int s, const double
       }
     }
     TRI_T(5);
-    cla_mbar_wait(&hbar[par], ph);  // tau_j and the held rows of v_j
-    if (rearm) cla_mbar_arm(&hbar[par], tri_tx_h(j + 2, s, (int)rank, CS));
+    cla_mbar_wait(&vbar[par], ph);  // tau_j and all rows of v_j
+    if (rearm) cla_mbar_arm(&vbar[par], 8u * (uint32_t)(sr - ((j + 2) & ~1)));
     TRI_T(1);
-    {
-      // the held rows (i = f + CS m) to every CTA: thread t serves destination t / TPD, rows
-      // m = t % TPD + TPD q
-      const int f = tri_held_first(j, (int)rank, CS);
-      const uint32_t v0 = cla_smem_u32(vj), b0 = cla_smem_u32(&vbar[par]);
-      const int dst = tid >> ltpd, mm = tid & (TPD - 1);
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const int i = f + CS * (mm + TPD * q);
-        if (i < s) cla_st_async(cla_mapa(v0 + 8u * (uint32_t)i, (uint32_t)dst), vj[i], cla_mapa(b0, (uint32_t)dst));
-      }
-    }
-    cla_mbar_wait(&vbar[par], ph);  // all rows of v_j
-    if (rearm) cla_mbar_arm(&vbar[par], 8u * (uint32_t)(s - j - 3));
     TRI_T(2);
     // ---- D: column sums of A[:, g] v_j (rows > j) for the own columns
     const double tj = vj[j];
@@ -987,7 +965,7 @@ __global__ void __launch_bounds__(256, 1) tridiag_reg_kernel(int s, const double
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
       const uint32_t b0 = cla_smem_u32(&pbar[par]);
-      const uint32_t p0 = cla_smem_u32(ploc + (size_t)par * s + g);
+      const uint32_t p0 = cla_smem_u32(ploc + (size_t)par * sr + g);
       const uint32_t w0 = cla_smem_u32(wpart + par * 32 + rank);
       for (int dst = warp; dst < CS; dst += 8) {
         if (act) cla_st_async(cla_mapa(p0, (uint32_t)dst), pg, cla_mapa(b0, (uint32_t)dst));
@@ -1016,8 +994,8 @@ __global__ void __launch_bounds__(256, 1) tridiag_reg_kernel(int s, const double
   // the last pending update (step s-3) on the trailing 2 x 2, then d, e of the last two columns
   if (s >= 3) {
     const int pl = (s - 3) & 1;
-    const double* vp = vloc + (size_t)pl * s;
-    const double* pq = ploc + (size_t)pl * s;
+    const double* vp = vloc + (size_t)pl * sr;
+    const double* pq = ploc + (size_t)pl * sr;
 #pragma unroll
     for (int c = 0; c < CR; ++c) {
       const int g = (int)rank + CS * (cg + TCG * c);
@@ -1040,7 +1018,7 @@ __global__ void __launch_bounds__(256, 1) tridiag_reg_kernel(int s, const double
   __syncthreads();
   for (int q = tid; q < ncl * s; q += NT) {
     int lc = q / s, i = q - lc * s, g = (int)rank + CS * lc;
-    if (g + 2 < s && i > g) Vh[IDX(i, g, ldv)] = refl[q];
+    if (g + 2 < s && i > g) Vh[IDX(i, g, ldv)] = refl[(size_t)lc * sr + i];
   }
   for (int lc = tid; lc < ncl; lc += NT) {
     int g = (int)rank + CS * lc;
@@ -1238,17 +1216,23 @@ __global__ void __launch_bounds__(256) larft_kernel(int s, const double* __restr
   }
 }
 
-template <int PL>
-__global__ void __launch_bounds__(256) backtransform_wy_kernel(int s, int m, const double* __restrict__ Vh, int ldv,
-                                                               const double* __restrict__ Tb,
-                                                               double* __restrict__ y, int ldy) {
+// CPB warps per CTA, one column each (CPB = 4: m = 130 columns -> 33 CTAs instead of 17 with 8):
+// per panel the 16 dot products of a column are reduced across the warp by one transposed
+// shuffle reduction (tri_xreduce) instead of 16 x 32 sequential shared-memory sums.
+__host__ __device__ inline size_t bt_wy_smem_doubles(int PL, int CPB) {
+  return (size_t)2 * WY_PB * 32 * PL + 2 * WY_PB * WY_PB + (size_t)CPB * 2 * WY_PB;
+}
+template <int PL, int CPB>
+__global__ void __launch_bounds__(32 * CPB) backtransform_wy_kernel(int s, int m, const double* __restrict__ Vh, int ldv,
+                                                                    const double* __restrict__ Tb,
+                                                                    double* __restrict__ y, int ldy) {
   // two panel buffers (WY_PB x 32 PL each, rows >= s zero) + T, streamed with cp.async
   extern __shared__ __align__(16) double pv[];
   const int LDP = 32 * PL;
   double* Ts = pv + (size_t)2 * WY_PB * LDP;  // 2 x WY_PB x WY_PB
-  double* wsm = Ts + 2 * WY_PB * WY_PB;       // per warp: 32 WY_PB partials + w + z
-  const int lane = threadIdx.x & 31;
-  const int col = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  double* wsm = Ts + 2 * WY_PB * WY_PB;       // per warp: w (WY_PB), z (WY_PB)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int col = blockIdx.x * CPB + warp;
   const bool active = col < m;
   double* yc = y + (size_t)(active ? col : 0) * ldy;
   double r[PL];
@@ -1262,16 +1246,25 @@ __global__ void __launch_bounds__(256) backtransform_wy_kernel(int s, int m, con
   auto issue = [&](int pnl, int buf) {
     const int lo = pnl * WY_PB, kb = min(WY_PB, nref - lo);
     double* dst = pv + (size_t)buf * WY_PB * LDP;
-    for (int e = threadIdx.x; e < WY_PB * LDP; e += blockDim.x) {
-      const int c = e / LDP, i = e - c * LDP, j = lo + c;
-      const bool ok = c < kb && i > j && i < s;
-      cp_async_8(dst + e, ok ? Vh + IDX(i, j, ldv) : Vh, ok ? 8 : 0);
+    // row pairs: one 16-byte copy (or zero fill) when both rows agree and the source is aligned
+    for (int e = threadIdx.x; e < WY_PB * (LDP / 2); e += blockDim.x) {
+      const int c = e / (LDP / 2), i = 2 * (e - c * (LDP / 2)), j = lo + c;
+      const bool ok0 = c < kb && i > j && i < s, ok1 = c < kb && i + 1 > j && i + 1 < s;
+      const double* src = Vh + IDX(i, (c < kb ? j : 0), ldv);
+      double* d0 = dst + (size_t)c * LDP + i;
+      if (ok0 == ok1 && (!ok0 || ((reinterpret_cast<uintptr_t>(src) & 15) == 0))) {
+        cp_async_16(d0, ok0 ? src : Vh, ok0 ? 16 : 0);
+      } else {
+        cp_async_8(d0, ok0 ? src : Vh, ok0 ? 8 : 0);
+        cp_async_8(d0 + 1, ok1 ? src + 1 : Vh, ok1 ? 8 : 0);
+      }
     }
     for (int e = threadIdx.x; e < WY_PB * WY_PB; e += blockDim.x)
       cp_async_8(Ts + (size_t)buf * WY_PB * WY_PB + e, Tb + (size_t)pnl * WY_PB * WY_PB + e, 8);
     cp_async_commit();
   };
   if (npan > 0) issue(npan - 1, (npan - 1) & 1);
+  double* wz = wsm + (size_t)warp * 2 * WY_PB;
   for (int pnl = npan - 1; pnl >= 0; --pnl) {
     const int buf = pnl & 1;
     if (pnl > 0) {
@@ -1284,38 +1277,28 @@ __global__ void __launch_bounds__(256) backtransform_wy_kernel(int s, int m, con
     if (active) {
       const double* V = pv + (size_t)buf * WY_PB * LDP;
       const double* T = Ts + (size_t)buf * WY_PB * WY_PB;
-      double* wp = wsm + (size_t)(threadIdx.x >> 5) * (32 * (WY_PB + 1) + 2 * WY_PB);  // [lane][c] partials (ld 17), w, z
-      // lane partials of w_c = v_c . y (c loop kept rolled: bounded registers)
-#pragma unroll 1
-      for (int c = 0; c < WY_PB; ++c) {
-        double a0 = 0.0, a1 = 0.0;
+      // lane partials of w_c = v_c . y for all c (16 independent chains), then one transposed
+      // reduction: lane l ends with w_{c(l)} (lanes l, l ^ 1 agree)
+      double a[WY_PB];
 #pragma unroll
-        for (int q = 0; q < PL; ++q) {
-          const double vv = V[(size_t)c * LDP + lane + 32 * q];
-          if (q & 1)
-            a1 = fma(vv, r[q], a1);
-          else
-            a0 = fma(vv, r[q], a0);
-        }
-        wp[lane * (WY_PB + 1) + c] = a0 + a1;
+      for (int c = 0; c < WY_PB; ++c) a[c] = 0.0;
+#pragma unroll
+      for (int q = 0; q < PL; ++q) {
+#pragma unroll
+        for (int c = 0; c < WY_PB; ++c) a[c] = fma(V[(size_t)c * LDP + lane + 32 * q], r[q], a[c]);
       }
-      __syncwarp();
-      if (lane < WY_PB) {  // w_c = sum over lanes (fixed order)
-        double acc = 0.0;
-#pragma unroll 8
-        for (int l = 0; l < 32; ++l) acc += wp[l * (WY_PB + 1) + lane];
-        wp[32 * (WY_PB + 1) + lane] = acc;
-      }
+      const double wl = tri_xreduce<WY_PB>(a, lane);
+      if ((lane & 1) == 0) wz[tri_xreduce_col<WY_PB>(lane)] = wl;
       __syncwarp();
       if (lane < WY_PB) {  // z = T w (T upper triangular, column-major)
         double acc = 0.0;
-        for (int bcol = lane; bcol < WY_PB; ++bcol) acc = fma(T[lane + bcol * WY_PB], wp[32 * (WY_PB + 1) + bcol], acc);
-        wp[32 * (WY_PB + 1) + WY_PB + lane] = acc;
+        for (int bcol = lane; bcol < WY_PB; ++bcol) acc = fma(T[lane + bcol * WY_PB], wz[bcol], acc);
+        wz[WY_PB + lane] = acc;
       }
       __syncwarp();
-#pragma unroll 1
+#pragma unroll
       for (int c = 0; c < WY_PB; ++c) {
-        const double zc = wp[32 * (WY_PB + 1) + WY_PB + c];
+        const double zc = wz[WY_PB + c];
 #pragma unroll
         for (int q = 0; q < PL; ++q) r[q] = fma(-V[(size_t)c * LDP + lane + 32 * q], zc, r[q]);
       }

@@ -363,9 +363,9 @@ static int cla_attrs() {
   CK(cudaFuncSetAttribute(trinv_panel_kernel<24>, cudaFuncAttributeMaxDynamicSharedMemorySize, tmx));
   CK(cudaFuncSetAttribute(trinv_panel_kernel<40>, cudaFuncAttributeMaxDynamicSharedMemorySize, tmx));
   const int bmx = CLA_SMEM_BYTES;
-  CK(cudaFuncSetAttribute(backtransform_wy_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, bmx));
-  CK(cudaFuncSetAttribute(backtransform_wy_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, bmx));
-  CK(cudaFuncSetAttribute(backtransform_wy_kernel<20>, cudaFuncAttributeMaxDynamicSharedMemorySize, bmx));
+  CK(cudaFuncSetAttribute(backtransform_wy_kernel<8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, bmx));
+  CK(cudaFuncSetAttribute(backtransform_wy_kernel<16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, bmx));
+  CK(cudaFuncSetAttribute(backtransform_wy_kernel<20, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, bmx));
   CK(cudaFuncSetAttribute(backtransform_panel_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, bmx));
   CK(cudaFuncSetAttribute(backtransform_panel_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, bmx));
   CK(cudaFuncSetAttribute(backtransform_panel_kernel<24>, cudaFuncAttributeMaxDynamicSharedMemorySize, bmx));
@@ -613,18 +613,41 @@ static int eigh_top(cudaStream_t st, int s, const double* Hs, int ldh, int m, do
     fprintf(stderr, "eigh s=%d m=%d mgs=%d tcs=%d sync=%s d0=%g\n", s, m, (int)mgs, tcs, cudaGetErrorString(e0), hb[0]);
   }
   TRY(w.mark(8));
+  static int bt_mode = -1;  // 0: compact-WY (default for s <= 640), 1: reflector-by-reflector panels
+  if (bt_mode < 0) bt_mode = getenv("PSDPROJ_BT_SIMPLE") ? 1 : 0;
+  const bool wy = s > 2 && bt_mode == 0 && s <= 32 * 20 && m > 0;
+  cudaEvent_t tri_side_join = nullptr;
+  if (wy) {
+    static thread_local cudaStream_t side = nullptr;
+    static thread_local cudaEvent_t ev_f = nullptr, ev_j = nullptr;
+    if (!side) {
+      CK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&ev_f, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&ev_j, cudaEventDisableTiming));
+    }
+    // the T factors of the compact-WY back-transformation need only the reflectors: computed on a
+    // side stream, hidden behind the bisection and inverse iteration (thread_local: batched calls
+    // come from several host threads)
+    CK(cudaEventRecord(ev_f, st));
+    CK(cudaStreamWaitEvent(side, ev_f, 0));
+    larft_kernel<<<cdiv(s - 2, WY_PB), 256, 0, side>>>(s, w.Vh, w.ldv, w.ttau, w.tG);
+    CKL();
+    CK(cudaEventRecord(ev_j, side));
+    tri_side_join = ev_j;
+  }
   tri_prep_kernel<<<1, 1024, 0, st>>>(s, w.td, w.te, w.te2, w.tbounds);
   CKL();
   tri_bisect_kernel<<<cdiv(m + 1, 2), 64, (size_t)2 * s * sizeof(double), st>>>(s, m, w.td, w.te2, w.tbounds, lam, npos);
   CKL();
-  if (m <= 0) return 0;
+  if (m <= 0) return 0;  // (wy is false for m <= 0: no side-stream work in flight)
   TRY(w.mark(9));
-  // inverse iteration: vectors per CTA so that 6 s doubles each fit in shared memory
-  int vpb = (int)std::min<size_t>(64, (220 * 1024) / ((size_t)6 * s * sizeof(double)));
-  int smem_ok = vpb >= 1;
+  // inverse iteration: vectors per CTA so that the per-thread arrays fit in shared memory
+  int vpb = 64;
+  while (vpb > 1 && tri_inviter_smem_bytes(s, vpb) > (size_t)220 * 1024) --vpb;
+  int smem_ok = tri_inviter_smem_bytes(s, vpb) <= (size_t)220 * 1024;
   if (!smem_ok) vpb = 64;
   if (!smem_ok && (size_t)6 * s * (size_t)m > w.tscr_elems) return set_err(PSDPROJ_E_CAPACITY, "eigensolver scratch");
-  size_t ism = smem_ok ? (size_t)6 * s * vpb * sizeof(double) : 0;
+  size_t ism = smem_ok ? tri_inviter_smem_bytes(s, vpb) : (size_t)2 * s * sizeof(double);
   if (mgs) {
     for (int pass = 0; pass < 2; ++pass) {
       tri_inviter_kernel<<<cdiv(m, vpb), vpb, ism, st>>>(s, m, w.td, w.te, lam, w.tbounds, Yv, ldy, w.tscr,
@@ -640,16 +663,12 @@ static int eigh_top(cudaStream_t st, int s, const double* Hs, int ldh, int m, do
   }
   TRY(w.mark(10));
   if (s > 2) {
-    static int bt_mode = -1;  // 0: compact-WY (default for s <= 768), 1: reflector-by-reflector panels
-    if (bt_mode < 0) bt_mode = getenv("PSDPROJ_BT_SIMPLE") ? 1 : 0;
-    const int npan = cdiv(s - 2, WY_PB);
-    if (bt_mode == 0 && s <= 32 * 20) {
-      double* Tb = w.tG;  // free after the tridiagonalisation
-      larft_kernel<<<npan, 256, 0, st>>>(s, w.Vh, w.ldv, w.ttau, Tb);
-      CKL();
-#define BT_WY(PL)                                                                                              \
-  backtransform_wy_kernel<PL><<<cdiv(m, 8), 256, ((size_t)2 * WY_PB * 32 * PL + 2 * WY_PB * WY_PB + 8 * (32 * (WY_PB + 1) + 2 * WY_PB)) * sizeof(double), \
-                                st>>>(s, m, w.Vh, w.ldv, Tb, Yv, ldy)
+    if (wy) {
+      double* Tb = w.tG;  // T factors from larft_kernel (side stream, launched after the tridiagonalisation)
+      CK(cudaStreamWaitEvent(st, tri_side_join, 0));
+#define BT_WY(PL)                                                                                          \
+  backtransform_wy_kernel<PL, 4><<<cdiv(m, 4), 128, bt_wy_smem_doubles(PL, 4) * sizeof(double), st>>>( \
+      s, m, w.Vh, w.ldv, Tb, Yv, ldy)
       if (s <= 32 * 8)
         BT_WY(8);
       else if (s <= 32 * 16)

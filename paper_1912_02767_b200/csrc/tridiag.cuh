@@ -170,21 +170,6 @@ __device__ __forceinline__ double fast_rcp(double x) {
   return fma(r, e, r);
 }
 
-// Sturm count: number of eigenvalues of T (d, e2 = e^2) strictly below x (GvL §8.4.1).
-__device__ __forceinline__ int sturm_count(int s, const double* __restrict__ d, const double* __restrict__ e2,
-                                           double x, double pivmin) {
-  int cnt = 0;
-  double q = d[0] - x;
-  if (fabs(q) < pivmin) q = -pivmin;
-  cnt += q < 0.0;
-  for (int i = 1; i < s; ++i) {
-    q = (d[i] - x) - e2[i - 1] * fast_rcp(q);
-    if (fabs(q) < pivmin) q = -pivmin;
-    cnt += q < 0.0;
-  }
-  return cnt;
-}
-
 // e2[i] = e[i]^2, bounds[0..1] = Gershgorin interval, bounds[2] = pivmin (one CTA)
 __global__ void tri_prep_kernel(int s, const double* __restrict__ d, const double* __restrict__ e,
                                 double* __restrict__ e2, double* __restrict__ bounds) {
@@ -219,30 +204,66 @@ __global__ void tri_prep_kernel(int s, const double* __restrict__ d, const doubl
   }
 }
 
-// One warp per wanted eigenvalue: ks-th largest, ks = blockIdx.x * warps + warp (ks < m),
-// 32-way multisection. out[ks] = eigenvalue (descending). Warp id == m computes npos =
-// #eigenvalues > 0 (s - count(0)).
+// Sturm count by the leading principal minors of T - x I (three-term recurrence
+// P_i = (d_i - x) P_{i-1} - e_{i-1}^2 P_{i-2}, GvL §8.4.1): the number of eigenvalues below x is the
+// number of sign changes in P_0 = 1, P_1, ..., P_s. Unlike the ratio form q_i = P_i / P_{i-1} it has
+// no division on the dependency chain (one FMA per step: e^2 P_{i-2} is formed a step early).
+// T is pre-scaled by a power of two to O(1) entries and the pair (P_i, P_{i-1}) is rescaled by a
+// power of two every 8 steps (exact), so the minors neither overflow nor underflow. An exact zero
+// minor is replaced by -2^-60 P_{i-1} (the ratio form's q_i = -pivmin).
+__device__ __forceinline__ int sturm_count_det(int s, const double* __restrict__ d, const double* __restrict__ e2,
+                                               double x) {
+  double pm = 1.0, p = d[0] - x;
+  if (p == 0.0) p = -0x1p-60;
+  int cnt = p < 0.0;
+  for (int i = 1; i < s; ++i) {
+    const double t = e2[i - 1] * pm;  // off the chain
+    double pn = fma(d[i] - x, p, -t);
+    if (pn == 0.0) pn = -0x1p-60 * p;
+    cnt += (pn < 0.0) != (p < 0.0);
+    pm = p;
+    p = pn;
+    if ((i & 7) == 0) {
+      const double mx = fmax(fabs(p), fabs(pm));
+      const int ex = (int)((__double_as_longlong(mx) >> 52) & 0x7ff);
+      if (ex > 0 && ex < 2047) {
+        const double sc = __longlong_as_double((long long)(2046 - ex) << 52);  // 2^(1023 - (ex - 1023))
+        p *= sc;
+        pm *= sc;
+      }
+    }
+  }
+  return cnt;
+}
+
+// Multisection bisection (dstebz-like). One warp per wanted eigenvalue: ks-th largest,
+// ks = blockIdx.x * warps + warp (ks < m), 32-way multisection. out[ks] = eigenvalue (descending).
+// Warp id == m computes npos = #eigenvalues > 0 (s - count(0)).
 __global__ void tri_bisect_kernel(int s, int m, const double* __restrict__ dg, const double* __restrict__ e2g,
                                   const double* __restrict__ bounds, double* __restrict__ out,
                                   int* __restrict__ npos) {
   extern __shared__ __align__(16) double bsm[];
   double* d = bsm;
   double* e2 = bsm + s;
+  // power-of-two scale to O(1): 1 / 2^ceil(log2 max(|lo|, |hi|))
+  const double span = fmax(fmax(fabs(bounds[0]), fabs(bounds[1])), 1e-300);
+  const int sex = (int)((__double_as_longlong(span) >> 52) & 0x7ff) - 1022;  // span < 2^sex
+  const double inv = ldexp(1.0, -sex), inv2 = inv * inv;
   for (int k = threadIdx.x; k < s; k += blockDim.x) {
-    d[k] = dg[k];
-    if (k + 1 < s) e2[k] = e2g[k];
+    d[k] = dg[k] * inv;
+    if (k + 1 < s) e2[k] = e2g[k] * inv2;
   }
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int ks = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (ks > m) return;
-  const double pivmin = bounds[2];
   if (ks == m) {
-    if (lane == 0) *npos = s - sturm_count(s, d, e2, 0.0, pivmin);
+    if (lane == 0) *npos = s - sturm_count_det(s, d, e2, 0.0);
     return;
   }
   const int k = s - 1 - ks;  // ascending index: count(lo) <= k < count(hi)
   double lo = bounds[0], hi = bounds[1];
+  const double pivmin = bounds[2];
   // absolute accuracy u ||T|| suffices: the Rayleigh-Ritz values enter absolute residual tests, and
   // bisection to a relative tolerance near zero would add rounds for no gain (dstebz's ABSTOL)
   const double atol = 4.0 * PSD_U * fmax(fabs(lo), fabs(hi));
@@ -250,7 +271,7 @@ __global__ void tri_bisect_kernel(int s, int m, const double* __restrict__ dg, c
     double w = hi - lo;
     if (w <= fmax(2.0 * PSD_U * fmax(fabs(lo), fabs(hi)), atol) + 4.0 * pivmin) break;
     double x = lo + w * (double)(lane + 1) / 33.0;
-    int c = sturm_count(s, d, e2, x, pivmin);
+    int c = sturm_count_det(s, d, e2, x * inv);
     unsigned below = __ballot_sync(0xffffffffu, c <= k);  // x still at or below the target
     // the first lane with count > k bounds the target from above
     int first_above = __ffs(~below) - 1;  // -1 if all lanes are below
@@ -271,78 +292,89 @@ __global__ void tri_bisect_kernel(int s, int m, const double* __restrict__ dg, c
 // Inverse iteration (GvL §8.4.2): one thread per eigenvector i < m (eigenvalue lam[i]):
 // LU with partial pivoting of T - lam I (LAPACK dgttrf), `iters` solves (dgttrs), each
 // normalised. y (s x m, ldy) holds the start vectors when `use_start`, else a fixed
-// pseudo-random start. scratch: 5 s doubles per vector.
-// Per-vector arrays live in shared memory when they fit (smem_ok), else in `scratch`.
+// pseudo-random start. The recurrences are sequential in k, so the kernel is latency-bound per
+// vector: d, e are staged once per CTA in shared memory (broadcast reads), the factorisation
+// carries the running pivot and super-diagonal in registers (one reciprocal per step on the
+// dependency chain), the random start is drawn inside the factorisation sweep, and the stored
+// pivots are reciprocals (the solves multiply).
+// Shared memory: 2 s doubles (d, e) + per thread 5 s doubles (1/pivot, L, U, U2, y) + s bytes
+// (interchanges), interleaved [k * blockDim + t] (conflict-free). smem_ok = 0: the per-thread
+// arrays live in `scratch` (5 s doubles + s bytes per vector) instead.
+__host__ __device__ inline size_t tri_inviter_smem_bytes(int s, int vpb) {
+  return (size_t)2 * s * sizeof(double) + (size_t)vpb * s * (5 * sizeof(double) + 1);
+}
 __global__ void tri_inviter_kernel(int s, int m, const double* __restrict__ d, const double* __restrict__ e,
                                    const double* __restrict__ lam, const double* __restrict__ bounds,
                                    double* __restrict__ y, int ldy, double* __restrict__ scratch, int iters,
                                    int use_start, int smem_ok) {
   extern __shared__ __align__(16) double ism[];
+  double* sd = ism;
+  double* se = ism + s;
+  for (int k = threadIdx.x; k < s; k += blockDim.x) {
+    sd[k] = d[k];
+    se[k] = (k + 1 < s) ? e[k] : 0.0;
+  }
+  __syncthreads();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= m) return;
-  // interleaved layout in smem: element k of thread t at [k * blockDim + t] (conflict-free)
   const int stride = smem_ok ? blockDim.x : 1;
-  double* base = smem_ok ? ism + threadIdx.x : scratch + (size_t)i * 6 * s;
-  double* dd = base;
-  double* du = base + (size_t)s * stride;
-  double* du2 = base + (size_t)2 * s * stride;
-  double* dl = base + (size_t)3 * s * stride;
-  double* pv = base + (size_t)4 * s * stride;  // pivots stored as doubles (0/1)
-  double* yy = base + (size_t)5 * s * stride;  // working vector
-  double* yi = y + (size_t)i * ldy;
-#define DD(k) dd[(size_t)(k) * stride]
+  double* base = smem_ok ? ism + 2 * (size_t)s + threadIdx.x : scratch + (size_t)i * 6 * s;
+  double* rd = base;                           // 1 / pivot
+  double* dl = base + (size_t)s * stride;      // L multipliers
+  double* du = base + (size_t)2 * s * stride;  // U super-diagonal
+  double* du2 = base + (size_t)3 * s * stride; // U second super-diagonal (interchanges)
+  double* yy = base + (size_t)4 * s * stride;  // working vector
+  unsigned char* pv = smem_ok ? reinterpret_cast<unsigned char*>(ism + 2 * (size_t)s + (size_t)5 * s * blockDim.x) + threadIdx.x
+                              : reinterpret_cast<unsigned char*>(scratch + (size_t)i * 6 * s + (size_t)5 * s);
+#define RD(k) rd[(size_t)(k) * stride]
+#define DL(k) dl[(size_t)(k) * stride]
 #define DU(k) du[(size_t)(k) * stride]
 #define DU2(k) du2[(size_t)(k) * stride]
-#define DL(k) dl[(size_t)(k) * stride]
-#define PV(k) pv[(size_t)(k) * stride]
 #define YY(k) yy[(size_t)(k) * stride]
+#define PV(k) pv[(size_t)(k) * stride]
+  double* yi = y + (size_t)i * ldy;
   const double span = fmax(fabs(bounds[0]), fabs(bounds[1]));
   const double eps_piv = PSD_U * span + 1e-300;
   const double lm = lam[i];
-  for (int k = 0; k < s; ++k) {
-    DD(k) = d[k] - lm;
-    if (k + 1 < s) { DU(k) = e[k]; DL(k) = e[k]; }
-    DU2(k) = 0.0;
-  }
-  for (int k = 0; k + 1 < s; ++k) {  // dgttrf
-    double dk = DD(k), lk = DL(k);
+  auto guarded_rcp = [&](double p, double r) {  // 1 / max(|p|, eps) with the sign of p (r = 1/p)
+    return (fabs(p) < eps_piv) ? ((p < 0.0) ? -1.0 / eps_piv : 1.0 / eps_piv) : r;
+  };
+  // dgttrf with the running pivot dk and super-diagonal uk in registers
+  uint32_t h = 0x9E3779B9u * (uint32_t)(i + 1) + 0x7F4A7C15u;
+  double dk = sd[0] - lm, uk = se[0];
+  for (int k = 0; k + 1 < s; ++k) {
+    const double lk = se[k], d1 = sd[k + 1] - lm, e1 = se[k + 1];  // se[s-1] = 0
     if (fabs(dk) >= fabs(lk)) {
       if (dk == 0.0) dk = eps_piv;
-      double fact = lk * fast_rcp(dk);
-      DD(k) = dk;
-      DL(k) = fact;
-      DD(k + 1) -= fact * DU(k);
+      const double r = fast_rcp(dk);
+      const double f = lk * r;
+      RD(k) = guarded_rcp(dk, r);
+      DL(k) = f;
+      DU(k) = uk;
       DU2(k) = 0.0;
-      PV(k) = 0.0;
+      PV(k) = 0;
+      dk = fma(-f, uk, d1);
+      uk = e1;
     } else {
-      double fact = dk * fast_rcp(lk);
-      DD(k) = lk;
-      DL(k) = fact;
-      double tmp = DU(k);
-      double dk1 = DD(k + 1);
-      DU(k) = dk1;
-      DD(k + 1) = tmp - fact * dk1;
-      if (k + 2 < s) {
-        double u1 = DU(k + 1);
-        DU2(k) = u1;
-        DU(k + 1) = -fact * u1;
-      } else {
-        DU2(k) = 0.0;
-      }
-      PV(k) = 1.0;
+      const double r = fast_rcp(lk);
+      const double f = dk * r;
+      RD(k) = guarded_rcp(lk, r);
+      DL(k) = f;
+      DU(k) = d1;
+      DU2(k) = e1;
+      PV(k) = 1;
+      dk = fma(-f, d1, uk);
+      uk = -f * e1;
     }
-  }
-  for (int k = 0; k < s; ++k) {  // DD <- 1 / pivot (the solves multiply)
-    double p = DD(k);
-    if (fabs(p) < eps_piv) p = (p < 0.0) ? -eps_piv : eps_piv;
-    DD(k) = fast_rcp(p);
-  }
-  if (!use_start) {
-    uint32_t h = 0x9E3779B9u * (uint32_t)(i + 1) + 0x7F4A7C15u;
-    for (int k = 0; k < s; ++k) {
+    if (!use_start) {
       h ^= h << 13; h ^= h >> 17; h ^= h << 5;
       YY(k) = 0.5 + (double)(h & 0xffffff) / 16777216.0;
     }
+  }
+  RD(s - 1) = guarded_rcp(dk, fast_rcp(dk == 0.0 ? eps_piv : dk));
+  if (!use_start) {
+    h ^= h << 13; h ^= h >> 17; h ^= h << 5;
+    YY(s - 1) = 0.5 + (double)(h & 0xffffff) / 16777216.0;
   } else {
     for (int k = 0; k < s; ++k) YY(k) = yi[k];
   }
@@ -354,12 +386,13 @@ __global__ void tri_inviter_kernel(int s, int m, const double* __restrict__ d, c
     double y0 = YY(0) * sc;
     for (int k = 0; k + 1 < s; ++k) {  // dgttrs forward (L with interchanges)
       const double y1 = YY(k + 1) * sc;
-      if (PV(k) == 0.0) {
+      const double lk = DL(k);
+      if (PV(k) == 0) {
         YY(k) = y0;
-        y0 = y1 - DL(k) * y0;
+        y0 = fma(-lk, y0, y1);
       } else {
         YY(k) = y1;
-        y0 = y0 - DL(k) * y1;
+        y0 = fma(-lk, y1, y0);
       }
     }
     YY(s - 1) = y0;
@@ -367,9 +400,9 @@ __global__ void tri_inviter_kernel(int s, int m, const double* __restrict__ d, c
     double b1 = 0.0, b2 = 0.0;  // YY(k + 1), YY(k + 2) of the back substitution
     for (int k = s - 1; k >= 0; --k) {  // back substitution with U
       double v = YY(k);
-      if (k + 1 < s) v -= DU(k) * b1;
-      if (k + 2 < s) v -= DU2(k) * b2;
-      v *= DD(k);
+      if (k + 1 < s) v = fma(-DU(k), b1, v);
+      if (k + 2 < s) v = fma(-DU2(k), b2, v);
+      v *= RD(k);
       YY(k) = v;
       b2 = b1;
       b1 = v;
@@ -382,7 +415,7 @@ __global__ void tri_inviter_kernel(int s, int m, const double* __restrict__ d, c
   }
   double inv = (n2 > 0.0) ? rsqrt(n2) : 0.0;
   for (int k = 0; k < s; ++k) yi[k] = YY(k) * inv;
-#undef DD
+#undef RD
 #undef DU
 #undef DU2
 #undef DL
