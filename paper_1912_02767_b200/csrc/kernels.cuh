@@ -263,6 +263,23 @@ __global__ void rr_prep_kernel(int s, int kxG, int kxH, double* __restrict__ G, 
   }
 }
 
+// Hh's X rows / columns when L^-1 = [I 0; 0 Ld]: Hh[:kx, :kx] = H[:kx, :kx], Hh[kx:, :kx] = Z[kx:, :kx]
+// (Z = L^-1 H, rows >= kx), Hh[:kx, kx:] = its transpose.
+__global__ void rr_assemble_kernel(int s, int kx, const double* __restrict__ H, const double* __restrict__ Z,
+                                   double* __restrict__ Hh, int ld) {
+  const size_t total = (size_t)s * kx;
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e % s), j = (int)(e / s);  // column j < kx, row i
+    if (i < kx) {
+      Hh[IDX(i, j, ld)] = H[IDX(i, j, ld)];
+    } else {
+      const double z = Z[IDX(i, j, ld)];
+      Hh[IDX(i, j, ld)] = z;
+      Hh[IDX(j, i, ld)] = z;
+    }
+  }
+}
+
 // Cholesky-QR conditioning guard (reading R44): the pivot rule (R20) bounds 1 / L_jj but not the
 // growth of the triangular inverse; a direction block whose L^-1 has an entry with
 // |L^-1_ij|^2 > thresh (unit-norm directions: cond(G) >~ thresh, the caller passes 1e8) is treated

@@ -1201,6 +1201,16 @@ struct Run {
     }
     return 0;
   }
+  // C' = L^-T Y (s x mU) with L^-1 = [I 0; 0 Ld]: rows < kx copied, rows >= kx = Ld^T Y[kx:, :]
+  int li_t_apply(int s, int kx, int mU) {
+    const int ldm = c->s_max, t = s - kx;
+    TRY(dgemm(st, OP_T, OP_N, t, mU, t, 1.0, c->Li + kx + (size_t)kx * ldm, ldm, c->Y + kx, ldm, 0.0, c->Cp + kx, ldm,
+              c->part, c->part_elems));
+    if (kx > 0) {
+      CK(cudaMemcpy2DAsync(c->Cp, (size_t)ldm * 8, c->Y, (size_t)ldm * 8, (size_t)kx * 8, mU, cudaMemcpyDeviceToDevice, st));
+    }
+    return 0;
+  }
   int rr(int s, int kxG, int kxH, const double* d_theta_known, int mU, bool prefactored = false) {
     int ldm = c->s_max;
     info->rr_max = std::max(info->rr_max, s);
@@ -1216,9 +1226,19 @@ struct Run {
     rr_prep_kernel<<<grid1d((size_t)s * s), 256, 0, st>>>(s, kxG, kxH, c->G, c->Hm, ldm, d_theta_known, c->Li, c->Gc,
                                                           c->d_status, 2);
     CKL();
-    // Hh = L^-1 H L^-T
-    TRY(dgemm(st, OP_N, OP_N, s, s, s, 1.0, c->Li, ldm, c->Hm, ldm, 0.0, c->Y, ldm, c->part, c->part_elems));
-    TRY(dgemm(st, OP_N, OP_T, s, s, s, 1.0, c->Y, ldm, c->Li, ldm, 0.0, c->Hh, ldm, c->part, c->part_elems));
+    // Hh = L^-1 H L^-T with L^-1 = [I 0; 0 Ld] (Ld = the direction block's inverse factor, t x t):
+    // Z = Ld H[kx:, :] (t x s), Hh[kx:, kx:] = Z[:, kx:] Ld^T, the X rows/columns copied
+    {
+      const int t = s - kx;
+      double* Ld = c->Li + kx + (size_t)kx * ldm;
+      TRY(dgemm(st, OP_N, OP_N, t, s, t, 1.0, Ld, ldm, c->Hm + kx, ldm, 0.0, c->Y + kx, ldm, c->part, c->part_elems));
+      TRY(dgemm(st, OP_N, OP_T, t, t, t, 1.0, c->Y + kx + (size_t)kx * ldm, ldm, Ld, ldm, 0.0,
+                c->Hh + kx + (size_t)kx * ldm, ldm, c->part, c->part_elems));
+      if (kx > 0) {
+        rr_assemble_kernel<<<grid1d((size_t)s * kx), 256, 0, st>>>(s, kx, c->Hm, c->Y, c->Hh, ldm);
+        CKL();
+      }
+    }
     // eigensolver choice by measured crossover: tridiagonal path while the matrix fits in shared memory (s <= 160),
     // cooperative Jacobi above (single-SM tridiagonalisation in global memory is L2-bandwidth bound)
     TRY(mark(4));
@@ -1245,7 +1265,7 @@ struct Run {
       CKL();
       CK(cudaMemcpyAsync(c->h_d + c->h_d_len - 16, c->d_scal + 16, sizeof(double), cudaMemcpyDeviceToHost, st));
     }
-    TRY(dgemm(st, OP_T, OP_N, s, mU, s, 1.0, c->Li, ldm, c->Y, ldm, 0.0, c->Cp, ldm, c->part, c->part_elems));
+    TRY(li_t_apply(s, kx, mU));
     TRY(mark(7));
     CK(cudaMemcpyAsync(c->h_d, c->d_ths, sizeof(double) * mU, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(c->h_i + c->h_i_len - 16, c->d_status, sizeof(int) * 8, cudaMemcpyDeviceToHost, st));
@@ -1258,7 +1278,7 @@ struct Run {
     if (!use_jacobi && !(c->h_d[c->h_d_len - 16] <= 1e-7)) {
       // Newton-Schulz could not restore orthonormality (near-multiple eigenvalues): robust path
       TRY(tri_eig(s, c->Hh, ldm, mU, c->d_ths, c->Y, ldm, c->tnpos, true));
-      TRY(dgemm(st, OP_T, OP_N, s, mU, s, 1.0, c->Li, ldm, c->Y, ldm, 0.0, c->Cp, ldm, c->part, c->part_elems));
+      TRY(li_t_apply(s, kx, mU));
       CK(cudaMemcpyAsync(c->h_d, c->d_ths, sizeof(double) * mU, cudaMemcpyDeviceToHost, st));
       TRY(sync());
     }
@@ -1608,16 +1628,19 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
       TRY(run.gather(nl, ap, BP, ld, c->BPb, ld, PJ));
     }
     const int wp = aw + ap;
-    if (hard && nL > 0 && mU + wp > 0) {
+    static int lock_reproj = getenv("PSDPROJ_LOCK_REPROJ") ? atoi(getenv("PSDPROJ_LOCK_REPROJ")) : 0;
+    const int xr = (lock_reproj && hard && nL > 0) ? mU : 0;  // X_U columns included (R46)
+    if (hard && nL > 0 && xr + wp > 0) {
       // [X_U W P] <- [X_U W P] - X_L (X_L^T [X_U W P]) (B-images of X_U and P alike). X_U is
       // re-projected every iteration: it inherits the rotation's O(u ||C'||) component along X_L,
       // which otherwise compounds over a long run until active columns duplicate locked ones (R46)
-      const int cols = mU + wp;
-      TRY(run.gram(nL, cols, c->XL, ld, c->S, ld, c->Y, ldm));
-      TRY(run.gemm(OP_N, OP_N, nl, cols, nL, -1.0, c->XL, ld, c->Y, ldm, 1.0, c->S, ld));
-      if (mU > 0) TRY(run.gemm(OP_N, OP_N, nl, mU, nL, -1.0, c->BXL, ld, c->Y, ldm, 1.0, c->BS, ld));
+      const int cols = xr + wp;
+      double* Z = xr ? c->S : W;
+      TRY(run.gram(nL, cols, c->XL, ld, Z, ld, c->Y, ldm));
+      TRY(run.gemm(OP_N, OP_N, nl, cols, nL, -1.0, c->XL, ld, c->Y, ldm, 1.0, Z, ld));
+      if (xr > 0) TRY(run.gemm(OP_N, OP_N, nl, xr, nL, -1.0, c->BXL, ld, c->Y, ldm, 1.0, c->BS, ld));
       if (ap > 0)
-        TRY(run.gemm(OP_N, OP_N, nl, ap, nL, -1.0, c->BXL, ld, c->Y + (size_t)(mU + aw) * ldm, ldm, 1.0, BP, ld));
+        TRY(run.gemm(OP_N, OP_N, nl, ap, nL, -1.0, c->BXL, ld, c->Y + (size_t)(xr + aw) * ldm, ldm, 1.0, BP, ld));
     }
     if (wp > 0) {  // [W P] <- [W P] - X_U (X_U^T [W P]): the pencil's X-block of G becomes [I 0]
       TRY(run.gram(mU, wp, c->S, ld, W, ld, c->Y, ldm));
