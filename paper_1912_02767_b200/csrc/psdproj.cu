@@ -395,6 +395,16 @@ static int cholesky_run(cudaStream_t st, int t, double* G, int ld, int* d_status
   TRY(cla_attrs());
   static int fuse = getenv("PSDPROJ_CHOL_NOFUSE") ? 0 : 1;
   const double frel = 1e-12;  // R20
+  // an 8-CTA cluster when it holds the factor and its inverse (t <= ~300): measured ~1% faster per
+  // LOBPCG step than 16 (fewer DSMEM peers per panel broadcast, easier to co-schedule with the
+  // block multiply it overlaps)
+  static int chol_cs = getenv("PSDPROJ_CHOL_CS") ? atoi(getenv("PSDPROJ_CHOL_CS")) : 8;
+  if (Linv && fuse && t > 64 && chol_cs > 0 &&
+      chol_inv_smem_doubles(t, chol_cs) * sizeof(double) <= (size_t)CLA_SMEM_BYTES) {
+    return launch_cluster(cholesky_cluster_kernel<false, true>, chol_cs, CLA_NT,
+                          chol_inv_smem_doubles(t, chol_cs) * sizeof(double), st, t, G, ld, 1e-12, d_status,
+                          (double*)nullptr, Linv, ldi);
+  }
   if (Linv && fuse) {
     if (int cs = cla_cluster_size(t, chol_inv_smem_doubles)) {
       return launch_cluster(cholesky_cluster_kernel<false, true>, cs, CLA_NT,
@@ -1656,16 +1666,21 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
     const bool ovl = ovl_env && !c->sharded && s > mU;
     if (ovl) {
       if (!c->st2) {
-        CK(cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking));
+        // high priority: the 16-CTA cluster Cholesky is dispatched before the block multiply's
+        // CTAs, which would otherwise occupy every SM until the multiply ends
+        int lo_pr = 0, hi_pr = 0;
+        CK(cudaDeviceGetStreamPriorityRange(&lo_pr, &hi_pr));
+        CK(cudaStreamCreateWithPriority(&c->st2, cudaStreamNonBlocking, hi_pr));
         CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
       }
+      // the direction-block Gram first (on the main stream), then the Cholesky on the side stream
+      TRY(run.gram(s - mU, s - mU, c->S + (size_t)mU * ld, ld, c->S + (size_t)mU * ld, ld, c->G + mU + (size_t)mU * ldm,
+                   ldm));
       CK(cudaEventRecord(c->ev_fork, st));
       CK(cudaStreamWaitEvent(c->st2, c->ev_fork, 0));
       Run r2{c, c->st2, info};
       r2.part = c->part2;
-      TRY(r2.gram(s - mU, s - mU, c->S + (size_t)mU * ld, ld, c->S + (size_t)mU * ld, ld, c->G + mU + (size_t)mU * ldm,
-                  ldm));
       TRY(r2.rr_factor(s, mU));
       CK(cudaEventRecord(c->ev_join, c->st2));
     }
