@@ -474,6 +474,7 @@ static int eigh_top(cudaStream_t st, int s, const double* Hs, int ldh, int m, do
     CK(cudaFuncSetAttribute(tridiag_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)((size_t)(TRI_SMEM_MAX * (TRI_SMEM_MAX + 1) + 10 * TRI_SMEM_MAX) * sizeof(double))));
     CK(cudaFuncSetAttribute(tri_inviter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    CK(cudaFuncSetAttribute(tri_twisted_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     CK(cudaFuncSetAttribute(tri_bisect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     attr = true;
   }
@@ -667,8 +668,13 @@ static int eigh_top(cudaStream_t st, int s, const double* Hs, int ldh, int m, do
       CKL();
     }
   } else {
-    tri_inviter_kernel<<<cdiv(m, vpb), vpb, ism, st>>>(s, m, w.td, w.te, lam, w.tbounds, Yv, ldy, w.tscr, 2, 0,
-                                                       smem_ok);
+    static int twisted = getenv("PSDPROJ_INVITER") ? 0 : 1;
+    if (twisted && (size_t)(7 * s + 2) * sizeof(double) <= (size_t)220 * 1024) {
+      tri_twisted_kernel<<<m, 32, (size_t)(7 * s + 2) * sizeof(double), st>>>(s, m, w.td, w.te, lam, Yv, ldy);
+    } else {
+      tri_inviter_kernel<<<cdiv(m, vpb), vpb, ism, st>>>(s, m, w.td, w.te, lam, w.tbounds, Yv, ldy, w.tscr, 2, 0,
+                                                         smem_ok);
+    }
     CKL();
   }
   TRY(w.mark(10));

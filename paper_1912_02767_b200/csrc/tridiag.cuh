@@ -248,10 +248,10 @@ __global__ void tri_bisect_kernel(int s, int m, const double* __restrict__ dg, c
   // power-of-two scale to O(1): 1 / 2^ceil(log2 max(|lo|, |hi|))
   const double span = fmax(fmax(fabs(bounds[0]), fabs(bounds[1])), 1e-300);
   const int sex = (int)((__double_as_longlong(span) >> 52) & 0x7ff) - 1022;  // span < 2^sex
-  const double inv = ldexp(1.0, -sex), inv2 = inv * inv;
+  const double inv = ldexp(1.0, -sex);  // <= 2^997: inv^2 would overflow for tiny spans
   for (int k = threadIdx.x; k < s; k += blockDim.x) {
     d[k] = dg[k] * inv;
-    if (k + 1 < s) e2[k] = e2g[k] * inv2;
+    if (k + 1 < s) e2[k] = (e2g[k] * inv) * inv;  // e^2 <= span^2: no intermediate overflow
   }
   __syncthreads();
   const int lane = threadIdx.x & 31;
@@ -421,6 +421,123 @@ __global__ void tri_inviter_kernel(int s, int m, const double* __restrict__ d, c
 #undef DL
 #undef PV
 #undef YY
+}
+
+// Eigenvectors by the twisted factorisation (Parlett & Dhillon; LAPACK dlar1v), one warp per
+// eigenvalue: T - lam I = L D+ L^T (top-down pivots D+) = U D- U^T (bottom-up pivots D-), twist
+// index r = argmin |gamma_k|, gamma_k = D+_k + D-_k - (d_k - lam), and z_r = 1,
+// z_i = -(e_i / D+_i) z_{i+1} (i < r), z_{i+1} = -(e_i / D-_{i+1}) z_i (i >= r), normalised.
+// The pivots are ratios of leading / trailing principal minors, P_i = (d_i - lam) P_{i-1} -
+// e_{i-1}^2 P_{i-2}: one FMA per step on the dependency chain (the division D_i = P_i / P_{i-1}
+// is off it), the pair (P_i, P_{i-1}) rescaled by a power of two every 8 steps; an exact zero
+// minor becomes -2^-60 P_{i-1} (dlar1v's zero-pivot replacement). Lane 0 runs the top chain,
+// lane 1 the bottom chain, in lockstep; the two z products likewise.
+// Shared memory per CTA (one warp): d, e, e^2 (staged), D+, l = e/D+, D-, u = e/D- (7 s + 2 doubles).
+__global__ void __launch_bounds__(32) tri_twisted_kernel(int s, int m, const double* __restrict__ d,
+                                                         const double* __restrict__ e,
+                                                         const double* __restrict__ lam, double* __restrict__ y,
+                                                         int ldy) {
+  extern __shared__ __align__(16) double tsm[];
+  // ec[k] = e_{k-1} (coupling of rows k-1, k; ec[0] = ec[s] = 0), e2[k] = ec[k]^2
+  double* sd = tsm;
+  double* ec = tsm + s;                   // s + 1
+  double* e2 = tsm + 2 * (size_t)s + 1;   // s + 1
+  double* Dp = tsm + 3 * (size_t)s + 2;
+  double* Lp = tsm + 4 * (size_t)s + 2;
+  double* Dm = tsm + 5 * (size_t)s + 2;
+  double* Um = tsm + 6 * (size_t)s + 2;
+  const int lane = threadIdx.x, iv = blockIdx.x;
+  if (iv >= m) return;
+  for (int k = lane; k <= s; k += 32) {
+    if (k < s) sd[k] = d[k];
+    const double c = (k > 0 && k < s) ? e[k - 1] : 0.0;
+    ec[k] = c;
+    e2[k] = c * c;
+  }
+  __syncwarp();
+  const double lm = lam[iv];
+  if (lane < 2) {
+    // lane 0: rows 0, 1, ..., s-1 (previous coupling ec[i], next ec[i+1]);
+    // lane 1: rows s-1, ..., 0 (previous coupling ec[i+1], next ec[i])
+    const bool top = lane == 0;
+    const int dir = top ? 1 : -1, op = top ? 0 : 1, on = top ? 1 : 0;
+    double* D = top ? Dp : Dm;
+    double* M = top ? Lp : Um;
+    double pm = 0.0, p = 1.0, rp = 1.0;  // P_{i-2}, P_{i-1}, 1 / P_{i-1}
+    int i = top ? 0 : s - 1;
+    auto step = [&]() {
+      const double a = sd[i] - lm;
+      double pn = fma(a, p, -e2[i + op] * pm);
+      if (pn == 0.0) pn = -0x1p-60 * p;
+      const double rn = fast_rcp(pn);  // off the P chain
+      D[i] = pn * rp;                  // D_i = P_i / P_{i-1}
+      M[i] = ec[i + on] * p * rn;      // e / D_i
+      pm = p;
+      p = pn;
+      rp = rn;
+      i += dir;
+    };
+    int st = 0;
+    for (; st + 8 <= s; st += 8) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) step();
+      const double mx = fmax(fabs(p), fabs(pm));
+      const int ex = (int)((__double_as_longlong(mx) >> 52) & 0x7ff);
+      if (ex > 0 && ex < 2047) {
+        const double sc = __longlong_as_double((long long)(2046 - ex) << 52);
+        const double isc = __longlong_as_double((long long)(ex) << 52);  // 1 / sc
+        p *= sc;
+        pm *= sc;
+        rp *= isc;
+      }
+    }
+    for (; st < s; ++st) step();
+  }
+  __syncwarp();
+  // twist index: argmin |gamma_k| (ties: the smallest k)
+  double best = INFINITY;
+  int bk = 0;
+  for (int k = lane; k < s; k += 32) {
+    const double g = fabs(Dp[k] + Dm[k] - (sd[k] - lm));
+    if (g < best) {
+      best = g;
+      bk = k;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int okk = __shfl_xor_sync(0xffffffffu, bk, o);
+    if (ob < best || (ob == best && okk < bk)) {
+      best = ob;
+      bk = okk;
+    }
+  }
+  const int r = bk;
+  // z (unnormalised) into Dp (free now): lane 0 upwards from r, lane 1 downwards
+  double* z = Dp;
+  if (lane == 0) {
+    double zz = 1.0;
+    z[r] = 1.0;
+    for (int k = r - 1; k >= 0; --k) {
+      zz = -Lp[k] * zz;
+      z[k] = zz;
+    }
+  } else if (lane == 1) {
+    double zz = 1.0;
+    for (int k = r + 1; k < s; ++k) {
+      zz = -Um[k] * zz;
+      z[k] = zz;
+    }
+  }
+  __syncwarp();
+  double n2 = 0.0;
+  for (int k = lane; k < s; k += 32) n2 = fma(z[k], z[k], n2);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+  const double inv = (n2 > 0.0) ? rsqrt(n2) : 0.0;
+  double* yv = y + (size_t)iv * ldy;
+  for (int k = lane; k < s; k += 32) yv[k] = z[k] * inv;
 }
 
 // Modified Gram-Schmidt inside clusters (dstein: |lam_i - lam_{i-1}| <= 1e-3 ||T||), one CTA,

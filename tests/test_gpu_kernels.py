@@ -152,3 +152,15 @@ def test_cholesky_breakdown(api):
     M[:, 17] = M[:, 3]
     L, rc = api.cholesky(_cm(M.T @ M))
     assert rc == 18
+
+
+@pytest.mark.parametrize("s", [4, 40, 100])
+@pytest.mark.parametrize("scale", [0.0, 1e-300, 1e300])
+def test_eigh_extreme_scales(api, s, scale):
+    """Sturm counts and eigenvalues at the ends of the exponent range (the bisection pre-scales T by
+    a power of two; the zero matrix has no positive eigenvalue)."""
+    A = np.diag(np.linspace(0.0, 1.0, s) * scale)
+    w, V, npos = api.eigh(_cm(A), s)
+    ref = np.sort(np.diag(A))[::-1]
+    assert npos == int(np.sum(ref > 0))
+    assert np.abs(w.cpu().numpy() - ref).max() <= 1e-13 * max(scale, 1e-300) * s
