@@ -158,9 +158,10 @@ def test_cholesky_breakdown(api):
 @pytest.mark.parametrize("scale", [0.0, 1e-300, 1e300])
 def test_eigh_extreme_scales(api, s, scale):
     """Sturm counts and eigenvalues at the ends of the exponent range (the bisection pre-scales T by
-    a power of two; the zero matrix has no positive eigenvalue)."""
+    a power of two; the zero matrix has no positive eigenvalue). Absolute accuracy floor: the
+    bisection stops at a bracket of 4 pivmin ~ 1e-306 (dstebz's safe-minimum floor)."""
     A = np.diag(np.linspace(0.0, 1.0, s) * scale)
     w, V, npos = api.eigh(_cm(A), s)
     ref = np.sort(np.diag(A))[::-1]
     assert npos == int(np.sum(ref > 0))
-    assert np.abs(w.cpu().numpy() - ref).max() <= 1e-13 * max(scale, 1e-300) * s
+    assert np.abs(w.cpu().numpy() - ref).max() <= 1e-13 * scale * s + 1e-306
