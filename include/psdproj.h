@@ -65,6 +65,8 @@ typedef struct {
   uint32_t ctx_id;/* Philox counter word c2 (distinct per cone block)                           */
   int profile;    /* bit 0: time every block-multiply (a3) launch; bit 1: per-phase timing       */
   int host_io;    /* 1: workspace also holds an n x n staging buffer for psdproj_project_host   */
+  int perp_steps; /* f2 (R48): 0 = the paper's bound (perp term ignored); k > 0 =  */
+                  /* k-step projected Lanczos estimate of the perp term added to err_bound        */
 } psdproj_params;
 
 typedef struct {
@@ -79,7 +81,7 @@ typedef struct {
   int rr_max;       /* largest Rayleigh-Ritz basis width s                                     */
   int locked;       /* hard-locked columns at exit                                             */
   long long a_cols; /* total columns multiplied by A                                           */
-  double err_bound; /* Theorem-3 bound on ||Pi~ - Pi(A)||_F (perp term 0)        */
+  double err_bound; /* Theorem-3 bound on ||Pi~ - Pi(A)||_F (perp term p^ = perp_est)           */
   double resid_fro; /* ||R+||_F over the kept pairs                                           */
   double resid_max; /* max_i r_i over the kept pairs                                          */
   double lock_defect; /* ||V+^T B V+ - diag(theta+)||_F (hard locking term, R36)             */
@@ -98,6 +100,7 @@ typedef struct {
                          5 rotation, 6 residual norms, 7 host round trips / locking / assembly,
                          8 RR bisection, 9 RR inverse iteration, 10 RR back-transformation,
                          11 RR re-orthonormalisation + C' = L^-T Y                          */
+  double perp_est;  /* f2 (R48): projected-Lanczos perp term p^ included in err_bound (0 if off) */
 } psdproj_info;
 
 /* Fill *p with the defaults documented above. */

@@ -9,6 +9,9 @@ Follows PAPER.md in its order and notation:
                   line 8), stopping rule (PAPER.md:493 / :507) and locking (BLOPEX active mask,
                   PAPER.md:502; optional hard locking, R35).
   error_bound     Theorem 3 with the perp term ignored.
+  estimate_perp   f2 (R48): k-step Lanczos on the deflated operator (I - V V^T) B (I - V V^T)
+                  ("projected Lanczos", PAPER.md:508), p^ = sqrt(n - p) max(mu + r, 0) in the
+                  Souto-2018 form.
   Context.project the side rule, negation and
                   Pi = V L V^T or A - V L V^T (R4).
 
@@ -317,6 +320,58 @@ def error_bound(B, V, theta, perp=0.0, delta_fp=None):
     if delta_fp is None:
         delta_fp = 4 * n * U * np.linalg.norm(B)
     return math.sqrt(2 * float(np.sum(R * R)) + perp ** 2) + float(np.linalg.norm(Hd)) + delta_fp
+
+
+def estimate_perp(B, V, steps, seed=0, stream=0, ctx=0, tag=0xC0000000):
+    """f2, reading R48: the perp term of Theorem 3 (PAPER.md:484, ignored by the paper, :508),
+    estimated by `steps` Lanczos steps on D = (I - V V^T) B (I - V V^T) from a Philox start
+    (stream, ctx, tag as the library), with full reorthogonalisation (two classical Gram-Schmidt
+    passes against V and the Lanczos basis). mu = the largest eigenvalue of the Lanczos matrix T_k
+    (cyclic Jacobi), r = beta_k |y_k| its residual norm (the distance from mu to the spectrum of
+    D is at most r), and p^ = sqrt(n - p) max(mu + r, 0): the Frobenius norm of the positive part
+    of D is at most sqrt(n - p) lambda_max(D) (P:37's form), and lambda_max(D) <= mu + r whenever
+    the Lanczos start vector has a component along the top eigenvector (a random start: with
+    probability 1). Returns (mu, r, p^); an empty complement or steps = 0 gives (0, 0, 0)."""
+    n = B.shape[0]
+    p = V.shape[1]
+    k = min(int(steps), n - p)
+    if k <= 0:
+        return 0.0, 0.0, 0.0
+
+    def deflate(w, Q):
+        for _ in range(2):
+            if p:
+                w = w - V @ (V.T @ w)
+            if Q.shape[1]:
+                w = w - Q @ (Q.T @ w)
+        return w
+
+    q = gaussian_block(n, 1, seed, stream, ctx=ctx, tag=tag)[:, 0]
+    q = deflate(q, np.zeros((n, 0)))
+    q = q / np.linalg.norm(q)
+    Q = q[:, None]
+    alpha, beta = [], []
+    anorm = float(np.linalg.norm(B))
+    for j in range(k):
+        w = B @ Q[:, j]
+        if p:
+            w = w - V @ (V.T @ w)
+        alpha.append(float(Q[:, j] @ w))
+        w = deflate(w, Q)
+        b = float(np.linalg.norm(w))
+        beta.append(b)
+        if b <= 1e-14 * max(anorm, 1e-300) or j == k - 1:
+            break
+        Q = np.column_stack([Q, w / b])
+    kk = len(alpha)
+    T = np.diag(alpha)
+    for i in range(kk - 1):
+        T[i, i + 1] = T[i + 1, i] = beta[i]
+    w_, Y, _ = jacobi_eig(T)
+    top = int(np.argmax(w_))
+    mu = float(w_[top])
+    r = abs(beta[kk - 1] * float(Y[kk - 1, top]))
+    return mu, r, math.sqrt(max(n - p, 0)) * max(mu + r, 0.0)
 
 
 # --------------------------------------------------------------------------- context

@@ -1410,6 +1410,114 @@ static int direct_path(Run& run, const double* A, int lda, double* Pi, int ldpi)
   return PSDPROJ_OK;
 }
 
+// ------------------------------------------------------------------ f2: perp term (R48)
+// Symmetric eigenvalues / last components of the top eigenvector of a small dense matrix (cyclic
+// Jacobi on the host: k <= m_max Lanczos steps).
+static void small_sym_top(int k, std::vector<double>& T, double* mu, double* ylast) {
+  std::vector<double> Vm((size_t)k * k, 0.0);
+  for (int i = 0; i < k; ++i) Vm[(size_t)i * k + i] = 1.0;
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    double off = 0.0, fro = 0.0;
+    for (int i = 0; i < k; ++i)
+      for (int j = 0; j < k; ++j) {
+        fro += T[(size_t)i * k + j] * T[(size_t)i * k + j];
+        if (i != j) off += T[(size_t)i * k + j] * T[(size_t)i * k + j];
+      }
+    if (off <= 1e-30 * fro || off == 0.0) break;
+    for (int pq = 0; pq < k; ++pq)
+      for (int qq = pq + 1; qq < k; ++qq) {
+        const double apq = T[(size_t)pq * k + qq];
+        if (apq == 0.0) continue;
+        const double app = T[(size_t)pq * k + pq], aqq = T[(size_t)qq * k + qq];
+        const double th = 0.5 * (aqq - app) / apq;
+        const double t = (th >= 0 ? 1.0 : -1.0) / (std::fabs(th) + std::sqrt(th * th + 1.0));
+        const double cs = 1.0 / std::sqrt(t * t + 1.0), sn = t * cs;
+        for (int r = 0; r < k; ++r) {  // columns pq, qq
+          const double a = T[(size_t)r * k + pq], b = T[(size_t)r * k + qq];
+          T[(size_t)r * k + pq] = cs * a - sn * b;
+          T[(size_t)r * k + qq] = sn * a + cs * b;
+        }
+        for (int r = 0; r < k; ++r) {  // rows pq, qq
+          const double a = T[(size_t)pq * k + r], b = T[(size_t)qq * k + r];
+          T[(size_t)pq * k + r] = cs * a - sn * b;
+          T[(size_t)qq * k + r] = sn * a + cs * b;
+        }
+        for (int r = 0; r < k; ++r) {
+          const double a = Vm[(size_t)r * k + pq], b = Vm[(size_t)r * k + qq];
+          Vm[(size_t)r * k + pq] = cs * a - sn * b;
+          Vm[(size_t)r * k + qq] = sn * a + cs * b;
+        }
+      }
+  }
+  int top = 0;
+  for (int i = 1; i < k; ++i)
+    if (T[(size_t)i * k + i] > T[(size_t)top * k + top]) top = i;
+  *mu = T[(size_t)top * k + top];
+  *ylast = Vm[(size_t)(k - 1) * k + top];
+}
+
+// k Lanczos steps on D = (I - V V^T) B (I - V V^T) (V: n x p, orthonormal) from a Philox start
+// (tag 0xC0000000), full reorthogonalisation (two CGS passes against V and the Lanczos basis, held in
+// c->R). mu = top eigenvalue of T_k, r = beta_k |y_k|, perp = sqrt(n - p) max(mu + r, 0).
+static int perp_estimate(Run& run, double sgn, const double* A, int lda, const double* V, int p, int steps,
+                         double* perp) {
+  psdproj_ctx_s* c = run.c;
+  const int n = c->n, ld = c->ld, ldm = c->s_max, nl = c->nr;
+  const int k = std::min(steps, std::min(n - p, c->m_max - 1));
+  *perp = 0.0;
+  if (k <= 0) return 0;
+  double* Q = c->R;   // n x (k + 1)
+  double* w = c->T2;  // n x 1 (free after the lock-defect term)
+  auto deflate = [&](double* z, int nq) -> int {
+    for (int pass = 0; pass < 2; ++pass) {
+      if (p > 0) {
+        TRY(run.gram(p, 1, V, ld, z, ld, c->Y, ldm));
+        TRY(run.gemm(OP_N, OP_N, nl, 1, p, -1.0, V, ld, c->Y, ldm, 1.0, z, ld));
+      }
+      if (nq > 0) {
+        TRY(run.gram(nq, 1, Q, ld, z, ld, c->Y, ldm));
+        TRY(run.gemm(OP_N, OP_N, nl, 1, nq, -1.0, Q, ld, c->Y, ldm, 1.0, z, ld));
+      }
+    }
+    return 0;
+  };
+  TRY(run.philox(1, Q, ld, 0xC0000000u));
+  TRY(deflate(Q, 0));
+  TRY(run.normalize(nl, 1, Q, ld, nullptr, 0));
+  std::vector<double> alpha, beta;
+  const double tiny = 1e-14 * std::max(run.anorm, 1e-300);
+  for (int j = 0; j < k; ++j) {
+    double* qj = Q + (size_t)j * ld;
+    TRY(run.amul(sgn, A, lda, qj, ld, 1, w, ld));
+    if (p > 0) {
+      TRY(run.gram(p, 1, V, ld, w, ld, c->Y, ldm));
+      TRY(run.gemm(OP_N, OP_N, nl, 1, p, -1.0, V, ld, c->Y, ldm, 1.0, w, ld));
+    }
+    TRY(run.gram(1, 1, qj, ld, w, ld, c->Y, ldm));  // alpha_j = q_j^T D q_j
+    CK(cudaMemcpyAsync(c->h_d, c->Y, sizeof(double), cudaMemcpyDeviceToHost, run.st));
+    TRY(deflate(w, j + 1));
+    TRY(run.normalize(nl, 1, w, ld, nullptr, 0));
+    CK(cudaMemcpyAsync(c->h_d + 1, c->d_norm, sizeof(double), cudaMemcpyDeviceToHost, run.st));
+    TRY(run.sync());
+    alpha.push_back(c->h_d[0]);
+    beta.push_back(c->h_d[1]);
+    if (c->h_d[1] <= tiny || j == k - 1) break;
+    CK(cudaMemcpy2DAsync(Q + (size_t)(j + 1) * ld, (size_t)ld * 8, w, (size_t)ld * 8, (size_t)nl * 8, 1,
+                         cudaMemcpyDeviceToDevice, run.st));
+  }
+  const int kk = (int)alpha.size();
+  std::vector<double> T((size_t)kk * kk, 0.0);
+  for (int i = 0; i < kk; ++i) {
+    T[(size_t)i * kk + i] = alpha[i];
+    if (i + 1 < kk) T[(size_t)i * kk + i + 1] = T[(size_t)(i + 1) * kk + i] = beta[i];
+  }
+  double mu = 0.0, yl = 0.0;
+  small_sym_top(kk, T, &mu, &yl);
+  const double r = std::fabs(beta[kk - 1] * yl);
+  *perp = std::sqrt((double)std::max(n - p, 0)) * std::max(mu + r, 0.0);
+  return 0;
+}
+
 // ------------------------------------------------------------------ LOBPCG path
 static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi, int ldpi, double tol,
                        bool& abort_direct) {
@@ -1821,11 +1929,16 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
     TRY(run.sync());
     lock_def = c->h_d[c->h_d_len - 8];
   }
-  // ---- Theorem 3 bound (R14-R16, R36): sqrt(2||R+||^2) + ||V+^T B V+ - Theta+||_F + 4 n u ||A||_F
+  // ---- f2 (R48): the perp term by projected Lanczos on (I - V V^T) B (I - V V^T), V = the kept
+  // positive Ritz vectors; p^ = sqrt(n - p) max(mu + r, 0) (0 unless perp_steps > 0)
+  double perp = 0.0;
+  if (c->prm.perp_steps > 0) TRY(perp_estimate(run, sgn, A, lda, V, p, c->prm.perp_steps, &perp));
+  info->perp_est = perp;
+  // ---- Theorem 3 bound (R14-R16, R36): sqrt(2||R+||^2 + p^2) + ||V+^T B V+ - Theta+||_F + 4 n u ||A||_F
   info->resid_fro = std::sqrt(rs);
   info->resid_max = rmax;
   info->lock_defect = lock_def;
-  info->err_bound = std::sqrt(2.0 * rs) + lock_def + 4.0 * n * PSD_U * run.anorm;
+  info->err_bound = std::sqrt(2.0 * rs + perp * perp) + lock_def + 4.0 * n * PSD_U * run.anorm;
   info->npos = p;
   // ---- a11: Pi = V Theta+ V^T (side +) or A + V Theta+ V^T (side -, pairs of -A)
   if (sgn < 0 && Pi != A) {
