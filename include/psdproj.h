@@ -158,20 +158,23 @@ int psdproj_destroy(psdproj_ctx ctx);
 /* Thread-local message of the last error ("" if none). */
 const char* psdproj_last_error(void);
 
-/* ---- f1: approximate ADMM (Alg. 1) for the MaxCut SDP (BASELINE configs[4]) ----
- * min <Q, X> s.t. diag(X) = 1, X in S+, as A x = z, z in C = {1}^n x S+ with A = [D; I], P = 0.
+/* ---- f1/f3: approximate ADMM (Alg. 1) for diagonal SDPs (MaxCut: BASELINE configs[4]) ----
+ * min <Q, X> s.t. X_ii = b_i for the i with w_i = 1, X in S+, as A x = z, z in C = {b}^w x S+ with
+ * A = [D_w; I], P = 0. b, w: device vectors of length n, or NULL for b = 1, w = 1 (MaxCut).
  * step1: the elementwise KKT solve of line 3 (A^T A is diagonal), the relaxation of line 4, and the
  * projection input V = alpha X~ + (1 - alpha) Zp + Yp / rho of line 5 (Zh = the relaxed z-hat,
  * zeh its diagonal part). The caller projects V with psdproj_project (Zp <- Pi(V), tolerance
  * 10/k^1.01). step2: the dual update of line 6 and the residual maxima
- * res_host[0..2] = (max|X - Zp|, max|diag X - 1|, max|Q + Yp + Diag(ye)|) (host, synchronous).
- * All matrices n x n, column-major, ld, device; ye, zeh length n, device. Reading R43. */
+ * res_host[0..2] = (max|X - Zp|, max_{w_i=1} |X_ii - b_i|, max|Q + Yp + Diag(w ye)|) (host,
+ * synchronous). All matrices n x n, column-major, ld, device; ye, zeh length n, device. The
+ * successive differences of (X, ye, Yp) are the infeasibility certificates of Theorem 1 (PAPER.md:100-119,
+ * f3, checked by the caller). Reading R43. */
 int psdproj_admm_maxcut_step1(int n, double* X, const double* Zp, const double* Yp, const double* ye,
                               const double* Q, int ld, double sigma, double rho, double alpha, double* Zh,
-                              double* V, double* zeh, void* stream);
+                              double* V, double* zeh, const double* b, const double* w, void* stream);
 int psdproj_admm_maxcut_step2(int n, const double* X, const double* Zp, const double* Zh, double* Yp, double* ye,
                               const double* zeh, const double* Q, int ld, double rho, double* res_host,
-                              void* stream);
+                              const double* b, const double* w, void* stream);
 
 /* ---- kernel-level entry points (tests and benchmarks call the same kernels the path uses) ---- */
 

@@ -1,6 +1,8 @@
-"""Oracle for f1 (TEST INFRASTRUCTURE; see oracle/__init__.py): Alg. 1 of PAPER.md:62-83 for the
-MaxCut SDP  max 1/4 <L, X>  s.t.  diag(X) = 1,  X PSD,  written step by step in the paper's
-notation with exact projections (O-EXACT, oracle/exact.py).
+"""Oracle for f1 / f3 (TEST INFRASTRUCTURE; see oracle/__init__.py): Alg. 1 of PAPER.md:62-83 for
+the diagonal SDP  min <Q, X>  s.t.  X_ii = b_i (i with w_i = 1),  X PSD  (MaxCut: Q = -L/4, b = 1,
+w = 1), written step by step in the paper's notation with exact projections (O-EXACT,
+oracle/exact.py), and the infeasibility certificates of Theorem 1 in the
+practical form of PAPER.md:563-587 (reading R49).
 
 Problem in the form of PAPER.md:50-57: minimise q^T x (P = 0) s.t. A x = z, z in C, with
 x = vec(X), q = vec(-L/4), A = [D; I] (D picks the diagonal), C = {1}^n x S+.
@@ -16,23 +18,32 @@ import numpy as np
 from .exact import project_exact
 
 
-def maxcut_admm(L, rho=0.1, sigma=1e-6, alpha=1.6, eps=1e-4, max_iter=5000, project=None):
-    n = L.shape[0]
+def diag_sdp_admm(Q, b=None, w=None, rho=0.1, sigma=1e-6, alpha=1.6, eps=1e-4, max_iter=5000, project=None,
+                  keep_last=False):
+    """Alg. 1 on min <Q, X> s.t. X_ii = b_i (w_i = 1), X PSD. Returns X, objective, iterations, the
+    residual history and (keep_last) the last two iterates (x, y) for the certificates."""
+    n = Q.shape[0]
+    b = np.ones(n) if b is None else np.asarray(b, dtype=np.float64)
+    w = np.ones(n) if w is None else np.asarray(w, dtype=np.float64)
+    eq = np.flatnonzero(w != 0)
     project = project or project_exact
     N = n * n
-    # A = [D; I] on vec(X) (column-major vec): D picks entries i + i n
-    D = np.zeros((n, N))
-    D[np.arange(n), np.arange(n) * (n + 1)] = 1.0
+    # A = [D_w; I] on vec(X) (column-major vec): D_w picks entries i + i n for the constrained i
+    D = np.zeros((eq.size, N))
+    D[np.arange(eq.size), eq * (n + 1)] = 1.0
     A = np.vstack([D, np.eye(N)])
-    q = (-0.25 * L).reshape(-1, order="F")
+    ne = eq.size
+    q = Q.reshape(-1, order="F")
     K = sigma * np.eye(N) + rho * (A.T @ A)
     Kinv = np.linalg.inv(K)  # K is fixed across iterations; line 3's solve is x~ = K^-1 rhs
     x = np.zeros(N)
-    z = np.concatenate([np.ones(n), np.zeros(N)])
-    y = np.zeros(n + N)
+    z = np.concatenate([b[eq], np.zeros(N)])
+    y = np.zeros(ne + N)
     hist = []
+    prev = None
     k = 0
     for k in range(1, max_iter + 1):
+        prev = (x.copy(), y.copy())
         rhs = sigma * x - q + rho * (A.T @ (z - y / rho))
         xt = Kinv @ rhs
         zt = A @ xt
@@ -40,9 +51,9 @@ def maxcut_admm(L, rho=0.1, sigma=1e-6, alpha=1.6, eps=1e-4, max_iter=5000, proj
         zh = alpha * zt + (1 - alpha) * z
         v = zh + y / rho
         znew = np.empty_like(z)
-        znew[:n] = 1.0                                           # projection onto {1}^n
-        Vm = v[n:].reshape(n, n, order="F")
-        znew[n:] = project(0.5 * (Vm + Vm.T)).reshape(-1, order="F")  # PSD block
+        znew[:ne] = b[eq]                                        # projection onto {b}
+        Vm = v[ne:].reshape(n, n, order="F")
+        znew[ne:] = project(0.5 * (Vm + Vm.T)).reshape(-1, order="F")  # PSD block
         y = y + rho * (zh - znew)
         z = znew
         r_prim = np.abs(A @ x - z).max()
@@ -51,4 +62,39 @@ def maxcut_admm(L, rho=0.1, sigma=1e-6, alpha=1.6, eps=1e-4, max_iter=5000, proj
         if r_prim <= eps and r_dual <= eps:
             break
     X = x.reshape(n, n, order="F")
-    return {"X": X, "objective": 0.25 * float(np.sum(L * X)), "iters": k, "hist": hist}
+    out = {"X": X, "objective": float(np.sum(Q * X)), "iters": k, "hist": hist}
+    if keep_last:
+        out.update({"x": x, "y": y, "x_prev": prev[0], "y_prev": prev[1], "A": A, "eq": eq, "b": b, "q": q})
+    return out
+
+
+def maxcut_admm(L, rho=0.1, sigma=1e-6, alpha=1.6, eps=1e-4, max_iter=5000, project=None):
+    out = diag_sdp_admm(-0.25 * L, rho=rho, sigma=sigma, alpha=alpha, eps=eps, max_iter=max_iter, project=project)
+    out["objective"] = -out["objective"]  # max 1/4 <L, X>
+    return out
+
+
+def certificates(run, n):
+    """Theorem 1 in the practical form of PAPER.md:563-587, reading R49, from the
+    last two iterates of diag_sdp_admm(..., keep_last=True): with y-bar = dy/||dy||, x-bar = dx/||dx||,
+      primal: ||A^T y-bar||_inf, dist_{C-polar}(y-bar) = ||Pi_S+(Y-bar)||_F, support b^T y-bar_eq
+      dual:   dist_{C-inf}(A x-bar) = sqrt(||diag_w(X-bar)||^2 + ||Pi_S+(-X-bar)||_F^2), q^T x-bar
+    (the PSD projections exact, O-EXACT). Returns a dict of the five numbers and the two norms."""
+    A, eq, b, q = run["A"], run["eq"], run["b"], run["q"]
+    ne = eq.size
+    dx = run["x"] - run["x_prev"]
+    dy = run["y"] - run["y_prev"]
+    out = {"ndx": float(np.linalg.norm(dx)), "ndy": float(np.linalg.norm(dy))}
+    if out["ndy"] > 1e-12:
+        yb = dy / out["ndy"]
+        Yb = yb[ne:].reshape(n, n, order="F")
+        out["p_at"] = float(np.abs(A.T @ yb).max())
+        out["p_dist"] = float(np.linalg.norm(project_exact(0.5 * (Yb + Yb.T))))
+        out["p_supp"] = float(b[eq] @ yb[:ne])
+    if out["ndx"] > 1e-12:
+        xb = dx / out["ndx"]
+        Xb = xb.reshape(n, n, order="F")
+        ax = A @ xb
+        out["d_dist"] = float(np.sqrt(np.sum(ax[:ne] ** 2) + np.sum(project_exact(-0.5 * (Xb + Xb.T)) ** 2)))
+        out["d_qx"] = float(q @ xb)
+    return out

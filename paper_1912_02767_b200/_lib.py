@@ -90,8 +90,8 @@ def load(path=SO_PATH):
     L.psdproj_eigh.argtypes = [i, vp, i, i, vp, vp, i, vp, vp, vp]
     L.psdproj_cholesky.argtypes = [i, vp, i, vp]
     L.psdproj_get_nccl_uid.argtypes = [vp]
-    L.psdproj_admm_maxcut_step1.argtypes = [i, vp, vp, vp, vp, vp, i, d, d, d, vp, vp, vp, vp]
-    L.psdproj_admm_maxcut_step2.argtypes = [i, vp, vp, vp, vp, vp, vp, vp, i, d, P(d), vp]
+    L.psdproj_admm_maxcut_step1.argtypes = [i, vp, vp, vp, vp, vp, i, d, d, d, vp, vp, vp, vp, vp, vp]
+    L.psdproj_admm_maxcut_step2.argtypes = [i, vp, vp, vp, vp, vp, vp, vp, i, d, P(d), vp, vp, vp]
     L.psdproj_workspace_bytes_sharded.argtypes = [i, i, i, P(Params)]
     L.psdproj_workspace_bytes_sharded.restype = sz
     L.psdproj_create_sharded.argtypes = [i, i, i, vp, i, i, P(Params), vp, sz, P(vp)]

@@ -22,16 +22,21 @@ def tol_schedule(k, c=10.0, p=1.01):
     return c / float(k) ** p
 
 
-class MaxCutADMM:
-    def __init__(self, L, rho=0.1, sigma=1e-6, alpha=1.6, device="cuda", params=None, tol_floor=0.0,
+class DiagSDPADMM:
+    """Alg. 1 on  min <Q, X>  s.t.  X_ii = b_i (i with w_i = 1),  X PSD  (b, w default to ones).
+    f3: `certificates()` evaluates Theorem 1's infeasibility certificates in the
+    practical form of PAPER.md:563-587 (reading R49) from the last two iterates; `solve(...,
+    check_every=40)` stops on a certificate (status 'primal_infeasible' / 'dual_infeasible')."""
+
+    def __init__(self, Q, b=None, w=None, rho=0.1, sigma=1e-6, alpha=1.6, device="cuda", params=None, tol_floor=0.0,
                  tol_override=None):
-        n = L.shape[0]
+        n = Q.shape[0]
         self.n, self.rho, self.sigma, self.alpha = n, float(rho), float(sigma), float(alpha)
         self.tol_floor, self.tol_override = tol_floor, tol_override
         dev = torch.device(device)
-        Lt = torch.as_tensor(L, dtype=torch.float64, device=dev)
-        self.Q = (-0.25 * Lt).contiguous()  # min <Q, X> = -max 1/4 <L, X>
-        self.L = Lt
+        self.Q = torch.as_tensor(Q, dtype=torch.float64, device=dev).contiguous()
+        vec = lambda v: None if v is None else torch.as_tensor(v, dtype=torch.float64, device=dev).contiguous()  # noqa: E731
+        self.b, self.w = vec(b), vec(w)
         z = lambda: torch.zeros(n, n, dtype=torch.float64, device=dev)  # noqa: E731
         self.X, self.Zp, self.Yp, self.Zh, self.V = z(), z(), z(), z(), z()
         self.ye = torch.zeros(n, dtype=torch.float64, device=dev)
@@ -39,37 +44,104 @@ class MaxCutADMM:
         self.ctx = api.Context(n, params=params if params is not None else api.default_params(seed=1912))
         self.k = 0
         self.infos = []
+        self.prev = None
+        self._cert_ctx = None
 
-    def step(self):
+    def step(self, save_prev=False):
         """One iteration of Alg. 1; returns (r_prim, r_dual, projection info)."""
         L_ = _lib.load()
         n, st = self.n, api._stream_ptr(None)
         p = api._ptr
+        pb = p(self.b) if self.b is not None else None
+        pw = p(self.w) if self.w is not None else None
+        if save_prev:
+            self.prev = (self.X.clone(), self.ye.clone(), self.Yp.clone())
         check(L_.psdproj_admm_maxcut_step1(n, p(self.X), p(self.Zp), p(self.Yp), p(self.ye), p(self.Q), n,
                                            self.sigma, self.rho, self.alpha, p(self.Zh), p(self.V), p(self.zeh),
-                                           st), "psdproj_admm_maxcut_step1")
+                                           pb, pw, st), "psdproj_admm_maxcut_step1")
         self.k += 1
         tol = self.tol_override if self.tol_override is not None else max(tol_schedule(self.k), self.tol_floor)
         _, info = self.ctx.project(self.V, tol, out=self.Zp)
         res = (ctypes.c_double * 3)()
         check(L_.psdproj_admm_maxcut_step2(n, p(self.X), p(self.Zp), p(self.Zh), p(self.Yp), p(self.ye),
-                                           p(self.zeh), p(self.Q), n, self.rho, res, st),
+                                           p(self.zeh), p(self.Q), n, self.rho, res, pb, pw, st),
               "psdproj_admm_maxcut_step2")
         self.infos.append(info)
         return max(res[0], res[1]), res[2], info
 
-    def solve(self, eps=1e-4, max_iter=5000):
+    def _psd_part(self, M):
+        """||Pi_S+(M)||_F by the library's DIRECT path (exact eigendecomposition)."""
+        if self._cert_ctx is None:
+            self._cert_ctx = api.Context(self.n, params=api.default_params(side=2))
+        Pi, _ = self._cert_ctx.project(0.5 * (M + M.T).contiguous(), 1e-12)
+        return float(torch.linalg.norm(Pi))
+
+    def certificates(self):
+        """Theorem 1's certificates from the successive differences of the last step (needs
+        step(save_prev=True)): with y = (w ye, Yp) and x = vec(X),
+          primal: ||A^T y-bar||_inf, dist_{C-polar}(y-bar) = ||Pi_S+(Y-bar)||_F, b^T y-bar_eq
+          dual:   dist_{C-inf}(A x-bar) = (||w diag X-bar||^2 + ||Pi_S+(-X-bar)||_F^2)^(1/2), <Q, X-bar>"""
+        X0, ye0, Yp0 = self.prev
+        w = self.w if self.w is not None else torch.ones_like(self.ye)
+        b = self.b if self.b is not None else torch.ones_like(self.ye)
+        dX, dye, dYp = self.X - X0, (self.ye - ye0) * w, self.Yp - Yp0
+        out = {"ndx": float(torch.linalg.norm(dX)), "ndy": float(torch.sqrt(torch.sum(dye ** 2) + torch.sum(dYp ** 2)))}
+        if out["ndy"] > 1e-12:
+            ye_b, Yb = dye / out["ndy"], dYp / out["ndy"]
+            out["p_at"] = float(torch.max(torch.abs(Yb + torch.diag(ye_b))))
+            out["p_dist"] = self._psd_part(Yb)
+            out["p_supp"] = float(torch.dot(b, ye_b))
+        if out["ndx"] > 1e-12:
+            Xb = dX / out["ndx"]
+            out["d_dist"] = float(torch.sqrt(torch.sum((w * torch.diagonal(Xb)) ** 2) + self._psd_part(-Xb) ** 2))
+            out["d_qx"] = float(torch.sum(self.Q * Xb))
+        return out
+
+    @staticmethod
+    def infeasible(cert, eps_pinf=1e-4, eps_dinf=1e-4):
+        """R49: primal if ||A^T y-bar|| < eps, dist < eps and the support b^T y-bar < -eps; dual if
+        dist < eps and q^T x-bar < -eps (Theorem 1's strict inequalities)."""
+        p = "p_at" in cert and cert["p_at"] < eps_pinf and cert["p_dist"] < eps_pinf and cert["p_supp"] < -eps_pinf
+        d = "d_dist" in cert and cert["d_dist"] < eps_dinf and cert["d_qx"] < -eps_dinf
+        return p, d
+
+    def solve(self, eps=1e-4, max_iter=5000, check_every=0, eps_pinf=1e-4, eps_dinf=1e-4):
         r_p = r_d = float("inf")
+        status, cert = "max_iter", None
         while self.k < max_iter:
-            r_p, r_d, _ = self.step()
+            chk = check_every > 0 and (self.k + 1) % check_every == 0
+            r_p, r_d, _ = self.step(save_prev=chk)
             if r_p <= eps and r_d <= eps:
+                status = "solved"
                 break
-        return {"iters": self.k, "r_prim": r_p, "r_dual": r_d, "objective": self.objective(),
-                "lobpcg_iters": sum(i["iters"] for i in self.infos)}
+            if chk:
+                cert = self.certificates()
+                pinf, dinf = self.infeasible(cert, eps_pinf, eps_dinf)
+                if pinf or dinf:
+                    status = "primal_infeasible" if pinf else "dual_infeasible"
+                    if pinf and dinf:
+                        status = "primal_dual_infeasible"
+                    break
+        return {"iters": self.k, "r_prim": r_p, "r_dual": r_d, "objective": self.objective(), "status": status,
+                "certificates": cert, "lobpcg_iters": sum(i["iters"] for i in self.infos)}
+
+    def objective(self):
+        """<Q, X> at the current (relaxed) primal iterate."""
+        return float((self.Q * self.X).sum())
+
+    def close(self):
+        self.ctx.close()
+        if self._cert_ctx is not None:
+            self._cert_ctx.close()
+
+
+class MaxCutADMM(DiagSDPADMM):
+    """MaxCut SDP (BASELINE configs[4]): max 1/4 <L, X> s.t. diag(X) = 1, X PSD."""
+
+    def __init__(self, L, **kw):
+        self.L = torch.as_tensor(L, dtype=torch.float64, device=kw.get("device", "cuda"))
+        super().__init__(-0.25 * self.L, **kw)
 
     def objective(self):
         """1/4 <L, X> at the current (relaxed) primal iterate."""
         return float(0.25 * (self.L * self.X).sum())
-
-    def close(self):
-        self.ctx.close()

@@ -892,47 +892,52 @@ __global__ void fro_partial_kernel(int rows, int cols, const double* __restrict_
 }  // namespace psd
 
 namespace psd {
-// ---------------------------------------------------------------- f1: approximate ADMM for the MaxCut SDP
-// Alg. 1 on  min <Q, X>  s.t.  diag(X) = 1,  X in S+  written as  A x = z, z in C
-// with x = vec(X), A = [D; I] (D extracts the diagonal), C = {1}^n x S+, P = 0. A^T A is diagonal
-// (2 on the diagonal entries, 1 elsewhere), so line 3's KKT solve is elementwise. Readings (R43):
-// line 5 projects alpha z~ + (1 - alpha) z^k + y^k / rho and line 6 updates y with that same
-// relaxed z-hat (COSMO / Stellato 2017 form; the printed lines drop (1 - alpha) z^k and write x~).
+// ---------------------------------------------------------------- f1/f3: approximate ADMM, diagonal SDP
+// Alg. 1 on  min <Q, X>  s.t.  X_ii = b_i (i with w_i = 1),  X in S+  written as
+// A x = z, z in C with x = vec(X), A = [D_w; I] (D_w extracts the constrained diagonal entries),
+// C = {b}^w x S+, P = 0 (MaxCut: b = 1, w = 1; f3's infeasible toys: some b_i < 0, or w = 0 with an
+// indefinite Q). A^T A is diagonal (1 + w_i on the diagonal entries, 1 elsewhere), so line 3's KKT
+// solve is elementwise. Readings (R43): line 5 projects alpha z~ + (1 - alpha) z^k + y^k / rho and
+// line 6 updates y with that same relaxed z-hat (COSMO / Stellato 2017 form).
+// b, w == nullptr mean b = 1, w = 1.
 //
 // Step 1 (lines 3-4 and the projection input of line 5): for every entry
-//   X~ = (sigma X - Q + rho Zp - Yp + [i = j] (rho - ye_i)) / (sigma + rho (1 + [i = j]))
+//   X~ = (sigma X - Q + rho Zp - Yp + [i = j] w_i (rho b_i - ye_i)) / (sigma + rho (1 + [i = j] w_i))
 //   X  <- alpha X~ + (1 - alpha) X;   Zh = alpha X~ + (1 - alpha) Zp;   V = Zh + Yp / rho
-//   zeh_i = alpha X~_ii + (1 - alpha)                      (z_eq = 1 after every projection)
+//   zeh_i = alpha X~_ii + (1 - alpha) b_i                  (z_eq = b after every projection)
 __global__ void admm_maxcut_step1_kernel(int n, double* __restrict__ X, const double* __restrict__ Zp,
                                          const double* __restrict__ Yp, const double* __restrict__ ye,
                                          const double* __restrict__ Q, double sigma, double rho, double alpha,
                                          double* __restrict__ Zh, double* __restrict__ V, double* __restrict__ zeh,
-                                         int ld) {
+                                         int ld, const double* __restrict__ bv, const double* __restrict__ wv) {
   const size_t total = (size_t)n * n;
   for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
     const int i = (int)(e % n), j = (int)(e / n);
     const size_t o = IDX(i, j, ld);
     const bool dg = i == j;
+    const double bi = (dg && bv) ? bv[i] : 1.0;
+    const double wi = dg ? (wv ? wv[i] : 1.0) : 0.0;
     double xt = sigma * X[o] - Q[o] + rho * Zp[o] - Yp[o];
-    if (dg) xt += rho - ye[i];
-    xt /= sigma + rho * (dg ? 2.0 : 1.0);
+    if (dg) xt += wi * (rho * bi - ye[i]);
+    xt /= sigma + rho * (1.0 + wi);
     X[o] = alpha * xt + (1.0 - alpha) * X[o];
     const double zh = alpha * xt + (1.0 - alpha) * Zp[o];
     Zh[o] = zh;
     V[o] = zh + Yp[o] / rho;
-    if (dg) zeh[i] = alpha * xt + (1.0 - alpha);
+    if (dg) zeh[i] = alpha * xt + (1.0 - alpha) * bi;
   }
 }
 
 // Step 2 (line 6) and residual maxima (COSMO termination, PAPER.md:500 footnote; R33 absolute):
-//   Yp <- Yp + rho (Zh - Zp),  ye <- ye + rho (zeh - 1)
-//   res[0] = max |X - Zp| (primal, PSD block), res[1] = max |diag X - 1| (primal, equalities),
-//   res[2] = max |Q + Yp + Diag(ye)| (dual: P x + q + A^T y)
+//   Yp <- Yp + rho (Zh - Zp),  ye <- ye + rho (zeh - b) (constrained i; ye = 0 elsewhere)
+//   res[0] = max |X - Zp| (primal, PSD block), res[1] = max |X_ii - b_i| over w_i = 1 (equalities),
+//   res[2] = max |Q + Yp + Diag(w ye)| (dual: P x + q + A^T y)
 __global__ void admm_maxcut_step2_kernel(int n, const double* __restrict__ X, const double* __restrict__ Zp,
                                          const double* __restrict__ Zh, double* __restrict__ Yp,
                                          double* __restrict__ ye, const double* __restrict__ zeh,
                                          const double* __restrict__ Q, double rho, int ld,
-                                         unsigned long long* __restrict__ res) {
+                                         unsigned long long* __restrict__ res, const double* __restrict__ bv,
+                                         const double* __restrict__ wv) {
   double r0 = 0.0, r1 = 0.0, r2 = 0.0;
   const size_t total = (size_t)n * n;
   for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
@@ -943,10 +948,13 @@ __global__ void admm_maxcut_step2_kernel(int n, const double* __restrict__ X, co
     r0 = fmax(r0, fabs(X[o] - Zp[o]));
     double dres = Q[o] + yp;
     if (i == j) {
-      const double y = ye[i] + rho * (zeh[i] - 1.0);
-      ye[i] = y;  // each diagonal entry is visited by exactly one thread
-      dres += y;
-      r1 = fmax(r1, fabs(X[o] - 1.0));
+      const double bi = bv ? bv[i] : 1.0, wi = wv ? wv[i] : 1.0;
+      if (wi != 0.0) {
+        const double y = ye[i] + rho * (zeh[i] - bi);
+        ye[i] = y;  // each diagonal entry is visited by exactly one thread
+        dres += y;
+        r1 = fmax(r1, fabs(X[o] - bi));
+      }
     }
     r2 = fmax(r2, fabs(dres));
   }

@@ -2303,29 +2303,29 @@ extern "C" int psdproj_cholesky(int t, double* G, int ld, void* stream) {
   return rc < 0 ? rc : h;
 }
 
-// ------------------------------------------------------------------ f1: approximate ADMM (MaxCut SDP)
+// ------------------------------------------------------------------ f1/f3: approximate ADMM (diagonal SDP)
 extern "C" int psdproj_admm_maxcut_step1(int n, double* X, const double* Zp, const double* Yp, const double* ye,
                                          const double* Q, int ld, double sigma, double rho, double alpha, double* Zh,
-                                         double* V, double* zeh, void* stream) {
+                                         double* V, double* zeh, const double* b, const double* w, void* stream) {
   if (n <= 0 || ld < n || !X || !Zp || !Yp || !ye || !Q || !Zh || !V || !zeh || !(rho > 0.0) || !(sigma >= 0.0) ||
       !(alpha > 0.0 && alpha < 2.0))
     return set_err(PSDPROJ_E_INVALID, "invalid admm step1 arguments");
   admm_maxcut_step1_kernel<<<grid1d((size_t)n * n), 256, 0, (cudaStream_t)stream>>>(n, X, Zp, Yp, ye, Q, sigma, rho,
-                                                                                     alpha, Zh, V, zeh, ld);
+                                                                                     alpha, Zh, V, zeh, ld, b, w);
   CKL();
   return 0;
 }
 
 extern "C" int psdproj_admm_maxcut_step2(int n, const double* X, const double* Zp, const double* Zh, double* Yp,
                                          double* ye, const double* zeh, const double* Q, int ld, double rho,
-                                         double* res_host, void* stream) {
+                                         double* res_host, const double* b, const double* w, void* stream) {
   if (n <= 0 || ld < n || !X || !Zp || !Zh || !Yp || !ye || !zeh || !Q || !res_host || !(rho > 0.0))
     return set_err(PSDPROJ_E_INVALID, "invalid admm step2 arguments");
   cudaStream_t st = (cudaStream_t)stream;
   static thread_local unsigned long long* dres = nullptr;
   if (!dres) CK(cudaMalloc(&dres, 4 * sizeof(unsigned long long)));
   CK(cudaMemsetAsync(dres, 0, 3 * sizeof(unsigned long long), st));
-  admm_maxcut_step2_kernel<<<grid1d((size_t)n * n), 256, 0, st>>>(n, X, Zp, Zh, Yp, ye, zeh, Q, rho, ld, dres);
+  admm_maxcut_step2_kernel<<<grid1d((size_t)n * n), 256, 0, st>>>(n, X, Zp, Zh, Yp, ye, zeh, Q, rho, ld, dres, b, w);
   CKL();
   CK(cudaMemcpyAsync(res_host, dres, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));

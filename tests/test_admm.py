@@ -90,3 +90,78 @@ def test_gpu_admm_schedule_converges_c5_small(api):
     assert np.linalg.eigvalsh(0.5 * (X + X.T)).min() >= -1e-3
     assert sum(i["cold"] for i in solver.infos) <= 2       # warm starts across ADMM iterations
     solver.close()
+
+
+# ---------------------------------------------------------------- f3: infeasibility certificates
+def _toys(n=6, seed=0):
+    rng = np.random.default_rng(seed)
+    M = rng.standard_normal((n, n))
+    Q = 0.5 * (M + M.T)
+    b = np.ones(n)
+    b[0] = -1.0  # X_00 = -1 with X PSD: primal infeasible
+    return Q, b, np.zeros(n)  # w = 0 (no equality rows) with an indefinite Q: dual infeasible
+
+
+def test_oracle_primal_infeasibility_certificate():
+    """Theorem 1 (i): dy -> a certificate with A^T y = 0, S_C(y) < 0, met in the
+    practical form of PAPER.md:582-587 at 1e-4 (R49); the direction is the diagonal row of the
+    offending constraint (b^T y-bar -> -1/sqrt(2): y_eq = -e_0 / sqrt 2, Y = e_0 e_0^T / sqrt 2 ... up
+    to the rest of the cone)."""
+    from oracle.admm import certificates, diag_sdp_admm
+    Q, b, _ = _toys()
+    run = diag_sdp_admm(Q, b=b, eps=0.0, max_iter=800, keep_last=True)
+    c = certificates(run, Q.shape[0])
+    assert c["ndy"] > 1e-3                                  # dy does not vanish
+    assert c["p_at"] < 1e-4 and c["p_dist"] < 1e-4 and c["p_supp"] < -1e-4
+    assert abs(c["p_supp"] + 1 / np.sqrt(2)) < 1e-3
+    assert not (c["d_dist"] < 1e-4 and c["d_qx"] < -1e-4)  # not dual infeasible
+
+
+def test_oracle_dual_infeasibility_certificate():
+    """Theorem 1 (ii): dx -> a direction with A dx in C^inf (PSD, no equality rows) and q^T dx < 0."""
+    from oracle.admm import certificates, diag_sdp_admm
+    Q, _, w = _toys()
+    run = diag_sdp_admm(Q, w=w, eps=0.0, max_iter=400, keep_last=True)
+    c = certificates(run, Q.shape[0])
+    assert c["ndx"] > 1.0
+    assert c["d_dist"] < 1e-4 and c["d_qx"] < -1e-4
+    # the unbounded direction is the normalised steepest descent ray in the cone, Pi_S+(-Q) / ||.||:
+    # q^T x-bar -> -||Pi_S+(-Q)||_F = -(sum of the squared negative eigenvalues of Q)^(1/2)
+    lam = np.linalg.eigvalsh(Q)
+    assert abs(c["d_qx"] + np.sqrt(np.sum(lam[lam < 0] ** 2))) < 1e-3
+
+
+def test_oracle_feasible_problem_never_certifies():
+    from oracle.admm import certificates, diag_sdp_admm
+    L = cycle(6)
+    for it in (40, 80, 120, 400):
+        c = certificates(diag_sdp_admm(-0.25 * L, eps=0.0, max_iter=it, keep_last=True), 6)
+        p = "p_at" in c and c["p_at"] < 1e-4 and c["p_dist"] < 1e-4 and c["p_supp"] < -1e-4
+        d = "d_dist" in c and c["d_dist"] < 1e-4 and c["d_qx"] < -1e-4
+        assert not (p or d), (it, c)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", ["primal", "dual", "feasible"])
+def test_gpu_admm_infeasibility_detection(api, kind):
+    """f3: the library's ADMM with approximate (LOBPCG) projections stops on Theorem 1's
+    certificate for the infeasible toys and never for a feasible MaxCut."""
+    from paper_1912_02767_b200.admm import DiagSDPADMM
+    Q, b, w = _toys()
+    if kind == "primal":
+        solver = DiagSDPADMM(Q, b=b)
+    elif kind == "dual":
+        solver = DiagSDPADMM(Q, w=w)
+    else:
+        solver = DiagSDPADMM(-0.25 * cycle(6))
+    out = solver.solve(eps=1e-7, max_iter=4000, check_every=40)
+    if kind == "primal":
+        assert out["status"] == "primal_infeasible", out
+        assert abs(out["certificates"]["p_supp"] + 1 / np.sqrt(2)) < 1e-2
+    elif kind == "dual":
+        assert out["status"] == "dual_infeasible", out
+        lam = np.linalg.eigvalsh(Q)
+        assert abs(out["certificates"]["d_qx"] + np.sqrt(np.sum(lam[lam < 0] ** 2))) < 1e-2
+    else:
+        assert out["status"] == "solved", out
+    solver.close()
