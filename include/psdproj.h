@@ -145,6 +145,16 @@ int psdproj_project_batched(psdproj_ctx* ctxs, int count, const double* const* A
                             double* const* Pi, const int* ldpi, const double* tol, void* stream,
                             psdproj_info* infos);
 
+/* f4: many tiny cone blocks (n_i <= 112) in one launch, one CTA per block: the exact
+ * projection by the one-CTA Jacobi eigensolver in shared memory, Pi_i = sum_{lambda > 0} lambda v v^T
+ * (or A_i - sum_{lambda < 0}, whichever side has fewer eigenvalues), exactly
+ * symmetric. No context and no warm state (the blocks are small enough for the exact path, R50).
+ * Host arrays n, A (device pointers), lda, Pi (device pointers, may equal A), ldpi of length count;
+ * npos_host (host, nullable) receives the positive-eigenvalue counts. Synchronous on `stream`.
+ * Errors: PSDPROJ_E_CAPACITY for n_i > 112, PSDPROJ_E_DEGENERATE if a Jacobi run does not converge. */
+int psdproj_project_tiny_batched(int count, const int* n, const double* const* A, const int* lda,
+                                 double* const* Pi, const int* ldpi, int* npos_host, void* stream);
+
 /* Warm block of the last call: vals_host (cap values, descending Ritz values of the side used,
  * sign as computed on B = side*A), vecs_dev (n x cap, ldv) may be NULL. Returns the count. */
 int psdproj_get_ritz(psdproj_ctx ctx, double* vals_host, int cap, double* vecs_dev, int ldv);

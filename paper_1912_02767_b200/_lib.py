@@ -17,7 +17,7 @@ LOCK_SOFT, LOCK_HARD = 1, 2
 # every symbol include/psdproj.h declares (checked by tests/test_abi.py)
 EXPORTS = [
     "psdproj_default_params", "psdproj_workspace_bytes", "psdproj_create", "psdproj_project",
-    "psdproj_project_host", "psdproj_project_batched", "psdproj_get_ritz", "psdproj_reset",
+    "psdproj_project_host", "psdproj_project_batched", "psdproj_project_tiny_batched", "psdproj_get_ritz", "psdproj_reset",
     "psdproj_destroy", "psdproj_last_error", "psdproj_dgemm", "psdproj_jacobi_ws_elems",
     "psdproj_jacobi", "psdproj_philox_raw", "psdproj_philox_gauss", "psdproj_eigh_ws_elems",
     "psdproj_eigh", "psdproj_cholesky", "psdproj_get_nccl_uid", "psdproj_workspace_bytes_sharded",
@@ -76,6 +76,7 @@ def load(path=SO_PATH):
     L.psdproj_project.argtypes = [vp, vp, i, vp, i, d, vp, P(Info)]
     L.psdproj_project_host.argtypes = [vp, vp, i, vp, i, d, vp, P(Info)]
     L.psdproj_project_batched.argtypes = [P(vp), i, P(vp), P(i), P(vp), P(i), P(d), vp, P(Info)]
+    L.psdproj_project_tiny_batched.argtypes = [i, P(i), P(vp), P(i), P(vp), P(i), P(i), vp]
     L.psdproj_get_ritz.argtypes = [vp, P(d), i, vp, i]
     L.psdproj_reset.argtypes = [vp]
     L.psdproj_destroy.argtypes = [vp]

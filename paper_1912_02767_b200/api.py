@@ -231,6 +231,23 @@ def project_batched(ctxs, As, tols, outs=None, stream=None):
     return outs, [inf.as_dict() for inf in infos]
 
 
+def project_tiny_batched(As, outs=None, stream=None):
+    """psdproj_project_tiny_batched: exact projections of many tiny blocks (n <= 112) in one launch.
+    Returns (outs, npos list)."""
+    L = _lib.load()
+    k = len(As)
+    outs = outs if outs is not None else [torch.empty_like(a) for a in As]
+    ns = (ctypes.c_int * k)(*[a.shape[0] for a in As])
+    Ap = (ctypes.c_void_p * k)(*[a.data_ptr() for a in As])
+    Op = (ctypes.c_void_p * k)(*[o.data_ptr() for o in outs])
+    la = (ctypes.c_int * k)(*[_ld_sym(a) for a in As])
+    lo = (ctypes.c_int * k)(*[_ld_sym(o) for o in outs])
+    npos = (ctypes.c_int * k)()
+    check(L.psdproj_project_tiny_batched(k, ns, Ap, la, Op, lo, npos, _stream_ptr(stream)),
+          "psdproj_project_tiny_batched")
+    return outs, list(npos)
+
+
 def dgemm(opA, opB, alpha, A, B, beta, C, ws=None, stream=None):
     """C = alpha op(A) op(B) + beta C on column-major device tensors (psdproj_dgemm)."""
     L = _lib.load()

@@ -432,11 +432,11 @@ constexpr int JAC_SMEM_MAX = 112;
 // info[0] = sweeps performed (-1: no convergence within max_sweeps).
 // Each thread owns a fixed set of (pair-slot k1 <= pair-slot k2) blocks (decoded once) and a
 // fixed set of (row, pair-slot) entries of V; per round only the rotation parameters change.
+// The sweeps, on shared memory sm (2 N (N + 1) doubles): on return the eigenvalues are on the
+// diagonal of M = sm (ld N + 1) and the eigenvectors are the columns of Q = sm + N (N + 1);
+// returns the sweeps performed (-1: no convergence within max_sweeps).
 template <int NT>
-__global__ void __launch_bounds__(NT) jacobi_smem_kernel(int s, const double* __restrict__ A, int lda,
-                                                         double* __restrict__ w, double* __restrict__ V, int ldv,
-                                                         int max_sweeps, int* __restrict__ info) {
-  extern __shared__ __align__(16) double sm[];
+__device__ int jacobi_smem_core(int s, const double* __restrict__ A, int lda, double* sm, int max_sweeps) {
   constexpr int HM = JAC_SMEM_MAX / 2;
   constexpr int MAXB = (HM * (HM + 1) / 2 + NT - 1) / NT;
   const int N = s + (s & 1);
@@ -532,12 +532,70 @@ __global__ void __launch_bounds__(NT) jacobi_smem_kernel(int s, const double* __
     done = (rot == 0);
     __syncthreads();
   }
+  return done ? sweep : -1;
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) jacobi_smem_kernel(int s, const double* __restrict__ A, int lda,
+                                                         double* __restrict__ w, double* __restrict__ V, int ldv,
+                                                         int max_sweeps, int* __restrict__ info) {
+  extern __shared__ __align__(16) double sm[];
+  const int sweeps = jacobi_smem_core<NT>(s, A, lda, sm, max_sweeps);
+  const int N = s + (s & 1), L = N + 1;
+  const double* M = sm;
+  const double* Q = sm + N * L;
   for (int i = threadIdx.x; i < s; i += NT) w[i] = M[i + i * L];
   for (int e = threadIdx.x; e < s * s; e += NT) {
     int i = e % s, j = e / s;
     V[IDX(i, j, ldv)] = Q[i + j * L];
   }
-  if (threadIdx.x == 0) { info[0] = done ? sweep : -1; info[1] = 0; }
+  if (threadIdx.x == 0) { info[0] = sweeps; info[1] = 0; }
+}
+
+// ---------------------------------------------------------------- f4: many tiny cone blocks
+// One CTA per block (n <= JAC_SMEM_MAX): the exact projection by the one-CTA Jacobi above, then
+// Pi = sum_{lambda > 0} lambda v v^T, or A - sum_{lambda < 0} lambda v v^T when fewer eigenvalues are
+// negative (the one-sided rule of PAPER.md:505 on the exact spectrum), each entry (i <= j) computed
+// once and mirrored. npos[b] = number of positive eigenvalues (-1: no convergence).
+struct TinyBlock {
+  const double* A;
+  double* Pi;
+  int n, lda, ldpi, pad;
+};
+template <int NT>
+__global__ void __launch_bounds__(NT) tiny_project_kernel(const TinyBlock* __restrict__ blocks, int max_sweeps,
+                                                          int* __restrict__ npos) {
+  extern __shared__ __align__(16) double sm[];
+  const TinyBlock bk = blocks[blockIdx.x];
+  const int s = bk.n;
+  if (s <= 0) return;
+  const int sweeps = jacobi_smem_core<NT>(s, bk.A, bk.lda, sm, max_sweeps);
+  const int N = s + (s & 1), L = N + 1;
+  const double* M = sm;
+  const double* Q = sm + N * L;
+  __shared__ int cnt[2];
+  if (threadIdx.x < 2) cnt[threadIdx.x] = 0;
+  __syncthreads();
+  for (int k = threadIdx.x; k < s; k += NT) {
+    const double lk = M[k + k * L];
+    if (lk > 0.0) atomicAdd(&cnt[0], 1);
+    if (lk < 0.0) atomicAdd(&cnt[1], 1);
+  }
+  __syncthreads();
+  const bool pos_side = cnt[0] <= cnt[1];
+  for (int e = threadIdx.x; e < s * s; e += NT) {
+    const int i = e % s, j = e / s;
+    if (i > j) continue;
+    double acc = 0.0;
+    for (int k = 0; k < s; ++k) {
+      const double lk = M[k + k * L];
+      if (pos_side ? (lk > 0.0) : (lk < 0.0)) acc = fma(lk * Q[i + k * L], Q[j + k * L], acc);
+    }
+    const double v = pos_side ? acc : 0.5 * (bk.A[IDX(i, j, bk.lda)] + bk.A[IDX(j, i, bk.lda)]) - acc;
+    bk.Pi[IDX(i, j, bk.ldpi)] = v;
+    bk.Pi[IDX(j, i, bk.ldpi)] = v;
+  }
+  if (threadIdx.x == 0 && npos) npos[blockIdx.x] = sweeps < 0 ? -1 : cnt[0];
 }
 
 // Cooperative multi-CTA variant for s > JAC_SMEM_MAX: the matrix is double-buffered in

@@ -2107,6 +2107,54 @@ extern "C" int psdproj_project_host(psdproj_ctx c, const double* A_host, int lda
   return rc;
 }
 
+// ------------------------------------------------------------------ f4: many tiny cone blocks
+extern "C" int psdproj_project_tiny_batched(int count, const int* n, const double* const* A, const int* lda,
+                                            double* const* Pi, const int* ldpi, int* npos_host, void* stream) {
+  if (count < 0 || (count > 0 && (!n || !A || !lda || !Pi || !ldpi)))
+    return set_err(PSDPROJ_E_INVALID, "invalid tiny-batch arguments");
+  if (count == 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  int nmax = 0;
+  std::vector<TinyBlock> hb((size_t)count);
+  for (int i = 0; i < count; ++i) {
+    if (n[i] < 0 || n[i] > JAC_SMEM_MAX || (n[i] > 0 && (!A[i] || !Pi[i] || lda[i] < n[i] || ldpi[i] < n[i])))
+      return set_err(n[i] > JAC_SMEM_MAX ? PSDPROJ_E_CAPACITY : PSDPROJ_E_INVALID,
+                     "tiny block %d: n = %d (supported 0..%d)", i, n[i], JAC_SMEM_MAX);
+    hb[i] = TinyBlock{A[i], Pi[i], n[i], lda[i], ldpi[i], 0};
+    nmax = std::max(nmax, n[i]);
+  }
+  // per-thread device descriptor / count buffers, grown on demand (batched calls from threads)
+  static thread_local TinyBlock* dblk = nullptr;
+  static thread_local int* dnpos = nullptr;
+  static thread_local int cap = 0;
+  if (count > cap) {
+    if (dblk) cudaFree(dblk);
+    if (dnpos) cudaFree(dnpos);
+    cap = std::max(count, 2 * cap);
+    CK(cudaMalloc(&dblk, sizeof(TinyBlock) * cap));
+    CK(cudaMalloc(&dnpos, sizeof(int) * cap));
+  }
+  CK(cudaMemcpyAsync(dblk, hb.data(), sizeof(TinyBlock) * count, cudaMemcpyHostToDevice, st));
+  const int N = nmax + (nmax & 1);
+  const size_t smem = (size_t)2 * N * (N + 1) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(tiny_project_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    attr = true;
+  }
+  tiny_project_kernel<256><<<count, 256, smem, st>>>(dblk, 60, dnpos);
+  CKL();
+  if (npos_host) {
+    CK(cudaMemcpyAsync(npos_host, dnpos, sizeof(int) * count, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int i = 0; i < count; ++i)
+      if (npos_host[i] < 0) return set_err(PSDPROJ_E_DEGENERATE, "tiny block %d: Jacobi did not converge", i);
+  } else {
+    CK(cudaStreamSynchronize(st));  // the host descriptor array may be reused by the caller
+  }
+  return 0;
+}
+
 extern "C" int psdproj_project_batched(psdproj_ctx* ctxs, int count, const double* const* A, const int* lda,
                                        double* const* Pi, const int* ldpi, const double* tol, void* stream,
                                        psdproj_info* infos) {

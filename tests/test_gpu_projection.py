@@ -265,3 +265,45 @@ def test_odd_sizes_parity(api, n, p):
         assert info["status"] in (0, 1)
         assert err / np.linalg.norm(A) <= 1e-9, (call, err, info["side"], info["iters"])
         assert info["err_bound"] >= err - 1e-12 * np.linalg.norm(A)
+
+
+def test_tiny_batched_parity(api):
+    """f4: many tiny blocks in one launch (one CTA each, exact one-CTA Jacobi): every block equals
+    the oracle's exact projection, exactly symmetric, with the right positive count."""
+    rng = np.random.default_rng(31)
+    sizes = [1, 2, 3, 7, 16, 33, 64, 100, 112, 5, 8, 40]
+    mats, expect = [], []
+    for k, n in enumerate(sizes):
+        kind = k % 4
+        if kind == 0:
+            A = rng.standard_normal((n, n))
+            A = 0.5 * (A + A.T)
+        elif kind == 1:  # PSD (rank deficient)
+            M = rng.standard_normal((n, max(1, n // 3)))
+            A = M @ M.T
+        elif kind == 2:  # NSD
+            M = rng.standard_normal((n, n))
+            A = -(M @ M.T)
+        else:            # planted spectrum with a near-zero cluster
+            lam = np.concatenate([rng.uniform(-3, 3, n - n // 4), rng.uniform(-1e-10, 1e-10, n // 4)])
+            A = planted(haar_q(rng, n), lam)
+        mats.append(A)
+        expect.append(project_exact(A))
+    outs, npos = api.project_tiny_batched([_dev(A) for A in mats])
+    for A, P, E, c in zip(mats, outs, expect, npos):
+        Pg = P.cpu().numpy()
+        assert np.linalg.norm(Pg - E) <= 1e-12 * max(1.0, np.linalg.norm(A)), A.shape
+        assert np.array_equal(Pg, Pg.T)
+        assert c == int(np.sum(np.linalg.eigvalsh(A) > 0)) or abs(np.sort(np.abs(np.linalg.eigvalsh(A)))[0]) < 1e-9
+
+
+def test_tiny_batched_in_place_and_capacity(api):
+    rng = np.random.default_rng(32)
+    A = rng.standard_normal((20, 20))
+    A = 0.5 * (A + A.T)
+    E = project_exact(A)
+    d = _dev(A)
+    api.project_tiny_batched([d], outs=[d])  # Pi may alias A
+    assert np.linalg.norm(d.cpu().numpy() - E) <= 1e-12 * np.linalg.norm(A)
+    with pytest.raises(api.PsdprojError):
+        api.project_tiny_batched([_dev(np.eye(113))])
