@@ -1819,20 +1819,15 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
       TRY(regram(sU));
       rc = run.rr(sU, mU, mU, c->d_thU, std::min(mU + qe, sU));
     }
-    // R41: still rank deficient -> drop the direction at the failing pivot (greedy rank-revealing
-    // Cholesky; the oracle's Householder fallback drops the same near-dependent columns)
+    // R41: still rank deficient -> truncate the basis at the failing pivot: the leading columns
+    // (whose Cholesky factor is the leading block of the failed one) are kept, the direction at
+    // the pivot and those after it wait for the next iteration (one retry instead of one per
+    // dependent column; the oracle's Householder fallback drops near-dependent columns)
     while (rc > 0 && sU > mU) {
       const int col = rc - 1;  // failing column of the basis (index in S)
       if (col < mU || col >= sU) return set_err(PSDPROJ_E_DEGENERATE, "Cholesky-QR failed at pivot %d (s=%d)", rc, sU);
-      const int last = sU - 1;
-      if (col != last) {
-        swap_cols_kernel<<<grid1d((size_t)nl), 256, 0, st>>>(nl, c->S, ld, col, last);
-        CKL();
-        swap_cols_kernel<<<grid1d((size_t)nl), 256, 0, st>>>(nl, c->BS, ld, col, last);
-        CKL();
-      }
-      --sU;
-      info->dropped++;
+      info->dropped += sU - col;
+      sU = col;
       TRY(regram(sU));
       rc = run.rr(sU, mU, mU, c->d_thU, std::min(mU + qe, sU));
     }
