@@ -466,8 +466,25 @@ struct EighScratch {
   int mark(int ph) const { return mark_fn ? mark_fn(mark_obj, ph) : 0; }
 };
 
+// `steps` Newton-Schulz steps Y <- Y (3I - Y^T Y) / 2; w.dev records max|Y^T Y - I| before the last
+// one (the deviation after it is about 3/4 of its square).
+static int ns_run(cudaStream_t st, int s, int m, double* Yv, int ldy, const EighScratch& w, double* part,
+                  size_t part_elems, int steps) {
+  for (int it = 0; it < steps; ++it) {
+    TRY(dgemm(st, OP_T, OP_N, m, m, s, 1.0, Yv, ldy, Yv, ldy, 0.0, w.nsM, m, part, part_elems));
+    const bool lastst = it == steps - 1;
+    if (lastst) CK(cudaMemsetAsync(w.dev, 0, sizeof(unsigned long long), st));
+    ns_coeff_kernel<<<grid1d((size_t)m * m), 256, 0, st>>>(m, w.nsM, m, w.nsZ, m, lastst ? w.dev : w.dev + 1);
+    CKL();
+    TRY(dgemm(st, OP_N, OP_N, s, m, m, 1.0, Yv, ldy, w.nsZ, m, 0.0, w.nsY, w.ldv, part, part_elems));
+    CK(cudaMemcpy2DAsync(Yv, (size_t)ldy * 8, w.nsY, (size_t)w.ldv * 8, (size_t)s * 8, m, cudaMemcpyDeviceToDevice,
+                         st));
+  }
+  return 0;
+}
+
 static int eigh_top(cudaStream_t st, int s, const double* Hs, int ldh, int m, double* lam, double* Yv, int ldy,
-                    int* npos, const EighScratch& w, double* part, size_t part_elems, bool mgs) {
+                    int* npos, const EighScratch& w, double* part, size_t part_elems, bool mgs, int ns_steps = 2) {
   TRY(cla_attrs());
   static bool attr = false;
   if (!attr) {
@@ -711,17 +728,7 @@ static int eigh_top(cudaStream_t st, int s, const double* Hs, int ldh, int m, do
   }
   TRY(w.mark(11));
   if (!mgs) {
-    // two Newton-Schulz steps; dev records max|Y^T Y - I| before the second step
-    for (int it = 0; it < 2; ++it) {
-      TRY(dgemm(st, OP_T, OP_N, m, m, s, 1.0, Yv, ldy, Yv, ldy, 0.0, w.nsM, m, part, part_elems));
-      if (it == 1) CK(cudaMemsetAsync(w.dev, 0, sizeof(unsigned long long), st));
-      ns_coeff_kernel<<<grid1d((size_t)m * m), 256, 0, st>>>(m, w.nsM, m, w.nsZ, m,
-                                                              it == 1 ? w.dev : w.dev + 1);
-      CKL();
-      TRY(dgemm(st, OP_N, OP_N, s, m, m, 1.0, Yv, ldy, w.nsZ, m, 0.0, w.nsY, w.ldv, part, part_elems));
-      CK(cudaMemcpy2DAsync(Yv, (size_t)ldy * 8, w.nsY, (size_t)w.ldv * 8, (size_t)s * 8, m, cudaMemcpyDeviceToDevice,
-                           st));
-    }
+    TRY(ns_run(st, s, m, Yv, ldy, w, part, part_elems, ns_steps));
   }
   return 0;
 }
@@ -1190,8 +1197,9 @@ struct Run {
     w.mark_fn = [](void* o, int ph) { return static_cast<Run*>(o)->mark(ph); };
     return w;
   }
-  int tri_eig(int s, const double* Hs, int ldh, int m, double* lam, double* Yv, int ldy, int* npos, bool mgs) {
-    return eigh_top(st, s, Hs, ldh, m, lam, Yv, ldy, npos, eig_scratch(), c->part, c->part_elems, mgs);
+  int tri_eig(int s, const double* Hs, int ldh, int m, double* lam, double* Yv, int ldy, int* npos, bool mgs,
+              int ns_steps = 2) {
+    return eigh_top(st, s, Hs, ldh, m, lam, Yv, ldy, npos, eig_scratch(), c->part, c->part_elems, mgs, ns_steps);
   }
   // Rayleigh-Ritz on the pencil (H, G) in c->G / c->Hm (s x s, ld s_max):
   // returns 0 (ok), >0 (Cholesky failed at that pivot), <0 error. Outputs Cp (s x mU), theta desc in h_d[0..s).
@@ -1275,7 +1283,7 @@ struct Run {
       gather_cols_kernel<<<grid1d((size_t)s * mU), 256, 0, st>>>(s, mU, c->Y, ldm, c->Vj, ldm, c->d_order);
       CKL();
     } else {
-      TRY(tri_eig(s, c->Hh, ldm, mU, c->d_ths, c->Y, ldm, c->tnpos, false));
+      TRY(tri_eig(s, c->Hh, ldm, mU, c->d_ths, c->Y, ldm, c->tnpos, false, 1));
       CK(cudaMemsetAsync(c->d_status + 4, 0, sizeof(int), st));
       set_int_kernel<<<1, 1, 0, st>>>(c->d_status + 4, 1);
       CKL();
@@ -1291,7 +1299,15 @@ struct Run {
     int sweeps = c->h_i[c->h_i_len - 16 + 4];
     rr_npos = c->h_i[c->h_i_len - 24];
     if (chol) return chol + kx;
-    if (!use_jacobi && !(c->h_d[c->h_d_len - 16] <= 1e-7)) {
+    // one Newton-Schulz step ran (the deviation before it is ~1e-15 for separated Ritz values); a
+    // deviation above 1e-4 gets a second step, one still above 1e-4 the robust path
+    if (!use_jacobi && !(c->h_d[c->h_d_len - 16] <= 1e-4) && c->h_d[c->h_d_len - 16] < 0.5) {
+      TRY(ns_run(st, s, mU, c->Y, ldm, eig_scratch(), c->part, c->part_elems, 1));
+      TRY(li_t_apply(s, kx, mU));
+      CK(cudaMemcpyAsync(c->h_d + c->h_d_len - 16, c->d_scal + 16, sizeof(double), cudaMemcpyDeviceToHost, st));
+      TRY(sync());
+    }
+    if (!use_jacobi && !(c->h_d[c->h_d_len - 16] <= 1e-4)) {
       // Newton-Schulz could not restore orthonormality (near-multiple eigenvalues): robust path
       TRY(tri_eig(s, c->Hh, ldm, mU, c->d_ths, c->Y, ldm, c->tnpos, true));
       TRY(li_t_apply(s, kx, mU));
