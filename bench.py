@@ -171,7 +171,7 @@ PHASES = ["a3_block_multiply", "w_p_projection", "gram_pencil", "cholesky_pencil
 
 def dominant_phase(infos, K, ms_step):
     """The phase that dominates a step (library profile bit 1, CUDA events on the launching stream).
-    At n = 4000 it is the Rayleigh-Ritz tridiagonalisation: latency-bound (three one-way DSMEM
+    At n = 4000 it is the Rayleigh-Ritz tridiagonalisation: latency-bound (two one-way DSMEM
     pushes per Householder step), so its roof is the push-hop floor measured by
     tools/micro/push_bench2.cu (profiles/push_bench_r01.txt), not HBM or FP64."""
     tot = [sum(i["phase_ms"][k] for i in infos) / K for k in range(len(PHASES))]
@@ -179,9 +179,10 @@ def dominant_phase(infos, K, ms_step):
     out = {"phase": PHASES[k], "ms_per_step": round(tot[k], 3), "share": round(tot[k] / ms_step, 4)}
     if PHASES[k] == "rr_tridiagonal":
         out.update({"bound": "latency", "kernel": "tridiag_reg_kernel (16-CTA cluster, registers, st.async pushes)",
-                    "floor_note": "per Householder step >= 3 st.async hops (~0.9k cycles each, push_bench2) + the "
-                                  "owner's Householder scalars = ~3.5k cycles; measured ~4.2k (s = 200) to ~5.8k "
-                                  "(s = 400) cycles/step (PSDPROJ_TRI_PROF)"})
+                    "floor_note": "per Householder step >= 2 DSMEM hops (bulk-copy broadcast of v_j, st.async "
+                                  "all-gather of p_j; ~0.9-1.2k cycles each, push_bench*) + the owner's Householder "
+                                  "update and scalars = ~3k cycles; measured ~4.2k (s = 200) to ~5.5k (s = 400) "
+                                  "cycles/step (PSDPROJ_TRI_PROF; profiles/ncu_r01/tridiag_reg_r01.json)"})
     return out
 
 
