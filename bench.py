@@ -178,7 +178,7 @@ def dominant_phase(infos, K, ms_step):
     k = max(range(len(PHASES)), key=lambda j: tot[j])
     out = {"phase": PHASES[k], "ms_per_step": round(tot[k], 3), "share": round(tot[k] / ms_step, 4)}
     if PHASES[k] == "rr_tridiagonal":
-        out.update({"bound": "latency", "kernel": "tridiag_reg_kernel (16-CTA cluster, registers, st.async pushes)",
+        out.update({"bound": "latency", "kernel": "tridiag_reg_kernel (16-CTA cluster, matrix in registers, DSMEM bulk-copy + st.async pushes)",
                     "floor_note": "per Householder step >= 2 DSMEM hops (bulk-copy broadcast of v_j, st.async "
                                   "all-gather of p_j; ~0.9-1.2k cycles each, push_bench*) + the owner's Householder "
                                   "update and scalars = ~3k cycles; measured ~4.2k (s = 200) to ~5.5k (s = 400) "
@@ -459,7 +459,7 @@ def main():
         achieved = amul_flops / (amul_ms / 1e3) / 1e12 if amul_ms > 0 else 0.0
         roof = {"bound": "tensor", "achieved": achieved, "peak": p64, "unit": "TFLOP/s",
                 "frac": achieved / p64, "traffic": traffic,
-                "kernel": "a3 block multiply B.Z (dgemm_kernel DMMA.8x8x4 [+ split-K reduce])",
+                "kernel": "a3 block multiply B.Z (dgemm_kp_kernel, mma.sync m8n8k4 f64 = SASS DMMA.8x8x4 [+ split-K reduce])",
                 "per_launch": {"mean_cols": cols, "flops": amul_flops / max(1, amul_launch),
                                "ms": amul_ms / max(1, amul_launch)},
                 "peak_source": "measured cuBLAS DGEMM 8192^3 (profiles/peaks_fp64_r01.json)"}
