@@ -254,11 +254,21 @@ __device__ __forceinline__ void load_tile_kp(double* sm, const double* __restric
 }
 
 // TAG only separates the a3 block multiply B.Z (TAG = 1) from the other GEMMs in profiles.
+// Two problems sharing op(B), M, N, K and the leading dimensions (A2 != nullptr): blockIdx.z =
+// problem * splits + split, problem 1 reads A2 and writes C2 (one launch for X = S C' and
+// BX = BS C' of the rotation).
 template <int OPA, int OPB, int BM, int BN, int STAGES, int TAG = 0>
 __global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32, (BM * BN >= 8192) ? 2 : 3)
     dgemm_kp_kernel(int M, int N, int K, double alpha, const double* __restrict__ A, int lda,
                     const double* __restrict__ B, int ldb, double beta, double* __restrict__ C, int ldc,
-                    double* __restrict__ partial, int ktiles_per_split) {
+                    double* __restrict__ partial, int ktiles_per_split, const double* __restrict__ A2,
+                    double* __restrict__ C2, int splits) {
+  if (A2 && (int)blockIdx.z >= splits) {  // problem 1
+    A = A2;
+    C = C2;
+    if (partial) partial += (size_t)splits * M * N;
+  }
+  const int zsplit = A2 ? (int)blockIdx.z % splits : (int)blockIdx.z;
   constexpr int WM = 32, WN = 32, BK = 16;
   constexpr int WARPS_M = BM / WM, THREADS = (BM / WM) * (BN / WN) * 32;
   constexpr int MI = WM / 8, NI = WN / 8;
@@ -269,7 +279,7 @@ __global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32, (BM * BN >= 8192) 
   const int wm = warp % WARPS_M, wn = warp / WARPS_M;
   const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
   const int KT = cdiv(K, BK);
-  const int kt0 = blockIdx.z * ktiles_per_split;
+  const int kt0 = zsplit * ktiles_per_split;
   const int nkt = max(0, min(KT, kt0 + ktiles_per_split) - kt0);
   double acc[MI][NI][2];
 #pragma unroll
@@ -329,7 +339,7 @@ __global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32, (BM * BN >= 8192) 
         if (col >= N) continue;
         const double v = acc[i][j][h];
         if (partial) {
-          partial[(size_t)blockIdx.z * M * N + IDX(row, col, M)] = v;
+          partial[(size_t)zsplit * M * N + IDX(row, col, M)] = v;
         } else {
           double* c = C + IDX(row, col, ldc);
           *c = (beta == 0.0) ? alpha * v : alpha * v + beta * (*c);

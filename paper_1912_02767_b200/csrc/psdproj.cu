@@ -147,7 +147,8 @@ int gemm_launch(cudaStream_t st, int M, int N, int K, double alpha, const double
 
 template <int OA, int OB, int BM, int BN, int ST, int TAG = 0>
 static int gemm_kp_launch(cudaStream_t st, int M, int N, int K, double alpha, const double* A, int lda,
-                          const double* B, int ldb, double beta, double* C, int ldc, double* part, size_t part_elems) {
+                          const double* B, int ldb, double beta, double* C, int ldc, double* part, size_t part_elems,
+                          const double* A2 = nullptr, double* C2 = nullptr) {
   constexpr int THREADS = (BM / 32) * (BN / 32) * 32;
   constexpr size_t SMEM = (size_t)ST * 8 * ((2 * BM + 4) + (2 * BN + 4)) * sizeof(double);
   auto kern = dgemm_kp_kernel<OA, OB, BM, BN, ST, TAG>;
@@ -160,24 +161,51 @@ static int gemm_kp_launch(cudaStream_t st, int M, int N, int K, double alpha, co
     attr = true;
   }
   const int KT = cdiv(std::max(K, 1), 16);
-  const int tiles = cdiv(M, BM) * cdiv(N, BN);
+  const int nprob = A2 ? 2 : 1;
+  const int tiles = cdiv(M, BM) * cdiv(N, BN) * nprob;
   const int slots = sms() * per_sm;
   int splits = 1;
   if (part && tiles < slots && KT >= 8) {
     splits = std::min(std::max(1, slots / tiles), KT / 4);
     splits = std::max(1, std::min(splits, 32));
-    while (splits > 1 && (size_t)splits * M * N > part_elems) --splits;
+    while (splits > 1 && (size_t)splits * nprob * M * N > part_elems) --splits;
   }
   const int ktps = cdiv(KT, splits);
   splits = cdiv(KT, ktps);
-  dim3 grid(cdiv(M, BM), cdiv(N, BN), splits);
-  kern<<<grid, THREADS, SMEM, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits > 1 ? part : nullptr, ktps);
+  dim3 grid(cdiv(M, BM), cdiv(N, BN), splits * nprob);
+  kern<<<grid, THREADS, SMEM, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits > 1 ? part : nullptr, ktps, A2,
+                                    C2, splits);
   CKL();
   if (splits > 1) {
     splitk_reduce_kernel<<<dim3(cdiv(M, 256), N), 256, 0, st>>>(M, N, splits, alpha, part, beta, C, ldc);
     CKL();
+    if (A2) {
+      splitk_reduce_kernel<<<dim3(cdiv(M, 256), N), 256, 0, st>>>(M, N, splits, alpha, part + (size_t)splits * M * N,
+                                                                   beta, C2, ldc);
+      CKL();
+    }
   }
   return 0;
+}
+
+// Two products C = alpha A B + beta C and C2 = alpha A2 B + beta C2 (same B, shapes and leading
+// dimensions) in one launch (k-paired kernel, 64 x 64 or 64 x 32 tiles).
+static int dgemm2(cudaStream_t st, int M, int N, int K, double alpha, const double* A, const double* A2, int lda,
+                  const double* B, int ldb, double beta, double* C, double* C2, int ldc, double* part,
+                  size_t part_elems) {
+  if (M <= 0 || N <= 0) return 0;
+  if (K <= 0) {
+    if (beta == 0.0) {
+      CK(cudaMemset2DAsync(C, (size_t)ldc * 8, 0, (size_t)M * 8, N, st));
+      CK(cudaMemset2DAsync(C2, (size_t)ldc * 8, 0, (size_t)M * 8, N, st));
+    }
+    return 0;
+  }
+  const bool narrow = N <= 96 && (N % 64) != 0 && (N % 64) <= 32;
+  return narrow ? gemm_kp_launch<OP_N, OP_N, 64, 32, 4>(st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, part,
+                                                         part_elems, A2, C2)
+                : gemm_kp_launch<OP_N, OP_N, 64, 64, 4>(st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, part,
+                                                         part_elems, A2, C2);
 }
 
 static int dgemm(cudaStream_t st, int opA, int opB, int M, int N, int K, double alpha, const double* A, int lda,
@@ -1854,10 +1882,11 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
     const int rr_npos = run.rr_npos;
     // ---- rotation (a8): X <- S C', BX <- BS C', P <- S_[R P] C'_[R P], BP likewise
     TRY(run.mark(5));
-    TRY(run.gemm(OP_N, OP_N, nl, mUn, sU, 1.0, c->S, ld, c->Cp, ldm, 0.0, c->S2, ld));
-    TRY(run.gemm(OP_N, OP_N, nl, mUn, sU, 1.0, c->BS, ld, c->Cp, ldm, 0.0, c->BS2, ld));
-    TRY(run.gemm(OP_N, OP_N, nl, mUn, sU - mU, 1.0, c->S + (size_t)mU * ld, ld, c->Cp + mU, ldm, 0.0, c->Pb, ld));
-    TRY(run.gemm(OP_N, OP_N, nl, mUn, sU - mU, 1.0, c->BS + (size_t)mU * ld, ld, c->Cp + mU, ldm, 0.0, c->BPb, ld));
+    // X and BX (S C', BS C') in one launch, P and BP likewise
+    TRY(dgemm2(st, nl, mUn, sU, 1.0, c->S, c->BS, ld, c->Cp, ldm, 0.0, c->S2, c->BS2, ld, c->part, c->part_elems));
+    TRY(dgemm2(st, nl, mUn, sU - mU, 1.0, c->S + (size_t)mU * ld, c->BS + (size_t)mU * ld, ld, c->Cp + mU, ldm, 0.0,
+               c->Pb, c->BPb, ld, c->part, c->part_elems));
+    info->flops += 8.0 * nl * (double)mUn * sU;
     std::swap(c->S, c->S2);
     std::swap(c->BS, c->BS2);
     if (getenv("PSDPROJ_TRACE")) {  // debugging: orthonormality of the new block
