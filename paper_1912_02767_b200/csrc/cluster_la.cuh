@@ -944,6 +944,17 @@ __global__ void __launch_bounds__(256, 1) tridiag_reg_kernel(int s, const double
         for (int c = 0; c < CR; ++c) acc[c] = fma(a[k][c], rj[k], acc[c]);
       }
     }
+    if constexpr (CRP > CR) {
+      // the thread's part of p.v_j / tau_j rides in the reduction's spare slot CR (no separate
+      // warp reduction before the push)
+      double q = 0.0;
+#pragma unroll
+      for (int c = 0; c < CR; ++c) {
+        const int g = (int)rank + CS * (cg + TCG * c);
+        if (g > j && g < s) q = fma(acc[c], vj[g], q);
+      }
+      acc[CR] = q;
+    }
     double* wr = wred + par * 256;
     {
       const double w = tri_xreduce<CRP>(acc, lane);
@@ -960,10 +971,17 @@ __global__ void __launch_bounds__(256, 1) tridiag_reg_kernel(int s, const double
       if (act) {
         const int cgl = lc % TCG, c = lc / TCG;
         pg = tj * (wr[(2 * cgl) * 32 + c] + wr[(2 * cgl + 1) * 32 + c]);
-        part = pg * vj[g];
       }
+      if constexpr (CRP > CR) {
+        double q = 0.0;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        for (int w = 0; w < 8; ++w) q += wr[w * 32 + CR];  // fixed order: identical in every warp
+        part = tj * q;
+      } else {
+        if (act) part = pg * vj[g];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      }
       const uint32_t b0 = cla_smem_u32(&pbar[par]);
       const uint32_t p0 = cla_smem_u32(ploc + (size_t)par * sr + g);
       const uint32_t w0 = cla_smem_u32(wpart + par * 32 + rank);
