@@ -16,6 +16,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -118,6 +119,11 @@ static inline int grid1d(size_t work, int nt = 256) {
   size_t cap = (size_t)sms() * 8;
   return (int)std::max<size_t>(1, std::min(b, cap));
 }
+
+// host-side profile of psdproj_project (PSDPROJ_HOSTPROF=1): time blocked in stream syncs
+static const bool g_hostprof = getenv("PSDPROJ_HOSTPROF") != nullptr;
+static thread_local double g_sync_s = 0.0;
+static thread_local long g_nsync = 0;
 
 // ------------------------------------------------------------------ GEMM dispatch
 namespace {
@@ -1092,6 +1098,14 @@ struct Run {
     return 0;
   }
   int sync() {
+    if (g_hostprof) {
+      const auto t0 = std::chrono::steady_clock::now();
+      CK(cudaStreamSynchronize(st));
+      g_sync_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      g_nsync++;
+      ihost = 0;
+      return 0;
+    }
     CK(cudaStreamSynchronize(st));
     ihost = 0;
     return 0;
@@ -2124,7 +2138,17 @@ extern "C" int psdproj_project(psdproj_ctx c, const double* A, int lda, double* 
     return info->status = set_err(PSDPROJ_E_INVALID, "invalid arguments (lda=%d ldpi=%d tol=%g)", lda, ldpi, tol);
   if ((const void*)Pi == (const void*)A && lda != ldpi)
     return info->status = set_err(PSDPROJ_E_INVALID, "aliased Pi needs ldpi == lda");
+  const auto t0 = std::chrono::steady_clock::now();
+  const double s0 = g_sync_s;
+  const long n0 = g_nsync;
   int rc = project_impl(c, A, lda, Pi, ldpi, tol, (cudaStream_t)stream, info);
+  if (g_hostprof) {
+    // host-side time split of the call: blocked in stream syncs vs issuing work
+    const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    std::fprintf(stderr, "[psdproj hostprof] wall %.1f ms, in syncs %.1f ms (%ld), issuing %.1f ms, iters %d, launches %ld\n",
+                 1e3 * wall, 1e3 * (g_sync_s - s0), g_nsync - n0, 1e3 * (wall - (g_sync_s - s0)), info->iters,
+                 (long)info->launches);
+  }
   if (rc == PSDPROJ_E_CUDA) c->poisoned = true;
   info->status = rc;
   return rc;
