@@ -18,6 +18,7 @@ on this box's host cores; rank 0 only.
 import argparse
 import json
 import os
+import math
 import statistics
 import subprocess
 import sys
@@ -419,15 +420,21 @@ def main():
     infos = []
     torch.cuda.synchronize()
     barrier(dist)
+    # per-call boundaries (events on the call's stream; no host sync inside the timed region)
+    evk = [torch.cuda.Event(enable_timing=True) for _ in range(K - 1)]
     ev0.record(st)
-    for k in range(1 + W, total):
+    for j, k in enumerate(range(1 + W, total)):
         _, inf = ctx.project(mats[k], tol, out=out)
         infos.append(inf)
+        if j < K - 1:
+            evk[j].record(st)
     ev1.record(st)
     torch.cuda.synchronize()
     barrier(dist)
     ck = clocks.stop()
     ms_local = ev0.elapsed_time(ev1)
+    bounds = [ev0] + evk + [ev1]
+    call_ms = sorted(bounds[j].elapsed_time(bounds[j + 1]) for j in range(K))
     ms = max_over_ranks(dist, ms_local)
     projections = sum_over_ranks(dist, float(K))
     value = projections / (ms / 1e3)
@@ -517,6 +524,8 @@ def main():
             "roofline": roof,
             "step_roofline": {"frac": step_frac, "t_roof_ms": t_roof * 1e3 / K, "flops": flops / K,
                               "bytes": byts / K, "definition": "max(bytes/HBM, flops/P64) / step time"},
+            "per_call_ms": {"median": round(statistics.median(call_ms), 3),
+                            "p90": round(call_ms[min(K - 1, int(math.ceil(0.9 * K)) - 1)], 3)},
             "phase_ms_per_step": {nm: round(sum(i["phase_ms"][k] for i in infos) / K, 3) for k, nm in enumerate(
                 ["a3_block_multiply", "w_p_projection", "gram_pencil", "cholesky_pencil", "rr_tridiagonal",
                  "rotation", "residual_norms", "host_locking_assembly", "rr_bisection", "rr_inverse_iteration",

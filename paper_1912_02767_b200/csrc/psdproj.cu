@@ -527,6 +527,7 @@ static int eigh_top(cudaStream_t st, int s, const double* Hs, int ldh, int m, do
     CK(cudaFuncSetAttribute(tri_inviter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     CK(cudaFuncSetAttribute(tri_twisted_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     CK(cudaFuncSetAttribute(tri_bisect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    CK(cudaFuncSetAttribute(tri_bisect_ms_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     attr = true;
   }
   if (s > EIG_MAX) return set_err(PSDPROJ_E_CAPACITY, "eigensolver supports s <= %d", EIG_MAX);
@@ -699,8 +700,16 @@ static int eigh_top(cudaStream_t st, int s, const double* Hs, int ldh, int m, do
   }
   tri_prep_kernel<<<1, 1024, 0, st>>>(s, w.td, w.te, w.te2, w.tbounds);
   CKL();
-  tri_bisect_kernel<<<cdiv(m + 1, 2), 64, (size_t)2 * s * sizeof(double), st>>>(s, m, w.td, w.te2, w.tbounds, lam, npos);
-  CKL();
+  {
+    // multisection points per eigenvalue (PSDPROJ_BISECT_G, multiple of 32; 32 = one warp each)
+    static const int bg = getenv("PSDPROJ_BISECT_G") ? std::max(32, std::min(1024, atoi(getenv("PSDPROJ_BISECT_G")) / 32 * 32)) : 256;
+    if (bg == 32)
+      tri_bisect_kernel<<<cdiv(m + 1, 2), 64, (size_t)2 * s * sizeof(double), st>>>(s, m, w.td, w.te2, w.tbounds, lam,
+                                                                                    npos);
+    else
+      tri_bisect_ms_kernel<<<m + 1, bg, (size_t)2 * s * sizeof(double), st>>>(s, m, w.td, w.te2, w.tbounds, lam, npos);
+    CKL();
+  }
   if (m <= 0) return 0;  // (wy is false for m <= 0: no side-stream work in flight)
   TRY(w.mark(9));
   // inverse iteration: vectors per CTA so that the per-thread arrays fit in shared memory

@@ -286,7 +286,73 @@ __global__ void tri_bisect_kernel(int s, int m, const double* __restrict__ dg, c
     lo = nlo;
     hi = nhi;
   }
-  if (lane == 0) out[ks] = 0.5 * (lo + hi);
+  // a final bracket around 0 cannot tell the sign: report the eigenvalue as 0 (non-positive, as the
+  // Sturm count at 0 does)
+  if (lane == 0) out[ks] = (lo <= 0.0 && hi >= 0.0) ? 0.0 : 0.5 * (lo + hi);
+}
+
+// Multisection with G = blockDim.x (a multiple of 32, <= 1024) points per round: one CTA per wanted
+// eigenvalue (ks = blockIdx.x < m, ks-th largest), the CTA's G threads evaluate the Sturm count at
+// the G interior points of a (G + 1)-section of [lo, hi]; block m computes npos. Each round narrows
+// the bracket by G + 1 (log2(G + 1) bits) for one Sturm chain of latency: a 128-point round gains 7
+// bits where one warp gains 5, and the threads are free (m is ~100 CTAs on 148 SMs).
+// The per-warp "count <= k" ballots go through shared memory (double-buffered by round parity: one
+// barrier per round); every thread derives the same new bracket.
+__global__ void tri_bisect_ms_kernel(int s, int m, const double* __restrict__ dg, const double* __restrict__ e2g,
+                                     const double* __restrict__ bounds, double* __restrict__ out,
+                                     int* __restrict__ npos) {
+  extern __shared__ __align__(16) double bsm[];
+  __shared__ unsigned masks[2][32];
+  double* d = bsm;
+  double* e2 = bsm + s;
+  const double span = fmax(fmax(fabs(bounds[0]), fabs(bounds[1])), 1e-300);
+  const int sex = (int)((__double_as_longlong(span) >> 52) & 0x7ff) - 1022;  // span < 2^sex
+  const double inv = ldexp(1.0, -sex);
+  for (int k = threadIdx.x; k < s; k += blockDim.x) {
+    d[k] = dg[k] * inv;
+    if (k + 1 < s) e2[k] = (e2g[k] * inv) * inv;
+  }
+  __syncthreads();
+  const int ks = blockIdx.x;
+  if (ks >= m) {
+    if (threadIdx.x == 0) *npos = s - sturm_count_det(s, d, e2, 0.0);
+    return;
+  }
+  const int G = blockDim.x, nw = G >> 5, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int k = s - 1 - ks;  // ascending index: count(lo) <= k < count(hi)
+  double lo = bounds[0], hi = bounds[1];
+  const double pivmin = bounds[2];
+  const double atol = 4.0 * PSD_U * fmax(fabs(lo), fabs(hi));
+  const double rg = 1.0 / (double)(G + 1);
+  for (int it = 0; it < 64; ++it) {
+    const double w = hi - lo;
+    if (w <= fmax(2.0 * PSD_U * fmax(fabs(lo), fabs(hi)), atol) + 4.0 * pivmin) break;
+    const double x = lo + w * (double)(t + 1) * rg;
+    const int c = sturm_count_det(s, d, e2, x * inv);
+    const unsigned below = __ballot_sync(0xffffffffu, c <= k);
+    if (lane == 0) masks[it & 1][warp] = below;
+    __syncthreads();
+    // first point (in order) with count > k bounds the target from above
+    int first_above = -1;
+    for (int q = 0; q < nw; ++q) {
+      const unsigned b = masks[it & 1][q];
+      if (b != 0xffffffffu) {
+        first_above = q * 32 + __ffs(~b) - 1;
+        break;
+      }
+    }
+    double nlo = lo, nhi = hi;
+    if (first_above < 0) {
+      nlo = lo + w * (double)G * rg;
+    } else {
+      nhi = lo + w * (double)(first_above + 1) * rg;
+      if (first_above > 0) nlo = lo + w * (double)first_above * rg;
+    }
+    if (nlo == lo && nhi == hi) break;
+    lo = nlo;
+    hi = nhi;
+  }
+  if (t == 0) out[ks] = (lo <= 0.0 && hi >= 0.0) ? 0.0 : 0.5 * (lo + hi);  // as tri_bisect_kernel
 }
 
 // Inverse iteration (GvL §8.4.2): one thread per eigenvector i < m (eigenvalue lam[i]):
