@@ -1332,6 +1332,107 @@ __global__ void __launch_bounds__(32 * CPB) backtransform_wy_kernel(int s, int m
   }
 }
 
+// One column per 256-thread CTA (m ~ 100 CTAs on 148 SMs): the rows of the column are split over
+// the CTA (thread t owns rows t + 256 q, q < PLW), so per panel every warp does PLW x 16 FMAs for
+// the dot products and as many for the update instead of a whole column's worth (the one-warp-per-
+// column kernel above is bound by its own instruction stream: ~3 cycles per issued instruction).
+// Per panel: lane partials of w = V^T y, a transposed warp reduction, the 8 warp sums added in
+// fixed order while z = T w is formed by 256 threads (one product T(r, b) w_b each, reduced over
+// the 16 lanes of b), then y -= V z.
+__host__ __device__ inline size_t bt_col_smem_doubles(int s) {
+  return (size_t)2 * WY_PB * ((s + 2) & ~1) + 2 * WY_PB * WY_PB + 8 * WY_PB + WY_PB;
+}
+template <int PLW>
+__global__ void __launch_bounds__(256) backtransform_wy_col_kernel(int s, int m, const double* __restrict__ Vh,
+                                                                   int ldv, const double* __restrict__ Tb,
+                                                                   double* __restrict__ y, int ldy) {
+  extern __shared__ __align__(16) double pv[];
+  const int LDP = (s + 2) & ~1;                // panel column pitch: row s exists and is zero-filled
+  double* Ts = pv + (size_t)2 * WY_PB * LDP;   // 2 x WY_PB x WY_PB
+  double* wp = Ts + 2 * WY_PB * WY_PB;         // 8 warps x WY_PB partial dot products
+  double* zs = wp + 8 * WY_PB;                 // z = T w
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  double* yc = y + (size_t)blockIdx.x * ldy;
+  double r[PLW];
+  int kk[PLW];  // panel row of y row k; rows >= s read the zero row s (their r stays 0)
+#pragma unroll
+  for (int q = 0; q < PLW; ++q) {
+    const int k = t + 256 * q;
+    r[q] = k < s ? yc[k] : 0.0;
+    kk[q] = min(k, s);
+  }
+  const int nref = s - 2;
+  const int npan = cdiv(max(nref, 0), WY_PB);
+  auto issue = [&](int pnl, int buf) {
+    const int lo = pnl * WY_PB, kb = min(WY_PB, nref - lo);
+    double* dst = pv + (size_t)buf * WY_PB * LDP;
+    for (int e = t; e < WY_PB * (LDP / 2); e += 256) {
+      const int c = e / (LDP / 2), i = 2 * (e - c * (LDP / 2)), j = lo + c;
+      const bool ok0 = c < kb && i > j && i < s, ok1 = c < kb && i + 1 > j && i + 1 < s;
+      const double* src = Vh + IDX(i, (c < kb ? j : 0), ldv);
+      double* d0 = dst + (size_t)c * LDP + i;
+      if (ok0 == ok1 && (!ok0 || ((reinterpret_cast<uintptr_t>(src) & 15) == 0))) {
+        cp_async_16(d0, ok0 ? src : Vh, ok0 ? 16 : 0);
+      } else {
+        cp_async_8(d0, ok0 ? src : Vh, ok0 ? 8 : 0);
+        cp_async_8(d0 + 1, ok1 ? src + 1 : Vh, ok1 ? 8 : 0);
+      }
+    }
+    for (int e = t; e < WY_PB * WY_PB; e += 256)
+      cp_async_8(Ts + (size_t)buf * WY_PB * WY_PB + e, Tb + (size_t)pnl * WY_PB * WY_PB + e, 8);
+    cp_async_commit();
+  };
+  if (npan > 0) issue(npan - 1, (npan - 1) & 1);
+  for (int pnl = npan - 1; pnl >= 0; --pnl) {
+    const int buf = pnl & 1;
+    if (pnl > 0) {
+      issue(pnl - 1, buf ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double* V = pv + (size_t)buf * WY_PB * LDP;
+    const double* T = Ts + (size_t)buf * WY_PB * WY_PB;
+    {
+      double a[WY_PB];
+#pragma unroll
+      for (int c = 0; c < WY_PB; ++c) a[c] = 0.0;
+#pragma unroll
+      for (int q = 0; q < PLW; ++q) {
+#pragma unroll
+        for (int c = 0; c < WY_PB; ++c) a[c] = fma(V[(size_t)c * LDP + kk[q]], r[q], a[c]);
+      }
+      const double wl = tri_xreduce<WY_PB>(a, lane);
+      if ((lane & 1) == 0) wp[warp * WY_PB + tri_xreduce_col<WY_PB>(lane)] = wl;
+    }
+    __syncthreads();
+    {
+      const int rr = t >> 4, b = t & 15;
+      double wb = 0.0;
+#pragma unroll
+      for (int wi = 0; wi < 8; ++wi) wb += wp[wi * WY_PB + b];
+      double pr = (b >= rr) ? T[rr + b * WY_PB] * wb : 0.0;
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) pr += __shfl_xor_sync(0xffffffffu, pr, o);
+      if (b == 0) zs[rr] = pr;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < WY_PB; ++c) {
+      const double zc = zs[c];
+#pragma unroll
+      for (int q = 0; q < PLW; ++q) r[q] = fma(-V[(size_t)c * LDP + kk[q]], zc, r[q]);
+    }
+    __syncthreads();  // buffer `buf` is refilled by the next issue
+  }
+#pragma unroll
+  for (int q = 0; q < PLW; ++q) {
+    const int k = t + 256 * q;
+    if (k < s) yc[k] = r[q];
+  }
+}
+
 // Newton-Schulz step towards the polar factor: Z = 1.5 I - 0.5 M for M = Y^T Y (m x m), and
 // dev = max |M - I| accumulated into *dev (as a non-negative double's bit pattern, atomicMax).
 __global__ void ns_coeff_kernel(int m, const double* __restrict__ M, int ldm, double* __restrict__ Z, int ldz,

@@ -400,6 +400,9 @@ static int cla_attrs() {
   CK(cudaFuncSetAttribute(backtransform_wy_kernel<8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, bmx));
   CK(cudaFuncSetAttribute(backtransform_wy_kernel<16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, bmx));
   CK(cudaFuncSetAttribute(backtransform_wy_kernel<20, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, bmx));
+  CK(cudaFuncSetAttribute(backtransform_wy_col_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, bmx));
+  CK(cudaFuncSetAttribute(backtransform_wy_col_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bmx));
+  CK(cudaFuncSetAttribute(backtransform_wy_col_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, bmx));
   CK(cudaFuncSetAttribute(backtransform_panel_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, bmx));
   CK(cudaFuncSetAttribute(backtransform_panel_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, bmx));
   CK(cudaFuncSetAttribute(backtransform_panel_kernel<24>, cudaFuncAttributeMaxDynamicSharedMemorySize, bmx));
@@ -678,7 +681,12 @@ static int eigh_top(cudaStream_t st, int s, const double* Hs, int ldh, int m, do
   TRY(w.mark(8));
   static int bt_mode = -1;  // 0: compact-WY (default for s <= 640), 1: reflector-by-reflector panels
   if (bt_mode < 0) bt_mode = getenv("PSDPROJ_BT_SIMPLE") ? 1 : 0;
-  const bool wy = s > 2 && bt_mode == 0 && s <= 32 * 20 && m > 0;
+  // one-CTA-per-column WY apply when the m CTAs fit in one wave (s <= 768)
+  static const int bt_col = getenv("PSDPROJ_BT_WARP") ? 0 : 1;
+  const size_t bt_col_smem = bt_col_smem_doubles(s) * sizeof(double);
+  const bool col_ok = bt_col && s <= 768 && bt_col_smem <= (size_t)CLA_SMEM_BYTES &&
+                      m <= sms() * (int)std::max<size_t>(1, (size_t)(228 * 1024) / (bt_col_smem + 1024));
+  const bool wy = s > 2 && bt_mode == 0 && (s <= 32 * 20 || col_ok) && m > 0;
   cudaEvent_t tri_side_join = nullptr;
   if (wy) {
     static thread_local cudaStream_t side = nullptr;
@@ -745,13 +753,24 @@ static int eigh_top(cudaStream_t st, int s, const double* Hs, int ldh, int m, do
 #define BT_WY(PL)                                                                                          \
   backtransform_wy_kernel<PL, 4><<<cdiv(m, 4), 128, bt_wy_smem_doubles(PL, 4) * sizeof(double), st>>>( \
       s, m, w.Vh, w.ldv, Tb, Yv, ldy)
-      if (s <= 32 * 8)
+#define BT_COL(PLW)                                                                                        \
+  backtransform_wy_col_kernel<PLW><<<m, 256, bt_col_smem_doubles(s) * sizeof(double), st>>>(s, m, w.Vh, w.ldv, \
+                                                                                           Tb, Yv, ldy)
+      if (col_ok) {
+        if (s <= 256)
+          BT_COL(1);
+        else if (s <= 512)
+          BT_COL(2);
+        else
+          BT_COL(3);
+      } else if (s <= 32 * 8)
         BT_WY(8);
       else if (s <= 32 * 16)
         BT_WY(16);
       else
         BT_WY(20);
 #undef BT_WY
+#undef BT_COL
       CKL();
     } else {
     const int pb = (int)std::max<size_t>(1, std::min<size_t>(BT_PB, (size_t)CLA_SMEM_BYTES / (2 * (size_t)s * sizeof(double))));
