@@ -93,12 +93,16 @@ template <bool GA = false, bool INV = false>
 __global__ void __launch_bounds__(CLA_NT) cholesky_cluster_kernel(int t, double* __restrict__ G, int ld,
                                                                    double fail_rel, int* __restrict__ status,
                                                                    double* __restrict__ gA,
-                                                                   double* __restrict__ Linv, int ldi) {
+                                                                   double* __restrict__ Linv, int ldi,
+                                                                   int* __restrict__ started = nullptr, int seq = 0) {
   extern __shared__ __align__(16) double sm[];
   __shared__ double red[33];
   __shared__ double xchs[4];
   const int CS = (int)gridDim.x;
   const unsigned rank = cla_rank();
+  // residency signal for a stream that holds back its own work until this cluster is on the SMs
+  if (started && rank == 0 && threadIdx.x == 0)
+    asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(started), "r"(seq) : "memory");
   const int ncl = chol_local_cols(t, CS);
   double* Al = GA ? gA + (size_t)rank * ncl * t : sm;  // ncl x t: local column lc = lb * NB + c <-> global (lb * CS + rank) * NB + c
   double* Xl = (INV && !GA) ? sm + (size_t)ncl * t : nullptr;  // ncl x t: own columns of L^-1

@@ -1028,4 +1028,19 @@ __global__ void admm_maxcut_step2_kernel(int n, const double* __restrict__ X, co
     if (r2 > 0.0) atomicMax(res + 2, (unsigned long long)__double_as_longlong(r2));
   }
 }
+// Holds its stream until *flag >= seq (a kernel on another stream announced that it is resident)
+// or timeout_ns passed; one thread.
+__global__ void wait_flag_kernel(const int* __restrict__ flag, int seq, long long timeout_ns) {
+  unsigned long long t0, t1;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    if (v >= seq) break;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    if ((long long)(t1 - t0) > timeout_ns) break;
+    __nanosleep(64);
+  }
+}
+
 }  // namespace psd

@@ -125,6 +125,10 @@ static const bool g_hostprof = getenv("PSDPROJ_HOSTPROF") != nullptr;
 static thread_local double g_sync_s = 0.0;
 static thread_local long g_nsync = 0;
 
+// SMs held by a concurrently running kernel (the overlapped Cholesky cluster): the split-K choice
+// of a GEMM launched meanwhile sizes its grid for the rest, so it stays one wave
+static thread_local int g_sm_reserve = 0;
+
 // ------------------------------------------------------------------ GEMM dispatch
 namespace {
 constexpr int GBM = 64, GBN = 64, GBK = 16, GWM = 32, GWN = 32, GST = 4;
@@ -169,7 +173,7 @@ static int gemm_kp_launch(cudaStream_t st, int M, int N, int K, double alpha, co
   const int KT = cdiv(std::max(K, 1), 16);
   const int nprob = A2 ? 2 : 1;
   const int tiles = cdiv(M, BM) * cdiv(N, BN) * nprob;
-  const int slots = sms() * per_sm;
+  const int slots = std::max(1, sms() - g_sm_reserve) * per_sm;
   int splits = 1;
   if (part && tiles < slots && KT >= 8) {
     splits = std::min(std::max(1, slots / tiles), KT / 4);
@@ -428,7 +432,8 @@ static int cla_attrs() {
 // separate panel-streamed inverse). Returns 0 or a negative error.
 static int trinv_run(cudaStream_t st, int t, const double* L, int ldl, double* Li, int ldi);
 static int cholesky_run(cudaStream_t st, int t, double* G, int ld, int* d_status, double* gscratch = nullptr,
-                        size_t gscratch_elems = 0, double* Linv = nullptr, int ldi = 0) {
+                        size_t gscratch_elems = 0, double* Linv = nullptr, int ldi = 0, int* started = nullptr,
+                        int seq = 0) {
   TRY(cla_attrs());
   static int fuse = getenv("PSDPROJ_CHOL_NOFUSE") ? 0 : 1;
   const double frel = 1e-12;  // R20
@@ -440,24 +445,28 @@ static int cholesky_run(cudaStream_t st, int t, double* G, int ld, int* d_status
       chol_inv_smem_doubles(t, chol_cs) * sizeof(double) <= (size_t)CLA_SMEM_BYTES) {
     return launch_cluster(cholesky_cluster_kernel<false, true>, chol_cs, CLA_NT,
                           chol_inv_smem_doubles(t, chol_cs) * sizeof(double), st, t, G, ld, 1e-12, d_status,
-                          (double*)nullptr, Linv, ldi);
+                          (double*)nullptr, Linv, ldi, started, seq);
   }
   if (Linv && fuse) {
     if (int cs = cla_cluster_size(t, chol_inv_smem_doubles)) {
       return launch_cluster(cholesky_cluster_kernel<false, true>, cs, CLA_NT,
                             chol_inv_smem_doubles(t, cs) * sizeof(double), st, t, G, ld, frel, d_status,
-                            (double*)nullptr, Linv, ldi);
+                            (double*)nullptr, Linv, ldi, started, seq);
     }
   }
   if (int cs = cla_cluster_size(t, chol_smem_doubles)) {
     TRY(launch_cluster(cholesky_cluster_kernel<false, false>, cs, CLA_NT, chol_smem_doubles(t, cs) * sizeof(double),
-                       st, t, G, ld, frel, d_status, (double*)nullptr, (double*)nullptr, 0));
+                       st, t, G, ld, frel, d_status, (double*)nullptr, (double*)nullptr, 0, started, seq));
     return Linv ? trinv_run(st, t, G, ld, Linv, ldi) : 0;
   }
   if (gscratch && (size_t)16 * chol_local_cols(t, 16) * t <= gscratch_elems && t <= 4096) {
     TRY(launch_cluster(cholesky_cluster_kernel<true, false>, 16, CLA_NT, chol_smem_doubles_ga(t, 16) * sizeof(double),
-                       st, t, G, ld, frel, d_status, gscratch, (double*)nullptr, 0));
+                       st, t, G, ld, frel, d_status, gscratch, (double*)nullptr, 0, started, seq));
     return Linv ? trinv_run(st, t, G, ld, Linv, ldi) : 0;
+  }
+  if (started) {
+    set_int_kernel<<<1, 1, 0, st>>>(started, seq);
+    CKL();
   }
   cholesky_kernel<1024><<<1, 1024, 0, st>>>(t, G, ld, frel, d_status);
   CKL();
@@ -841,6 +850,9 @@ struct psdproj_ctx_s {
   // side stream: the direction-block Gram and its Cholesky run there, overlapping the block multiply
   cudaStream_t st2 = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  int* d_flag = nullptr;  // residency signal of the side-stream Cholesky (sequence number)
+  int chol_seq = 0;
+  int chol_cs_used = 8;  // SMs the overlapped Cholesky cluster holds
   double* part2 = nullptr;
 };
 
@@ -1073,6 +1085,7 @@ extern "C" int psdproj_destroy(psdproj_ctx c) {
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
   if (c->st2) cudaStreamDestroy(c->st2);
+  if (c->d_flag) cudaFree(c->d_flag);
   delete c;
   return PSDPROJ_OK;
 }
@@ -1275,14 +1288,14 @@ struct Run {
   // returns 0 (ok), >0 (Cholesky failed at that pivot), <0 error. Outputs Cp (s x mU), theta desc in h_d[0..s).
   // G side of the pencil: known blocks of G, Li = [I 0; 0 0], Cholesky (+ L^-1) of the direction
   // block D (size s - kxG). May run on the side stream (stream_, part_ of a Run bound to it).
-  int rr_factor(int s, int kxG) {
+  int rr_factor(int s, int kxG, int* started = nullptr, int seq = 0) {
     const int ldm = c->s_max, kx = kxG, t = s - kxG;
     rr_prep_kernel<<<grid1d((size_t)s * s), 256, 0, st>>>(s, kxG, 0, c->G, c->Hm, ldm, nullptr, c->Li, c->Gc,
                                                           c->d_status, 1);
     CKL();
     if (t > 0) {
       TRY(cholesky_run(st, t, c->Gc, ldm, c->d_status, c->tG, (size_t)c->s_max * c->s_max + 16 * (size_t)c->s_max + 2048,
-                       c->Li + kx + (size_t)kx * ldm, ldm));
+                       c->Li + kx + (size_t)kx * ldm, ldm, started, seq));
       // R44: reject a direction block with max |L^-1|^2 > 1e8 (unit-norm directions: cond(G) >~ 1e8).
       // Cholesky-QR leaves the new block orthonormal only to ~u cond(G), and the pencil takes
       // X^T X = I for granted in the next step; the pivot rule (R20) alone admits cond(G) ~ 1e12
@@ -1873,6 +1886,9 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
         CK(cudaStreamCreateWithPriority(&c->st2, cudaStreamNonBlocking, hi_pr));
         CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+        CK(cudaMalloc(&c->d_flag, sizeof(int)));
+        CK(cudaMemsetAsync(c->d_flag, 0, sizeof(int), st));
+        c->chol_seq = 0;
       }
       // the direction-block Gram first (on the main stream), then the Cholesky on the side stream
       TRY(run.gram(s - mU, s - mU, c->S + (size_t)mU * ld, ld, c->S + (size_t)mU * ld, ld, c->G + mU + (size_t)mU * ldm,
@@ -1881,11 +1897,23 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
       CK(cudaStreamWaitEvent(c->st2, c->ev_fork, 0));
       Run r2{c, c->st2, info};
       r2.part = c->part2;
-      TRY(r2.rr_factor(s, mU));
+      // the block multiply waits (on the device, bounded) until the Cholesky cluster is resident:
+      // dispatched after the multiply's CTAs it finds no 8 free SMs and runs after the multiply
+      static int hold = getenv("PSDPROJ_CHOL_HOLD") ? atoi(getenv("PSDPROJ_CHOL_HOLD")) : 1;
+      const int seq = hold ? ++c->chol_seq : 0;
+      TRY(r2.rr_factor(s, mU, hold ? c->d_flag : nullptr, seq));
       CK(cudaEventRecord(c->ev_join, c->st2));
+      if (hold) {
+        wait_flag_kernel<<<1, 32, 0, st>>>(c->d_flag, seq, 200000LL);
+        CKL();
+      }
     }
     TRY(run.mark(0));
-    TRY(run.amul(sgn, A, lda, W, ld, aw, c->BS + (size_t)offW * ld, ld));
+    static int hold_env = getenv("PSDPROJ_CHOL_HOLD") ? atoi(getenv("PSDPROJ_CHOL_HOLD")) : 1;
+    g_sm_reserve = (ovl && hold_env) ? c->chol_cs_used : 0;
+    rc = run.amul(sgn, A, lda, W, ld, aw, c->BS + (size_t)offW * ld, ld);
+    g_sm_reserve = 0;
+    TRY(rc);
     TRY(run.mark(2));
     if (!ovl)
       TRY(run.gram(s - mU, s - mU, c->S + (size_t)mU * ld, ld, c->S + (size_t)mU * ld, ld, c->G + mU + (size_t)mU * ldm,
