@@ -852,7 +852,6 @@ struct psdproj_ctx_s {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int* d_flag = nullptr;  // residency signal of the side-stream Cholesky (sequence number)
   int chol_seq = 0;
-  int chol_cs_used = 8;  // SMs the overlapped Cholesky cluster holds
   double* part2 = nullptr;
 };
 
@@ -1910,7 +1909,8 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
     }
     TRY(run.mark(0));
     static int hold_env = getenv("PSDPROJ_CHOL_HOLD") ? atoi(getenv("PSDPROJ_CHOL_HOLD")) : 1;
-    g_sm_reserve = (ovl && hold_env) ? c->chol_cs_used : 0;
+    static const int chol_sms = getenv("PSDPROJ_CHOL_CS") ? std::max(1, atoi(getenv("PSDPROJ_CHOL_CS"))) : 8;
+    g_sm_reserve = (ovl && hold_env) ? chol_sms : 0;  // the Cholesky cluster's CTAs (one SM each)
     rc = run.amul(sgn, A, lda, W, ld, aw, c->BS + (size_t)offW * ld, ld);
     g_sm_reserve = 0;
     TRY(rc);
