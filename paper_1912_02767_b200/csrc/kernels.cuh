@@ -73,6 +73,32 @@ __global__ void __launch_bounds__(NT) colnorm_kernel(int n, const double* __rest
   if (threadIdx.x == 0) out[j] = squared ? acc : sqrt(acc);
 }
 
+// colnorm_kernel + scale_cols_kernel in one pass per column (unsharded): norm[j] = ||Z[:, j]||,
+// then Z[:, j] /= norm[j] (Z2 likewise; a zero norm leaves the column unchanged). Same reduction
+// and the same per-element arithmetic as the two kernels.
+template <int NT>
+__global__ void __launch_bounds__(NT) colnorm_scale_kernel(int n, double* __restrict__ Z, int ld,
+                                                           double* __restrict__ Z2, int ld2,
+                                                           double* __restrict__ out) {
+  __shared__ double red[32];
+  int j = blockIdx.x;
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < n; i += NT) {
+    double v = Z[IDX(i, j, ld)];
+    acc += v * v;
+  }
+  acc = block_sum<NT>(acc, red);
+  const double s = sqrt(acc);
+  if (threadIdx.x == 0) out[j] = s;
+  if (s > 0.0) {
+    const double inv = 1.0 / s;
+    for (int i = threadIdx.x; i < n; i += NT) {
+      Z[IDX(i, j, ld)] *= inv;
+      if (Z2) Z2[IDX(i, j, ld2)] *= inv;
+    }
+  }
+}
+
 __global__ void i2d_kernel(const int* __restrict__ f, double* __restrict__ d) {
   if (threadIdx.x == 0) d[0] = (double)f[0];
 }

@@ -1256,6 +1256,11 @@ struct Run {
   }
   int normalize(int n, int cols, double* Z, int ldz, double* Z2, int ldz2) {
     if (cols <= 0) return 0;
+    if (!c->sharded) {
+      colnorm_scale_kernel<256><<<cols, 256, 0, st>>>(n, Z, ldz, Z2, ldz2, c->d_norm);
+      CKL();
+      return 0;
+    }
     colnorm_kernel<256><<<cols, 256, 0, st>>>(n, Z, ldz, c->d_norm, c->sharded ? 1 : 0);
     CKL();
     if (c->sharded) {
