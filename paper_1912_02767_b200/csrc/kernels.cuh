@@ -158,6 +158,34 @@ __global__ void gather_cols_kernel(int n, int cols, double* __restrict__ dst, in
   }
 }
 
+// Up to four column gathers in one launch: job q copies dst_q[:, j] = src_q[:, idx_q[j]]
+// (idx_q null: src_q[:, j]) for j < cols_q; elements enumerated job by job.
+struct GatherJob {
+  double* dst;
+  const double* src;
+  const int* idx;
+  int ldd, lds, cols;
+};
+struct GatherJobs {
+  GatherJob j[4];
+  int nj;
+};
+__global__ void gather_multi_kernel(int n, GatherJobs g) {
+  size_t total = 0;
+  for (int q = 0; q < g.nj; ++q) total += (size_t)n * g.j[q].cols;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+    size_t w = e;
+    int q = 0;
+    while (q + 1 < g.nj && w >= (size_t)n * g.j[q].cols) {
+      w -= (size_t)n * g.j[q].cols;
+      ++q;
+    }
+    const GatherJob& jb = g.j[q];
+    const int i = (int)(w % n), c = (int)(w / n);
+    jb.dst[IDX(i, c, jb.ldd)] = jb.src[IDX(i, jb.idx ? jb.idx[c] : c, jb.lds)];
+  }
+}
+
 // dst[:, j] = src[:, j] * w[j]
 __global__ void scale_copy_cols_kernel(int n, int cols, double* __restrict__ dst, int ldd,
                                        const double* __restrict__ src, int lds, const double* __restrict__ w) {

@@ -22,6 +22,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <initializer_list>
 #include <numeric>
 #include <string>
 #include <thread>
@@ -1248,6 +1249,37 @@ struct Run {
     CKL();
     return 0;
   }
+  // several gathers (idx empty: plain column copy) in one launch, their indices in one upload
+  struct GJ {
+    double* dst;
+    int ldd;
+    const double* src;
+    int lds;
+    int cols;
+    const std::vector<int>* idx;
+  };
+  int gather_multi(int n, std::initializer_list<GJ> jobs) {
+    GatherJobs g{};
+    std::vector<int> all;
+    std::vector<int> offs;
+    for (const GJ& j : jobs) {
+      if (j.cols <= 0) continue;
+      offs.push_back(j.idx ? (int)all.size() : -1);
+      if (j.idx) all.insert(all.end(), j.idx->begin(), j.idx->end());
+      g.j[g.nj++] = GatherJob{j.dst, j.src, nullptr, j.ldd, j.lds, j.cols};
+    }
+    if (g.nj == 0) return 0;
+    int* d = c->d_idx + ihost;
+    TRY(upload_idx(all, d));
+    size_t total = 0;
+    for (int q = 0; q < g.nj; ++q) {
+      if (offs[q] >= 0) g.j[q].idx = d + offs[q];
+      total += (size_t)n * g.j[q].cols;
+    }
+    gather_multi_kernel<<<grid1d(total), 256, 0, st>>>(n, g);
+    CKL();
+    return 0;
+  }
   int copy_cols(int n, int cols, double* dst, int ldd, const double* src, int lds) {
     if (cols <= 0) return 0;
     CK(cudaMemcpy2DAsync(dst, (size_t)ldd * 8, src, (size_t)lds * 8, (size_t)n * 8, cols, cudaMemcpyDeviceToDevice,
@@ -1844,16 +1876,14 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
     // W = R_J (+ pending expansion E) and P_J sit contiguously in S: [W E P] at offW; both are
     // projected against the locked block and X_U in one pass (one Gram + one update GEMM each)
     TRY(run.mark(1));
-    TRY(run.gather(nl, a, c->S + (size_t)offW * ld, ld, c->R, ld, Jorig));
-    TRY(run.copy_cols(nl, qe, c->S + (size_t)offE * ld, ld, c->E, ld));
     int aw = a + qe;
     double* W = c->S + (size_t)offW * ld;
     double* P = c->S + (size_t)offP * ld;
     double* BP = c->BS + (size_t)offP * ld;
-    if (ap > 0) {
-      TRY(run.gather(nl, ap, P, ld, c->Pb, ld, PJ));
-      TRY(run.gather(nl, ap, BP, ld, c->BPb, ld, PJ));
-    }
+    TRY(run.gather_multi(nl, {{W, ld, c->R, ld, a, &Jorig},
+                              {c->S + (size_t)offE * ld, ld, c->E, ld, qe, nullptr},
+                              {P, ld, c->Pb, ld, ap, &PJ},
+                              {BP, ld, c->BPb, ld, ap, &PJ}}));
     const int wp = aw + ap;
     static int lock_reproj = getenv("PSDPROJ_LOCK_REPROJ") ? atoi(getenv("PSDPROJ_LOCK_REPROJ")) : 0;
     const int xr = (lock_reproj && hard && nL > 0) ? mU : 0;  // X_U columns included (R46)
