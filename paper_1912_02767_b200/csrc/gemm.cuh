@@ -202,6 +202,7 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, BK, WM, WN, STAGES>::THREADS)
 // splits issued before the ordered adds.
 __global__ void splitk_reduce_kernel(int M, int N, int splits, double alpha, const double* __restrict__ part,
                                      double beta, double* __restrict__ C, int ldc) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // see dgemm_kp_kernel
   const int row = blockIdx.x * blockDim.x + threadIdx.x, col = blockIdx.y;
   if (row >= M) return;
   const size_t total = (size_t)M * N, e = (size_t)row + (size_t)col * M;
@@ -263,6 +264,9 @@ __global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32, (BM * BN >= 8192) 
                     const double* __restrict__ B, int ldb, double beta, double* __restrict__ C, int ldc,
                     double* __restrict__ partial, int ktiles_per_split, const double* __restrict__ A2,
                     double* __restrict__ C2, int splits) {
+  // programmatic dependent launch: nothing before this line touches memory the previous kernel
+  // in the stream writes (a no-op for an ordinary launch)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (A2 && (int)blockIdx.z >= splits) {  // problem 1
     A = A2;
     C = C2;
@@ -327,6 +331,8 @@ __global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32, (BM * BN >= 8192) 
     }
   }
   cp_async_wait<0>();
+  // the next kernel (split-K reduce) may be scheduled now; it waits for this grid's completion
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 #pragma unroll
   for (int i = 0; i < MI; ++i) {
     const int row = m0 + wm * WM + i * 8 + fr;

@@ -130,6 +130,31 @@ static thread_local long g_nsync = 0;
 // of a GEMM launched meanwhile sizes its grid for the rest, so it stays one wave
 static thread_local int g_sm_reserve = 0;
 
+// kernels that begin with griddepcontrol.wait are launched as programmatic dependents of the
+// previous kernel in the stream (their launch overlaps its tail); PSDPROJ_PDL=0: ordinary launches
+static const bool g_pdl = !(getenv("PSDPROJ_PDL") && atoi(getenv("PSDPROJ_PDL")) == 0);
+template <typename... KArgs, typename... Args>
+static int launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  if (!g_pdl) {
+    kern<<<grid, block, smem, st>>>(args...);
+    CKL();
+    return 0;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, kern, ((KArgs)args)...));
+  ++g_launches;
+  return 0;
+}
+
 // ------------------------------------------------------------------ GEMM dispatch
 namespace {
 constexpr int GBM = 64, GBN = 64, GBK = 16, GWM = 32, GWN = 32, GST = 4;
@@ -184,17 +209,14 @@ static int gemm_kp_launch(cudaStream_t st, int M, int N, int K, double alpha, co
   const int ktps = cdiv(KT, splits);
   splits = cdiv(KT, ktps);
   dim3 grid(cdiv(M, BM), cdiv(N, BN), splits * nprob);
-  kern<<<grid, THREADS, SMEM, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits > 1 ? part : nullptr, ktps, A2,
-                                    C2, splits);
-  CKL();
+  TRY(launch_pdl(kern, grid, dim3(THREADS), SMEM, st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc,
+                 splits > 1 ? part : (double*)nullptr, ktps, A2, C2, splits));
   if (splits > 1) {
-    splitk_reduce_kernel<<<dim3(cdiv(M, 256), N), 256, 0, st>>>(M, N, splits, alpha, part, beta, C, ldc);
-    CKL();
-    if (A2) {
-      splitk_reduce_kernel<<<dim3(cdiv(M, 256), N), 256, 0, st>>>(M, N, splits, alpha, part + (size_t)splits * M * N,
-                                                                   beta, C2, ldc);
-      CKL();
-    }
+    TRY(launch_pdl(splitk_reduce_kernel, dim3(cdiv(M, 256), N), dim3(256), 0, st, M, N, splits, alpha,
+                   (const double*)part, beta, C, ldc));
+    if (A2)
+      TRY(launch_pdl(splitk_reduce_kernel, dim3(cdiv(M, 256), N), dim3(256), 0, st, M, N, splits, alpha,
+                     (const double*)(part + (size_t)splits * M * N), beta, C2, ldc));
   }
   return 0;
 }
