@@ -1441,6 +1441,7 @@ __global__ void __launch_bounds__(256) backtransform_wy_col_kernel(int s, int m,
 // dev = max |M - I| accumulated into *dev (as a non-negative double's bit pattern, atomicMax).
 __global__ void ns_coeff_kernel(int m, const double* __restrict__ M, int ldm, double* __restrict__ Z, int ldz,
                                 unsigned long long* __restrict__ dev) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL (launch_pdl)
   double mx = 0.0;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < (int64_t)m * m;
        q += (int64_t)gridDim.x * blockDim.x) {

@@ -46,6 +46,7 @@ __global__ void __launch_bounds__(NT) resid_norm_kernel(int n, const double* __r
                                                         const double* __restrict__ BX, int ldb,
                                                         const double* __restrict__ theta, double* __restrict__ R,
                                                         int ldr, double* __restrict__ rnorm, int squared = 0) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL (launch_pdl)
   __shared__ double red[32];
   int j = blockIdx.x;
   double th = theta[j];
@@ -80,6 +81,7 @@ template <int NT>
 __global__ void __launch_bounds__(NT) colnorm_scale_kernel(int n, double* __restrict__ Z, int ld,
                                                            double* __restrict__ Z2, int ld2,
                                                            double* __restrict__ out) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL (launch_pdl)
   __shared__ double red[32];
   int j = blockIdx.x;
   double acc = 0.0;
@@ -171,6 +173,7 @@ struct GatherJobs {
   int nj;
 };
 __global__ void gather_multi_kernel(int n, GatherJobs g) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL (launch_pdl)
   size_t total = 0;
   for (int q = 0; q < g.nj; ++q) total += (size_t)n * g.j[q].cols;
   for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
@@ -290,6 +293,7 @@ __global__ void insert_known_kernel(int s, int kxG, int kxH, double* __restrict_
 __global__ void rr_prep_kernel(int s, int kxG, int kxH, double* __restrict__ G, double* __restrict__ H, int ld,
                                const double* __restrict__ theta, double* __restrict__ Li, double* __restrict__ Gc,
                                int* __restrict__ status, int parts) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL (launch_pdl)
   int total = s * s;
   const bool gs = parts & 1, hs = parts & 2;
   if (gs && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -321,6 +325,7 @@ __global__ void rr_prep_kernel(int s, int kxG, int kxH, double* __restrict__ G, 
 // (Z = L^-1 H, rows >= kx), Hh[:kx, kx:] = its transpose.
 __global__ void rr_assemble_kernel(int s, int kx, const double* __restrict__ H, const double* __restrict__ Z,
                                    double* __restrict__ Hh, int ld) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL (launch_pdl)
   const size_t total = (size_t)s * kx;
   for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
     const int i = (int)(e % s), j = (int)(e / s);  // column j < kx, row i

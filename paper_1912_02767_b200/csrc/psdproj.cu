@@ -543,8 +543,8 @@ static int ns_run(cudaStream_t st, int s, int m, double* Yv, int ldy, const Eigh
     TRY(dgemm(st, OP_T, OP_N, m, m, s, 1.0, Yv, ldy, Yv, ldy, 0.0, w.nsM, m, part, part_elems));
     const bool lastst = it == steps - 1;
     if (lastst) CK(cudaMemsetAsync(w.dev, 0, sizeof(unsigned long long), st));
-    ns_coeff_kernel<<<grid1d((size_t)m * m), 256, 0, st>>>(m, w.nsM, m, w.nsZ, m, lastst ? w.dev : w.dev + 1);
-    CKL();
+    TRY(launch_pdl(ns_coeff_kernel, dim3(grid1d((size_t)m * m)), dim3(256), 0, st, m, (const double*)w.nsM, m, w.nsZ,
+                   m, lastst ? w.dev : w.dev + 1));
     TRY(dgemm(st, OP_N, OP_N, s, m, m, 1.0, Yv, ldy, w.nsZ, m, 0.0, w.nsY, w.ldv, part, part_elems));
     CK(cudaMemcpy2DAsync(Yv, (size_t)ldy * 8, w.nsY, (size_t)w.ldv * 8, (size_t)s * 8, m, cudaMemcpyDeviceToDevice,
                          st));
@@ -1298,8 +1298,7 @@ struct Run {
       if (offs[q] >= 0) g.j[q].idx = d + offs[q];
       total += (size_t)n * g.j[q].cols;
     }
-    gather_multi_kernel<<<grid1d(total), 256, 0, st>>>(n, g);
-    CKL();
+    TRY(launch_pdl(gather_multi_kernel, dim3(grid1d(total)), dim3(256), 0, st, n, g));
     return 0;
   }
   int copy_cols(int n, int cols, double* dst, int ldd, const double* src, int lds) {
@@ -1311,8 +1310,7 @@ struct Run {
   int normalize(int n, int cols, double* Z, int ldz, double* Z2, int ldz2) {
     if (cols <= 0) return 0;
     if (!c->sharded) {
-      colnorm_scale_kernel<256><<<cols, 256, 0, st>>>(n, Z, ldz, Z2, ldz2, c->d_norm);
-      CKL();
+      TRY(launch_pdl(colnorm_scale_kernel<256>, dim3(cols), dim3(256), 0, st, n, Z, ldz, Z2, ldz2, c->d_norm));
       return 0;
     }
     colnorm_kernel<256><<<cols, 256, 0, st>>>(n, Z, ldz, c->d_norm, c->sharded ? 1 : 0);
@@ -1388,9 +1386,8 @@ struct Run {
     } else {
       TRY(rr_factor(s, kxG));
     }
-    rr_prep_kernel<<<grid1d((size_t)s * s), 256, 0, st>>>(s, kxG, kxH, c->G, c->Hm, ldm, d_theta_known, c->Li, c->Gc,
-                                                          c->d_status, 2);
-    CKL();
+    TRY(launch_pdl(rr_prep_kernel, dim3(grid1d((size_t)s * s)), dim3(256), 0, st, s, kxG, kxH, c->G, c->Hm, ldm,
+                   d_theta_known, c->Li, c->Gc, c->d_status, 2));
     // Hh = L^-1 H L^-T with L^-1 = [I 0; 0 Ld] (Ld = the direction block's inverse factor, t x t):
     // Z = Ld H[kx:, :] (t x s), Hh[kx:, kx:] = Z[:, kx:] Ld^T, the X rows/columns copied
     {
@@ -1400,8 +1397,8 @@ struct Run {
       TRY(dgemm(st, OP_N, OP_T, t, t, t, 1.0, c->Y + kx + (size_t)kx * ldm, ldm, Ld, ldm, 0.0,
                 c->Hh + kx + (size_t)kx * ldm, ldm, c->part, c->part_elems));
       if (kx > 0) {
-        rr_assemble_kernel<<<grid1d((size_t)s * kx), 256, 0, st>>>(s, kx, c->Hm, c->Y, c->Hh, ldm);
-        CKL();
+        TRY(launch_pdl(rr_assemble_kernel, dim3(grid1d((size_t)s * kx)), dim3(256), 0, st, s, kx, (const double*)c->Hm,
+                       (const double*)c->Y, c->Hh, ldm));
       }
     }
     // eigensolver choice by measured crossover: tridiagonal path while the matrix fits in shared memory (s <= 160),
@@ -1772,8 +1769,8 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
     }
     // ---- line 5: R = B X - X Theta, r_i = ||R_i|| (unlocked columns)
     TRY(run.mark(6));
-    resid_norm_kernel<256><<<mU, 256, 0, st>>>(nl, c->S, ld, c->BS, ld, c->d_thU, c->R, ld, c->d_r, c->sharded ? 1 : 0);
-    CKL();
+    TRY(launch_pdl(resid_norm_kernel<256>, dim3(mU), dim3(256), 0, st, nl, (const double*)c->S, ld,
+                   (const double*)c->BS, ld, (const double*)c->d_thU, c->R, ld, c->d_r, c->sharded ? 1 : 0));
     if (c->sharded) {  // column sums of squares over the ranks' rows
       TRY(run.allreduce(c->d_r, mU));
       sqrt_inplace_kernel<<<cdiv(mU, 256), 256, 0, st>>>(mU, c->d_r);
