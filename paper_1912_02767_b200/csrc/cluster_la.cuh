@@ -1350,6 +1350,7 @@ template <int PLW>
 __global__ void __launch_bounds__(256) backtransform_wy_col_kernel(int s, int m, const double* __restrict__ Vh,
                                                                    int ldv, const double* __restrict__ Tb,
                                                                    double* __restrict__ y, int ldy) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL (launch_pdl)
   extern __shared__ __align__(16) double pv[];
   const int LDP = (s + 2) & ~1;                // panel column pitch: row s exists and is zero-filled
   double* Ts = pv + (size_t)2 * WY_PB * LDP;   // 2 x WY_PB x WY_PB

@@ -743,12 +743,14 @@ static int eigh_top(cudaStream_t st, int s, const double* Hs, int ldh, int m, do
   {
     // multisection points per eigenvalue (PSDPROJ_BISECT_G, multiple of 32; 32 = one warp each)
     static const int bg = getenv("PSDPROJ_BISECT_G") ? std::max(32, std::min(1024, atoi(getenv("PSDPROJ_BISECT_G")) / 32 * 32)) : 256;
-    if (bg == 32)
+    if (bg == 32) {
       tri_bisect_kernel<<<cdiv(m + 1, 2), 64, (size_t)2 * s * sizeof(double), st>>>(s, m, w.td, w.te2, w.tbounds, lam,
                                                                                     npos);
-    else
-      tri_bisect_ms_kernel<<<m + 1, bg, (size_t)2 * s * sizeof(double), st>>>(s, m, w.td, w.te2, w.tbounds, lam, npos);
-    CKL();
+      CKL();
+    } else {
+      TRY(launch_pdl(tri_bisect_ms_kernel, dim3(m + 1), dim3(bg), (size_t)2 * s * sizeof(double), st, s, m,
+                     (const double*)w.td, (const double*)w.te2, (const double*)w.tbounds, lam, npos));
+    }
   }
   if (m <= 0) return 0;  // (wy is false for m <= 0: no side-stream work in flight)
   TRY(w.mark(9));
@@ -770,12 +772,13 @@ static int eigh_top(cudaStream_t st, int s, const double* Hs, int ldh, int m, do
   } else {
     static int twisted = getenv("PSDPROJ_INVITER") ? 0 : 1;
     if (twisted && (size_t)(7 * s + 2) * sizeof(double) <= (size_t)220 * 1024) {
-      tri_twisted_kernel<<<m, 32, (size_t)(7 * s + 2) * sizeof(double), st>>>(s, m, w.td, w.te, lam, Yv, ldy);
+      TRY(launch_pdl(tri_twisted_kernel, dim3(m), dim3(32), (size_t)(7 * s + 2) * sizeof(double), st, s, m,
+                     (const double*)w.td, (const double*)w.te, (const double*)lam, Yv, ldy));
     } else {
       tri_inviter_kernel<<<cdiv(m, vpb), vpb, ism, st>>>(s, m, w.td, w.te, lam, w.tbounds, Yv, ldy, w.tscr, 2, 0,
                                                          smem_ok);
+      CKL();
     }
-    CKL();
   }
   TRY(w.mark(10));
   if (s > 2) {

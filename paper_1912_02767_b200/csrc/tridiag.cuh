@@ -301,6 +301,7 @@ __global__ void tri_bisect_kernel(int s, int m, const double* __restrict__ dg, c
 __global__ void tri_bisect_ms_kernel(int s, int m, const double* __restrict__ dg, const double* __restrict__ e2g,
                                      const double* __restrict__ bounds, double* __restrict__ out,
                                      int* __restrict__ npos) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL (launch_pdl)
   extern __shared__ __align__(16) double bsm[];
   __shared__ unsigned masks[2][32];
   double* d = bsm;
@@ -503,6 +504,7 @@ __global__ void __launch_bounds__(32) tri_twisted_kernel(int s, int m, const dou
                                                          const double* __restrict__ e,
                                                          const double* __restrict__ lam, double* __restrict__ y,
                                                          int ldy) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL (launch_pdl)
   extern __shared__ __align__(16) double tsm[];
   // ec[k] = e_{k-1} (coupling of rows k-1, k; ec[0] = ec[s] = 0), e2[k] = ec[k]^2
   double* sd = tsm;
