@@ -155,6 +155,16 @@ static int launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem
   return 0;
 }
 
+// D2D copy of a rows x cols block as a (PDL) kernel: stays inside the chain of dependent launches
+// where a copy-engine memcpy would break it
+static int copy_block_pdl(cudaStream_t st, int rows, int cols, double* dst, int ldd, const double* src, int lds) {
+  if (rows <= 0 || cols <= 0) return 0;
+  GatherJobs g{};
+  g.j[0] = GatherJob{dst, src, nullptr, ldd, lds, cols};
+  g.nj = 1;
+  return launch_pdl(gather_multi_kernel, dim3(grid1d((size_t)rows * cols)), dim3(256), 0, st, rows, g);
+}
+
 // ------------------------------------------------------------------ GEMM dispatch
 namespace {
 constexpr int GBM = 64, GBN = 64, GBK = 16, GWM = 32, GWN = 32, GST = 4;
@@ -546,8 +556,7 @@ static int ns_run(cudaStream_t st, int s, int m, double* Yv, int ldy, const Eigh
     TRY(launch_pdl(ns_coeff_kernel, dim3(grid1d((size_t)m * m)), dim3(256), 0, st, m, (const double*)w.nsM, m, w.nsZ,
                    m, lastst ? w.dev : w.dev + 1));
     TRY(dgemm(st, OP_N, OP_N, s, m, m, 1.0, Yv, ldy, w.nsZ, m, 0.0, w.nsY, w.ldv, part, part_elems));
-    CK(cudaMemcpy2DAsync(Yv, (size_t)ldy * 8, w.nsY, (size_t)w.ldv * 8, (size_t)s * 8, m, cudaMemcpyDeviceToDevice,
-                         st));
+    TRY(copy_block_pdl(st, s, m, Yv, ldy, w.nsY, w.ldv));
   }
   return 0;
 }
@@ -1373,7 +1382,7 @@ struct Run {
     TRY(dgemm(st, OP_T, OP_N, t, mU, t, 1.0, c->Li + kx + (size_t)kx * ldm, ldm, c->Y + kx, ldm, 0.0, c->Cp + kx, ldm,
               c->part, c->part_elems));
     if (kx > 0) {
-      CK(cudaMemcpy2DAsync(c->Cp, (size_t)ldm * 8, c->Y, (size_t)ldm * 8, (size_t)kx * 8, mU, cudaMemcpyDeviceToDevice, st));
+      TRY(copy_block_pdl(st, kx, mU, c->Cp, ldm, c->Y, ldm));
     }
     return 0;
   }
@@ -2035,7 +2044,7 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
       fprintf(stderr, "   rotation: s=%d mUn=%d |XU'XU-I| %g |XL'XU| %g  theta %g..%g\n", sU, mUn, oU, oL,
               ths.empty() ? 0.0 : ths.back(), ths.empty() ? 0.0 : ths.front());
     }
-    CK(cudaMemcpyAsync(c->d_thU, c->d_ths, sizeof(double) * mUn, cudaMemcpyDeviceToDevice, st));
+    TRY(copy_block_pdl(st, mUn, 1, c->d_thU, mUn, c->d_ths, mUn));
     thU.assign(ths.begin(), ths.begin() + mUn);
     rU.assign(mUn, INFINITY);
     hasP.assign(mUn, 1);
