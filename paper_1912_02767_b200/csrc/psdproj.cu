@@ -1434,9 +1434,6 @@ struct Run {
       CKL();
     } else {
       TRY(tri_eig(s, c->Hh, ldm, mU, c->d_ths, c->Y, ldm, c->tnpos, false, 1));
-      CK(cudaMemsetAsync(c->d_status + 4, 0, sizeof(int), st));
-      set_int_kernel<<<1, 1, 0, st>>>(c->d_status + 4, 1);
-      CKL();
       CK(cudaMemcpyAsync(c->h_d + c->h_d_len - 16, c->d_scal + 16, sizeof(double), cudaMemcpyDeviceToHost, st));
     }
     TRY(li_t_apply(s, kx, mU));
@@ -1464,7 +1461,7 @@ struct Run {
       CK(cudaMemcpyAsync(c->h_d, c->d_ths, sizeof(double) * mU, cudaMemcpyDeviceToHost, st));
       TRY(sync());
     }
-    if (sweeps < 0) return set_err(PSDPROJ_E_DEGENERATE, "Jacobi did not converge (s=%d)", s);
+    if (use_jacobi && sweeps < 0) return set_err(PSDPROJ_E_DEGENERATE, "Jacobi did not converge (s=%d)", s);
     return 0;
   }
 };
