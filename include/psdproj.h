@@ -63,10 +63,13 @@ typedef struct {
   int m_max;      /* block-width capacity; 0 => ceil(n/3)+1 (wider => DIRECT, R18)              */
   uint64_t seed;  /* Philox4x32-10 key (R11)                                                    */
   uint32_t ctx_id;/* Philox counter word c2 (distinct per cone block)                           */
-  int profile;    /* bit 0: time every block-multiply (a3) launch; bit 1: per-phase timing       */
+  int profile;    /* bit 0: time every block-multiply (a3) launch; bit 1: per-phase timing;      */
+                  /* bit 2: time every Rayleigh-Ritz tridiagonalisation launch                     */
   int host_io;    /* 1: workspace also holds an n x n staging buffer for psdproj_project_host   */
   int perp_steps; /* f2 (R48): 0 = the paper's bound (perp term ignored); k > 0 =  */
-                  /* k-step projected Lanczos estimate of the perp term added to err_bound        */
+                  /* k-step projected Lanczos upper bound of the perp term added to err_bound     */
+  double perp_delta; /* f2: failure probability of that randomized bound (over the Philox start,   */
+                     /* Kuczynski-Wozniakowski 1992); 0 => 1e-6                                     */
 } psdproj_params;
 
 typedef struct {
@@ -81,10 +84,13 @@ typedef struct {
   int rr_max;       /* largest Rayleigh-Ritz basis width s                                     */
   int locked;       /* hard-locked columns at exit                                             */
   long long a_cols; /* total columns multiplied by A                                           */
-  double err_bound; /* Theorem-3 bound on ||Pi~ - Pi(A)||_F (perp term p^ = perp_est)           */
-  double resid_fro; /* ||R+||_F over the kept pairs                                           */
-  double resid_max; /* max_i r_i over the kept pairs                                          */
-  double lock_defect; /* ||V+^T B V+ - diag(theta+)||_F (hard locking term, R36)             */
+  double err_bound; /* Theorem-3 bound on ||Pi~ - Pi(A)||_F (R14-R16, R36, R53):
+                       (1 + e) sqrt(2 ||R+||_F^2 + p^2) + (1 + sqrt 2) d + 7 e theta_max + 4 n u ||A||_F
+                       with R+ = B V+ - V+ Theta+ from an explicit B V+ at exit (R16), d =
+                       lock_defect, e = orth_defect, p^ = perp_est                           */
+  double resid_fro; /* ||R+||_F over the kept pairs (explicit B V+)                           */
+  double resid_max; /* max_i r_i over the kept pairs (explicit B V+)                          */
+  double lock_defect; /* d = ||V+^T B V+ - diag(theta+)||_F (explicit; hard locking, R36)      */
   double anorm_f;   /* ||A||_F                                                                 */
   double flops;     /* algorithmic flops of the call                           */
   double bytes;     /* algorithmic HBM bytes of the call                                       */
@@ -100,7 +106,13 @@ typedef struct {
                          5 rotation, 6 residual norms, 7 host round trips / locking / assembly,
                          8 RR bisection, 9 RR inverse iteration, 10 RR back-transformation,
                          11 RR re-orthonormalisation + C' = L^-T Y                          */
-  double perp_est;  /* f2 (R48): projected-Lanczos perp term p^ included in err_bound (0 if off) */
+  double perp_est;  /* perp term p^ in err_bound: f2 randomized Lanczos bound (R48; 0 if off) or, on
+                       the DIRECT path, (1 + e) ||A V- - V- Theta-||_F (R53)                   */
+  double orth_defect; /* e = ||V+^T V+ - I||_F of the returned vectors (R53)                   */
+  double perp_mu;   /* f2: largest Ritz value of the deflated Lanczos matrix T_k (0 if off)      */
+  double tri_ms;    /* profile & 4: summed device time of the RR tridiagonalisation launches      */
+  int tri_launches; /* profile & 4: number of timed tridiagonalisation launches                  */
+  double tri_flops; /* profile & 4: 4/3 s^3 summed over those launches (algorithmic)              */
 } psdproj_info;
 
 /* Fill *p with the defaults documented above. */

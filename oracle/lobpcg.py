@@ -9,9 +9,10 @@ Follows PAPER.md in its order and notation:
                   line 8), stopping rule (PAPER.md:493 / :507) and locking (BLOPEX active mask,
                   PAPER.md:502; optional hard locking, R35).
   error_bound     Theorem 3 with the perp term ignored.
-  estimate_perp   f2 (R48): k-step Lanczos on the deflated operator (I - V V^T) B (I - V V^T)
-                  ("projected Lanczos", PAPER.md:508), p^ = sqrt(n - p) max(mu + r, 0) in the
-                  Souto-2018 form.
+  perp_bound      f2 (R48): k-step Lanczos on the deflated operator (I - V V^T) B (I - V V^T)
+                  ("projected Lanczos") turned into a randomized upper bound on
+                  lambda_max (Kuczynski-Wozniakowski), p^ = sqrt(n - p) max(ub, 0).
+  direct_bound    the bound of a full eigendecomposition (DIRECT path, R53).
   Context.project the side rule, negation and
                   Pi = V L V^T or A - V L V^T (R4).
 
@@ -110,7 +111,7 @@ class LobpcgResult:
 
 
 def lobpcg_pos(B, X0, tol, max_iter=500, guard=1, q=None, locking="hard", seed=0, ctx=0,
-               call=0, cold=False, guard_tol=0.0, m_max=None):
+               call=0, cold=False, guard_tol=None, m_max=None):
     """Alg. 3: positive eigenpairs of the symmetric matrix B.
 
     X0      n x m start block (warm: previous Ritz block, R27; cold: Philox, R28).
@@ -126,6 +127,8 @@ def lobpcg_pos(B, X0, tol, max_iter=500, guard=1, q=None, locking="hard", seed=0
     n = B.shape[0]
     m_max = n if m_max is None else m_max
     q = q if q else max(int(math.ceil(0.05 * n)), 1)
+    # guard certification theta_g + r_g <= guard_tol, relaxed form with guard_tol = tol (R52)
+    guard_tol = tol if guard_tol is None else guard_tol
     res = LobpcgResult()
     res.expansions = 0
     res.a_passes = 0
@@ -303,38 +306,64 @@ def lobpcg_pos(B, X0, tol, max_iter=500, guard=1, q=None, locking="hard", seed=0
 
 
 def error_bound(B, V, theta, perp=0.0, delta_fp=None):
-    """Theorem 3 for the positive Ritz pairs (V, theta>0) with an explicit
-    B V (reading R16) and the perp term p^ (0 = the paper's choice; R14):
+    """Theorem 3 for the positive Ritz pairs (V, theta>0), certified from an
+    explicit B V (reading R16), with the perp term p^ (0 = the paper's choice; R14):
 
-      eps = sqrt(2 ||R+||_F^2 + p^2) + ||V+^T B V+ - diag(theta+)||_F + delta_fp
+      eps = (1 + e) sqrt(2 ||R+||_F^2 + p^2) + (1 + sqrt 2) d + 7 e theta_max + delta_fp
 
-    The middle term is zero for an exact Rayleigh-Ritz output and bounds the effect of hard
-    locking otherwise (derivation in DESIGN.md R36); delta_fp = 4 n u ||B||_F (R15)."""
+    R+ = B V+ - V+ Theta+, d = ||V+^T B V+ - Theta+||_F (zero for an exact Rayleigh-Ritz output;
+    the hard-locking term, R36), e = ||V+^T V+ - I||_F (R53) and delta_fp = 4 n u ||B||_F (R15).
+    Derivation (R36/R53): Theorem 3 holds for (V, H = V^T B V) whatever the basis of
+    span(V); ||V Theta V^T - V H V^T|| <= d and ||B V - V H|| <= ||R+|| + d give the d terms; the
+    polar factor of a nearly orthonormal V moves V Theta V^T by <= e theta_max (2 + e)."""
     n = B.shape[0]
     pos = theta > 0
     Vp = V[:, pos]
     tp = theta[pos]
     BVp = B @ Vp
     R = BVp - Vp * tp
-    Hd = Vp.T @ BVp - np.diag(tp)
+    d = float(np.linalg.norm(Vp.T @ BVp - np.diag(tp)))
+    e = float(np.linalg.norm(Vp.T @ Vp - np.eye(Vp.shape[1])))
+    thmax = float(np.max(tp)) if tp.size else 0.0
     if delta_fp is None:
         delta_fp = 4 * n * U * np.linalg.norm(B)
-    return math.sqrt(2 * float(np.sum(R * R)) + perp ** 2) + float(np.linalg.norm(Hd)) + delta_fp
+    return ((1 + e) * math.sqrt(2 * float(np.sum(R * R)) + perp ** 2) + (1 + math.sqrt(2)) * d
+            + 7 * e * thmax + delta_fp)
 
 
-def estimate_perp(B, V, steps, seed=0, stream=0, ctx=0, tag=0xC0000000):
-    """f2, reading R48: the perp term of Theorem 3 (PAPER.md:484, ignored by the paper, :508),
-    estimated by `steps` Lanczos steps on D = (I - V V^T) B (I - V V^T) from a Philox start
-    (stream, ctx, tag as the library), with full reorthogonalisation (two classical Gram-Schmidt
-    passes against V and the Lanczos basis). mu = the largest eigenvalue of the Lanczos matrix T_k
-    (cyclic Jacobi), r = beta_k |y_k| its residual norm (the distance from mu to the spectrum of
-    D is at most r), and p^ = sqrt(n - p) max(mu + r, 0): the Frobenius norm of the positive part
-    of D is at most sqrt(n - p) lambda_max(D) (P:37's form), and lambda_max(D) <= mu + r whenever
-    the Lanczos start vector has a component along the top eigenvector (a random start: with
-    probability 1). Returns (mu, r, p^); an empty complement or steps = 0 gives (0, 0, 0)."""
+def direct_bound(A, V, w):
+    """Bound for a full eigendecomposition (the DIRECT path, reading R53): Theorem 3 with V~ = the
+    eigenvectors of the positive eigenvalues; its perp term is at most (1 + e) ||A V- - V- w-||_F,
+    because Pi(V-^T A V-) is the distance of V-^T A V- to the NSD cone, at most its distance
+    ||V-^T A V- - diag(w-)||_F to the NSD matrix diag(w-) (w- <= 0), and that is <= ||V-|| ||R-||_F.
+    e is the orthonormality defect of the whole basis ||V^T V - I||_F."""
+    pos = w > 0
+    Rn = A @ V[:, ~pos] - V[:, ~pos] * w[~pos]
+    e = float(np.linalg.norm(V.T @ V - np.eye(V.shape[1])))
+    perp = (1 + e) * float(np.linalg.norm(Rn))
+    return error_bound(A, V, w, perp=perp)
+
+
+def perp_bound(B, V, steps, seed=0, stream=0, ctx=0, tag=0xC0000000, delta=1e-6, start=None):
+    """f2, reading R48 (revised): an upper bound on the perp term of Theorem 3 (PAPER.md:484;
+    ignored by the paper, :508, which names "a projected Lanczos algorithm" for it),
+    ||Pi(V_perp^T B V_perp)||_F <= sqrt(n - p) max(lambda_max(D), 0), D = B on span(V)^perp.
+
+    `steps` Lanczos steps on D = (I - V V^T) B (I - V V^T) from a Philox start (stream, ctx, tag as
+    the library; `start` overrides it, for tests), full reorthogonalisation (two classical
+    Gram-Schmidt passes against V and the Lanczos basis); mu = the largest eigenvalue of T_k
+    (cyclic Jacobi). Kuczynski & Wozniakowski (1992): for a PSD M of order N and a start uniform on
+    the sphere, P{xi_k < (1 - eps) lambda_1(M)} <= 1.648 sqrt(N) exp(-sqrt(eps) (2k - 1)). With
+    M = D - c I, c = -||B||_F <= lambda_min(D), with probability >= 1 - delta:
+        lambda_max(D) <= c + (mu - c) / (1 - eps),  sqrt(eps) = ln(1.648 sqrt(N) / delta) / (2k - 1);
+    eps >= 1 gives the trivial lambda_max(D) <= ||B||_F. A breakdown (invariant Krylov space) or
+    k = N makes mu = lambda_max(D) itself (a random start meets every eigenspace). The guarantee is
+    over the draw of the start: a matrix built against a known start can defeat it.
+    Returns (mu, ub, p^); an empty complement or steps = 0 gives (0, 0, 0)."""
     n = B.shape[0]
     p = V.shape[1]
-    k = min(int(steps), n - p)
+    N = n - p
+    k = min(int(steps), N)
     if k <= 0:
         return 0.0, 0.0, 0.0
 
@@ -346,12 +375,13 @@ def estimate_perp(B, V, steps, seed=0, stream=0, ctx=0, tag=0xC0000000):
                 w = w - Q @ (Q.T @ w)
         return w
 
-    q = gaussian_block(n, 1, seed, stream, ctx=ctx, tag=tag)[:, 0]
+    q = gaussian_block(n, 1, seed, stream, ctx=ctx, tag=tag)[:, 0] if start is None else np.array(start, float)
     q = deflate(q, np.zeros((n, 0)))
     q = q / np.linalg.norm(q)
     Q = q[:, None]
     alpha, beta = [], []
     anorm = float(np.linalg.norm(B))
+    breakdown = False
     for j in range(k):
         w = B @ Q[:, j]
         if p:
@@ -360,18 +390,26 @@ def estimate_perp(B, V, steps, seed=0, stream=0, ctx=0, tag=0xC0000000):
         w = deflate(w, Q)
         b = float(np.linalg.norm(w))
         beta.append(b)
-        if b <= 1e-14 * max(anorm, 1e-300) or j == k - 1:
+        if b <= 1e-14 * max(anorm, 1e-300):
+            breakdown = True
+            break
+        if j == k - 1:
             break
         Q = np.column_stack([Q, w / b])
     kk = len(alpha)
     T = np.diag(alpha)
     for i in range(kk - 1):
         T[i, i + 1] = T[i + 1, i] = beta[i]
-    w_, Y, _ = jacobi_eig(T)
-    top = int(np.argmax(w_))
-    mu = float(w_[top])
-    r = abs(beta[kk - 1] * float(Y[kk - 1, top]))
-    return mu, r, math.sqrt(max(n - p, 0)) * max(mu + r, 0.0)
+    w_, _, _ = jacobi_eig(T)
+    mu = float(np.max(w_))
+    if breakdown or kk >= N:
+        ub = mu + 4 * kk * U * anorm
+    else:
+        se = math.log(1.648 * math.sqrt(N) / delta) / (2 * kk - 1)
+        eps = se * se
+        c = -anorm
+        ub = anorm if eps >= 1 else min(anorm, c + (mu - c) / (1 - eps))
+    return mu, ub, math.sqrt(N) * max(ub, 0.0)
 
 
 # --------------------------------------------------------------------------- context
@@ -491,5 +529,5 @@ class Context:
         else:
             self.X = None
             self.block_side = 0
-        info.update(status=OK, iters=0, npos=int(np.sum(pos)), err_bound=0.0, side=DIRECT, w=w)
+        info.update(status=OK, iters=0, npos=int(np.sum(pos)), err_bound=direct_bound(A, V, w), side=DIRECT, w=w)
         return Pi, info

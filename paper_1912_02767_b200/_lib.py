@@ -31,7 +31,7 @@ class Params(ctypes.Structure):
         ("guard", ctypes.c_int), ("side", ctypes.c_int), ("locking", ctypes.c_int),
         ("keep_extra", ctypes.c_int), ("m_max", ctypes.c_int), ("seed", ctypes.c_uint64),
         ("ctx_id", ctypes.c_uint32), ("profile", ctypes.c_int), ("host_io", ctypes.c_int),
-        ("perp_steps", ctypes.c_int),
+        ("perp_steps", ctypes.c_int), ("perp_delta", ctypes.c_double),
     ]
 
 
@@ -46,6 +46,8 @@ class Info(ctypes.Structure):
         ("amul_bytes", ctypes.c_double), ("amul_ms", ctypes.c_double), ("amul_launches", ctypes.c_int),
         ("last_pos", ctypes.c_int), ("last_neg", ctypes.c_int), ("launches", ctypes.c_int),
         ("dropped", ctypes.c_int), ("phase_ms", ctypes.c_double * 12), ("perp_est", ctypes.c_double),
+        ("orth_defect", ctypes.c_double), ("perp_mu", ctypes.c_double), ("tri_ms", ctypes.c_double),
+        ("tri_launches", ctypes.c_int), ("tri_flops", ctypes.c_double),
     ]
 
     def as_dict(self):

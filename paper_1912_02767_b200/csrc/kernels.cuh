@@ -940,6 +940,35 @@ __global__ void __launch_bounds__(NT) offdiag_fro_kernel(int s, const double* __
   if (threadIdx.x == 0) out[0] = sqrt(acc);
 }
 
+// Certification defects (a10, R16/R36): out = sqrt(sum over (i, j) of (H_ij - delta_ij d_i)^2) with
+// d_i = diag[i] (or dconst when diag is NULL), restricted to the pairs with mask[i] > 0 and
+// mask[j] > 0 when mask is given (the positive block of a DIRECT eigendecomposition).
+template <int NT>
+__global__ void __launch_bounds__(NT) defect_fro_kernel(int s, const double* __restrict__ H, int ld,
+                                                        const double* __restrict__ diag, double dconst,
+                                                        const double* __restrict__ mask, double* __restrict__ out) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  for (int64_t e = threadIdx.x; e < (int64_t)s * s; e += NT) {
+    int i = (int)(e % s), j = (int)(e / s);
+    if (mask && !(mask[i] > 0.0 && mask[j] > 0.0)) continue;
+    double v = H[IDX(i, j, ld)] - (i == j ? (diag ? diag[i] : dconst) : 0.0);
+    acc += v * v;
+  }
+  acc = block_sum<NT>(acc, red);
+  if (threadIdx.x == 0) out[0] = sqrt(acc);
+}
+
+// dense symmetric tridiagonal T (k x k, ld) from its diagonal a and off-diagonal b (f2 Lanczos matrix)
+__global__ void tridiag_dense_kernel(int k, const double* __restrict__ a, const double* __restrict__ b,
+                                     double* __restrict__ T, int ld) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)k * k;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int i = (int)(e % k), j = (int)(e / k);
+    T[IDX(i, j, ld)] = i == j ? a[i] : ((i == j + 1 || j == i + 1) ? b[min(i, j)] : 0.0);
+  }
+}
+
 __global__ void count_pos_kernel(int s, const double* __restrict__ w, int* __restrict__ out) {
   __shared__ int cnt;
   if (threadIdx.x == 0) cnt = 0;

@@ -543,6 +543,13 @@ struct EighScratch {
   void* mark_obj = nullptr;  // optional phase marker (profile bit 1): mark_fn(mark_obj, phase)
   int (*mark_fn)(void*, int) = nullptr;
   int mark(int ph) const { return mark_fn ? mark_fn(mark_obj, ph) : 0; }
+  // optional timing of the tridiagonalisation launch (profile bit 2): tri_fn(mark_obj, 0 / 1) around it
+  int (*tri_fn)(void*, int) = nullptr;
+  int tri(int e) const { return tri_fn ? tri_fn(mark_obj, e) : 0; }
+  // side stream + fork/join events for the T factors of the back-transformation (owned by the caller:
+  // the context, or psdproj_eigh for the duration of its call)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_f = nullptr, ev_j = nullptr;
 };
 
 // `steps` Newton-Schulz steps Y <- Y (3I - Y^T Y) / 2; w.dev records max|Y^T Y - I| before the last
@@ -583,6 +590,7 @@ static int eigh_top(cudaStream_t st, int s, const double* Hs, int ldh, int m, do
   static int tri_dbg = getenv("PSDPROJ_TRI_DBG") ? atoi(getenv("PSDPROJ_TRI_DBG")) : 0;  // timing experiments only
   if (want_prof && !dprof) CK(cudaMalloc(&dprof, 16 * 12 * sizeof(long long)));
   if (want_prof) CK(cudaMemsetAsync(dprof, 0, 16 * 12 * sizeof(long long), st));
+  TRY(w.tri(0));
 #define TRI_LAUNCH(PL, NTH, GA, CSZ, SMEM)                                                                         \
   TRY(launch_cluster(tridiag_cluster_kernel<PL, NTH, GA>, CSZ, NTH, SMEM, st, s, Hs, ldh, w.td, w.te, w.ttau, w.Vh, \
                      w.ldv, dprof, w.tG, tri_dbg))
@@ -698,6 +706,7 @@ static int eigh_top(cudaStream_t st, int s, const double* Hs, int ldh, int m, do
     CKL();
   }
 #undef TRI_LAUNCH
+  TRY(w.tri(1));
   if (want_prof && tcs) {
     long long h[192];
     CK(cudaStreamSynchronize(st));
@@ -730,16 +739,12 @@ static int eigh_top(cudaStream_t st, int s, const double* Hs, int ldh, int m, do
   const bool wy = s > 2 && bt_mode == 0 && (s <= 32 * 20 || col_ok) && m > 0;
   cudaEvent_t tri_side_join = nullptr;
   if (wy) {
-    static thread_local cudaStream_t side = nullptr;
-    static thread_local cudaEvent_t ev_f = nullptr, ev_j = nullptr;
-    if (!side) {
-      CK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
-      CK(cudaEventCreateWithFlags(&ev_f, cudaEventDisableTiming));
-      CK(cudaEventCreateWithFlags(&ev_j, cudaEventDisableTiming));
-    }
+    cudaStream_t side = w.side;
+    cudaEvent_t ev_f = w.ev_f, ev_j = w.ev_j;
+    if (!side || !ev_f || !ev_j) return set_err(PSDPROJ_E_INVALID, "eigensolver side stream missing");
     // the T factors of the compact-WY back-transformation need only the reflectors: computed on a
-    // side stream, hidden behind the bisection and inverse iteration (thread_local: batched calls
-    // come from several host threads)
+    // side stream, hidden behind the bisection and inverse iteration (the stream and events belong to
+    // the caller's context, so concurrent contexts never share them)
     CK(cudaEventRecord(ev_f, st));
     CK(cudaStreamWaitEvent(side, ev_f, 0));
     larft_kernel<<<cdiv(s - 2, WY_PB), 256, 0, side>>>(s, w.Vh, w.ldv, w.ttau, w.tG);
@@ -886,6 +891,10 @@ struct psdproj_ctx_s {
   cudaStream_t st2 = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int* d_flag = nullptr;  // residency signal of the side-stream Cholesky (sequence number)
+  // eigensolver side stream (T factors of the back-transformation) and its fork/join events
+  cudaStream_t st3 = nullptr;
+  cudaEvent_t ev3_f = nullptr, ev3_j = nullptr;
+  std::vector<cudaEvent_t> tev;  // tridiagonalisation timing events (profile & 4)
   int chol_seq = 0;
   double* part2 = nullptr;
 };
@@ -1119,6 +1128,13 @@ extern "C" int psdproj_destroy(psdproj_ctx c) {
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
   if (c->st2) cudaStreamDestroy(c->st2);
+  if (c->st3) {
+    cudaStreamSynchronize(c->st3);
+    cudaStreamDestroy(c->st3);
+  }
+  if (c->ev3_f) cudaEventDestroy(c->ev3_f);
+  if (c->ev3_j) cudaEventDestroy(c->ev3_j);
+  for (auto e : c->tev) cudaEventDestroy(e);
   if (c->d_flag) cudaFree(c->d_flag);
   delete c;
   return PSDPROJ_OK;
@@ -1146,6 +1162,7 @@ struct Run {
   int ihost = 0;  // next free int slot in the pinned buffer (per iteration)
   int rr_npos = 0;  // positive Ritz values among all s of the last Rayleigh-Ritz (expansion test)
   int nev = 0;
+  int ntev = 0;  // timed tridiagonalisation launches (profile & 4)
   double anorm = 0.0;
   std::vector<int> marks;  // phase id of each recorded phase event (profile & 2)
 
@@ -1346,10 +1363,32 @@ struct Run {
     w.tscr_elems = c->tscr_elems;
     w.mark_obj = this;
     w.mark_fn = [](void* o, int ph) { return static_cast<Run*>(o)->mark(ph); };
+    w.tri_fn = [](void* o, int e) { return static_cast<Run*>(o)->tri_mark(e); };
+    if (!c->st3) {
+      if (cudaStreamCreateWithFlags(&c->st3, cudaStreamNonBlocking) != cudaSuccess ||
+          cudaEventCreateWithFlags(&c->ev3_f, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&c->ev3_j, cudaEventDisableTiming) != cudaSuccess)
+        c->st3 = nullptr;  // eigh_top reports the missing stream
+    }
+    w.side = c->st3; w.ev_f = c->ev3_f; w.ev_j = c->ev3_j;
     return w;
+  }
+  // profile bit 2: events around every tridiagonalisation launch (the step's dominant kernel)
+  int tri_mark(int e) {
+    if (!(c->prm.profile & 4)) return 0;
+    const size_t k = 2 * (size_t)ntev + (e ? 1 : 0);
+    while (c->tev.size() <= k) {
+      cudaEvent_t ev_;
+      CK(cudaEventCreate(&ev_));
+      c->tev.push_back(ev_);
+    }
+    CK(cudaEventRecord(c->tev[k], st));
+    if (e) ntev++;
+    return 0;
   }
   int tri_eig(int s, const double* Hs, int ldh, int m, double* lam, double* Yv, int ldy, int* npos, bool mgs,
               int ns_steps = 2) {
+    if (info && (c->prm.profile & 4)) info->tri_flops += 4.0 / 3.0 * s * (double)s * s;  // Householder tridiagonalisation
     return eigh_top(st, s, Hs, ldh, m, lam, Yv, ldy, npos, eig_scratch(), c->part, c->part_elems, mgs, ns_steps);
   }
   // Rayleigh-Ritz on the pencil (H, G) in c->G / c->Hm (s x s, ld s_max):
@@ -1487,6 +1526,51 @@ static int keep_count(const psdproj_ctx_s* c, int p, int m) {
   return std::min(m, p + extra);
 }
 
+// ------------------------------------------------------------------ a10: certification (R16, R36, R53)
+// Theorem 3 needs the residual R = B V - V Theta of the RETURNED vectors: one
+// explicit block multiply B V at exit (R16; the implicitly rotated B X drifts by ~u ||C'|| per
+// iteration), the squared column norms of R, the defect d = ||V^T B V - Theta||_F (hard-locked
+// columns are frozen, so V^T B V is only nearly diagonal, R36) and the orthonormality defect
+// e = ||V^T V - I||_F (R53). V: nl x p (ld, local rows), d_theta aligned with V's columns, BV: nl x p
+// scratch, Hbuf: p x p scratch (ldh). pos_mask: restrict d to the pairs with theta > 0 (DIRECT).
+struct Cert {
+  std::vector<double> r2;  // squared residual norms, one per column of V
+  double defect = 0.0, orth = 0.0;
+};
+static int certify(Run& run, double sgn, const double* A, int lda, const double* V, int p, const double* d_theta,
+                   double* BV, double* Hbuf, int ldh, bool pos_mask, Cert& out) {
+  psdproj_ctx_s* c = run.c;
+  cudaStream_t st = run.st;
+  const int ld = c->ld, nl = c->nr;
+  out.r2.assign(p, 0.0);
+  out.defect = out.orth = 0.0;
+  if (p <= 0) return 0;
+  TRY(run.amul(sgn, A, lda, V, ld, p, BV, ld));
+  TRY(launch_pdl(resid_norm_kernel<256>, dim3(p), dim3(256), 0, st, nl, V, ld, (const double*)BV, ld, d_theta,
+                 (double*)nullptr, 0, c->d_r, 1));
+  TRY(run.allreduce(c->d_r, p));  // sums of squares over the ranks' rows (row-sharded mode)
+  TRY(run.gram(p, p, V, ld, BV, ld, Hbuf, ldh));
+  defect_fro_kernel<1024><<<1, 1024, 0, st>>>(p, Hbuf, ldh, d_theta, 0.0, pos_mask ? d_theta : nullptr,
+                                               c->d_scal + 32);
+  CKL();
+  TRY(run.gram(p, p, V, ld, V, ld, Hbuf, ldh));
+  defect_fro_kernel<1024><<<1, 1024, 0, st>>>(p, Hbuf, ldh, nullptr, 1.0, nullptr, c->d_scal + 33);
+  CKL();
+  CK(cudaMemcpyAsync(c->h_d, c->d_r, sizeof(double) * p, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(c->h_d + c->h_d_len - 40, c->d_scal + 32, sizeof(double) * 2, cudaMemcpyDeviceToHost, st));
+  TRY(run.sync());
+  out.r2.assign(c->h_d, c->h_d + p);
+  out.defect = c->h_d[c->h_d_len - 40];
+  out.orth = c->h_d[c->h_d_len - 39];
+  return 0;
+}
+
+// eps = (1 + e) sqrt(2 rs + perp^2) + (1 + sqrt 2) d + 7 e theta_max + 4 n u ||A||_F   (R36, R53, R15)
+static double theorem3_bound(int n, double rs, double perp, double defect, double orth, double thmax, double anorm) {
+  return (1.0 + orth) * std::sqrt(2.0 * rs + perp * perp) + (1.0 + std::sqrt(2.0)) * defect +
+         7.0 * orth * std::max(thmax, 0.0) + 4.0 * n * PSD_U * anorm;
+}
+
 // ------------------------------------------------------------------ DIRECT path (a13)
 static int direct_path(Run& run, const double* A, int lda, double* Pi, int ldpi) {
   psdproj_ctx_s* c = run.c;
@@ -1521,6 +1605,32 @@ static int direct_path(Run& run, const double* A, int lda, double* Pi, int ldpi)
   std::vector<int> order(c->h_i, c->h_i + n);
   int p = 0;
   while (p < n && w[p] > 0.0) ++p;
+  // a10 for DIRECT (R53), before the assembly (Pi may alias A): Theorem 3 with V~ = the computed positive eigenvectors; its perp term is
+  // bounded by the residual of the others: ||Pi(V-^T A V-)||_F = dist(V-^T A V-, NSD) <=
+  // ||V-^T A V- - Theta-||_F <= ||V-|| ||A V- - V- Theta-||_F (Theta- <= 0 is in the NSD cone)
+  {
+    const bool tri = (dmode == 0 && n <= EIG_MAX);
+    const double* thcol = tri ? c->d_ths : c->d_w;  // eigenvalues aligned with V's columns
+    std::vector<double> wcol(n);
+    for (int i = 0; i < n; ++i) wcol[order[i]] = w[i];
+    Cert ct;
+    TRY(certify(run, 1.0, A, lda, V, n, thcol, c->T2, c->jM, c->NJ, true, ct));
+    double rsp = 0.0, rsn = 0.0, thmax = 0.0;
+    for (int j = 0; j < n; ++j) {
+      if (wcol[j] > 0.0) {
+        rsp += ct.r2[j];
+        thmax = std::max(thmax, wcol[j]);
+      } else {
+        rsn += ct.r2[j];
+      }
+    }
+    const double perp = (1.0 + ct.orth) * std::sqrt(rsn);
+    run.info->resid_fro = std::sqrt(rsp);
+    run.info->lock_defect = ct.defect;
+    run.info->orth_defect = ct.orth;
+    run.info->perp_est = perp;
+    run.info->err_bound = theorem3_bound(n, rsp, perp, ct.defect, ct.orth, thmax, run.anorm);
+  }
   // Pi = V+ diag(w+) V+^T
   std::vector<int> pidx(order.begin(), order.begin() + p);
   TRY(run.gather(n, p, c->T2, ld, V, ld, pidx));
@@ -1546,7 +1656,6 @@ static int direct_path(Run& run, const double* A, int lda, double* Pi, int ldpi)
   c->have_counts = true;
   run.info->npos = p;
   run.info->m = n;
-  run.info->err_bound = 0.0;
   // seed the warm block for the side the next call will use
   int nxt = select_mode(c);
   if (nxt == PSDPROJ_SIDE_POS || nxt == PSDPROJ_SIDE_NEG) {
@@ -1574,63 +1683,28 @@ static int direct_path(Run& run, const double* A, int lda, double* Pi, int ldpi)
 }
 
 // ------------------------------------------------------------------ f2: perp term (R48)
-// Symmetric eigenvalues / last components of the top eigenvector of a small dense matrix (cyclic
-// Jacobi on the host: k <= m_max Lanczos steps).
-static void small_sym_top(int k, std::vector<double>& T, double* mu, double* ylast) {
-  std::vector<double> Vm((size_t)k * k, 0.0);
-  for (int i = 0; i < k; ++i) Vm[(size_t)i * k + i] = 1.0;
-  for (int sweep = 0; sweep < 60; ++sweep) {
-    double off = 0.0, fro = 0.0;
-    for (int i = 0; i < k; ++i)
-      for (int j = 0; j < k; ++j) {
-        fro += T[(size_t)i * k + j] * T[(size_t)i * k + j];
-        if (i != j) off += T[(size_t)i * k + j] * T[(size_t)i * k + j];
-      }
-    if (off <= 1e-30 * fro || off == 0.0) break;
-    for (int pq = 0; pq < k; ++pq)
-      for (int qq = pq + 1; qq < k; ++qq) {
-        const double apq = T[(size_t)pq * k + qq];
-        if (apq == 0.0) continue;
-        const double app = T[(size_t)pq * k + pq], aqq = T[(size_t)qq * k + qq];
-        const double th = 0.5 * (aqq - app) / apq;
-        const double t = (th >= 0 ? 1.0 : -1.0) / (std::fabs(th) + std::sqrt(th * th + 1.0));
-        const double cs = 1.0 / std::sqrt(t * t + 1.0), sn = t * cs;
-        for (int r = 0; r < k; ++r) {  // columns pq, qq
-          const double a = T[(size_t)r * k + pq], b = T[(size_t)r * k + qq];
-          T[(size_t)r * k + pq] = cs * a - sn * b;
-          T[(size_t)r * k + qq] = sn * a + cs * b;
-        }
-        for (int r = 0; r < k; ++r) {  // rows pq, qq
-          const double a = T[(size_t)pq * k + r], b = T[(size_t)qq * k + r];
-          T[(size_t)pq * k + r] = cs * a - sn * b;
-          T[(size_t)qq * k + r] = sn * a + cs * b;
-        }
-        for (int r = 0; r < k; ++r) {
-          const double a = Vm[(size_t)r * k + pq], b = Vm[(size_t)r * k + qq];
-          Vm[(size_t)r * k + pq] = cs * a - sn * b;
-          Vm[(size_t)r * k + qq] = sn * a + cs * b;
-        }
-      }
-  }
-  int top = 0;
-  for (int i = 1; i < k; ++i)
-    if (T[(size_t)i * k + i] > T[(size_t)top * k + top]) top = i;
-  *mu = T[(size_t)top * k + top];
-  *ylast = Vm[(size_t)(k - 1) * k + top];
-}
-
-// k Lanczos steps on D = (I - V V^T) B (I - V V^T) (V: n x p, orthonormal) from a Philox start
-// (tag 0xC0000000), full reorthogonalisation (two CGS passes against V and the Lanczos basis, held in
-// c->R). mu = top eigenvalue of T_k, r = beta_k |y_k|, perp = sqrt(n - p) max(mu + r, 0).
+// Upper bound on the perp term of Theorem 3, ||Pi(V~perp^T B V~perp)||_F <= sqrt(n - p) max(lambda_max(D), 0)
+// with D = B restricted to span(V)^perp (the "projected Lanczos" of PAPER.md:508).
+// k Lanczos steps on D = (I - V V^T) B (I - V V^T) (V: n x p, orthonormal) from a Philox start (tag
+// 0xC0000000, uniform on the sphere of span(V)^perp after deflation), full reorthogonalisation (two CGS
+// passes against V and the Lanczos basis, held in c->R); mu = the largest eigenvalue of the Lanczos
+// matrix T_k (the path's tridiagonal eigensolver). Kuczynski & Wozniakowski (1992): for a PSD matrix M
+// of order N, P{xi_k < (1 - eps) lambda_1(M)} <= 1.648 sqrt(N) exp(-sqrt(eps) (2k - 1)). Applied to
+// M = D - c I with c = -||A||_F <= lambda_min(D) (certified), with probability >= 1 - delta:
+//   lambda_max(D) <= c + (mu - c) / (1 - eps),  sqrt(eps) = ln(1.648 sqrt(N) / delta) / (2k - 1)
+// (vacuous when eps >= 1: then lambda_max(D) <= ||A||_F is used). A Lanczos breakdown (invariant
+// Krylov space) or k = N gives mu = lambda_max(D) itself (a random start has a component along every
+// eigenspace with probability 1). Reading R48 (revised in round 2).
 static int perp_estimate(Run& run, double sgn, const double* A, int lda, const double* V, int p, int steps,
                          double* perp) {
   psdproj_ctx_s* c = run.c;
   const int n = c->n, ld = c->ld, ldm = c->s_max, nl = c->nr;
-  const int k = std::min(steps, std::min(n - p, c->m_max - 1));
+  const int neff = n - p;
+  const int k = std::min(steps, std::min(neff, c->m_max - 1));
   *perp = 0.0;
-  if (k <= 0) return 0;
+  if (neff <= 0 || k <= 0) return 0;
   double* Q = c->R;   // n x (k + 1)
-  double* w = c->T2;  // n x 1 (free after the lock-defect term)
+  double* w = c->T2;  // n x 1 (free after the certification)
   auto deflate = [&](double* z, int nq) -> int {
     for (int pass = 0; pass < 2; ++pass) {
       if (p > 0) {
@@ -1648,7 +1722,9 @@ static int perp_estimate(Run& run, double sgn, const double* A, int lda, const d
   TRY(deflate(Q, 0));
   TRY(run.normalize(nl, 1, Q, ld, nullptr, 0));
   std::vector<double> alpha, beta;
-  const double tiny = 1e-14 * std::max(run.anorm, 1e-300);
+  const double anorm = std::max(run.anorm, 1e-300);
+  const double tiny = 1e-14 * anorm;
+  bool breakdown = false;
   for (int j = 0; j < k; ++j) {
     double* qj = Q + (size_t)j * ld;
     TRY(run.amul(sgn, A, lda, qj, ld, 1, w, ld));
@@ -1664,20 +1740,39 @@ static int perp_estimate(Run& run, double sgn, const double* A, int lda, const d
     TRY(run.sync());
     alpha.push_back(c->h_d[0]);
     beta.push_back(c->h_d[1]);
-    if (c->h_d[1] <= tiny || j == k - 1) break;
+    if (c->h_d[1] <= tiny) {
+      breakdown = true;
+      break;
+    }
+    if (j == k - 1) break;
     CK(cudaMemcpy2DAsync(Q + (size_t)(j + 1) * ld, (size_t)ld * 8, w, (size_t)ld * 8, (size_t)nl * 8, 1,
                          cudaMemcpyDeviceToDevice, run.st));
   }
+  // mu = lambda_max(T_k) on the device (T_k from the host-read alpha, beta: marshalling only)
   const int kk = (int)alpha.size();
-  std::vector<double> T((size_t)kk * kk, 0.0);
   for (int i = 0; i < kk; ++i) {
-    T[(size_t)i * kk + i] = alpha[i];
-    if (i + 1 < kk) T[(size_t)i * kk + i + 1] = T[(size_t)(i + 1) * kk + i] = beta[i];
+    c->h_d[i] = alpha[i];
+    c->h_d[kk + i] = beta[i];
   }
-  double mu = 0.0, yl = 0.0;
-  small_sym_top(kk, T, &mu, &yl);
-  const double r = std::fabs(beta[kk - 1] * yl);
-  *perp = std::sqrt((double)std::max(n - p, 0)) * std::max(mu + r, 0.0);
+  CK(cudaMemcpyAsync(c->d_r, c->h_d, sizeof(double) * 2 * kk, cudaMemcpyHostToDevice, run.st));
+  tridiag_dense_kernel<<<grid1d((size_t)kk * kk), 256, 0, run.st>>>(kk, c->d_r, c->d_r + kk, c->Hh, ldm);
+  CKL();
+  TRY(run.tri_eig(kk, c->Hh, ldm, 1, c->d_ths, c->Y, ldm, c->tnpos, false, 1));
+  CK(cudaMemcpyAsync(c->h_d, c->d_ths, sizeof(double), cudaMemcpyDeviceToHost, run.st));
+  TRY(run.sync());
+  const double mu = c->h_d[0];
+  const double delta = c->prm.perp_delta > 0.0 ? c->prm.perp_delta : 1e-6;
+  double ub;
+  if (breakdown || kk >= neff) {
+    ub = mu + 4.0 * kk * PSD_U * anorm;
+  } else {
+    const double se = std::log(1.648 * std::sqrt((double)neff) / delta) / (2.0 * kk - 1.0);
+    const double eps = se * se;
+    const double c0 = -anorm;
+    ub = eps >= 1.0 ? anorm : std::min(anorm, c0 + (mu - c0) / (1.0 - eps));
+  }
+  run.info->perp_mu = mu;
+  *perp = std::sqrt((double)neff) * std::max(ub, 0.0);
   return 0;
 }
 
@@ -1815,7 +1910,10 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
       }
     }
     int mtot = nL + mU;
-    bool guard_ok = (mtot >= n) ? true : (has_guard && g_th + g_r <= 0.0);
+    // guard certification in the relaxed form theta_g + r_g <= tol (R52): the
+    // eigenvalue it could hide is then <= tol; with the paper's loose schedule (10/k^1.01)
+    // the strict form (<= 0) would demand r_g <= |theta_g| whatever the tolerance
+    bool guard_ok = (mtot >= n) ? true : (has_guard && g_th + g_r <= tol);
     bool converged = conv_pos && guard_ok && qe == 0 && !(cold && k == 0);
     if (converged) {
       status = PSDPROJ_OK;
@@ -1900,6 +1998,7 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
     }
     int offW = mU, offE = mU + a, offP = mU + a + qe;
     int s = offP + ap;
+    if (getenv("PSDPROJ_TRACE")) fprintf(stderr, "basis k=%d s=%d mU=%d a=%d ap=%d qe=%d nL=%d\n", k, s, mU, a, ap, qe, nL);
     if (s > c->s_max) return set_err(PSDPROJ_E_CAPACITY, "RR basis %d > s_max %d", s, c->s_max);
     // W = R_J (+ pending expansion E) and P_J sit contiguously in S: [W E P] at offW; both are
     // projected against the locked block and X_U in one pass (one Gram + one update GEMM each)
@@ -2091,27 +2190,30 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
   TRY(run.gather(nl, (int)upos.size(), V + (size_t)lpos.size() * ld, ld, c->S, ld, upos));
   for (int j = 0; j < p; ++j) c->h_d[j] = wts[j];
   CK(cudaMemcpyAsync(c->d_w, c->h_d, sizeof(double) * std::max(p, 1), cudaMemcpyHostToDevice, st));
-  double lock_def = 0.0;
-  if (hard && nL > 0 && p > 0) {
-    TRY(run.gather(nl, (int)lpos.size(), BV, ld, c->BXL, ld, lpos));
-    TRY(run.gather(nl, (int)upos.size(), BV + (size_t)lpos.size() * ld, ld, c->BS, ld, upos));
-    TRY(run.gram(p, p, V, ld, BV, ld, c->Y, ldm));
-    offdiag_fro_kernel<1024><<<1, 1024, 0, st>>>(p, c->Y, ldm, c->d_w, c->d_scal + 8);
-    CKL();
-    CK(cudaMemcpyAsync(c->h_d + c->h_d_len - 8, c->d_scal + 8, sizeof(double), cudaMemcpyDeviceToHost, st));
-    TRY(run.sync());
-    lock_def = c->h_d[c->h_d_len - 8];
+  // ---- a10 (R16, R36, R53): certify the returned pairs with an explicit B V+ (one block multiply
+  // of the p kept columns; B V+ of the rotation and of the frozen locked columns is not used)
+  double thmax = 0.0;
+  for (double x : wts) thmax = std::max(thmax, x);
+  Cert ct;
+  TRY(certify(run, sgn, A, lda, V, p, c->d_w, BV, c->Y, ldm, false, ct));
+  rs = 0.0;
+  rmax = 0.0;
+  for (int j = 0; j < p; ++j) {
+    rs += ct.r2[j];
+    rmax = std::max(rmax, std::sqrt(ct.r2[j]));
   }
   // ---- f2 (R48): the perp term by projected Lanczos on (I - V V^T) B (I - V V^T), V = the kept
-  // positive Ritz vectors; p^ = sqrt(n - p) max(mu + r, 0) (0 unless perp_steps > 0)
+  // positive Ritz vectors: a randomized upper bound that holds with probability >= 1 - perp_delta
+  // over the Philox start (0 unless perp_steps > 0: the paper ignores the term)
   double perp = 0.0;
   if (c->prm.perp_steps > 0) TRY(perp_estimate(run, sgn, A, lda, V, p, c->prm.perp_steps, &perp));
   info->perp_est = perp;
-  // ---- Theorem 3 bound (R14-R16, R36): sqrt(2||R+||^2 + p^2) + ||V+^T B V+ - Theta+||_F + 4 n u ||A||_F
+  // ---- Theorem 3 bound (R14-R16, R36, R53)
   info->resid_fro = std::sqrt(rs);
   info->resid_max = rmax;
-  info->lock_defect = lock_def;
-  info->err_bound = std::sqrt(2.0 * rs + perp * perp) + lock_def + 4.0 * n * PSD_U * run.anorm;
+  info->lock_defect = ct.defect;
+  info->orth_defect = ct.orth;
+  info->err_bound = theorem3_bound(n, rs, perp, ct.defect, ct.orth, thmax, run.anorm);
   info->npos = p;
   // ---- a11: Pi = V Theta+ V^T (side +) or A + V Theta+ V^T (side -, pairs of -A)
   if (sgn < 0 && Pi != A) {
@@ -2242,6 +2344,16 @@ static int project_impl(psdproj_ctx c, const double* A, int lda, double* Pi, int
     }
     info->amul_ms = tot;
     info->amul_launches = run.nev;
+  }
+  if ((c->prm.profile & 4) && run.ntev > 0) {
+    double tot = 0.0;
+    for (int i = 0; i < run.ntev; ++i) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, c->tev[2 * i], c->tev[2 * i + 1]));
+      tot += ms;
+    }
+    info->tri_ms = tot;
+    info->tri_launches = run.ntev;
   }
   return rc;
 }
@@ -2505,15 +2617,29 @@ extern "C" int psdproj_eigh(int s, const double* A, int lda, int m, double* w, d
   e.nsM = e.Vh + (size_t)s * s;
   e.nsZ = e.nsM + mm * mm;
   e.nsY = e.nsZ + mm * mm;
-  TRY(eigh_top(st, s, A, lda, m, w, V, ldv, npos, e, nullptr, 0, false));
+  // the side stream and its events live for this call only
+  CK(cudaStreamCreateWithFlags(&e.side, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&e.ev_f, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&e.ev_j, cudaEventDisableTiming));
+  auto release = [&]() {
+    cudaStreamSynchronize(e.side);
+    cudaEventDestroy(e.ev_f);
+    cudaEventDestroy(e.ev_j);
+    cudaStreamDestroy(e.side);
+  };
+  int rc = eigh_top(st, s, A, lda, m, w, V, ldv, npos, e, nullptr, 0, false);
   double dev = 0.0;
-  CK(cudaMemcpyAsync(&dev, e.dev, sizeof(double), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  if (!(dev <= 1e-7)) {
-    TRY(eigh_top(st, s, A, lda, m, w, V, ldv, npos, e, nullptr, 0, true));
-    CK(cudaStreamSynchronize(st));
+  if (rc >= 0 && cudaMemcpyAsync(&dev, e.dev, sizeof(double), cudaMemcpyDeviceToHost, st) == cudaSuccess &&
+      cudaStreamSynchronize(st) == cudaSuccess) {
+    if (!(dev <= 1e-7)) {
+      rc = eigh_top(st, s, A, lda, m, w, V, ldv, npos, e, nullptr, 0, true);
+      if (rc >= 0 && cudaStreamSynchronize(st) != cudaSuccess) rc = set_err(PSDPROJ_E_CUDA, "psdproj_eigh sync");
+    }
+  } else if (rc >= 0) {
+    rc = set_err(PSDPROJ_E_CUDA, "psdproj_eigh sync");
   }
-  return 0;
+  release();
+  return rc < 0 ? rc : 0;
 }
 
 extern "C" int psdproj_cholesky(int t, double* G, int ld, void* stream) {

@@ -14,9 +14,10 @@ def _dev(a):
 
 
 def test_c1_sequence_parity(api):
+    """BASELINE configs[0], all 50 steps of the warm sequence against O-EXACT."""
     cfg = C1()
     ctx = api.Context(cfg.n, seed=7)
-    for t, A, _ in drift_sequence(cfg, steps=6):
+    for t, A, _ in drift_sequence(cfg, steps=cfg.steps):
         Pi, info = ctx.project(_dev(A), 1e-10)
         Pe = project_exact(A)
         Pg = Pi.cpu().numpy()
@@ -40,7 +41,7 @@ def test_planted_parity(api, n, p, side):
         Pi, info = ctx.project(_dev(A), 1e-10)
         err = np.linalg.norm(Pi.cpu().numpy() - Pstar)
         assert err / np.linalg.norm(A) <= 1e-9, (call, err, info)
-        assert info["err_bound"] >= err - 1e-12 * np.linalg.norm(A)
+        assert info["err_bound"] >= err, (call, err, info["err_bound"])
 
 
 # ---------------------------------------------------------------- edge cases
@@ -82,7 +83,7 @@ def test_edge_cases(api, case):
         err = np.linalg.norm(Pi.cpu().numpy() - expect)
         assert info["status"] in (0, 1), info
         assert err <= 1e-9 * max(1.0, np.linalg.norm(A)), (case, call, err, info)
-        assert info["err_bound"] >= err - 1e-12
+        assert info["err_bound"] >= err, (case, call, err, info["err_bound"])
 
 
 def test_nonfinite_input_is_rejected(api):
@@ -105,7 +106,10 @@ def test_direct_path_mixed_spectrum(api):
     Pi, info = ctx.project(_dev(A), 1e-10)
     assert info["side"] == 2
     Pstar = project_exact(A)
-    assert np.linalg.norm(Pi.cpu().numpy() - Pstar) <= 1e-11 * np.linalg.norm(A)
+    err = np.linalg.norm(Pi.cpu().numpy() - Pstar)
+    assert err <= 1e-11 * np.linalg.norm(A)
+    # R53: a real bound on the DIRECT path (explicit residuals of all n pairs), at the rounding level
+    assert err <= info["err_bound"] <= 200 * n * 2.0 ** -53 * np.linalg.norm(A), (err, info["err_bound"])
 
 
 def test_host_io_matches_device(api):
@@ -151,48 +155,46 @@ def test_c4_batched_parity(api):
             nA = np.linalg.norm(mats[k])
             assert infos[k]["status"] in (0, 1), (i, infos[k])
             assert err / nA <= 1e-9, (rnd, i, cfg.sizes[i], err / nA, infos[k]["side"])
-            assert infos[k]["err_bound"] >= err - 1e-12 * nA
+            assert infos[k]["err_bound"] >= err, (rnd, i, err, infos[k]["err_bound"])
         mats = [A + cfg.drift(i, rnd) for A, i in zip(mats, ids)]
 
 
 def test_c3r_reduced_sequence(api):
-    """C3-R at n = 1000 (configs[2] spectrum; closed-form Pi*_t = Q_t max(L, 0) Q_t^T): the
-    returned bound dominates the true error up to the positive eigenvalues the block missed
-    (Theorem 3's perp term, ignored by the paper's bound)."""
+    """C3-R at n = 1000 (configs[2] spectrum; closed-form Pi*_t = Q_t max(L, 0) Q_t^T), every step of
+    a 26-step warm run, run to convergence (status OK): the bound dominates the true error on every
+    call (no allowance) and the error is within the config's accuracy; at tol 1e-10 (steps 0 and 25)
+    the BJ parity threshold 1e-9 holds."""
     from workloads.generators import C3R, rotation_sequence
     cfg = C3R(1000)
-    ctx = api.Context(cfg.n, params=api.default_params(seed=4, max_iter=150))
-    for t, A, Q, lam in rotation_sequence(cfg, steps=3):
-        Pi, info = ctx.project(_dev(A), cfg.tol)
-        Pstar = (Q * np.maximum(lam, 0)) @ Q.T
-        err = np.linalg.norm(Pi.cpu().numpy() - Pstar)
-        pos = np.sort(lam[lam > 0])[::-1]
-        missed = np.sqrt(np.sum(pos[info["npos"]:] ** 2)) if info["npos"] < pos.size else 0.0
-        assert info["npos"] <= pos.size                       # interlacing (PAPER.md:381)
-        assert err <= info["err_bound"] + missed + 1e-9, (t, err, info["err_bound"], missed, info["npos"])
-        assert err / np.linalg.norm(A) <= 1e-4
+    ctx = api.Context(cfg.n, params=api.default_params(seed=4, max_iter=6000))
+    for t, A, Q, lam in rotation_sequence(cfg, steps=26, device="cuda"):
+        tol = 1e-10 if t in (0, 25) else cfg.tol
+        Pi, info = ctx.project(A.contiguous(), tol)
+        Pstar = (Q * torch.clamp(lam, min=0)) @ Q.T
+        err = float(torch.linalg.norm(Pi - Pstar))
+        nA = float(torch.linalg.norm(A))
+        assert info["status"] == 0, (t, info["iters"])
+        assert info["npos"] == 50                              # exactly 5% positive at every step
+        assert info["err_bound"] >= err, (t, err, info["err_bound"])
+        assert err / nA <= (1e-9 if tol == 1e-10 else 2e-9), (t, err / nA)
 
 
-def test_full_size_sampled_entries(api):
-    """BASELINE's full size n = 4000 (the bench workload), one warm C3-R call in the bench's launch
-    configuration: sampled entries of Pi against the closed form, within the Frobenius bound."""
+def test_full_size_full_matrix(api):
+    """BASELINE's full size n = 4000 in the bench's launch configuration (C3-R, tol 1e-7, the bench's
+    max_iter): the whole Pi against the closed form on the GPU, every call bound-verified."""
     from workloads.generators import C3R, rotation_sequence
     cfg = C3R(4000)
-    ctx = api.Context(cfg.n, params=api.default_params(seed=1912, max_iter=60, profile=3))
-    rng = np.random.default_rng(0)
-    for t, A, Q, lam in rotation_sequence(cfg, steps=2, device="cuda"):
+    ctx = api.Context(cfg.n, params=api.default_params(seed=1912, max_iter=4000, profile=0))
+    for t, A, Q, lam in rotation_sequence(cfg, steps=3, device="cuda"):
         Pi, info = ctx.project(A.contiguous(), cfg.tol)
-        if t == 0:
-            continue
-        i = rng.integers(0, cfg.n, 400)
-        j = rng.integers(0, cfg.n, 400)
-        lp = torch.clamp(lam, min=0)
-        ref = ((Q[i] * lp) * Q[j]).sum(dim=1).cpu().numpy()
-        got = Pi[i, j].cpu().numpy()
-        lamc = lam.cpu().numpy()
-        pos = np.sort(lamc[lamc > 0])[::-1]
-        missed = np.sqrt(np.sum(pos[info["npos"]:] ** 2)) if info["npos"] < pos.size else 0.0
-        assert np.abs(got - ref).max() <= info["err_bound"] + missed + 1e-9
+        Pstar = (Q * torch.clamp(lam, min=0)) @ Q.T
+        err = float(torch.linalg.norm(Pi - Pstar))
+        nA = float(torch.linalg.norm(A))
+        assert info["status"] == 0, (t, info)
+        assert info["npos"] == 200
+        assert info["err_bound"] >= err, (t, err, info["err_bound"])
+        assert err / nA <= 2e-9 and info["err_bound"] / nA <= 2e-9, (t, err / nA, info["err_bound"] / nA)
+        assert torch.equal(Pi, Pi.T)
         assert info["launches"] > 0
 
 
@@ -230,7 +232,7 @@ def test_locking_modes_parity(api, locking):
     err = np.linalg.norm(Pi.cpu().numpy() - Pstar)
     assert info["status"] == 0, info
     assert err / np.linalg.norm(A) <= 1e-9
-    assert info["err_bound"] >= err - 1e-12 * np.linalg.norm(A)
+    assert info["err_bound"] >= err, (err, info["err_bound"])
     if locking == 1:
         assert info["locked"] == 0
 
@@ -264,7 +266,7 @@ def test_odd_sizes_parity(api, n, p):
         err = np.linalg.norm(Pi.cpu().numpy() - Pstar)
         assert info["status"] in (0, 1)
         assert err / np.linalg.norm(A) <= 1e-9, (call, err, info["side"], info["iters"])
-        assert info["err_bound"] >= err - 1e-12 * np.linalg.norm(A)
+        assert info["err_bound"] >= err, (call, err, info["err_bound"])
 
 
 def test_tiny_batched_parity(api):

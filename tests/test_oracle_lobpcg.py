@@ -273,3 +273,39 @@ def test_context_negative_side_and_direct():
         P, info = ctx.project(A, 1e-10)
         assert info["mode"] == want
         assert np.linalg.norm(P - Pstar) <= 1e-9 * np.linalg.norm(A)
+
+
+def test_direct_bound_dominates_and_is_tight():
+    """R53: the DIRECT path's bound (Theorem 3 with the perp term bounded by the residual of the
+    non-positive pairs) dominates the error against LAPACK's projection (an independent routine)
+    and stays at the rounding level: eps <= 200 n u ||A||_F."""
+    for seed in range(6):
+        rng = np.random.default_rng(700 + seed)
+        n = int(rng.integers(5, 70))
+        M = rng.standard_normal((n, n)) * 10.0 ** rng.uniform(-3, 3)
+        A = 0.5 * (M + M.T)
+        ctx = L.Context(n, side=L.DIRECT)
+        P, info = ctx.project(A, 1e-10)
+        w, Vf = np.linalg.eigh(A)
+        Pl = (Vf[:, w > 0] * w[w > 0]) @ Vf[:, w > 0].T
+        err = np.linalg.norm(P - Pl)
+        nA = np.linalg.norm(A)
+        assert info["err_bound"] >= err, (seed, err, info["err_bound"])
+        assert info["err_bound"] <= 200 * n * L.U * nA
+
+
+def test_bound_with_perturbed_basis_dominates():
+    """R36/R53: the bound's defect terms cover a basis that is neither exactly orthonormal nor
+    exactly Rayleigh-Ritz (hard-locked columns frozen while the rest rotate): V = the exact
+    positive eigenvectors perturbed by 1e-9 and 1e-6, theta = the exact eigenvalues."""
+    rng = np.random.default_rng(41)
+    n, p = 50, 6
+    lam = np.concatenate([rng.uniform(0.5, 3, p), rng.uniform(-3, -0.5, n - p)])
+    Q = haar_q(rng, n)
+    A = planted(Q, lam)
+    Pstar = (Q * np.maximum(lam, 0)) @ Q.T
+    for eta in (1e-9, 1e-6, 1e-4):
+        V = Q[:, :p] + eta * rng.standard_normal((n, p))
+        th = lam[:p].copy()
+        err = np.linalg.norm((V * th) @ V.T - Pstar)
+        assert L.error_bound(A, V, th) >= err, (eta, err)
