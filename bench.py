@@ -298,7 +298,7 @@ def run_c5_bench(args, rank, world, local, dist):
     from workloads.generators import maxcut_graph
     n = args.n or 2000
     L = maxcut_graph(n=n, p_edge=0.01, seed=501)
-    solver = MaxCutADMM(L, device=f"cuda:{local}")
+    solver = MaxCutADMM(L, device=f"cuda:{local}", adapt_every=40)
     for _ in range(max(args.warmup, 0)):
         solver.step()
     torch.cuda.synchronize()
@@ -318,7 +318,9 @@ def run_c5_bench(args, rank, world, local, dist):
                 "warmup": args.warmup, "ms_per_step": ms / max(its, 1), "higher_is_better": True,
                 "scaling": "none", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": f"C5 MaxCut SDP, ER n={n}, p=0.01, +-1 weights (configs[4]), eps 1e-4",
-                           "rho": solver.rho, "sigma": solver.sigma, "alpha": solver.alpha},
+                           "rho": solver.rho, "sigma": solver.sigma, "alpha": solver.alpha,
+                           "rho_adaptation": "residual balancing every 40 iterations (R58)",
+                           "rho_history": solver.rho_history},
                 "solve_s": ms / 1e3, "admm_iters": out["iters"], "r_prim": out["r_prim"], "r_dual": out["r_dual"],
                 "objective": out["objective"],
                 "lobpcg_iters_per_admm_iter": sum(i["iters"] for i in infos) / max(len(infos), 1),

@@ -59,7 +59,7 @@ typedef struct {
   int guard;      /* minimum non-positive guard columns (R8, R12); default 1                    */
   int side;       /* PSDPROJ_SIDE_*: 0 = one-third rule                          */
   int locking;    /* PSDPROJ_LOCK_SOFT (BLOPEX active mask) or _HARD (default, R35)             */
-  int keep_extra; /* non-positive columns kept in the warm block; <0 => max(guard, ceil(p/10))  */
+  int keep_extra; /* non-positive columns kept in the warm block; <0 => max(guard, ceil(p/10), 16) */
   int m_max;      /* block-width capacity; 0 => ceil(n/3)+1 (wider => DIRECT, R18)              */
   uint64_t seed;  /* Philox4x32-10 key (R11)                                                    */
   uint32_t ctx_id;/* Philox counter word c2 (distinct per cone block)                           */
@@ -70,6 +70,7 @@ typedef struct {
                   /* k-step projected Lanczos upper bound of the perp term added to err_bound     */
   double perp_delta; /* f2: failure probability of that randomized bound (over the Philox start,   */
                      /* Kuczynski-Wozniakowski 1992); 0 => 1e-6                                     */
+  double lock_factor; /* hard locking of a positive pair at r <= lock_factor * tol (R55); 0 => 1     */
 } psdproj_params;
 
 typedef struct {

@@ -19,7 +19,7 @@ from .exact import project_exact
 
 
 def diag_sdp_admm(Q, b=None, w=None, rho=0.1, sigma=1e-6, alpha=1.6, eps=1e-4, max_iter=5000, project=None,
-                  keep_last=False):
+                  keep_last=False, adapt_every=0, adapt_ratio=5.0):
     """Alg. 1 on min <Q, X> s.t. X_ii = b_i (w_i = 1), X PSD. Returns X, objective, iterations, the
     residual history and (keep_last) the last two iterates (x, y) for the certificates."""
     n = Q.shape[0]
@@ -34,8 +34,9 @@ def diag_sdp_admm(Q, b=None, w=None, rho=0.1, sigma=1e-6, alpha=1.6, eps=1e-4, m
     A = np.vstack([D, np.eye(N)])
     ne = eq.size
     q = Q.reshape(-1, order="F")
-    K = sigma * np.eye(N) + rho * (A.T @ A)
-    Kinv = np.linalg.inv(K)  # K is fixed across iterations; line 3's solve is x~ = K^-1 rhs
+    AtA = A.T @ A
+    Kinv = np.linalg.inv(sigma * np.eye(N) + rho * AtA)  # line 3's solve is x~ = K^-1 rhs
+    rhos = [(0, rho)]
     x = np.zeros(N)
     z = np.concatenate([b[eq], np.zeros(N)])
     y = np.zeros(ne + N)
@@ -61,15 +62,23 @@ def diag_sdp_admm(Q, b=None, w=None, rho=0.1, sigma=1e-6, alpha=1.6, eps=1e-4, m
         hist.append((r_prim, r_dual))
         if r_prim <= eps and r_dual <= eps:
             break
+        # reading R58: residual balancing every adapt_every iterations (COSMO); K changes with rho
+        if adapt_every > 0 and k % adapt_every == 0 and r_prim > 0 and r_dual > 0:
+            ratio = r_prim / r_dual
+            if ratio > adapt_ratio or ratio < 1.0 / adapt_ratio:
+                rho = min(1e6, max(1e-6, rho * ratio ** 0.5))
+                Kinv = np.linalg.inv(sigma * np.eye(N) + rho * AtA)
+                rhos.append((k, rho))
     X = x.reshape(n, n, order="F")
-    out = {"X": X, "objective": float(np.sum(Q * X)), "iters": k, "hist": hist}
+    out = {"X": X, "objective": float(np.sum(Q * X)), "iters": k, "hist": hist, "rhos": rhos}
     if keep_last:
         out.update({"x": x, "y": y, "x_prev": prev[0], "y_prev": prev[1], "A": A, "eq": eq, "b": b, "q": q})
     return out
 
 
-def maxcut_admm(L, rho=0.1, sigma=1e-6, alpha=1.6, eps=1e-4, max_iter=5000, project=None):
-    out = diag_sdp_admm(-0.25 * L, rho=rho, sigma=sigma, alpha=alpha, eps=eps, max_iter=max_iter, project=project)
+def maxcut_admm(L, rho=0.1, sigma=1e-6, alpha=1.6, eps=1e-4, max_iter=5000, project=None, adapt_every=0):
+    out = diag_sdp_admm(-0.25 * L, rho=rho, sigma=sigma, alpha=alpha, eps=eps, max_iter=max_iter, project=project,
+                        adapt_every=adapt_every)
     out["objective"] = -out["objective"]  # max 1/4 <L, X>
     return out
 

@@ -111,7 +111,7 @@ class LobpcgResult:
 
 
 def lobpcg_pos(B, X0, tol, max_iter=500, guard=1, q=None, locking="hard", seed=0, ctx=0,
-               call=0, cold=False, guard_tol=None, m_max=None):
+               call=0, cold=False, guard_tol=None, m_max=None, lock_factor=1.0):
     """Alg. 3: positive eigenpairs of the symmetric matrix B.
 
     X0      n x m start block (warm: previous Ritz block, R27; cold: Philox, R28).
@@ -181,7 +181,7 @@ def lobpcg_pos(B, X0, tol, max_iter=500, guard=1, q=None, locking="hard", seed=0
             break
         # locking (R35): hard mode locks converged positive pairs
         if locking == "hard":
-            locked |= pos & (r <= tol)
+            locked |= pos & (r <= lock_factor * tol)  # R55
         Uidx = np.flatnonzero(~locked)
         Lidx = np.flatnonzero(locked)
         # active set J (BLOPEX active mask): unlocked columns with r_i > tol
@@ -463,7 +463,8 @@ class Context:
 
     def _keep(self, theta, m):
         p = int(np.sum(theta > 0))
-        extra = self.keep_extra if self.keep_extra is not None else max(self.guard, int(math.ceil(0.1 * p)), 1)
+        # R37 revised (R56): a guard band of at least 16 columns beyond the positives
+        extra = self.keep_extra if self.keep_extra is not None else max(self.guard, int(math.ceil(0.1 * p)), 16)
         return min(m, p + extra)
 
     def project(self, A, tol):

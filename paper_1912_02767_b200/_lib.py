@@ -31,7 +31,7 @@ class Params(ctypes.Structure):
         ("guard", ctypes.c_int), ("side", ctypes.c_int), ("locking", ctypes.c_int),
         ("keep_extra", ctypes.c_int), ("m_max", ctypes.c_int), ("seed", ctypes.c_uint64),
         ("ctx_id", ctypes.c_uint32), ("profile", ctypes.c_int), ("host_io", ctypes.c_int),
-        ("perp_steps", ctypes.c_int), ("perp_delta", ctypes.c_double),
+        ("perp_steps", ctypes.c_int), ("perp_delta", ctypes.c_double), ("lock_factor", ctypes.c_double),
     ]
 
 

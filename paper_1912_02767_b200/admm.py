@@ -29,9 +29,11 @@ class DiagSDPADMM:
     check_every=40)` stops on a certificate (status 'primal_infeasible' / 'dual_infeasible')."""
 
     def __init__(self, Q, b=None, w=None, rho=0.1, sigma=1e-6, alpha=1.6, device="cuda", params=None, tol_floor=0.0,
-                 tol_override=None):
+                 tol_override=None, adapt_every=0, adapt_ratio=5.0):
         n = Q.shape[0]
         self.n, self.rho, self.sigma, self.alpha = n, float(rho), float(sigma), float(alpha)
+        self.adapt_every, self.adapt_ratio = int(adapt_every), float(adapt_ratio)
+        self.rho_history = [(0, self.rho)]
         self.tol_floor, self.tol_override = tol_floor, tol_override
         dev = torch.device(device)
         self.Q = torch.as_tensor(Q, dtype=torch.float64, device=dev).contiguous()
@@ -67,7 +69,21 @@ class DiagSDPADMM:
                                            p(self.zeh), p(self.Q), n, self.rho, res, pb, pw, st),
               "psdproj_admm_maxcut_step2")
         self.infos.append(info)
-        return max(res[0], res[1]), res[2], info
+        r_p, r_d = max(res[0], res[1]), res[2]
+        self._adapt(r_p, r_d)
+        return r_p, r_d, info
+
+    def _adapt(self, r_p, r_d):
+        """Reading R58 (COSMO-style residual balancing; the paper runs COSMO.jl): every
+        `adapt_every` iterations (0 = fixed rho), if one residual exceeds the other by more than
+        `adapt_ratio`, rho <- rho sqrt(r_prim / r_dual), clipped to [1e-6, 1e6]. Line 3's matrix
+        sigma I + rho A^T A is diagonal here, so a new rho costs nothing; y is kept."""
+        if self.adapt_every <= 0 or self.k % self.adapt_every or not (r_p > 0 and r_d > 0):
+            return
+        ratio = r_p / r_d
+        if ratio > self.adapt_ratio or ratio < 1.0 / self.adapt_ratio:
+            self.rho = min(1e6, max(1e-6, self.rho * ratio ** 0.5))
+            self.rho_history.append((self.k, self.rho))
 
     def _psd_part(self, M):
         """||Pi_S+(M)||_F by the library's DIRECT path (exact eigendecomposition)."""

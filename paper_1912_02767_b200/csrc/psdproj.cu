@@ -34,6 +34,7 @@
 #include "kernels.cuh"
 #include "tridiag.cuh"
 #include "cluster_la.cuh"
+#include "tridiag_tile.cuh"
 
 using namespace psd;
 
@@ -591,12 +592,31 @@ static int eigh_top(cudaStream_t st, int s, const double* Hs, int ldh, int m, do
   if (want_prof && !dprof) CK(cudaMalloc(&dprof, 16 * 12 * sizeof(long long)));
   if (want_prof) CK(cudaMemsetAsync(dprof, 0, 16 * 12 * sizeof(long long), st));
   TRY(w.tri(0));
+  // one-CTA tiled tridiagonalisation (tridiag_tile.cuh) up to s = PSDPROJ_TRI_TILE (default 64: measured
+  // 145 vs 234 us at s = 64 against the one-CTA shared-memory kernel; the 16-CTA cluster kernel is
+  // faster from s ~ 100 up, 230 vs 339 us at s = 128, 567 vs 1183 us at s = 256 -- DESIGN.md §6)
+  static const int tri_tile = getenv("PSDPROJ_TRI_TILE") ? atoi(getenv("PSDPROJ_TRI_TILE")) : 64;
+  const bool use_tile = tri_mode == 0 && s >= 3 && s <= std::min(tri_tile, TT_SMAX);
+  if (use_tile) {
+    static bool tattr = false;
+    if (!tattr) {
+      CK(cudaFuncSetAttribute(tridiag_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)(tri_tile_smem_doubles(TT_SMAX) * sizeof(double))));
+      tattr = true;
+    }
+    tridiag_tile_kernel<<<1, TT_NT, tri_tile_smem_doubles(s) * sizeof(double), st>>>(s, Hs, ldh, w.td, w.te, w.ttau,
+                                                                                      w.Vh, w.ldv);
+    CKL();
+    tcs = 0;
+  }
 #define TRI_LAUNCH(PL, NTH, GA, CSZ, SMEM)                                                                         \
   TRY(launch_cluster(tridiag_cluster_kernel<PL, NTH, GA>, CSZ, NTH, SMEM, st, s, Hs, ldh, w.td, w.te, w.ttau, w.Vh, \
                      w.ldv, dprof, w.tG, tri_dbg))
   static int tri_reg = getenv("PSDPROJ_TRI_NOREG") ? 0 : 1;
   const int kr = cdiv(s, 64), cr = tcs ? cdiv(cdiv(s, tcs), TRI_TCG) : 99;
-  if (tcs && tri_reg && kr <= 8 && cr <= 8 &&
+  if (use_tile) {
+    // done above
+  } else if (tcs && tri_reg && kr <= 8 && cr <= 8 &&
       tri_reg_smem_doubles(s, tcs) * sizeof(double) <= (size_t)CLA_SMEM_BYTES) {
     const size_t tsm = tri_reg_smem_doubles(s, tcs) * sizeof(double);
 #define TRI_REG(KR, CR) \
@@ -1521,8 +1541,11 @@ static int select_mode(psdproj_ctx_s* c) {
 }
 
 static int keep_count(const psdproj_ctx_s* c, int p, int m) {
+  // R37 (revised, R56): p + max(g, ceil(p/10), 16) columns -- a guard band at least 16 wide, so that a
+  // near-zero cluster (C2-cl: 20 eigenvalues within +-5e-3 of 0 next to a gap to -0.1) sits inside the
+  // warm block instead of straddling its edge, where the block's convergence rate collapses
   int extra = c->prm.keep_extra >= 0 ? c->prm.keep_extra
-                                     : std::max(c->prm.guard, std::max(1, (int)std::ceil(0.1 * p)));
+                                     : std::max(std::max(c->prm.guard, 16), std::max(1, (int)std::ceil(0.1 * p)));
   return std::min(m, p + extra);
 }
 
@@ -1687,7 +1710,7 @@ static int direct_path(Run& run, const double* A, int lda, double* Pi, int ldpi)
 // with D = B restricted to span(V)^perp (the "projected Lanczos" of PAPER.md:508).
 // k Lanczos steps on D = (I - V V^T) B (I - V V^T) (V: n x p, orthonormal) from a Philox start (tag
 // 0xC0000000, uniform on the sphere of span(V)^perp after deflation), full reorthogonalisation (two CGS
-// passes against V and the Lanczos basis, held in c->R); mu = the largest eigenvalue of the Lanczos
+// passes against V and the Lanczos basis, held in c->E); mu = the largest eigenvalue of the Lanczos
 // matrix T_k (the path's tridiagonal eigensolver). Kuczynski & Wozniakowski (1992): for a PSD matrix M
 // of order N, P{xi_k < (1 - eps) lambda_1(M)} <= 1.648 sqrt(N) exp(-sqrt(eps) (2k - 1)). Applied to
 // M = D - c I with c = -||A||_F <= lambda_min(D) (certified), with probability >= 1 - delta:
@@ -1700,10 +1723,10 @@ static int perp_estimate(Run& run, double sgn, const double* A, int lda, const d
   psdproj_ctx_s* c = run.c;
   const int n = c->n, ld = c->ld, ldm = c->s_max, nl = c->nr;
   const int neff = n - p;
-  const int k = std::min(steps, std::min(neff, c->m_max - 1));
+  const int k = std::min(std::min(steps, c->s_max), std::min(neff, c->tcols - 1));
   *perp = 0.0;
   if (neff <= 0 || k <= 0) return 0;
-  double* Q = c->R;   // n x (k + 1)
+  double* Q = c->E;   // n x (k + 1): the expansion buffer (ld x max(s_max, n)) is free at exit
   double* w = c->T2;  // n x 1 (free after the certification)
   auto deflate = [&](double* z, int nq) -> int {
     for (int pass = 0; pass < 2; ++pass) {
@@ -1754,8 +1777,9 @@ static int perp_estimate(Run& run, double sgn, const double* A, int lda, const d
     c->h_d[i] = alpha[i];
     c->h_d[kk + i] = beta[i];
   }
-  CK(cudaMemcpyAsync(c->d_r, c->h_d, sizeof(double) * 2 * kk, cudaMemcpyHostToDevice, run.st));
-  tridiag_dense_kernel<<<grid1d((size_t)kk * kk), 256, 0, run.st>>>(kk, c->d_r, c->d_r + kk, c->Hh, ldm);
+  CK(cudaMemcpyAsync(c->d_r, c->h_d, sizeof(double) * kk, cudaMemcpyHostToDevice, run.st));
+  CK(cudaMemcpyAsync(c->d_thU, c->h_d + kk, sizeof(double) * kk, cudaMemcpyHostToDevice, run.st));
+  tridiag_dense_kernel<<<grid1d((size_t)kk * kk), 256, 0, run.st>>>(kk, c->d_r, c->d_thU, c->Hh, ldm);
   CKL();
   TRY(run.tri_eig(kk, c->Hh, ldm, 1, c->d_ths, c->Y, ldm, c->tnpos, false, 1));
   CK(cudaMemcpyAsync(c->h_d, c->d_ths, sizeof(double), cudaMemcpyDeviceToHost, run.st));
@@ -1920,11 +1944,13 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
       break;
     }
     if (k >= c->prm.max_iter) break;
-    // ---- hard locking (R35)
+    // ---- hard locking (R35) at lock_tol = lock_factor * tol (R55: a locked vector is frozen with its
+    // error ~ r / gap, which bounds the residual the columns kept orthogonal to it can reach)
     TRY(run.mark(7));
+    const double lock_tol = (c->prm.lock_factor > 0.0 ? c->prm.lock_factor : 1.0) * tol;
     std::vector<int> keep, lock;
     for (int j = 0; j < mU; ++j) {
-      if (hard && thU[j] > 0 && rU[j] <= tol)
+      if (hard && thU[j] > 0 && rU[j] <= lock_tol)
         lock.push_back(j);
       else
         keep.push_back(j);

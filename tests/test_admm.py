@@ -48,6 +48,21 @@ def test_oracle_admm_residuals_decrease():
     assert h[len(h) // 2:].max() <= h[:len(h) // 4].max()
 
 
+def test_oracle_adaptive_rho_same_answer():
+    """R58: residual balancing every 40 iterations reaches the same SDP values as fixed rho = 0.1 (the
+    closed-form cases, and a random +-1 graph at eps 1e-6)."""
+    for name, L, value in CASES:
+        res = maxcut_admm(L, eps=1e-7, max_iter=20000, adapt_every=40)
+        assert abs(res["objective"] - value) <= 1e-4 * max(1.0, value), (name, res["objective"], value)
+    rng = np.random.default_rng(3)
+    n = 12
+    edges = [(i, j, rng.choice([-1.0, 1.0])) for i in range(n) for j in range(i + 1, n) if rng.uniform() < 0.4]
+    fixed = maxcut_admm(laplacian(n, edges), eps=1e-6, max_iter=20000)
+    adap = maxcut_admm(laplacian(n, edges), eps=1e-6, max_iter=20000, adapt_every=40)
+    assert max(adap["hist"][-1]) <= 1e-6
+    assert abs(adap["objective"] - fixed["objective"]) <= 1e-4 * abs(fixed["objective"])
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("name,L,value", CASES[1:])
 def test_gpu_admm_closed_form_values(api, name, L, value):
@@ -75,17 +90,33 @@ def test_gpu_admm_follows_oracle_iterates(api):
 
 
 @pytest.mark.gpu
+def test_gpu_admm_adaptive_follows_oracle_iterates(api):
+    """R58 on both sides (residual balancing every 40 iterations): near-exact projections track the
+    oracle through the rho changes."""
+    from paper_1912_02767_b200.admm import MaxCutADMM
+    from workloads.generators import maxcut_graph
+    L = maxcut_graph(n=30, p_edge=0.3, seed=7)
+    ref = maxcut_admm(L, eps=0.0, max_iter=200, adapt_every=40)
+    solver = MaxCutADMM(L, tol_override=1e-12, adapt_every=40)
+    for _ in range(200):
+        solver.step()
+    assert [r for _, r in solver.rho_history] == pytest.approx([r for _, r in ref["rhos"]], rel=1e-12)
+    X = solver.X.cpu().numpy()
+    assert np.linalg.norm(X - ref["X"]) <= 1e-7 * np.linalg.norm(ref["X"])
+    solver.close()
+
+
+@pytest.mark.gpu
 def test_gpu_admm_schedule_converges_c5_small(api):
-    """configs[4] recipe at reduced size (n = 200) with the paper's 10/k^1.01 schedule: the dual
-    residual reaches 1e-4 (R33) and the primal residual 1e-3 within 1500 iterations (with rho fixed
-    at 0.1 the loose late tolerances keep the primal residual near 1e-4), the answer is nearly PSD
-    and the LOBPCG calls stay warm."""
+    """configs[4] recipe at reduced size (n = 200) with the paper's 10/k^1.01 schedule and residual
+    balancing (R58): both residuals reach 1e-4 (R33), the answer is nearly PSD and the LOBPCG calls
+    stay warm."""
     from paper_1912_02767_b200.admm import MaxCutADMM
     from workloads.generators import maxcut_graph
     L = maxcut_graph(n=200, p_edge=0.05, seed=501)
-    solver = MaxCutADMM(L)
-    out = solver.solve(eps=1e-4, max_iter=1500)
-    assert out["r_prim"] <= 1e-3 and out["r_dual"] <= 1e-4, out
+    solver = MaxCutADMM(L, adapt_every=40)
+    out = solver.solve(eps=1e-4, max_iter=3000)
+    assert out["r_prim"] <= 1e-4 and out["r_dual"] <= 1e-4, out
     X = solver.X.cpu().numpy()
     assert np.linalg.eigvalsh(0.5 * (X + X.T)).min() >= -1e-3
     assert sum(i["cold"] for i in solver.infos) <= 2       # warm starts across ADMM iterations
