@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the phase / cold / sched companion lines")
     ap.add_argument("--admm-max-iter", type=int, default=5000)
+    ap.add_argument("--adapt-every", type=int, default=0)
+    ap.add_argument("--tol-ratio", type=float, default=0.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-sample-iters", type=int, default=4)
     return ap.parse_args()
@@ -298,7 +300,7 @@ def run_c5_bench(args, rank, world, local, dist):
     from workloads.generators import maxcut_graph
     n = args.n or 2000
     L = maxcut_graph(n=n, p_edge=0.01, seed=501)
-    solver = MaxCutADMM(L, device=f"cuda:{local}", adapt_every=40)
+    solver = MaxCutADMM(L, device=f"cuda:{local}", adapt_every=args.adapt_every, tol_ratio=args.tol_ratio)
     for _ in range(max(args.warmup, 0)):
         solver.step()
     torch.cuda.synchronize()
@@ -319,7 +321,8 @@ def run_c5_bench(args, rank, world, local, dist):
                 "scaling": "none", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": f"C5 MaxCut SDP, ER n={n}, p=0.01, +-1 weights (configs[4]), eps 1e-4",
                            "rho": solver.rho, "sigma": solver.sigma, "alpha": solver.alpha,
-                           "rho_adaptation": "residual balancing every 40 iterations (R58)",
+                           "rho_adaptation": f"residual balancing every {args.adapt_every} iterations (R58; 0 = fixed)",
+                           "projection_tol": f"min(10/k^1.01, {args.tol_ratio} x min ADMM residual) (R59; 0 = the paper's schedule)",
                            "rho_history": solver.rho_history},
                 "solve_s": ms / 1e3, "admm_iters": out["iters"], "r_prim": out["r_prim"], "r_dual": out["r_dual"],
                 "objective": out["objective"],

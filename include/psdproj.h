@@ -71,6 +71,8 @@ typedef struct {
   double perp_delta; /* f2: failure probability of that randomized bound (over the Philox start,   */
                      /* Kuczynski-Wozniakowski 1992); 0 => 1e-6                                     */
   double lock_factor; /* hard locking of a positive pair at r <= lock_factor * tol (R55); 0 => 1     */
+  int krylov_depth; /* R57 (an extension, NOT the paper's Alg. 3): trial subspace span(X, R, B R, ...,  */
+                    /* B^(d-1) R, dX) instead of span(X, R, dX); 0 or 1 => Alg. 3      */
 } psdproj_params;
 
 typedef struct {

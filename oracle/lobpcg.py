@@ -111,7 +111,7 @@ class LobpcgResult:
 
 
 def lobpcg_pos(B, X0, tol, max_iter=500, guard=1, q=None, locking="hard", seed=0, ctx=0,
-               call=0, cold=False, guard_tol=None, m_max=None, lock_factor=1.0):
+               call=0, cold=False, guard_tol=None, m_max=None, lock_factor=1.0, krylov_depth=1):
     """Alg. 3: positive eigenpairs of the symmetric matrix B.
 
     X0      n x m start block (warm: previous Ritz block, R27; cold: Philox, R28).
@@ -208,6 +208,25 @@ def lobpcg_pos(B, X0, tol, max_iter=500, guard=1, q=None, locking="hard", seed=0
             BPm = BPm - BX[:, Lidx] @ cP
         Pm, pn = _unit_cols(Pm)
         BPm = BPm / pn
+        # R57 (an extension, not Alg. 3): block-Krylov directions K_k = B K_{k-1} (K_1 = the normalised
+        # R_J), each projected against X_L, X_U and R_J and normalised, appended after P
+        a = len(J)
+        Kb, BKb = [], []
+        prev = BW[:, :a]
+        for _ in range(1, krylov_depth if a else 1):
+            K = prev.copy()
+            if locking == "hard" and XL.shape[1]:
+                K = K - XL @ (XL.T @ K)
+            K = K - Xs @ (Xs.T @ K)
+            K = K - W[:, :a] @ (W[:, :a].T @ K)
+            K, _ = _unit_cols(K)
+            BK = mul(K)
+            Kb.append(K)
+            BKb.append(BK)
+            prev = BK
+        if Kb:
+            Pm = np.hstack([Pm] + Kb)
+            BPm = np.hstack([BPm] + BKb)
         mU = Xs.shape[1] + (E.shape[1] if E is not None else 0)
         E = None
         # line 6: Rayleigh-Ritz on span(X, R, P) (R6: P empty at k = 0) via Cholesky QR
@@ -421,7 +440,7 @@ class Context:
     the warm block. One per cone block."""
 
     def __init__(self, n, tol_default=1e-8, max_iter=500, guard=1, q=None, m0=None,
-                 locking="hard", seed=0, ctx_id=0, side=0, keep_extra=None):
+                 locking="hard", seed=0, ctx_id=0, side=0, keep_extra=None, krylov_depth=1):
         self.n = n
         self.max_iter = max_iter
         self.guard = guard
@@ -432,6 +451,7 @@ class Context:
         self.ctx_id = ctx_id
         self.side_param = side
         self.keep_extra = keep_extra
+        self.krylov_depth = krylov_depth
         # capacity ceil(n/3)+1: a wider block is the exact-eig regime (R18)
         self.m_max = min(n, (n + 2) // 3 + 1)
         self.reset()
@@ -485,7 +505,7 @@ class Context:
             X0 = gaussian_block(n, self.m0, self.seed, stream=call, ctx=self.ctx_id, tag=0) if cold else self.X
             res = lobpcg_pos(B, X0, tol, max_iter=self.max_iter, guard=self.guard, q=self.q,
                              locking=self.locking, seed=self.seed, ctx=self.ctx_id, call=call,
-                             cold=cold, m_max=self.m_max)
+                             cold=cold, m_max=self.m_max, krylov_depth=self.krylov_depth)
             if res.abort_direct:
                 mode = DIRECT
                 info["mode"] = mode

@@ -29,10 +29,12 @@ class DiagSDPADMM:
     check_every=40)` stops on a certificate (status 'primal_infeasible' / 'dual_infeasible')."""
 
     def __init__(self, Q, b=None, w=None, rho=0.1, sigma=1e-6, alpha=1.6, device="cuda", params=None, tol_floor=0.0,
-                 tol_override=None, adapt_every=0, adapt_ratio=5.0):
+                 tol_override=None, adapt_every=0, adapt_ratio=5.0, tol_ratio=0.0):
         n = Q.shape[0]
         self.n, self.rho, self.sigma, self.alpha = n, float(rho), float(sigma), float(alpha)
         self.adapt_every, self.adapt_ratio = int(adapt_every), float(adapt_ratio)
+        self.tol_ratio = float(tol_ratio)
+        self.last_res = None
         self.rho_history = [(0, self.rho)]
         self.tol_floor, self.tol_override = tol_floor, tol_override
         dev = torch.device(device)
@@ -63,6 +65,10 @@ class DiagSDPADMM:
                                            pb, pw, st), "psdproj_admm_maxcut_step1")
         self.k += 1
         tol = self.tol_override if self.tol_override is not None else max(tol_schedule(self.k), self.tol_floor)
+        if self.tol_override is None and self.tol_ratio > 0 and self.last_res is not None:
+            # R59: never looser than tol_ratio x the current ADMM residual (the paper's summable schedule
+            # 10/k^1.01, stays the upper bound)
+            tol = min(tol, max(self.tol_ratio * min(self.last_res), 1e-12))
         _, info = self.ctx.project(self.V, tol, out=self.Zp)
         res = (ctypes.c_double * 3)()
         check(L_.psdproj_admm_maxcut_step2(n, p(self.X), p(self.Zp), p(self.Zh), p(self.Yp), p(self.ye),
@@ -70,6 +76,7 @@ class DiagSDPADMM:
               "psdproj_admm_maxcut_step2")
         self.infos.append(info)
         r_p, r_d = max(res[0], res[1]), res[2]
+        self.last_res = (r_p, r_d)
         self._adapt(r_p, r_d)
         return r_p, r_d, info
 

@@ -69,6 +69,7 @@ static thread_local long long g_launches = 0;  // kernels issued by this thread 
 
 static inline int rup(int x, int a) { return (x + a - 1) / a * a; }
 constexpr int EIG_MAX = 2048;  // largest dense eigenproblem of the RR / DIRECT eigensolver
+constexpr int TRINV_MAX = 1280;  // largest direction block of the pencil's triangular inverse (trinv_run)
 
 // ------------------------------------------------------------------ NCCL (row-sharded mode, §8.e)
 // Loaded on first use with dlopen (the library in the process -- torch's -- or PSDPROJ_NCCL_LIB), so
@@ -915,6 +916,9 @@ struct psdproj_ctx_s {
   cudaStream_t st3 = nullptr;
   cudaEvent_t ev3_f = nullptr, ev3_j = nullptr;
   std::vector<cudaEvent_t> tev;  // tridiagonalisation timing events (profile & 4)
+  // psdproj_project_batched: this context's stream and fork / join events (created on first use)
+  cudaStream_t bst = nullptr;
+  cudaEvent_t bev_fork = nullptr, bev_join = nullptr;
   int chol_seq = 0;
   double* part2 = nullptr;
 };
@@ -943,9 +947,11 @@ static void resolve(int n, const psdproj_params* in, psdproj_params& p, int& m0,
   // default capacity n/3: a wider block is the exact-eig regime anyway (R18)
   m_max = p.m_max > 0 ? std::min(p.m_max, n) : std::min(n, (n + 2) / 3 + 1);
   m_max = std::max(m_max, std::min(n, m0));
-  m_max = std::max(1, std::min(m_max, (EIG_MAX - q) / 3));  // the RR basis (<= 3 m + q) must fit the eigensolver
+  const int dpt = std::max(1, p.krylov_depth);
+  m_max = std::max(1, std::min(m_max, (EIG_MAX - q) / (dpt + 2)));  // the RR basis (<= (d + 2) m + q) must fit the eigensolver
+  m_max = std::max(1, std::min(m_max, (TRINV_MAX - q) / (dpt + 1)));  // and its direction block (<= (d + 1) m + q) the L^-1 kernel
   m0 = std::min(m0, m_max);
-  s_max = 3 * m_max + q;
+  s_max = (dpt + 2) * m_max + q;
   NJ = sharded ? s_max : std::max(s_max, n);  // the sharded mode has no DIRECT path
   NJ += NJ & 1;
   tcols = sharded ? s_max : std::max(s_max, n);
@@ -1155,6 +1161,12 @@ extern "C" int psdproj_destroy(psdproj_ctx c) {
   if (c->ev3_f) cudaEventDestroy(c->ev3_f);
   if (c->ev3_j) cudaEventDestroy(c->ev3_j);
   for (auto e : c->tev) cudaEventDestroy(e);
+  if (c->bst) {
+    cudaStreamSynchronize(c->bst);
+    cudaStreamDestroy(c->bst);
+  }
+  if (c->bev_fork) cudaEventDestroy(c->bev_fork);
+  if (c->bev_join) cudaEventDestroy(c->bev_join);
   if (c->d_flag) cudaFree(c->d_flag);
   delete c;
   return PSDPROJ_OK;
@@ -2023,7 +2035,10 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
       info->expansions++;
     }
     int offW = mU, offE = mU + a, offP = mU + a + qe;
-    int s = offP + ap;
+    // R57 (krylov_depth d > 1): d - 1 block-Krylov directions B^k R_J follow P in the basis
+    const int depth = std::max(1, c->prm.krylov_depth);
+    const int aK = depth > 1 ? a : 0;
+    int s = offP + ap + (depth - 1) * aK;
     if (getenv("PSDPROJ_TRACE")) fprintf(stderr, "basis k=%d s=%d mU=%d a=%d ap=%d qe=%d nL=%d\n", k, s, mU, a, ap, qe, nL);
     if (s > c->s_max) return set_err(PSDPROJ_E_CAPACITY, "RR basis %d > s_max %d", s, c->s_max);
     // W = R_J (+ pending expansion E) and P_J sit contiguously in S: [W E P] at offW; both are
@@ -2063,7 +2078,7 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
     // block of G is needed (X^T X = I, X^T [W P] = 0 by construction); it does not depend on B W, so
     // its Gram and Cholesky run on the side stream, overlapping the block multiply (unsharded mode)
     static int ovl_env = getenv("PSDPROJ_NO_OVERLAP") ? 0 : 1;
-    const bool ovl = ovl_env && !c->sharded && s > mU;
+    const bool ovl = ovl_env && !c->sharded && s > mU && depth == 1;
     if (ovl) {
       if (!c->st2) {
         // high priority: the 16-CTA cluster Cholesky is dispatched before the block multiply's
@@ -2102,6 +2117,31 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
     rc = run.amul(sgn, A, lda, W, ld, aw, c->BS + (size_t)offW * ld, ld);
     g_sm_reserve = 0;
     TRY(rc);
+    // R57: K_k = B K_{k-1} (K_1 = the normalised R_J block), each projected against X_L, X_U and R_J,
+    // normalised, and multiplied by B (one more block multiply of a columns per depth level)
+    if (depth > 1 && aK > 0) {
+      TRY(run.mark(1));
+      int offK = offP + ap;
+      const double* BKprev = c->BS + (size_t)offW * ld;
+      for (int dk = 2; dk <= depth; ++dk, offK += aK) {
+        double* K = c->S + (size_t)offK * ld;
+        double* BK = c->BS + (size_t)offK * ld;
+        TRY(copy_block_pdl(st, nl, aK, K, ld, BKprev, ld));
+        if (hard && nL > 0) {
+          TRY(run.gram(nL, aK, c->XL, ld, K, ld, c->Y, ldm));
+          TRY(run.gemm(OP_N, OP_N, nl, aK, nL, -1.0, c->XL, ld, c->Y, ldm, 1.0, K, ld));
+        }
+        TRY(run.gram(mU, aK, c->S, ld, K, ld, c->Y, ldm));
+        TRY(run.gemm(OP_N, OP_N, nl, aK, mU, -1.0, c->S, ld, c->Y, ldm, 1.0, K, ld));
+        TRY(run.gram(aK, aK, W, ld, K, ld, c->Y, ldm));
+        TRY(run.gemm(OP_N, OP_N, nl, aK, aK, -1.0, W, ld, c->Y, ldm, 1.0, K, ld));
+        TRY(run.normalize(nl, aK, K, ld, nullptr, 0));
+        TRY(run.mark(0));
+        TRY(run.amul(sgn, A, lda, K, ld, aK, BK, ld));
+        BKprev = BK;
+      }
+      TRY(run.mark(2));
+    }
     TRY(run.mark(2));
     if (!ovl)
       TRY(run.gram(s - mU, s - mU, c->S + (size_t)mU * ld, ld, c->S + (size_t)mU * ld, ld, c->G + mU + (size_t)mU * ldm,
@@ -2116,8 +2156,8 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
                    c->G + mU + (size_t)mU * ldm, ldm));
       return run.gram(sr, sr, c->S, ld, c->BS, ld, c->Hm, ldm);
     };
-    if (rc > 0 && ap > 0) {
-      sU = s - ap;  // drop P and retry (R20)
+    if (rc > 0 && s > offP) {
+      sU = offP;  // drop P (and the Krylov blocks after it, R57) and retry (R20)
       TRY(regram(sU));
       rc = run.rr(sU, mU, mU, c->d_thU, std::min(mU + qe, sU));
     }
@@ -2482,9 +2522,13 @@ extern "C" int psdproj_project_batched(psdproj_ctx* ctxs, int count, const doubl
   if (count < 0 || (count > 0 && (!ctxs || !A || !lda || !Pi || !ldpi || !tol || !infos)))
     return set_err(PSDPROJ_E_INVALID, "invalid batched arguments");
   if (count == 0) return PSDPROJ_OK;
-  // Independent blocks are driven by up to PSDPROJ_BATCH_THREADS host threads (default 8), each on
-  // its own stream forked from / joined back to the caller's stream, so the latency-bound
-  // per-iteration work of different blocks overlaps on the GPU.
+  for (int i = 0; i < count; ++i)
+    for (int k = 0; k < i && k < 64; ++k)
+      if (ctxs[k] == ctxs[i]) return set_err(PSDPROJ_E_INVALID, "batched contexts must be distinct");
+  // Independent blocks are driven by up to PSDPROJ_BATCH_THREADS host threads (default 8); every item
+  // runs on its own context's stream (created once, destroyed with the context), forked from and
+  // joined back to the caller's stream by the context's events, so the latency-bound per-iteration
+  // work of different blocks overlaps on the GPU and no stream or event is created per call.
   int nth = 8;
   if (const char* e = getenv("PSDPROJ_BATCH_THREADS")) nth = std::max(1, atoi(e));
   nth = std::min(nth, count);
@@ -2498,15 +2542,17 @@ extern "C" int psdproj_project_batched(psdproj_ctx* ctxs, int count, const doubl
     }
     return worst;
   }
-  std::vector<cudaStream_t> ss(nth);
-  std::vector<cudaEvent_t> evs(nth + 1);
-  for (int t = 0; t < nth; ++t) {
-    CK(cudaStreamCreateWithFlags(&ss[t], cudaStreamNonBlocking));
-    CK(cudaEventCreateWithFlags(&evs[t], cudaEventDisableTiming));
+  for (int i = 0; i < count; ++i) {
+    psdproj_ctx c = ctxs[i];
+    if (!c) return set_err(PSDPROJ_E_INVALID, "ctx NULL in batch");
+    if (!c->bst) {
+      CK(cudaStreamCreateWithFlags(&c->bst, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&c->bev_fork, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&c->bev_join, cudaEventDisableTiming));
+    }
   }
-  CK(cudaEventCreateWithFlags(&evs[nth], cudaEventDisableTiming));
-  CK(cudaEventRecord(evs[nth], st));
-  for (int t = 0; t < nth; ++t) CK(cudaStreamWaitEvent(ss[t], evs[nth], 0));
+  CK(cudaEventRecord(ctxs[0]->bev_fork, st));
+  for (int i = 0; i < count; ++i) CK(cudaStreamWaitEvent(ctxs[i]->bst, ctxs[0]->bev_fork, 0));
   std::vector<int> rcs(nth, PSDPROJ_OK);
   std::vector<std::string> errs(nth);
   int dev = 0;
@@ -2517,7 +2563,7 @@ extern "C" int psdproj_project_batched(psdproj_ctx* ctxs, int count, const doubl
       cudaSetDevice(dev);
       int worst = PSDPROJ_OK;
       for (int i = t; i < count; i += nth) {
-        int rc = psdproj_project(ctxs[i], A[i], lda[i], Pi[i], ldpi[i], tol[i], ss[t], &infos[i]);
+        int rc = psdproj_project(ctxs[i], A[i], lda[i], Pi[i], ldpi[i], tol[i], ctxs[i]->bst, &infos[i]);
         if (rc < 0) {
           worst = rc;
           errs[t] = g_err;
@@ -2530,9 +2576,9 @@ extern "C" int psdproj_project_batched(psdproj_ctx* ctxs, int count, const doubl
   }
   for (auto& x : th) x.join();
   int worst = PSDPROJ_OK;
-  for (int t = 0; t < nth; ++t) {
-    CK(cudaEventRecord(evs[t], ss[t]));
-    CK(cudaStreamWaitEvent(st, evs[t], 0));
+  for (int i = 0; i < count; ++i) {
+    CK(cudaEventRecord(ctxs[i]->bev_join, ctxs[i]->bst));
+    CK(cudaStreamWaitEvent(st, ctxs[i]->bev_join, 0));
   }
   for (int t = 0; t < nth; ++t) {
     if (rcs[t] < 0 && worst >= 0) {
@@ -2542,8 +2588,6 @@ extern "C" int psdproj_project_batched(psdproj_ctx* ctxs, int count, const doubl
       worst = std::max(worst, rcs[t]);
     }
   }
-  for (int t = 0; t <= nth; ++t) cudaEventDestroy(evs[t]);
-  for (int t = 0; t < nth; ++t) cudaStreamDestroy(ss[t]);
   return worst;
 }
 

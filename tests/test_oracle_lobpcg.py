@@ -309,3 +309,24 @@ def test_bound_with_perturbed_basis_dominates():
         th = lam[:p].copy()
         err = np.linalg.norm((V * th) @ V.T - Pstar)
         assert L.error_bound(A, V, th) >= err, (eta, err)
+
+
+def test_krylov_depth_extension_same_projection_fewer_iterations():
+    """R57 (an extension of Alg. 3, off by default): the trial subspace span(X, R, B R, B^2 R, dX)
+    reaches the same projection (planted closed form) in fewer iterations on a spectrum with a small
+    gap at zero (the C3-R regime), and the Ritz count still interlaces."""
+    rng = np.random.default_rng(57)
+    n, p = 300, 15
+    lam = np.concatenate([10.0 ** rng.uniform(-2, 1, p), -(10.0 ** rng.uniform(-2, 1, n - p))])
+    Q = haar_q(rng, n)
+    A = planted(Q, lam)
+    Pstar = (Q * np.maximum(lam, 0)) @ Q.T
+    its = {}
+    for d in (1, 3):
+        ctx = L.Context(n, seed=3, krylov_depth=d)
+        P, info = ctx.project(A, 1e-9)
+        assert info["status"] == L.OK and info["npos"] == p
+        assert np.linalg.norm(P - Pstar) <= 1e-9 * np.linalg.norm(A)
+        assert info["err_bound"] >= np.linalg.norm(P - Pstar)
+        its[d] = info["iters"]
+    assert its[3] * 1.5 <= its[1], its
