@@ -116,6 +116,8 @@ typedef struct {
   double tri_ms;    /* profile & 4: summed device time of the RR tridiagonalisation launches      */
   int tri_launches; /* profile & 4: number of timed tridiagonalisation launches                  */
   double tri_flops; /* profile & 4: 4/3 s^3 summed over those launches (algorithmic)              */
+  double pi_fro;    /* sqrt(sum of theta+^2): ||Pi(A)||_F on the + side and DIRECT, ||Pi(-A)||_F on
+                       the - side (the f3 certificates' PSD-part distances)                      */
 } psdproj_info;
 
 /* Fill *p with the defaults documented above. */
@@ -200,6 +202,17 @@ int psdproj_admm_maxcut_step1(int n, double* X, const double* Zp, const double* 
 int psdproj_admm_maxcut_step2(int n, const double* X, const double* Zp, const double* Zh, double* Yp, double* ye,
                               const double* zeh, const double* Q, int ld, double rho, double* res_host,
                               const double* b, const double* w, void* stream);
+
+/* f3 (Theorem 1; practical tests PAPER.md:563-587, reading R49): the certificate
+ * terms of two successive iterates (X, ye, Yp) and (X0, ye0, Yp0) of the diagonal-SDP ADMM above, in
+ * one pass on the device: terms_host[0..6] (host) = ||dX||_F^2, ||w dye||^2, ||dYp||_F^2, b.(w dye),
+ * <Q, dX>, ||w diag dX||^2, max|dYp + Diag(w dye)| (d = difference). Also writes dY_sym = sym(dYp) and
+ * mdX_sym = -sym(dX) (n x n, ld, device), whose PSD parts the caller takes with psdproj_project
+ * (DIRECT). work: device scratch of work_elems doubles (>= 7 (2 SMs + 1)). Synchronous on stream. */
+int psdproj_admm_certificate_terms(int n, const double* X, const double* X0, const double* ye, const double* ye0,
+                                   const double* Yp, const double* Yp0, const double* Q, int ld, const double* b,
+                                   const double* w, double* dY_sym, double* mdX_sym, double* work, size_t work_elems,
+                                   double* terms_host, void* stream);
 
 /* ---- kernel-level entry points (tests and benchmarks call the same kernels the path uses) ---- */
 

@@ -22,6 +22,7 @@ EXPORTS = [
     "psdproj_jacobi", "psdproj_philox_raw", "psdproj_philox_gauss", "psdproj_eigh_ws_elems",
     "psdproj_eigh", "psdproj_cholesky", "psdproj_get_nccl_uid", "psdproj_workspace_bytes_sharded",
     "psdproj_create_sharded", "psdproj_admm_maxcut_step1", "psdproj_admm_maxcut_step2",
+    "psdproj_admm_certificate_terms",
 ]
 
 
@@ -48,7 +49,7 @@ class Info(ctypes.Structure):
         ("last_pos", ctypes.c_int), ("last_neg", ctypes.c_int), ("launches", ctypes.c_int),
         ("dropped", ctypes.c_int), ("phase_ms", ctypes.c_double * 12), ("perp_est", ctypes.c_double),
         ("orth_defect", ctypes.c_double), ("perp_mu", ctypes.c_double), ("tri_ms", ctypes.c_double),
-        ("tri_launches", ctypes.c_int), ("tri_flops", ctypes.c_double),
+        ("tri_launches", ctypes.c_int), ("tri_flops", ctypes.c_double), ("pi_fro", ctypes.c_double),
     ]
 
     def as_dict(self):
@@ -96,6 +97,7 @@ def load(path=SO_PATH):
     L.psdproj_get_nccl_uid.argtypes = [vp]
     L.psdproj_admm_maxcut_step1.argtypes = [i, vp, vp, vp, vp, vp, i, d, d, d, vp, vp, vp, vp, vp, vp]
     L.psdproj_admm_maxcut_step2.argtypes = [i, vp, vp, vp, vp, vp, vp, vp, i, d, P(d), vp, vp, vp]
+    L.psdproj_admm_certificate_terms.argtypes = [i, vp, vp, vp, vp, vp, vp, vp, i, vp, vp, vp, vp, vp, sz, P(d), vp]
     L.psdproj_workspace_bytes_sharded.argtypes = [i, i, i, P(Params)]
     L.psdproj_workspace_bytes_sharded.restype = sz
     L.psdproj_create_sharded.argtypes = [i, i, i, vp, i, i, P(Params), vp, sz, P(vp)]

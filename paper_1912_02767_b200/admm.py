@@ -93,31 +93,43 @@ class DiagSDPADMM:
             self.rho_history.append((self.k, self.rho))
 
     def _psd_part(self, M):
-        """||Pi_S+(M)||_F by the library's DIRECT path (exact eigendecomposition)."""
+        """||Pi_S+(M)||_F of a symmetric device matrix by the library's DIRECT path (exact
+        eigendecomposition; info pi_fro = sqrt of the sum of the squared positive eigenvalues)."""
         if self._cert_ctx is None:
             self._cert_ctx = api.Context(self.n, params=api.default_params(side=2))
-        Pi, _ = self._cert_ctx.project(0.5 * (M + M.T).contiguous(), 1e-12)
-        return float(torch.linalg.norm(Pi))
+            self._cert_out = torch.empty_like(M)
+        _, info = self._cert_ctx.project(M, 1e-12, out=self._cert_out)
+        return info["pi_fro"]
 
     def certificates(self):
         """Theorem 1's certificates from the successive differences of the last step (needs
-        step(save_prev=True)): with y = (w ye, Yp) and x = vec(X),
+        step(save_prev=True)), reading R49. The terms are formed on the device in one pass
+        (psdproj_admm_certificate_terms) and the two PSD-part distances by the DIRECT projection;
+        only the normalisation of a few scalars happens here. With y = (w ye, Yp), x = vec(X):
           primal: ||A^T y-bar||_inf, dist_{C-polar}(y-bar) = ||Pi_S+(Y-bar)||_F, b^T y-bar_eq
           dual:   dist_{C-inf}(A x-bar) = (||w diag X-bar||^2 + ||Pi_S+(-X-bar)||_F^2)^(1/2), <Q, X-bar>"""
+        L_ = _lib.load()
         X0, ye0, Yp0 = self.prev
-        w = self.w if self.w is not None else torch.ones_like(self.ye)
-        b = self.b if self.b is not None else torch.ones_like(self.ye)
-        dX, dye, dYp = self.X - X0, (self.ye - ye0) * w, self.Yp - Yp0
-        out = {"ndx": float(torch.linalg.norm(dX)), "ndy": float(torch.sqrt(torch.sum(dye ** 2) + torch.sum(dYp ** 2)))}
-        if out["ndy"] > 1e-12:
-            ye_b, Yb = dye / out["ndy"], dYp / out["ndy"]
-            out["p_at"] = float(torch.max(torch.abs(Yb + torch.diag(ye_b))))
-            out["p_dist"] = self._psd_part(Yb)
-            out["p_supp"] = float(torch.dot(b, ye_b))
-        if out["ndx"] > 1e-12:
-            Xb = dX / out["ndx"]
-            out["d_dist"] = float(torch.sqrt(torch.sum((w * torch.diagonal(Xb)) ** 2) + self._psd_part(-Xb) ** 2))
-            out["d_qx"] = float(torch.sum(self.Q * Xb))
+        n, p = self.n, api._ptr
+        if not hasattr(self, "_cert_buf"):
+            self._cert_buf = (torch.empty_like(self.X), torch.empty_like(self.X),
+                              torch.empty(7 * (2 * 148 * 4 + 1), dtype=torch.float64, device=self.X.device))
+        dYs, mdXs, work = self._cert_buf
+        t = (ctypes.c_double * 7)()
+        check(L_.psdproj_admm_certificate_terms(n, p(self.X), p(X0), p(self.ye), p(ye0), p(self.Yp), p(Yp0),
+                                                p(self.Q), n, p(self.b) if self.b is not None else None,
+                                                p(self.w) if self.w is not None else None, p(dYs), p(mdXs),
+                                                p(work), work.numel(), t, api._stream_ptr(None)),
+              "psdproj_admm_certificate_terms")
+        ndx, ndy = t[0] ** 0.5, (t[1] + t[2]) ** 0.5
+        out = {"ndx": ndx, "ndy": ndy}
+        if ndy > 1e-12:
+            out["p_at"] = t[6] / ndy
+            out["p_dist"] = self._psd_part(dYs) / ndy      # positive homogeneity of Pi_S+
+            out["p_supp"] = t[3] / ndy
+        if ndx > 1e-12:
+            out["d_dist"] = (t[5] + self._psd_part(mdXs) ** 2) ** 0.5 / ndx
+            out["d_qx"] = t[4] / ndx
         return out
 
     @staticmethod

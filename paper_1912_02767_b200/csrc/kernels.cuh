@@ -1116,6 +1116,68 @@ __global__ void admm_maxcut_step2_kernel(int n, const double* __restrict__ X, co
     if (r2 > 0.0) atomicMax(res + 2, (unsigned long long)__double_as_longlong(r2));
   }
 }
+// f3 (Theorem 1; reading R49): the certificate terms of two successive ADMM
+// iterates in one pass. Per block, partial sums (fixed order) of
+//   0 ||dX||_F^2, 1 ||w dye||^2, 2 ||dYp||_F^2, 3 b . (w dye), 4 <Q, dX>, 5 ||w diag(dX)||^2
+// and the maximum 6 max |dYp + Diag(w dye)|, with dX = X - X0, dye = ye - ye0, dYp = Yp - Yp0; also
+// writes sym(dYp) and -sym(dX) (the arguments of the two PSD-part distances).
+constexpr int CERT_TERMS = 7;
+__global__ void admm_cert_partial_kernel(int n, const double* __restrict__ X, const double* __restrict__ X0,
+                                         const double* __restrict__ ye, const double* __restrict__ ye0,
+                                         const double* __restrict__ Yp, const double* __restrict__ Yp0,
+                                         const double* __restrict__ Q, int ld, const double* __restrict__ bv,
+                                         const double* __restrict__ wv, double* __restrict__ dYs,
+                                         double* __restrict__ mdXs, double* __restrict__ part) {
+  __shared__ double red[32];
+  double a[CERT_TERMS] = {0, 0, 0, 0, 0, 0, 0};
+  const size_t total = (size_t)n * n;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e % n), j = (int)(e / n);
+    const size_t o = IDX(i, j, ld), ot = IDX(j, i, ld);
+    const double dx = X[o] - X0[o], dy = Yp[o] - Yp0[o];
+    dYs[o] = 0.5 * (dy + (Yp[ot] - Yp0[ot]));
+    mdXs[o] = -0.5 * (dx + (X[ot] - X0[ot]));
+    a[0] += dx * dx;
+    a[2] += dy * dy;
+    a[4] += Q[o] * dx;
+    double m = dy;
+    if (i == j) {
+      const double wi = wv ? wv[i] : 1.0, bi = bv ? bv[i] : 1.0;
+      const double dye = wi * (ye[i] - ye0[i]);
+      a[1] += dye * dye;
+      a[3] += bi * dye;
+      a[5] += (wi * dx) * (wi * dx);
+      m += dye;
+    }
+    a[6] = fmax(a[6], fabs(m));
+  }
+  for (int t = 0; t < CERT_TERMS; ++t) {
+    double v = t == 6 ? a[t] : a[t];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double u = __shfl_xor_sync(0xffffffffu, v, o);
+      v = t == 6 ? fmax(v, u) : v + u;
+    }
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double r = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r = t == 6 ? fmax(r, red[w]) : r + red[w];
+      part[(size_t)t * gridDim.x + blockIdx.x] = r;
+    }
+    __syncthreads();
+  }
+}
+
+// fixed-order final reduction of admm_cert_partial_kernel's partials (one block)
+__global__ void admm_cert_final_kernel(int nb, const double* __restrict__ part, double* __restrict__ out) {
+  const int t = threadIdx.x;
+  if (t >= CERT_TERMS) return;
+  double r = 0.0;
+  for (int b = 0; b < nb; ++b) r = t == 6 ? fmax(r, part[(size_t)t * nb + b]) : r + part[(size_t)t * nb + b];
+  out[t] = r;
+}
+
 // Holds its stream until *flag >= seq (a kernel on another stream announced that it is resident)
 // or timeout_ns passed; one thread.
 __global__ void wait_flag_kernel(const int* __restrict__ flag, int seq, long long timeout_ns) {

@@ -1640,6 +1640,11 @@ static int direct_path(Run& run, const double* A, int lda, double* Pi, int ldpi)
   std::vector<int> order(c->h_i, c->h_i + n);
   int p = 0;
   while (p < n && w[p] > 0.0) ++p;
+  {
+    double f2 = 0.0;
+    for (int i = 0; i < p; ++i) f2 += w[i] * w[i];
+    run.info->pi_fro = std::sqrt(f2);  // ||Pi(A)||_F of the returned projection's eigenvalues
+  }
   // a10 for DIRECT (R53), before the assembly (Pi may alias A): Theorem 3 with V~ = the computed positive eigenvectors; its perp term is
   // bounded by the residual of the others: ||Pi(V-^T A V-)||_F = dist(V-^T A V-, NSD) <=
   // ||V-^T A V- - Theta-||_F <= ||V-|| ||A V- - V- Theta-||_F (Theta- <= 0 is in the NSD cone)
@@ -2258,8 +2263,12 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
   CK(cudaMemcpyAsync(c->d_w, c->h_d, sizeof(double) * std::max(p, 1), cudaMemcpyHostToDevice, st));
   // ---- a10 (R16, R36, R53): certify the returned pairs with an explicit B V+ (one block multiply
   // of the p kept columns; B V+ of the rotation and of the frozen locked columns is not used)
-  double thmax = 0.0;
-  for (double x : wts) thmax = std::max(thmax, x);
+  double thmax = 0.0, th2 = 0.0;
+  for (double x : wts) {
+    thmax = std::max(thmax, x);
+    th2 += x * x;
+  }
+  info->pi_fro = std::sqrt(th2);  // ||V Theta+ V^T||_F (side +) -- of the computed side's part
   Cert ct;
   TRY(certify(run, sgn, A, lda, V, p, c->d_w, BV, c->Y, ldm, false, ct));
   rs = 0.0;
@@ -2740,6 +2749,28 @@ extern "C" int psdproj_admm_maxcut_step1(int n, double* X, const double* Zp, con
   admm_maxcut_step1_kernel<<<grid1d((size_t)n * n), 256, 0, (cudaStream_t)stream>>>(n, X, Zp, Yp, ye, Q, sigma, rho,
                                                                                      alpha, Zh, V, zeh, ld, b, w);
   CKL();
+  return 0;
+}
+
+extern "C" int psdproj_admm_certificate_terms(int n, const double* X, const double* X0, const double* ye,
+                                              const double* ye0, const double* Yp, const double* Yp0, const double* Q,
+                                              int ld, const double* b, const double* w, double* dY_sym,
+                                              double* mdX_sym, double* work, size_t work_elems, double* terms_host,
+                                              void* stream) {
+  if (n <= 0 || ld < n || !X || !X0 || !ye || !ye0 || !Yp || !Yp0 || !Q || !dY_sym || !mdX_sym || !work ||
+      !terms_host)
+    return set_err(PSDPROJ_E_INVALID, "invalid certificate arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  int nb = std::min(sms() * 2, std::max(1, (int)(((size_t)n * n + 255) / 256)));
+  if (work_elems < (size_t)CERT_TERMS * (nb + 1)) nb = (int)(work_elems / CERT_TERMS) - 1;
+  if (nb < 1) return set_err(PSDPROJ_E_WORKSPACE, "certificate work buffer too small");
+  admm_cert_partial_kernel<<<nb, 256, 0, st>>>(n, X, X0, ye, ye0, Yp, Yp0, Q, ld, b, w, dY_sym, mdX_sym, work);
+  CKL();
+  admm_cert_final_kernel<<<1, 32, 0, st>>>(nb, work, work + (size_t)CERT_TERMS * nb);
+  CKL();
+  CK(cudaMemcpyAsync(terms_host, work + (size_t)CERT_TERMS * nb, CERT_TERMS * sizeof(double), cudaMemcpyDeviceToHost,
+                     st));
+  CK(cudaStreamSynchronize(st));
   return 0;
 }
 
