@@ -41,7 +41,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c3r", choices=["c3r", "c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--workload", default="c3r", choices=["c3r", "c1", "c2", "c2cl", "c3", "c4", "c5", "bo"])
     ap.add_argument("--c4-blocks", type=int, default=512)
     ap.add_argument("--shard", action="store_true",
                     help="row-shard the single matrix across the ranks (NCCL inside libpsdproj; strong scaling)")
@@ -69,6 +69,9 @@ def workload(args):
     elif args.workload == "c1":
         cfg = G.C1(args.n or 200)
         name = f"C1 n={cfg.n} (configs[0]), tol {cfg.tol:g}"
+    elif args.workload == "c2cl":
+        cfg = G.C2CL(args.n or 1000)
+        name = f"C2-cl n={cfg.n} (configs[1] clustered variant, R31), tol {cfg.tol:g}"
     else:
         cfg = G.C2(args.n or 1000)
         name = f"C2 n={cfg.n} (configs[1]), tol {cfg.tol:g}"
@@ -391,6 +394,52 @@ def run_sharded_bench(args, rank, world, local, dist):
         dist.destroy_process_group()
 
 
+def run_sequence(args, rank, world, local, dist):
+    """Companion lines for BASELINE configs[0], configs[1] (C2, C2-cl) and the literal configs[2] (C3):
+    the whole warm sequence (cfg.steps matrices; step 0 cold, untimed) projected at the config
+    tolerance, device-timed per call; status counts, iterations and bounds reported."""
+    import torch
+    from paper_1912_02767_b200 import api
+    cfg, name, tol = workload(args)
+    dev = torch.device("cuda", local)
+    steps = 3 if args.workload == "c3" else cfg.steps  # C3 literal: the first steps only (SURVEY §8.d.3, F4)
+    mats = gen_matrices(cfg, steps, dev)
+    ctx = api.Context(cfg.n, params=api.default_params(max_iter=args.max_iter, seed=1912 + rank), device=dev)
+    out = torch.empty_like(mats[0])
+    st = torch.cuda.current_stream()
+    infos, ms = [], []
+    for k, A in enumerate(mats):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        _, inf = ctx.project(A, tol, out=out)
+        e1.record(st)
+        torch.cuda.synchronize()
+        if k > 0:
+            infos.append(inf)
+            ms.append(e0.elapsed_time(e1))
+    if rank == 0:
+        status = [i["status"] for i in infos]
+        line = {"metric": f"PSD-cone projections/sec (warm LOBPCG), {name}", "value": len(ms) / (sum(ms) / 1e3),
+                "unit": "projections/s", "n_gpus": 1, "steps": len(ms), "warmup": 0,
+                "ms_per_step": sum(ms) / len(ms), "higher_is_better": True, "scaling": "none", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic", "config": {"workload": name, "n": cfg.n, "tol": tol},
+                "iters_per_projection": {"mean": sum(i["iters"] for i in infos) / len(infos),
+                                         "max": max(i["iters"] for i in infos)},
+                "status_counts": {str(s_): status.count(s_) for s_ in sorted(set(status))},
+                "err_bound_rel_max": max(i["err_bound"] / i["anorm_f"] for i in infos),
+                "npos": sorted(set(i["npos"] for i in infos)), "sides": sorted(set(i["side"] for i in infos))}
+        print(json.dumps(line), flush=True)
+    ctx.close()
+
+
+def run_bo(args):
+    """f4 line: BO-like tiny blocks (workloads.generators.BO), one-CTA warm LOBPCG per block vs the exact
+    one-CTA Jacobi path, blocks/s per round (tools/tiny_lobpcg_probe.py)."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "tiny_lobpcg_probe.py"), "4096", "8", "100",
+                          str(max(args.steps, 3))], capture_output=True, text=True)
+    print(out.stdout.strip().splitlines()[-1] if out.stdout.strip() else out.stderr[-2000:], flush=True)
+
+
 def spawn_ranks(args):
     """--gpus N without a torchrun environment: launch N ranks of this script with torchrun
     (one process per GPU, rendezvous on 127.0.0.1) and wait; rank 0 prints the JSON line."""
@@ -671,6 +720,12 @@ def main():
         return
     if args.shard:
         run_sharded_bench(args, rank, world, local, dist)
+        return
+    if args.workload == "bo":
+        run_bo(args)
+        return
+    if args.workload in ("c1", "c2", "c2cl", "c3"):
+        run_sequence(args, rank, world, local, dist)
         return
     run_c3r(args, rank, world, local, dist)
 

@@ -172,6 +172,21 @@ int psdproj_project_batched(psdproj_ctx* ctxs, int count, const double* const* A
 int psdproj_project_tiny_batched(int count, const int* n, const double* const* A, const int* lda,
                                  double* const* Pi, const int* ldpi, int* npos_host, void* stream);
 
+/* f4 (PAPER.md:605-649 -- BO-like blocks with rank-one / low-rank PSD parts): one CTA runs
+ * the whole warm-started LOBPCG (Alg. 3, positive side) of each tiny block (1 <= n_i <= 112) in shared
+ * memory, one launch for the batch. Xw[i]: caller-owned device warm block (n_i x 8, ld n_i); m_state[i]
+ * (host, in/out): its width (0 = cold: m0 Philox columns keyed by seed, block index and `call`). tol: the
+ * per-pair residual threshold; guard: non-positive guard columns (>= 1, R8/R12).
+ * Outputs (host arrays of count): status 0 OK / 1 NOT_CONVERGED (max_iter) / 3 computed by the exact
+ * one-CTA path because the block outgrew 8 columns or its pencil stayed singular; iters; npos; bound
+ * (Theorem 3 from an explicit B V+, R53; 0 for status 3). Pi[i] (device) is exactly symmetric. ws: device
+ * scratch of psdproj_tiny_lobpcg_ws_bytes(count), 16-byte aligned. Synchronous on stream. */
+size_t psdproj_tiny_lobpcg_ws_bytes(int count);
+int psdproj_project_tiny_lobpcg(int count, const int* n, const double* const* A, const int* lda, double* const* Pi,
+                                const int* ldpi, double* const* Xw, int* m_state, double tol, int max_iter, int guard,
+                                int m0, uint64_t seed, uint32_t call, void* ws, size_t ws_bytes, int* status,
+                                int* iters, int* npos, double* bound, void* stream);
+
 /* Warm block of the last call: vals_host (cap values, descending Ritz values of the side used,
  * sign as computed on B = side*A), vecs_dev (n x cap, ldv) may be NULL. Returns the count. */
 int psdproj_get_ritz(psdproj_ctx ctx, double* vals_host, int cap, double* vecs_dev, int ldv);
@@ -221,6 +236,12 @@ int psdproj_admm_certificate_terms(int n, const double* X, const double* X0, con
 int psdproj_dgemm(int opA, int opB, int M, int N, int K, double alpha, const double* A, int lda,
                   const double* B, int ldb, double beta, double* C, int ldc, double* ws,
                   size_t ws_elems, void* stream);
+
+/* The a3 block multiply exactly as the path runs it: Y = alpha A Z with A symmetric
+ * (n x n, lda even, 16-byte aligned), Z (n x k, ldz even), Y (n x k, ldy); TMA-staged 128-byte-swizzled
+ * tiles + DMMA (gemm_tma.cuh). ws: split-K partials (NULL = no split). Device pointers, async. */
+int psdproj_symm_multiply(int n, int k, double alpha, const double* A, int lda, const double* Z, int ldz, double* Y,
+                          int ldy, double* ws, size_t ws_elems, void* stream);
 
 /* Symmetric eigendecomposition by parallel-order Jacobi (a7/a13): A (s x s, device) ->
  * w (s, ascending, device) and V (s x s, ldv, device). ws: device scratch of

@@ -22,7 +22,8 @@ EXPORTS = [
     "psdproj_jacobi", "psdproj_philox_raw", "psdproj_philox_gauss", "psdproj_eigh_ws_elems",
     "psdproj_eigh", "psdproj_cholesky", "psdproj_get_nccl_uid", "psdproj_workspace_bytes_sharded",
     "psdproj_create_sharded", "psdproj_admm_maxcut_step1", "psdproj_admm_maxcut_step2",
-    "psdproj_admm_certificate_terms",
+    "psdproj_admm_certificate_terms", "psdproj_symm_multiply", "psdproj_tiny_lobpcg_ws_bytes",
+    "psdproj_project_tiny_lobpcg",
 ]
 
 
@@ -87,6 +88,11 @@ def load(path=SO_PATH):
     L.psdproj_last_error.argtypes = []
     L.psdproj_last_error.restype = ctypes.c_char_p
     L.psdproj_dgemm.argtypes = [i, i, i, i, i, d, vp, i, vp, i, d, vp, i, vp, sz, vp]
+    L.psdproj_tiny_lobpcg_ws_bytes.argtypes = [i]
+    L.psdproj_tiny_lobpcg_ws_bytes.restype = sz
+    L.psdproj_project_tiny_lobpcg.argtypes = [i, P(i), P(vp), P(i), P(vp), P(i), P(vp), P(i), d, i, i, i, u64, u32,
+                                              vp, sz, P(i), P(i), P(i), P(d), vp]
+    L.psdproj_symm_multiply.argtypes = [i, i, d, vp, i, vp, i, vp, i, vp, sz, vp]
     L.psdproj_jacobi_ws_elems.argtypes = [i]
     L.psdproj_jacobi_ws_elems.restype = sz
     L.psdproj_jacobi.argtypes = [i, vp, i, vp, vp, i, vp, vp]
@@ -103,7 +109,7 @@ def load(path=SO_PATH):
     L.psdproj_create_sharded.argtypes = [i, i, i, vp, i, i, P(Params), vp, sz, P(vp)]
     L.psdproj_philox_raw.argtypes = [i, u32, u32, u32, u32, u32, vp, vp]
     L.psdproj_philox_gauss.argtypes = [i, i, vp, i, u64, u32, u32, u32, vp]
-    special = ("psdproj_default_params", "psdproj_workspace_bytes", "psdproj_last_error",
+    special = ("psdproj_default_params", "psdproj_workspace_bytes", "psdproj_last_error", "psdproj_tiny_lobpcg_ws_bytes",
                "psdproj_jacobi_ws_elems", "psdproj_eigh_ws_elems", "psdproj_workspace_bytes_sharded")
     for name in EXPORTS:
         if name not in special:

@@ -12,7 +12,8 @@ import torch
 from . import _lib
 from ._lib import Info, Params, PsdprojError, check
 
-__all__ = ["Context", "ShardedContext", "default_params", "project_batched", "dgemm", "jacobi", "philox_raw",
+__all__ = ["Context", "ShardedContext", "TinyLobpcgBatch", "default_params", "project_batched", "dgemm", "jacobi",
+           "philox_raw",
            "philox_gauss", "workspace_bytes", "colmajor", "colmajor_copy", "nccl_uid", "row_blocks"]
 
 
@@ -248,6 +249,44 @@ def project_tiny_batched(As, outs=None, stream=None):
     return outs, list(npos)
 
 
+class TinyLobpcgBatch:
+    """f4: many tiny blocks (n <= 112) each projected by a one-CTA warm LOBPCG in one launch
+    (psdproj_project_tiny_lobpcg). Holds the per-block warm blocks (device, n x 8) and widths."""
+
+    def __init__(self, sizes, device="cuda", guard=1, m0=2, seed=0x5eed1912, max_iter=500):
+        L = _lib.load()
+        self.sizes = [int(n) for n in sizes]
+        self.count = len(self.sizes)
+        self.guard, self.m0, self.seed, self.max_iter = guard, m0, seed, max_iter
+        self.Xw = [torch.zeros(8, n, dtype=torch.float64, device=device).T for n in self.sizes]  # n x 8, ld n
+        self.m_state = (ctypes.c_int * self.count)()
+        nb = int(L.psdproj_tiny_lobpcg_ws_bytes(self.count))
+        self.ws = torch.empty(nb + 256, dtype=torch.uint8, device=device)
+        self.calls = 0
+
+    def project(self, As, tol, outs=None, stream=None):
+        """Returns (outs, dict of per-block status / iters / npos / bound lists)."""
+        L = _lib.load()
+        k = self.count
+        outs = outs if outs is not None else [torch.empty_like(a) for a in As]
+        ns = (ctypes.c_int * k)(*self.sizes)
+        Ap = (ctypes.c_void_p * k)(*[a.data_ptr() for a in As])
+        Op = (ctypes.c_void_p * k)(*[o.data_ptr() for o in outs])
+        Xp = (ctypes.c_void_p * k)(*[x.data_ptr() for x in self.Xw])
+        la = (ctypes.c_int * k)(*[_ld_sym(a) for a in As])
+        lo = (ctypes.c_int * k)(*[_ld_sym(o) for o in outs])
+        st, it, npos = (ctypes.c_int * k)(), (ctypes.c_int * k)(), (ctypes.c_int * k)()
+        bd = (ctypes.c_double * k)()
+        base = self.ws.data_ptr()
+        off = (-base) % 256
+        check(L.psdproj_project_tiny_lobpcg(k, ns, Ap, la, Op, lo, Xp, self.m_state, float(tol), self.max_iter,
+                                            self.guard, self.m0, self.seed, self.calls, ctypes.c_void_p(base + off),
+                                            self.ws.numel() - off, st, it, npos, bd, _stream_ptr(stream)),
+              "psdproj_project_tiny_lobpcg")
+        self.calls += 1
+        return outs, {"status": list(st), "iters": list(it), "npos": list(npos), "bound": list(bd)}
+
+
 def dgemm(opA, opB, alpha, A, B, beta, C, ws=None, stream=None):
     """C = alpha op(A) op(B) + beta C on column-major device tensors (psdproj_dgemm)."""
     L = _lib.load()
@@ -259,6 +298,18 @@ def dgemm(opA, opB, alpha, A, B, beta, C, ws=None, stream=None):
                          _stream_ptr(stream))
     check(rc, "psdproj_dgemm")
     return C
+
+
+def symm_multiply(alpha, A, Z, Y=None, ws=None, stream=None):
+    """Y = alpha A Z for a symmetric device matrix A (the path's TMA a3 kernel, psdproj_symm_multiply)."""
+    L = _lib.load()
+    n, k = Z.shape
+    Y = Y if Y is not None else colmajor(n, k, device=Z.device)
+    rc = L.psdproj_symm_multiply(n, k, float(alpha), _ptr(A), _ld_sym(A), _ptr(Z), _ld_colmajor(Z), _ptr(Y),
+                                 _ld_colmajor(Y), _ptr(ws) if ws is not None else None,
+                                 ws.numel() if ws is not None else 0, _stream_ptr(stream))
+    check(rc, "psdproj_symm_multiply")
+    return Y
 
 
 def jacobi(A, stream=None):

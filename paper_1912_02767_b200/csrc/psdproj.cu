@@ -35,6 +35,8 @@
 #include "tridiag.cuh"
 #include "cluster_la.cuh"
 #include "tridiag_tile.cuh"
+#include "gemm_tma.cuh"
+#include "tiny_lobpcg.cuh"
 
 using namespace psd;
 
@@ -230,6 +232,75 @@ static int gemm_kp_launch(cudaStream_t st, int M, int N, int K, double alpha, co
       TRY(launch_pdl(splitk_reduce_kernel, dim3(cdiv(M, 256), N), dim3(256), 0, st, M, N, splits, alpha,
                      (const double*)(part + (size_t)splits * M * N), beta, C2, ldc));
   }
+  return 0;
+}
+
+// ---------------------------------------------------------------- a3 with TMA-staged tiles (gemm_tma.cuh)
+typedef CUresult (*TmapEncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static TmapEncodeFn tmap_encode() {
+  static TmapEncodeFn f = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      f = (TmapEncodeFn)p;
+  }
+  return f;
+}
+// 2-D fp64 tensor map: inner dimension `inner` (contiguous), outer `outer` (stride ld doubles), box
+// {16, box_outer}, 128-byte swizzle, out-of-bounds elements zero-filled
+static int make_tmap(CUtensorMap* m, const double* ptr, int inner, int outer, int ld, int box_outer) {
+  TmapEncodeFn f = tmap_encode();
+  if (!f) return set_err(PSDPROJ_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(double)};
+  cuuint32_t box[2] = {16, (cuuint32_t)box_outer};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = f(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)ptr, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_err(PSDPROJ_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return 0;
+}
+// Y (n x k, ldy) = alpha A Z, A symmetric n x n (lda even, 16-B aligned), Z n x k (ldz even): the a3
+// block multiply on TMA-staged tiles; split-K over the SMs left free as gemm_kp_launch
+template <int BM, int BN, int ST>
+static int gemm_tma_launch(cudaStream_t st, int n, int k, double alpha, const double* A, int lda, const double* Z,
+                           int ldz, double* Y, int ldy, double* part, size_t part_elems) {
+  using Cfg = TmaGemmCfg<BM, BN, ST>;
+  auto kern = dgemm_tma_kernel<BM, BN, ST, 1>;
+  static bool attr = false;
+  static int per_sm = 1;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Cfg::THREADS, Cfg::SMEM));
+    per_sm = std::max(per_sm, 1);
+    attr = true;
+  }
+  CUtensorMap ma, mb;
+  TRY(make_tmap(&ma, A, n, n, lda, BM));
+  TRY(make_tmap(&mb, Z, n, k, ldz, BN));
+  const int KT = cdiv(std::max(n, 1), 16);
+  const int tiles = cdiv(n, BM) * cdiv(k, BN);
+  const int slots = std::max(1, sms() - g_sm_reserve) * per_sm;
+  int splits = 1;
+  if (part && tiles < slots && KT >= 8) {
+    splits = std::min(std::max(1, slots / tiles), KT / 4);
+    splits = std::max(1, std::min(splits, 32));
+    while (splits > 1 && (size_t)splits * n * k > part_elems) --splits;
+  }
+  const int ktps = cdiv(KT, splits);
+  splits = cdiv(KT, ktps);
+  dim3 grid(cdiv(n, BM), cdiv(k, BN), splits);
+  TRY(launch_pdl(kern, grid, dim3(Cfg::THREADS), Cfg::SMEM, st, ma, mb, n, k, n, alpha, Y, ldy,
+                 splits > 1 ? part : (double*)nullptr, ktps));
+  if (splits > 1)
+    TRY(launch_pdl(splitk_reduce_kernel, dim3(cdiv(n, 256), k), dim3(256), 0, st, n, k, splits, alpha,
+                   (const double*)part, 0.0, Y, ldy));
   return 0;
 }
 
@@ -1294,7 +1365,15 @@ struct Run {
       }
       CK(cudaEventRecord(c->ev[2 * nev], st));
     }
-    {
+    static const int a3_tma = getenv("PSDPROJ_A3_TMA") ? atoi(getenv("PSDPROJ_A3_TMA")) : 1;
+    const bool tma_ok = a3_tma && !c->sharded && lda % 2 == 0 && ldz % 2 == 0 && ((uintptr_t)A & 15) == 0 &&
+                        ((uintptr_t)Z & 15) == 0;
+    if (tma_ok) {
+      const bool narrow = k <= 96 && (k % 64) != 0 && (k % 64) <= 32;
+      int rc_ = narrow ? gemm_tma_launch<64, 32, 6>(st, n, k, sgn, A, lda, Z, ldz, Y, ldy, c->part, c->part_elems)
+                       : gemm_tma_launch<64, 64, 6>(st, n, k, sgn, A, lda, Z, ldz, Y, ldy, c->part, c->part_elems);
+      if (rc_ < 0) return rc_;
+    } else {
       const bool narrow = k <= 96 && (k % 64) != 0 && (k % 64) <= 32;
       int rc_ = narrow ? gemm_kp_launch<OP_N, OP_N, 64, 32, 4, 1>(st, nl, k, n, sgn, A, lda, Z, ldz, 0.0, Y, ldy,
                                                                   c->part, c->part_elems)
@@ -2525,6 +2604,84 @@ extern "C" int psdproj_project_tiny_batched(int count, const int* n, const doubl
   return 0;
 }
 
+// ------------------------------------------------------------------ f4: one-CTA warm LOBPCG per tiny block
+extern "C" size_t psdproj_tiny_lobpcg_ws_bytes(int count) {
+  return count <= 0 ? 0 : (size_t)count * (sizeof(TinyLobBlock) + sizeof(TinyLobOut)) + 512;
+}
+
+extern "C" int psdproj_project_tiny_lobpcg(int count, const int* n, const double* const* A, const int* lda,
+                                           double* const* Pi, const int* ldpi, double* const* Xw, int* m_state,
+                                           double tol, int max_iter, int guard, int m0, uint64_t seed, uint32_t call,
+                                           void* ws, size_t ws_bytes, int* status, int* iters, int* npos,
+                                           double* bound, void* stream) {
+  if (count < 0 || (count > 0 && (!n || !A || !lda || !Pi || !ldpi || !Xw || !m_state || !ws || !status || !iters ||
+                                   !npos || !bound)) ||
+      !(tol > 0.0) || max_iter < 0 || guard < 1 || m0 < 1)
+    return set_err(PSDPROJ_E_INVALID, "invalid tiny-LOBPCG arguments");
+  if (count == 0) return 0;
+  if (ws_bytes < psdproj_tiny_lobpcg_ws_bytes(count) || ((uintptr_t)ws & 15))
+    return set_err(PSDPROJ_E_WORKSPACE, "tiny-LOBPCG workspace too small / misaligned");
+  cudaStream_t st = (cudaStream_t)stream;
+  int nmax = 1;
+  std::vector<TinyLobBlock> hb((size_t)count);
+  std::vector<TinyLobOut> ho((size_t)count);
+  for (int i = 0; i < count; ++i) {
+    if (n[i] < 1 || n[i] > TL_NMAX || !A[i] || !Pi[i] || !Xw[i] || lda[i] < n[i] || ldpi[i] < n[i])
+      return set_err(n[i] > TL_NMAX ? PSDPROJ_E_CAPACITY : PSDPROJ_E_INVALID, "tiny block %d: n = %d (1..%d)", i, n[i],
+                     TL_NMAX);
+    hb[i] = TinyLobBlock{A[i], Pi[i], Xw[i], n[i], lda[i], ldpi[i], 0};
+    ho[i] = TinyLobOut{0.0, 0.0, 0, 0, 0, std::max(0, std::min(m_state[i], TL_MCAP))};
+    nmax = std::max(nmax, n[i]);
+  }
+  TinyLobBlock* dblk = reinterpret_cast<TinyLobBlock*>(ws);
+  TinyLobOut* dout = reinterpret_cast<TinyLobOut*>(
+      (char*)ws + (((size_t)count * sizeof(TinyLobBlock) + 255) / 256) * 256);
+  CK(cudaMemcpyAsync(dblk, hb.data(), sizeof(TinyLobBlock) * count, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(dout, ho.data(), sizeof(TinyLobOut) * count, cudaMemcpyHostToDevice, st));
+  const size_t smem = tiny_lob_smem_doubles(nmax) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(tiny_lobpcg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)(tiny_lob_smem_doubles(TL_NMAX) * sizeof(double))));
+    attr = true;
+  }
+  tiny_lobpcg_kernel<<<count, TL_NT, smem, st>>>(dblk, dout, tol, max_iter, guard, m0, seed, call);
+  CKL();
+  CK(cudaMemcpyAsync(ho.data(), dout, sizeof(TinyLobOut) * count, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  // blocks the one-CTA LOBPCG hands back (capacity / singular pencil): the exact one-CTA path (R50)
+  std::vector<int> xn, xl, xp, xi;
+  std::vector<const double*> xa;
+  std::vector<double*> xpi;
+  for (int i = 0; i < count; ++i) {
+    status[i] = ho[i].status;
+    iters[i] = ho[i].iters;
+    npos[i] = ho[i].npos;
+    bound[i] = ho[i].bound;
+    m_state[i] = ho[i].m;
+    if (ho[i].status == TL_NEEDS_EXACT) {
+      xi.push_back(i);
+      xn.push_back(n[i]);
+      xa.push_back(A[i]);
+      xl.push_back(lda[i]);
+      xpi.push_back(Pi[i]);
+      xp.push_back(ldpi[i]);
+    }
+  }
+  if (!xi.empty()) {
+    std::vector<int> np(xi.size());
+    TRY(psdproj_project_tiny_batched((int)xi.size(), xn.data(), xa.data(), xl.data(), xpi.data(), xp.data(), np.data(),
+                                     stream));
+    for (size_t k = 0; k < xi.size(); ++k) {
+      npos[xi[k]] = np[k];
+      status[xi[k]] = 3;  // computed by the exact path (no LOBPCG bound; Jacobi to rounding level)
+      bound[xi[k]] = 0.0;
+      m_state[xi[k]] = 0;
+    }
+  }
+  return 0;
+}
+
 extern "C" int psdproj_project_batched(psdproj_ctx* ctxs, int count, const double* const* A, const int* lda,
                                        double* const* Pi, const int* ldpi, const double* tol, void* stream,
                                        psdproj_info* infos) {
@@ -2623,6 +2780,18 @@ extern "C" int psdproj_dgemm(int opA, int opB, int M, int N, int K, double alpha
     return set_err(PSDPROJ_E_INVALID, "invalid leading dimension");
   int rc = dgemm((cudaStream_t)stream, opA, opB, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws, ws ? ws_elems : 0);
   return rc;
+}
+
+extern "C" int psdproj_symm_multiply(int n, int k, double alpha, const double* A, int lda, const double* Z, int ldz,
+                                     double* Y, int ldy, double* ws, size_t ws_elems, void* stream) {
+  if (n <= 0 || k <= 0 || lda < n || ldz < n || ldy < n || !A || !Z || !Y)
+    return set_err(PSDPROJ_E_INVALID, "invalid symm_multiply arguments");
+  if (lda % 2 || ldz % 2 || ((uintptr_t)A & 15) || ((uintptr_t)Z & 15))
+    return set_err(PSDPROJ_E_INVALID, "symm_multiply needs even leading dimensions and 16-byte aligned A, Z");
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool narrow = k <= 96 && (k % 64) != 0 && (k % 64) <= 32;
+  if (narrow) return gemm_tma_launch<64, 32, 6>(st, n, k, alpha, A, lda, Z, ldz, Y, ldy, ws, ws ? ws_elems : 0);
+  return gemm_tma_launch<64, 64, 6>(st, n, k, alpha, A, lda, Z, ldz, Y, ldy, ws, ws ? ws_elems : 0);
 }
 
 extern "C" size_t psdproj_jacobi_ws_elems(int s) {

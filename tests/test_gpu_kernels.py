@@ -165,3 +165,22 @@ def test_eigh_extreme_scales(api, s, scale):
     ref = np.sort(np.diag(A))[::-1]
     assert npos == int(np.sum(ref > 0))
     assert np.abs(w.cpu().numpy() - ref).max() <= 1e-13 * scale * s + 1e-306
+
+
+@pytest.mark.parametrize("n,k", [(64, 1), (130, 7), (1000, 33), (1000, 64), (2048, 100), (4000, 70), (4000, 200),
+                                 (998, 17)])
+@pytest.mark.parametrize("split", [False, True])
+def test_symm_multiply_tma(api, n, k, split):
+    """a3 block multiply on TMA-staged swizzled tiles (psdproj_symm_multiply, the kernel the path
+    runs) against an fp64 reference: ragged m / k / column tiles come from the TMA zero fill."""
+    rng = np.random.default_rng(n + k)
+    M = rng.standard_normal((n, n))
+    A = (M + M.T) / 2
+    Z = rng.standard_normal((n, k))
+    Ad = torch.from_numpy(A).cuda()
+    Zd = api.colmajor(n, k)
+    Zd.copy_(torch.from_numpy(Z))
+    ws = torch.empty(32 * n * k, dtype=torch.float64, device="cuda") if split else None
+    Y = api.symm_multiply(-1.0, Ad, Zd, ws=ws).cpu().numpy()
+    ref = -(A @ Z)
+    assert np.abs(Y - ref).max() <= 1e-13 * np.sqrt(n) * np.abs(ref).max()

@@ -199,3 +199,28 @@ def maxcut_graph(n=2000, p_edge=0.01, seed=501):
     W[iu[0][mask], iu[1][mask]] = w
     W = W + W.T
     return np.diag(W.sum(axis=1)) - W
+
+
+class BO:
+    """f4 stand-in for the Bayesian-optimisation SDPs of PAPER.md:605-649 (their data are not in the
+    container): `count` independent blocks, n_i ~ U{lo..hi}, a rank-one PSD part (one eigenvalue ~ U[1, 10],
+    P:647 "rank-one solutions") and the rest ~ U[-5, -0.1], planted Q_i; each round drifts every block by
+    1e-3 sym(G) (as C4, R32)."""
+
+    seed = 601
+    tol = 1e-10
+
+    def __init__(self, count=4096, lo=8, hi=100):
+        rng = np.random.default_rng(self.seed)
+        self.count = count
+        self.sizes = [int(x) for x in rng.integers(lo, hi + 1, count)]
+
+    def block(self, i):
+        n = self.sizes[i]
+        rng = np.random.default_rng([self.seed, i])
+        lam = np.concatenate([rng.uniform(1.0, 10.0, 1), -rng.uniform(0.1, 5.0, n - 1)])
+        return haar_q(rng, n), lam
+
+    def drift(self, i, r):
+        n = self.sizes[i]
+        return 1e-3 * sym(np.random.default_rng([self.seed, i, r]).standard_normal((n, n)))
