@@ -127,7 +127,7 @@ def lobpcg_pos(B, X0, tol, max_iter=500, guard=1, q=None, locking="hard", seed=0
     n = B.shape[0]
     m_max = n if m_max is None else m_max
     q = q if q else max(int(math.ceil(0.05 * n)), 1)
-    # guard certification theta_g + r_g <= guard_tol, relaxed form with guard_tol = tol (R52)
+    # guard certification theta_g + r_g <= guard_tol and r_g <= max(guard_tol, |theta_g|/2) (R52, R60)
     guard_tol = tol if guard_tol is None else guard_tol
     res = LobpcgResult()
     res.expansions = 0
@@ -172,7 +172,8 @@ def lobpcg_pos(B, X0, tol, max_iter=500, guard=1, q=None, locking="hard", seed=0
             guard_ok = False
         else:
             g = int(np.argmax(np.where(pos, -np.inf, theta)))
-            guard_ok = bool(theta[g] + r[g] <= guard_tol)
+            # R52 relaxed form, R60: the guard itself must be within max(tol, |theta_g|/2) of convergence
+            guard_ok = bool(theta[g] + r[g] <= guard_tol and r[g] <= max(guard_tol, 0.5 * abs(theta[g])))
         converged = conv_pos and guard_ok and E is None and not (cold and k == 0)
         if converged:
             status = OK

@@ -58,7 +58,8 @@ __device__ __forceinline__ void dmma_884t(double (&d)[2], double a, double b) {
 
 template <int BM, int BN, int STAGES>
 struct TmaGemmCfg {
-  static constexpr int THREADS = (BM / 32) * (BN / 32) * 32;
+  static constexpr int WN = BN < 32 ? BN : 32;  // warp tile width (BN = 16: the HBM-bound small-k variant)
+  static constexpr int THREADS = (BM / 32) * (BN / WN) * 32;
   static constexpr int A_BYTES = BM * 128, B_BYTES = BN * 128, STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + 1024 + 64;  // + 1024-B alignment, barriers
 };
@@ -72,7 +73,7 @@ __global__ void __launch_bounds__(TmaGemmCfg<BM, BN, STAGES>::THREADS, (BM * BN 
                      int ktiles_per_split) {
   using Cfg = TmaGemmCfg<BM, BN, STAGES>;
   asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL (launch_pdl): inputs written by the predecessor
-  constexpr int WM = 32, WN = 32, BK = 16;
+  constexpr int WM = 32, WN = Cfg::WN, BK = 16;
   constexpr int WARPS_M = BM / WM;
   constexpr int MI = WM / 8, NI = WN / 8;
   extern __shared__ __align__(16) unsigned char tma_smem_raw[];
@@ -80,7 +81,8 @@ __global__ void __launch_bounds__(TmaGemmCfg<BM, BN, STAGES>::THREADS, (BM * BN 
   uint64_t* full = reinterpret_cast<uint64_t*>(base + (size_t)STAGES * Cfg::STAGE_BYTES);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp % WARPS_M, wn = warp / WARPS_M;
-  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  // column tiles fastest: the CTAs that share a row panel of A run together and read it from L2 once
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
   const int KT = cdiv(K, BK);
   const int kt0 = blockIdx.z * ktiles_per_split;
   const int nkt = max(0, min(KT, kt0 + ktiles_per_split) - kt0);

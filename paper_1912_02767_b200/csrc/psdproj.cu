@@ -287,15 +287,23 @@ static int gemm_tma_launch(cudaStream_t st, int n, int k, double alpha, const do
   const int KT = cdiv(std::max(n, 1), 16);
   const int tiles = cdiv(n, BM) * cdiv(k, BN);
   const int slots = std::max(1, sms() - g_sm_reserve) * per_sm;
+  // split-K count with the best wave efficiency tiles * splits / (waves * slots) (fewer splits on ties)
   int splits = 1;
-  if (part && tiles < slots && KT >= 8) {
-    splits = std::min(std::max(1, slots / tiles), KT / 4);
-    splits = std::max(1, std::min(splits, 32));
-    while (splits > 1 && (size_t)splits * n * k > part_elems) --splits;
+  if (part && KT >= 8) {
+    double best = 0.0;
+    for (int sp = 1; sp <= std::min(16, KT / 4); ++sp) {
+      if ((size_t)sp * n * k > part_elems) break;
+      const int waves = cdiv(tiles * sp, slots);
+      const double eff = (double)tiles * sp / ((double)waves * slots);
+      if (eff > best + 0.02) {
+        best = eff;
+        splits = sp;
+      }
+    }
   }
   const int ktps = cdiv(KT, splits);
   splits = cdiv(KT, ktps);
-  dim3 grid(cdiv(n, BM), cdiv(k, BN), splits);
+  dim3 grid(cdiv(k, BN), cdiv(n, BM), splits);
   TRY(launch_pdl(kern, grid, dim3(Cfg::THREADS), Cfg::SMEM, st, ma, mb, n, k, n, alpha, Y, ldy,
                  splits > 1 ? part : (double*)nullptr, ktps));
   if (splits > 1)
@@ -951,7 +959,7 @@ struct psdproj_ctx_s {
   int m0 = 0, q = 0, m_max = 0, s_max = 0, NJ = 0, tcols = 0;
   // device (carved from the caller's workspace)
   double *S = nullptr, *BS = nullptr, *S2 = nullptr, *BS2 = nullptr, *T = nullptr, *T2 = nullptr, *E = nullptr;
-  double *Pb = nullptr, *BPb = nullptr, *XL = nullptr, *BXL = nullptr, *R = nullptr, *Xw = nullptr;
+  double *Pb = nullptr, *BPb = nullptr, *R = nullptr, *Xw = nullptr;
   double *G = nullptr, *Hm = nullptr, *Gc = nullptr, *Li = nullptr, *Y = nullptr, *Hh = nullptr, *Vj = nullptr,
          *Cp = nullptr;
   double *jM = nullptr, *jM2 = nullptr, *jQ = nullptr;
@@ -1023,6 +1031,9 @@ static void resolve(int n, const psdproj_params* in, psdproj_params& p, int& m0,
   m_max = std::max(1, std::min(m_max, (TRINV_MAX - q) / (dpt + 1)));  // and its direction block (<= (d + 1) m + q) the L^-1 kernel
   m0 = std::min(m0, m_max);
   s_max = (dpt + 2) * m_max + q;
+  // the DIRECT path (tridiagonal eigensolver for n <= EIG_MAX) runs in the s_max-sized eigensolver
+  // scratch (reflectors, column store, Newton-Schulz buffers): keep s_max >= n there
+  if (!sharded && n <= EIG_MAX) s_max = std::max(s_max, n);
   NJ = sharded ? s_max : std::max(s_max, n);  // the sharded mode has no DIRECT path
   NJ += NJ & 1;
   tcols = sharded ? s_max : std::max(s_max, n);
@@ -1034,12 +1045,18 @@ static size_t carve(psdproj_ctx_s* c, int n, const psdproj_params& p, int m_max,
   if (nl < 0) nl = n;
   int ld = rup(std::max(nl, 1), 8);
   size_t nS = (size_t)ld * s_max, nM = (size_t)ld * m_max, nT = (size_t)ld * tcols, s2 = (size_t)s_max * s_max;
-  c->S = cv.take<double>(nS); c->BS = cv.take<double>(nS);
-  c->S2 = cv.take<double>(nS); c->BS2 = cv.take<double>(nS);
+  // S, BS and their rotation targets each carry an m_max-column prefix: the hard-locked block X_L (and
+  // B X_L) lives right-aligned in front of S (mirrored in front of S2), so [X_L | X_U] is one
+  // contiguous n x (nL + mU) block for the projections (one Gram and one update GEMM, not two)
+  const size_t pre = (size_t)ld * m_max;
+  c->S = cv.take<double>(nS + pre); c->BS = cv.take<double>(nS + pre);
+  c->S2 = cv.take<double>(nS + pre); c->BS2 = cv.take<double>(nS + pre);
+  if (!dry) {
+    c->S += pre; c->BS += pre; c->S2 += pre; c->BS2 += pre;
+  }
   c->T = cv.take<double>(nT); c->T2 = cv.take<double>(nT);
   c->E = cv.take<double>(nT);
   c->Pb = cv.take<double>(nM); c->BPb = cv.take<double>(nM);
-  c->XL = cv.take<double>(nM); c->BXL = cv.take<double>(nM);
   c->R = cv.take<double>(nM); c->Xw = cv.take<double>(nM);
   c->G = cv.take<double>(s2); c->Hm = cv.take<double>(s2); c->Gc = cv.take<double>(s2);
   c->Li = cv.take<double>(s2); c->Y = cv.take<double>(s2); c->Hh = cv.take<double>(s2);
@@ -1369,9 +1386,12 @@ struct Run {
     const bool tma_ok = a3_tma && !c->sharded && lda % 2 == 0 && ldz % 2 == 0 && ((uintptr_t)A & 15) == 0 &&
                         ((uintptr_t)Z & 15) == 0;
     if (tma_ok) {
+      // column tile: 16 for k <= 16 (HBM-bound: no DMMA on zero padding), 32 when the last 64-tile
+      // would be at most half full, else 64
       const bool narrow = k <= 96 && (k % 64) != 0 && (k % 64) <= 32;
-      int rc_ = narrow ? gemm_tma_launch<64, 32, 6>(st, n, k, sgn, A, lda, Z, ldz, Y, ldy, c->part, c->part_elems)
-                       : gemm_tma_launch<64, 64, 6>(st, n, k, sgn, A, lda, Z, ldz, Y, ldy, c->part, c->part_elems);
+      int rc_ = k <= 16 ? gemm_tma_launch<64, 16, 6>(st, n, k, sgn, A, lda, Z, ldz, Y, ldy, c->part, c->part_elems)
+                : narrow ? gemm_tma_launch<64, 32, 4>(st, n, k, sgn, A, lda, Z, ldz, Y, ldy, c->part, c->part_elems)
+                         : gemm_tma_launch<64, 64, 4>(st, n, k, sgn, A, lda, Z, ldz, Y, ldy, c->part, c->part_elems);
       if (rc_ < 0) return rc_;
     } else {
       const bool narrow = k <= 96 && (k % 64) != 0 && (k % 64) <= 32;
@@ -1947,6 +1967,10 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
   CK(cudaMemcpyAsync(c->d_thU, c->d_ths, sizeof(double) * m, cudaMemcpyDeviceToDevice, st));
 
   int mU = m, nL = 0, qe = 0;
+  // the hard-locked block X_L / B X_L: right-aligned in the prefix of the current S / BS (mirrored in
+  // front of S2 / BS2), so that [X_L | X_U] is contiguous
+  auto XLp = [&]() { return c->S - (size_t)nL * ld; };
+  auto BXLp = [&]() { return c->BS - (size_t)nL * ld; };
   std::vector<double> rU(m, INFINITY), thL, rL;
   std::vector<char> hasP(m, 0);
   int status = PSDPROJ_NOT_CONVERGED;
@@ -1960,8 +1984,8 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
     if (restart > 0 && k > 0 && k % restart == 0 && mU > 0) {
       TRY(run.mark(0));
       if (hard && nL > 0) {
-        TRY(run.gram(nL, mU, c->XL, ld, c->S, ld, c->Y, ldm));
-        TRY(run.gemm(OP_N, OP_N, nl, mU, nL, -1.0, c->XL, ld, c->Y, ldm, 1.0, c->S, ld));
+        TRY(run.gram(nL, mU, XLp(), ld, c->S, ld, c->Y, ldm));
+        TRY(run.gemm(OP_N, OP_N, nl, mU, nL, -1.0, XLp(), ld, c->Y, ldm, 1.0, c->S, ld));
       }
       TRY(run.amul(sgn, A, lda, c->S, ld, mU, c->BS, ld));
       int rr0;
@@ -2030,10 +2054,13 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
       }
     }
     int mtot = nL + mU;
-    // guard certification in the relaxed form theta_g + r_g <= tol (R52): the
-    // eigenvalue it could hide is then <= tol; with the paper's loose schedule (10/k^1.01)
-    // the strict form (<= 0) would demand r_g <= |theta_g| whatever the tolerance
-    bool guard_ok = (mtot >= n) ? true : (has_guard && g_th + g_r <= tol);
+    // guard certification theta_g + r_g <= tol (R52: its inclusion interval lies below tol) and
+    // r_g <= max(tol, |theta_g| / 2) (R60): a guard whose residual exceeds both the tolerance and half
+    // its distance to zero is too far from convergence to vouch for the block (a cold 2-column block
+    // passed R52 at k = 1 with theta_g = -0.86, r_g = 0.83 and missed the only positive eigenvalue);
+    // with the paper's loose schedule (10/k^1.01) both reduce to r_g <= tol-ish
+    bool guard_ok = (mtot >= n) ? true
+                                : (has_guard && g_th + g_r <= tol && g_r <= std::max(tol, 0.5 * std::fabs(g_th)));
     bool converged = conv_pos && guard_ok && qe == 0 && !(cold && k == 0);
     if (converged) {
       status = PSDPROJ_OK;
@@ -2052,11 +2079,20 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
         keep.push_back(j);
     }
     if (!lock.empty()) {
-      TRY(run.gather(nl, (int)lock.size(), c->XL + (size_t)nL * ld, ld, c->S, ld, lock));
-      TRY(run.gather(nl, (int)lock.size(), c->BXL + (size_t)nL * ld, ld, c->BS, ld, lock));
-      for (int j : lock) {
-        thL.push_back(thU[j]);
-        rL.push_back(rU[j]);
+      // the newly locked columns join X_L at its front (in both S prefixes and both BS prefixes)
+      const size_t nw = (size_t)(nL + lock.size()) * ld;
+      TRY(run.gather(nl, (int)lock.size(), c->S - nw, ld, c->S, ld, lock));
+      TRY(run.gather(nl, (int)lock.size(), c->S2 - nw, ld, c->S, ld, lock));
+      TRY(run.gather(nl, (int)lock.size(), c->BS - nw, ld, c->BS, ld, lock));
+      TRY(run.gather(nl, (int)lock.size(), c->BS2 - nw, ld, c->BS, ld, lock));
+      {
+        std::vector<double> th0, r0;
+        for (int j : lock) {
+          th0.push_back(thU[j]);
+          r0.push_back(rU[j]);
+        }
+        thL.insert(thL.begin(), th0.begin(), th0.end());
+        rL.insert(rL.begin(), r0.begin(), r0.end());
       }
       nL += (int)lock.size();
       // compact U (X, BX, P, BP, theta)
@@ -2112,8 +2148,8 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
       }
       TRY(run.philox(qq, c->E, ld, (uint32_t)(k + 1) | 0x80000000u));
       for (int pass = 0; pass < 2 && nL > 0; ++pass) {
-        TRY(run.gram(nL, qq, c->XL, ld, c->E, ld, c->Y, ldm));
-        TRY(run.gemm(OP_N, OP_N, nl, qq, nL, -1.0, c->XL, ld, c->Y, ldm, 1.0, c->E, ld));
+        TRY(run.gram(nL, qq, XLp(), ld, c->E, ld, c->Y, ldm));
+        TRY(run.gemm(OP_N, OP_N, nl, qq, nL, -1.0, XLp(), ld, c->Y, ldm, 1.0, c->E, ld));
       }
       qe = qq;
       info->expansions++;
@@ -2139,22 +2175,21 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
     const int wp = aw + ap;
     static int lock_reproj = getenv("PSDPROJ_LOCK_REPROJ") ? atoi(getenv("PSDPROJ_LOCK_REPROJ")) : 0;
     const int xr = (lock_reproj && hard && nL > 0) ? mU : 0;  // X_U columns included (R46)
-    if (hard && nL > 0 && xr + wp > 0) {
-      // [X_U W P] <- [X_U W P] - X_L (X_L^T [X_U W P]) (B-images of X_U and P alike). X_U is
-      // re-projected every iteration: it inherits the rotation's O(u ||C'||) component along X_L,
-      // which otherwise compounds over a long run until active columns duplicate locked ones (R46)
-      const int cols = xr + wp;
-      double* Z = xr ? c->S : W;
-      TRY(run.gram(nL, cols, c->XL, ld, Z, ld, c->Y, ldm));
-      TRY(run.gemm(OP_N, OP_N, nl, cols, nL, -1.0, c->XL, ld, c->Y, ldm, 1.0, Z, ld));
-      if (xr > 0) TRY(run.gemm(OP_N, OP_N, nl, xr, nL, -1.0, c->BXL, ld, c->Y, ldm, 1.0, c->BS, ld));
-      if (ap > 0)
-        TRY(run.gemm(OP_N, OP_N, nl, ap, nL, -1.0, c->BXL, ld, c->Y + (size_t)(xr + aw) * ldm, ldm, 1.0, BP, ld));
+    if (xr > 0) {
+      // R46 (off by default): X_U (and B X_U) re-projected against X_L
+      TRY(run.gram(nL, xr, XLp(), ld, c->S, ld, c->Y, ldm));
+      TRY(run.gemm(OP_N, OP_N, nl, xr, nL, -1.0, XLp(), ld, c->Y, ldm, 1.0, c->S, ld));
+      TRY(run.gemm(OP_N, OP_N, nl, xr, nL, -1.0, BXLp(), ld, c->Y, ldm, 1.0, c->BS, ld));
     }
-    if (wp > 0) {  // [W P] <- [W P] - X_U (X_U^T [W P]): the pencil's X-block of G becomes [I 0]
-      TRY(run.gram(mU, wp, c->S, ld, W, ld, c->Y, ldm));
-      TRY(run.gemm(OP_N, OP_N, nl, wp, mU, -1.0, c->S, ld, c->Y, ldm, 1.0, W, ld));
-      if (ap > 0) TRY(run.gemm(OP_N, OP_N, nl, ap, mU, -1.0, c->BS, ld, c->Y + (size_t)aw * ldm, ldm, 1.0, BP, ld));
+    if (wp > 0) {
+      // [W P] <- [W P] - [X_L X_U] ([X_L X_U]^T [W P]) in one pass over the contiguous block (B P
+      // likewise with [B X_L, B X_U]): the pencil's X-block of G becomes [I 0]
+      const int nX = (hard ? nL : 0) + mU;
+      double* Xall = hard ? XLp() : c->S;
+      double* BXall = hard ? BXLp() : c->BS;
+      TRY(run.gram(nX, wp, Xall, ld, W, ld, c->Y, ldm));
+      TRY(run.gemm(OP_N, OP_N, nl, wp, nX, -1.0, Xall, ld, c->Y, ldm, 1.0, W, ld));
+      if (ap > 0) TRY(run.gemm(OP_N, OP_N, nl, ap, nX, -1.0, BXall, ld, c->Y + (size_t)aw * ldm, ldm, 1.0, BP, ld));
     }
     TRY(run.normalize(nl, aw, W, ld, nullptr, 0));
     if (ap > 0) TRY(run.normalize(nl, ap, P, ld, BP, ld));
@@ -2212,8 +2247,8 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
         double* BK = c->BS + (size_t)offK * ld;
         TRY(copy_block_pdl(st, nl, aK, K, ld, BKprev, ld));
         if (hard && nL > 0) {
-          TRY(run.gram(nL, aK, c->XL, ld, K, ld, c->Y, ldm));
-          TRY(run.gemm(OP_N, OP_N, nl, aK, nL, -1.0, c->XL, ld, c->Y, ldm, 1.0, K, ld));
+          TRY(run.gram(nL, aK, XLp(), ld, K, ld, c->Y, ldm));
+          TRY(run.gemm(OP_N, OP_N, nl, aK, nL, -1.0, XLp(), ld, c->Y, ldm, 1.0, K, ld));
         }
         TRY(run.gram(mU, aK, c->S, ld, K, ld, c->Y, ldm));
         TRY(run.gemm(OP_N, OP_N, nl, aK, mU, -1.0, c->S, ld, c->Y, ldm, 1.0, K, ld));
@@ -2281,7 +2316,7 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
         for (int i = 0; i < mUn; ++i) oU = std::max(oU, std::fabs(hY[(size_t)j * ldm + i] - (i == j)));
       double oL = 0;
       if (nL > 0) {
-        TRY(run.gram(nL, mUn, c->XL, ld, c->S, ld, c->Y, ldm));
+        TRY(run.gram(nL, mUn, XLp(), ld, c->S, ld, c->Y, ldm));
         TRY(run.sync());
         CK(cudaMemcpy(hY.data(), c->Y, sizeof(double) * (size_t)ldm * mUn, cudaMemcpyDeviceToHost));
         for (int j = 0; j < mUn; ++j)
@@ -2311,8 +2346,8 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
       TRY(run.philox(qq, c->E, ld, (uint32_t)k));
       for (int pass = 0; pass < 2; ++pass) {
         if (nL > 0) {
-          TRY(run.gram(nL, qq, c->XL, ld, c->E, ld, c->Y, ldm));
-          TRY(run.gemm(OP_N, OP_N, nl, qq, nL, -1.0, c->XL, ld, c->Y, ldm, 1.0, c->E, ld));
+          TRY(run.gram(nL, qq, XLp(), ld, c->E, ld, c->Y, ldm));
+          TRY(run.gemm(OP_N, OP_N, nl, qq, nL, -1.0, XLp(), ld, c->Y, ldm, 1.0, c->E, ld));
         }
         TRY(run.gram(mU, qq, c->S, ld, c->E, ld, c->Y, ldm));
         TRY(run.gemm(OP_N, OP_N, nl, qq, mU, -1.0, c->S, ld, c->Y, ldm, 1.0, c->E, ld));
@@ -2336,7 +2371,7 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
   int p = (int)wts.size();
   double* V = c->T;
   double* BV = c->T2;
-  TRY(run.gather(nl, (int)lpos.size(), V, ld, c->XL, ld, lpos));
+  TRY(run.gather(nl, (int)lpos.size(), V, ld, XLp(), ld, lpos));
   TRY(run.gather(nl, (int)upos.size(), V + (size_t)lpos.size() * ld, ld, c->S, ld, upos));
   for (int j = 0; j < p; ++j) c->h_d[j] = wts[j];
   CK(cudaMemcpyAsync(c->d_w, c->h_d, sizeof(double) * std::max(p, 1), cudaMemcpyHostToDevice, st));
@@ -2403,7 +2438,7 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
     if (cols[i].src == 0) { li.push_back(cols[i].j); pos_l.push_back(i); }
     else { ui.push_back(cols[i].j); pos_u.push_back(i); }
   }
-  TRY(run.gather(nl, (int)li.size(), c->T2, ld, c->XL, ld, li));
+  TRY(run.gather(nl, (int)li.size(), c->T2, ld, XLp(), ld, li));
   TRY(run.gather(nl, (int)ui.size(), c->T2 + (size_t)li.size() * ld, ld, c->S, ld, ui));
   std::vector<int> perm(keepn);  // Xw[:, pos] = T2[:, staged index]
   for (size_t i = 0; i < pos_l.size(); ++i) perm[pos_l[i]] = (int)i;
@@ -2629,7 +2664,8 @@ extern "C" int psdproj_project_tiny_lobpcg(int count, const int* n, const double
     if (n[i] < 1 || n[i] > TL_NMAX || !A[i] || !Pi[i] || !Xw[i] || lda[i] < n[i] || ldpi[i] < n[i])
       return set_err(n[i] > TL_NMAX ? PSDPROJ_E_CAPACITY : PSDPROJ_E_INVALID, "tiny block %d: n = %d (1..%d)", i, n[i],
                      TL_NMAX);
-    hb[i] = TinyLobBlock{A[i], Pi[i], Xw[i], n[i], lda[i], ldpi[i], 0};
+    static const int dbg = getenv("PSDPROJ_TINY_DEBUG") ? atoi(getenv("PSDPROJ_TINY_DEBUG")) : -1;
+    hb[i] = TinyLobBlock{A[i], Pi[i], Xw[i], n[i], lda[i], ldpi[i], i == dbg ? 1 : 0};
     ho[i] = TinyLobOut{0.0, 0.0, 0, 0, 0, std::max(0, std::min(m_state[i], TL_MCAP))};
     nmax = std::max(nmax, n[i]);
   }
@@ -2790,8 +2826,9 @@ extern "C" int psdproj_symm_multiply(int n, int k, double alpha, const double* A
     return set_err(PSDPROJ_E_INVALID, "symm_multiply needs even leading dimensions and 16-byte aligned A, Z");
   cudaStream_t st = (cudaStream_t)stream;
   const bool narrow = k <= 96 && (k % 64) != 0 && (k % 64) <= 32;
-  if (narrow) return gemm_tma_launch<64, 32, 6>(st, n, k, alpha, A, lda, Z, ldz, Y, ldy, ws, ws ? ws_elems : 0);
-  return gemm_tma_launch<64, 64, 6>(st, n, k, alpha, A, lda, Z, ldz, Y, ldy, ws, ws ? ws_elems : 0);
+  if (k <= 16) return gemm_tma_launch<64, 16, 6>(st, n, k, alpha, A, lda, Z, ldz, Y, ldy, ws, ws ? ws_elems : 0);
+  if (narrow) return gemm_tma_launch<64, 32, 4>(st, n, k, alpha, A, lda, Z, ldz, Y, ldy, ws, ws ? ws_elems : 0);
+  return gemm_tma_launch<64, 64, 4>(st, n, k, alpha, A, lda, Z, ldz, Y, ldy, ws, ws ? ws_elems : 0);
 }
 
 extern "C" size_t psdproj_jacobi_ws_elems(int s) {

@@ -184,7 +184,8 @@ __global__ void __launch_bounds__(TL_NT) tiny_lobpcg_kernel(const TinyLobBlock* 
   fro = sqrt(block_sum<TL_NT>(fro, scal));
   int m = out->m;
   const bool cold = m <= 0;
-  if (cold) m = min(m0, TL_MCAP);
+  // cold: max(m0, ceil(n/10)) Philox columns (R28's width), within the block capacity and 3 m + 1 <= n
+  if (cold) m = min(min(max(m0, (n + 9) / 10), TL_MCAP), max(1, (n - 1) / 3));
   if (tid == 0) {
     out->anorm = fro;
     sh_state = (n < 3 * m + 1 || m > TL_MCAP) ? TL_NEEDS_EXACT : -1;
@@ -286,8 +287,13 @@ __global__ void __launch_bounds__(TL_NT) tiny_lobpcg_kernel(const TinyLobBlock* 
     __syncthreads();
     tl_colnorms(n, T1, m, rr);
     __syncthreads();
+    if (tid == 0 && bk.pad == 1) {  // debugging (PSDPROJ_TINY_DEBUG = block index)
+      printf("tiny k=%d m=%d qe=%d:", k, m, sh_qe);
+      for (int j = 0; j < m; ++j) printf(" (%.6g, %.3g)", th[j], rr[j]);
+      printf("\n");
+    }
     if (tid == 0) {
-      // stopping rule (R12, R52): positives r <= tol, largest non-positive theta_g + r_g <= tol, k >= 1 cold
+      // stopping rule (R12, R52, R60): positives r <= tol, largest non-positive: theta_g + r_g <= tol, r_g <= max(tol, |theta_g|/2); k >= 1 cold
       int npos = 0, g = -1;
       bool conv = true;
       for (int j = 0; j < m; ++j) {
@@ -298,7 +304,8 @@ __global__ void __launch_bounds__(TL_NT) tiny_lobpcg_kernel(const TinyLobBlock* 
           g = j;
         }
       }
-      const bool guard_ok = (m >= n) || (g >= 0 && th[g] + rr[g] <= tol);
+      const bool guard_ok =
+          (m >= n) || (g >= 0 && th[g] + rr[g] <= tol && rr[g] <= fmax(tol, 0.5 * fabs(th[g])));  // R52, R60
       sh_conv = conv && guard_ok && sh_qe == 0 && !(cold && k == 0);
       (void)npos;
       int a = 0;

@@ -333,3 +333,22 @@ def test_krylov_depth_parity(api, depth):
         its[d] = tot
         ctx.close()
     assert its[depth] * 1.4 <= its[1], its
+
+
+def test_direct_path_large_order(api):
+    """DIRECT on the tridiagonal eigensolver at n = 2000 (n <= EIG_MAX but > 3 m_max: the eigensolver
+    scratch must be sized for n, not for the LOBPCG basis): a half-positive planted spectrum, cold
+    call on the positive side expands past m_max and hands over to DIRECT (R18), then the one-third
+    rule keeps it there; closed-form Pi*, the R53 bound dominates."""
+    rng = np.random.default_rng(2000)
+    n = 2000
+    lam = rng.uniform(-1, 1, n)
+    Q = haar_q(rng, n)
+    A = planted(Q, lam)
+    Pstar = (Q * np.maximum(lam, 0)) @ Q.T
+    ctx = api.Context(n, seed=2)
+    for call in range(2):
+        Pi, info = ctx.project(_dev(A), 1e-10)
+        err = np.linalg.norm(Pi.cpu().numpy() - Pstar)
+        assert info["side"] == 2, info["side"]
+        assert err <= 1e-11 * np.linalg.norm(A) and info["err_bound"] >= err, (call, err, info["err_bound"])
