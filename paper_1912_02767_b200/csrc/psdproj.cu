@@ -37,6 +37,7 @@
 #include "tridiag_tile.cuh"
 #include "gemm_tma.cuh"
 #include "tiny_lobpcg.cuh"
+#include "sbr.cuh"
 
 using namespace psd;
 
@@ -537,6 +538,9 @@ static int cla_attrs() {
   TRI_REG_ATTR(7, 7)
   TRI_REG_ATTR(8, 8)
 #undef TRI_REG_ATTR
+  CK(cudaFuncSetAttribute(sb1_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  CK(cudaFuncSetAttribute(sb1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  CK(cudaFuncSetAttribute(sb2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   done = true;
   return 0;
 }
@@ -676,7 +680,27 @@ static int eigh_top(cudaStream_t st, int s, const double* Hs, int ldh, int m, do
   // 145 vs 234 us at s = 64 against the one-CTA shared-memory kernel; the 16-CTA cluster kernel is
   // faster from s ~ 100 up, 230 vs 339 us at s = 128, 567 vs 1183 us at s = 256 -- DESIGN.md §6)
   static const int tri_tile = getenv("PSDPROJ_TRI_TILE") ? atoi(getenv("PSDPROJ_TRI_TILE")) : 64;
-  const bool use_tile = tri_mode == 0 && s >= 3 && s <= std::min(tri_tile, TT_SMAX);
+  // two-stage reduction (sbr.cuh: dense -> band on a 16-CTA cluster, band -> tridiagonal in one CTA) for
+  // PSDPROJ_SBR_MIN <= s <= PSDPROJ_SBR_MAX when its shared memory and the scratch fit
+  static const int sbr_min = getenv("PSDPROJ_SBR_MIN") ? atoi(getenv("PSDPROJ_SBR_MIN")) : 96;
+  static const int sbr_max = getenv("PSDPROJ_SBR_MAX") ? atoi(getenv("PSDPROJ_SBR_MAX")) : SB_MAX;
+  static const int sbr_on = getenv("PSDPROJ_SBR") ? atoi(getenv("PSDPROJ_SBR")) : 0;  // measured slower
+  const bool use_sbr = sbr_on && tri_mode == 0 && s >= std::max(sbr_min, 3 * SB) && s <= std::min(sbr_max, SB_MAX) &&
+                       sb1_smem_doubles(s, 16) * sizeof(double) <= (size_t)CLA_SMEM_BYTES &&
+                       ((size_t)s * SB_LDW + SB2_NW * SB + s) * sizeof(double) <= (size_t)CLA_SMEM_BYTES &&
+                       sb_refl_doubles(s) + (size_t)SB_LDW * s <= (size_t)s * s;
+  double* sb_Vr = w.tG;
+  double* sb_Bg = w.tG + (size_t)s * s - (size_t)SB_LDW * s;
+  double* sb_Tq = w.tG + (size_t)s * s;
+  if (use_sbr) {
+    TRY(launch_cluster(sb1_kernel, 16, SB1_NT, sb1_smem_doubles(s, 16) * sizeof(double), st, s, Hs, ldh, sb_Bg, w.Vh,
+                       w.ldv, sb_Tq));
+    sb2_kernel<<<1, SB2_NW * 32, ((size_t)s * SB_LDW + SB2_NW * SB + s) * sizeof(double), st>>>(s, sb_Bg, w.td, w.te,
+                                                                                            sb_Vr);
+    CKL();
+    tcs = 0;
+  }
+  const bool use_tile = !use_sbr && tri_mode == 0 && s >= 3 && s <= std::min(tri_tile, TT_SMAX);
   if (use_tile) {
     static bool tattr = false;
     if (!tattr) {
@@ -694,7 +718,7 @@ static int eigh_top(cudaStream_t st, int s, const double* Hs, int ldh, int m, do
                      w.ldv, dprof, w.tG, tri_dbg))
   static int tri_reg = getenv("PSDPROJ_TRI_NOREG") ? 0 : 1;
   const int kr = cdiv(s, 64), cr = tcs ? cdiv(cdiv(s, tcs), TRI_TCG) : 99;
-  if (use_tile) {
+  if (use_tile || use_sbr) {
     // done above
   } else if (tcs && tri_reg && kr <= 8 && cr <= 8 &&
       tri_reg_smem_doubles(s, tcs) * sizeof(double) <= (size_t)CLA_SMEM_BYTES) {
@@ -836,7 +860,7 @@ static int eigh_top(cudaStream_t st, int s, const double* Hs, int ldh, int m, do
   const size_t bt_col_smem = bt_col_smem_doubles(s) * sizeof(double);
   const bool col_ok = bt_col && s <= 768 && bt_col_smem <= (size_t)CLA_SMEM_BYTES &&
                       m <= sms() * (int)std::max<size_t>(1, (size_t)(228 * 1024) / (bt_col_smem + 1024));
-  const bool wy = s > 2 && bt_mode == 0 && (s <= 32 * 20 || col_ok) && m > 0;
+  const bool wy = !use_sbr && s > 2 && bt_mode == 0 && (s <= 32 * 20 || col_ok) && m > 0;
   cudaEvent_t tri_side_join = nullptr;
   if (wy) {
     cudaStream_t side = w.side;
@@ -895,7 +919,10 @@ static int eigh_top(cudaStream_t st, int s, const double* Hs, int ldh, int m, do
     }
   }
   TRY(w.mark(10));
-  if (s > 2) {
+  if (s > 2 && use_sbr) {
+    sbr_bt_kernel<<<m, SBT_NT, (size_t)(s + 2 * SB) * sizeof(double), st>>>(s, m, sb_Vr, w.Vh, w.ldv, sb_Tq, Yv, ldy);
+    CKL();
+  } else if (s > 2) {
     if (wy) {
       double* Tb = w.tG;  // T factors from larft_kernel (side stream, launched after the tridiagonalisation)
       CK(cudaStreamWaitEvent(st, tri_side_join, 0));

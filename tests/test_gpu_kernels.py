@@ -184,3 +184,26 @@ def test_symm_multiply_tma(api, n, k, split):
     Y = api.symm_multiply(-1.0, Ad, Zd, ws=ws).cpu().numpy()
     ref = -(A @ Z)
     assert np.abs(Y - ref).max() <= 1e-13 * np.sqrt(n) * np.abs(ref).max()
+
+
+def test_eigh_two_stage_reduction_subprocess():
+    """The optional two-stage tridiagonalisation (sbr.cuh, PSDPROJ_SBR=1: dense -> band on a cluster,
+    band -> tridiagonal by bulge chasing, back-transformation through both) against LAPACK. The
+    switch is read once per process, hence the subprocess (tools/sbr_probe.py)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PSDPROJ_SBR="1", PROBE_REPS="1")
+    out = subprocess.run([sys.executable, os.path.join(root, "tools", "sbr_probe.py"), "48,100,161,272,384"],
+                         env=env, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("s=")]
+    assert len(lines) == 5, out.stdout
+    for l in lines:
+        f = dict(kv.split("=") for kv in l.split())
+        s = int(f["s"])
+        assert float(f["eig_relerr"]) <= 1e-13, l
+        assert float(f["orth"]) <= 1e-12 * max(1, s / 20), l
+        assert float(f["resid"]) <= 1e-11 * max(1, s / 20), l
+        assert f["npos_ok"] == "True", l
