@@ -87,21 +87,21 @@ __device__ __forceinline__ void tl_colnorms(int n, const double* __restrict__ Z,
 // In-place Cholesky of the leading t x t block of G (ld ldg), right-looking, all threads; returns 0 or
 // (failing pivot + 1) when a pivot is <= 1e-12 max diag (R20). Upper triangle left untouched.
 __device__ int tl_cholesky(int t, double* __restrict__ G, int ldg, int* __restrict__ flag) {
+  (void)flag;
   double dmax = 0.0;
   for (int i = 0; i < t; ++i) dmax = fmax(dmax, G[i + i * ldg]);
-  if (threadIdx.x == 0) *flag = 0;
-  __syncthreads();
+  __syncthreads();  // every thread has read the diagonal before thread 0 overwrites it
   for (int j = 0; j < t; ++j) {
+    int bad = 0;
     if (threadIdx.x == 0) {
       const double d = G[j + j * ldg];
-      if (!(d > 1e-12 * dmax)) {
-        *flag = j + 1;
-      } else {
+      if (!(d > 1e-12 * dmax))
+        bad = 1;
+      else
         G[j + j * ldg] = sqrt(d);
-      }
     }
-    __syncthreads();
-    if (*flag) return *flag;
+    // the failure decision travels with the barrier itself: identical in every thread
+    if (__syncthreads_or(bad)) return j + 1;
     const double ljj = G[j + j * ldg];
     for (int i = j + 1 + threadIdx.x; i < t; i += TL_NT) G[i + j * ldg] /= ljj;
     __syncthreads();
