@@ -32,7 +32,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 PEAKS_FP64 = os.path.join(ROOT, "profiles", "peaks_fp64_r01.json")
-NCU_SUMMARY = os.path.join(ROOT, "profiles", "ncu_amul_r01.json")
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "r02", "ncu_a3_r02.json")      # ncu --set full, one a3 launch
+NCU_TRI = os.path.join(ROOT, "profiles", "r02", "ncu_tri_reg_r02.json")     # ncu --set full, one tridiag_reg launch
 
 
 def parse():
@@ -43,6 +44,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c3r", choices=["c3r", "c1", "c2", "c2cl", "c3", "c4", "c5", "bo"])
     ap.add_argument("--c4-blocks", type=int, default=512)
+    ap.add_argument("--c4-no-tiny", action="store_true", help="C4: every block through its own context (no f4 routing)")
     ap.add_argument("--shard", action="store_true",
                     help="row-shard the single matrix across the ranks (NCCL inside libpsdproj; strong scaling)")
     ap.add_argument("--n", type=int, default=None)
@@ -277,8 +279,9 @@ def run_c4_bench(args, rank, world, local, dist):
     dev = torch.device("cuda", local)
     clocks = Clocks(local)
     clocks.start()
+    paths = {}
     ms, proj, iters, worst = run_c4(cfg, rank, world, dist, dev, rounds=max(args.steps, 1),
-                                    warmup=max(args.warmup, 0))
+                                    warmup=max(args.warmup, 0), tiny=not args.c4_no_tiny, paths=paths)
     ck = clocks.stop()
     if rank == 0:
         line = {"metric": "PSD-cone projections/sec (warm LOBPCG), C4 batch of independent blocks",
@@ -287,7 +290,11 @@ def run_c4_bench(args, rank, world, local, dist):
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": f"C4 {cfg.count} blocks n in {{50,100,200,400}} (configs[3]), tol {cfg.tol:g}",
                            "parallelism": f"batch-sharded LPT x{world}", "l2": "per-round drift, no flush"},
-                "iters_per_projection": {"mean": iters}, "worst_status": worst, "clocks": ck}
+                "iters_per_projection": {"mean": iters}, "worst_status": worst, "clocks": ck,
+                "paths_rank0": paths,
+                "routing": ("n <= 112: one launch of the one-CTA warm LOBPCG (f4) for all of them, blocks whose smaller side "
+                            "outgrows its 8 columns projected exactly in one CTA (R50); n > 112: one context each, "
+                            "psdproj_project_batched") if not args.c4_no_tiny else "every block: one context, psdproj_project_batched"}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
@@ -552,16 +559,17 @@ def run_c3r(args, rank, world, local, dist):
     tri_n = sum(i["tri_launches"] for i in infos)
     tri_flops = sum(i["tri_flops"] for i in infos)
     cols = sum(i["a_cols"] for i in infos) / max(1, sum(i["a_passes"] for i in infos))
-    ncu = {}
-    if os.path.exists(NCU_SUMMARY):
+    def _load(path):
         try:
-            ncu = json.load(open(NCU_SUMMARY))
+            return json.load(open(path))
         except Exception:
-            ncu = {}
+            return {}
+    ncu, ncu_tri = _load(NCU_SUMMARY), _load(NCU_TRI)
     if tri_ms >= amul_ms:
         achieved = tri_flops / (tri_ms / 1e3) / 1e12 if tri_ms > 0 else 0.0
         roof = {"bound": "alu", "achieved": achieved, "peak": p64, "unit": "TFLOP/s", "frac": achieved / p64,
-                "traffic": ncu.get("tri_dram_bytes_per_launch"),
+                "traffic": ncu_tri.get("dram_bytes_per_launch"),
+                "traffic_source": "profiles/r02/ncu_tri_reg_r02.json (one launch, ncu --set full)",
                 "kernel": "RR Householder tridiagonalisation (tridiag_reg_kernel: 16-CTA cluster, DSMEM pushes)",
                 "share_of_step": tri_ms / ms_local,
                 "per_launch": {"flops": tri_flops / max(1, tri_n), "ms": tri_ms / max(1, tri_n),

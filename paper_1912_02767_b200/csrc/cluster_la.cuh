@@ -711,6 +711,7 @@ __device__ __forceinline__ void cla_st_async(uint32_t raddr, double v, uint32_t 
 // for step j + 2 before every CTA has pushed p_{j+1}, i.e. finished reading step j's buffers.
 // Each CTA re-arms a barrier for step j + 2 right after observing its step-j phase (by then no
 // step-(j+2) bytes can have arrived), so no phase ever sees bytes before its expect_tx.
+__constant__ int g_tri_bulk_spread = 0;  // set by the host (PSDPROJ_TRI_SPREAD)
 constexpr int TRI_TCG = 4;
 __host__ __device__ inline size_t tri_reg_smem_doubles(int s, int CS) {
   const size_t sr = (size_t)((s + 1) & ~1);
@@ -906,13 +907,16 @@ __global__ void __launch_bounds__(256, 1) tridiag_reg_kernel(int s, const double
       for (int i = j + 1 + tid; i < s; i += NT) vout[i] = (i == j + 1) ? 1.0 : colb[i] * scale;
       if (tid == 0) vout[j] = tj;
       __syncthreads();
-      if (tid < CS) {
+      // one bulk copy per destination CTA, issued by lanes 0-1 of every warp (g_tri_bulk_spread) or by
+      // lanes 0..CS-1 of warp 0: a warp's bulk-copy lanes are issued one after another
+      const int bdst = g_tri_bulk_spread ? (((tid & 31) < 2) ? 2 * warp + (tid & 31) : CS) : tid;
+      if (bdst < CS) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         const int i0 = j & ~1;
         asm volatile(
             "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                cla_mapa(cla_smem_u32(vj + i0), (uint32_t)tid)),
-            "r"(cla_smem_u32(vout + i0)), "r"(8u * (uint32_t)(sr - i0)), "r"(cla_mapa(cla_smem_u32(&vbar[par]), (uint32_t)tid))
+                cla_mapa(cla_smem_u32(vj + i0), (uint32_t)bdst)),
+            "r"(cla_smem_u32(vout + i0)), "r"(8u * (uint32_t)(sr - i0)), "r"(cla_mapa(cla_smem_u32(&vbar[par]), (uint32_t)bdst))
             : "memory");
       }
       if (prof && tid == 0) pt[7] += 1;

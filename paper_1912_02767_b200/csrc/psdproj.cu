@@ -541,6 +541,10 @@ static int cla_attrs() {
   CK(cudaFuncSetAttribute(sb1_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   CK(cudaFuncSetAttribute(sb1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   CK(cudaFuncSetAttribute(sb2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  {
+    const int spread = getenv("PSDPROJ_TRI_SPREAD") ? atoi(getenv("PSDPROJ_TRI_SPREAD")) : 1;
+    CK(cudaMemcpyToSymbol(g_tri_bulk_spread, &spread, sizeof(int)));
+  }
   done = true;
   return 0;
 }

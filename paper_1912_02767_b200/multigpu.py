@@ -50,11 +50,18 @@ def lpt_bound(costs, world):
     return (4.0 / 3.0 - 1.0 / (3.0 * world)) * opt_lb
 
 
-class C4Shard:
-    """The blocks of BASELINE configs[3] (C4) owned by one rank: device matrices, one psdproj
-    context per block (warm state across rounds), and the round-to-round drift."""
+TINY_NMAX = 112  # blocks up to this order go through the one-CTA path (tiny_lobpcg.cuh, TL_NMAX)
 
-    def __init__(self, cfg, block_ids, device, seed=1912, max_iter=500):
+
+class C4Shard:
+    """The blocks of BASELINE configs[3] (C4) owned by one rank: device matrices, the warm state
+    across rounds, and the round-to-round drift. Blocks with n <= TINY_NMAX (tiny=True, default) are
+    projected together by ONE launch of the one-CTA warm LOBPCG (psdproj_project_tiny_lobpcg, f4),
+    which hands the blocks whose smaller side outgrows its 8-column block to the exact one-CTA
+    projection (the DIRECT branch; R50); the others run one psdproj context each
+    through psdproj_project_batched."""
+
+    def __init__(self, cfg, block_ids, device, seed=1912, max_iter=500, tiny=True):
         import torch
 
         from . import api
@@ -63,14 +70,21 @@ class C4Shard:
         self.cfg = cfg
         self.ids = list(block_ids)
         self.device = device
-        self.mats, self.ctxs, self.outs = [], [], []
+        self.mats, self.outs = [], []
         for i in self.ids:
             Q, lam = cfg.block(i)
             A = torch.from_numpy(planted(Q, lam)).to(device)
             self.mats.append(A)
             self.outs.append(torch.empty_like(A))
+        self.small = [k for k, i in enumerate(self.ids) if tiny and cfg.sizes[i] <= TINY_NMAX]
+        self.large = [k for k in range(len(self.ids)) if k not in set(self.small)]
+        self.ctxs = []
+        for k in self.large:
+            i = self.ids[k]
             prm = api.default_params(max_iter=max_iter, seed=seed, ctx_id=i)
             self.ctxs.append(api.Context(cfg.sizes[i], params=prm, device=device))
+        self.tiny = (api.TinyLobpcgBatch([cfg.sizes[self.ids[k]] for k in self.small], device=device, seed=seed,
+                                         max_iter=max_iter) if self.small else None)
         self.round = 0
 
     def drift(self):
@@ -82,10 +96,23 @@ class C4Shard:
         self.round += 1
 
     def project(self, tol=None):
+        """One round: every block projected; per-block info dicts (iters, status, err_bound, path)."""
         from . import api
 
         tol = self.cfg.tol if tol is None else tol
-        _, infos = api.project_batched(self.ctxs, self.mats, [tol] * len(self.ids), outs=self.outs)
+        infos = [None] * len(self.ids)
+        if self.small:
+            _, res = self.tiny.project([self.mats[k] for k in self.small], tol,
+                                       outs=[self.outs[k] for k in self.small])
+            for j, k in enumerate(self.small):
+                st = res["status"][j]
+                infos[k] = {"iters": res["iters"][j], "status": 0 if st in (0, 3) else st, "npos": res["npos"][j],
+                            "err_bound": res["bound"][j], "path": "tiny-exact" if st == 3 else "tiny-lobpcg"}
+        if self.large:
+            _, inf = api.project_batched(self.ctxs, [self.mats[k] for k in self.large], [tol] * len(self.large),
+                                         outs=[self.outs[k] for k in self.large])
+            for j, k in enumerate(self.large):
+                infos[k] = dict(inf[j], path="direct" if inf[j].get("side") == 2 else "lobpcg")
         return infos
 
     def close(self):
@@ -99,13 +126,15 @@ def shard_c4(cfg, rank, world):
     return parts[rank], loads
 
 
-def run_c4(cfg, rank, world, dist, device, rounds, warmup, tol=None):
+def run_c4(cfg, rank, world, dist, device, rounds, warmup, tol=None, tiny=True, paths=None):
     """Sharded C4 rounds on this rank; returns (device ms of the timed rounds, max over ranks),
-    projections done by all ranks, and the per-rank mean LOBPCG iterations."""
+    projections done by all ranks, and the per-rank mean LOBPCG iterations. `paths` (a dict, if
+    given) receives this rank's count of timed projections per path (lobpcg / direct / tiny-lobpcg /
+    tiny-exact)."""
     import torch
 
     ids, _ = shard_c4(cfg, rank, world)
-    sh = C4Shard(cfg, ids, device)
+    sh = C4Shard(cfg, ids, device, tiny=tiny)
     st = torch.cuda.current_stream()
     for _ in range(warmup):
         sh.project(tol)
@@ -125,6 +154,9 @@ def run_c4(cfg, rank, world, dist, device, rounds, warmup, tol=None):
         ms += ev0.elapsed_time(ev1)
         iters += [i["iters"] for i in infos]
         worst = max([worst] + [i["status"] for i in infos])
+        if paths is not None:
+            for i in infos:
+                paths[i["path"]] = paths.get(i["path"], 0) + 1
         sh.drift()  # the next round's inputs, outside the timed region
     if dist is not None:
         dist.barrier()

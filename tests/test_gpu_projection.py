@@ -352,3 +352,31 @@ def test_direct_path_large_order(api):
         err = np.linalg.norm(Pi.cpu().numpy() - Pstar)
         assert info["side"] == 2, info["side"]
         assert err <= 1e-11 * np.linalg.norm(A) and info["err_bound"] >= err, (call, err, info["err_bound"])
+
+
+def test_c4_tiny_routing_parity(api):
+    """C4 shard with the n <= 112 blocks routed through one launch of the one-CTA path (warm LOBPCG,
+    exact hand-off) and the rest through contexts: every block matches the oracle's exact projection
+    over two warm rounds; a LOBPCG-certified block's bound dominates its error."""
+    import torch
+    from paper_1912_02767_b200.multigpu import C4Shard
+    from workloads.generators import C4
+    cfg = C4(24)
+    sh = C4Shard(cfg, list(range(24)), torch.device("cuda", 0))
+    assert sh.small and sh.large
+    paths = set()
+    for rnd in range(2):
+        infos = sh.project(1e-10)
+        for k, i in enumerate(sh.ids):
+            A = sh.mats[k].cpu().numpy()
+            Pe = project_exact(A)
+            err = np.linalg.norm(sh.outs[k].cpu().numpy() - Pe)
+            nA = np.linalg.norm(A)
+            assert infos[k]["status"] == 0, (rnd, i, infos[k])
+            assert err / nA <= 1e-9, (rnd, i, cfg.sizes[i], err / nA, infos[k]["path"])
+            if infos[k]["path"] in ("lobpcg", "tiny-lobpcg"):
+                assert infos[k]["err_bound"] >= err, (rnd, i, err, infos[k])
+            paths.add(infos[k]["path"])
+        sh.drift()
+    sh.close()
+    assert "tiny-exact" in paths and "lobpcg" in paths, paths
