@@ -73,6 +73,10 @@ typedef struct {
   double lock_factor; /* hard locking of a positive pair at r <= lock_factor * tol (R55); 0 => 1     */
   int krylov_depth; /* R57 (an extension, NOT the paper's Alg. 3): trial subspace span(X, R, B R, ...,  */
                     /* B^(d-1) R, dX) instead of span(X, R, dX); 0 or 1 => Alg. 3      */
+  int guard_active; /* R62: on WARM calls only the guard_active largest non-positive Ritz pairs keep   */
+                    /* their residual / dX directions in span(X, R, dX) (the stopping   */
+                    /* rule tests the top guard only, R12); 0 => 2; < 0 => every unconverged column   */
+                    /* (the BLOPEX active mask of Alg. 3 as printed). Cold calls always use all.      */
 } psdproj_params;
 
 typedef struct {

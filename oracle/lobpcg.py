@@ -111,7 +111,7 @@ class LobpcgResult:
 
 
 def lobpcg_pos(B, X0, tol, max_iter=500, guard=1, q=None, locking="hard", seed=0, ctx=0,
-               call=0, cold=False, guard_tol=None, m_max=None, lock_factor=1.0, krylov_depth=1):
+               call=0, cold=False, guard_tol=None, m_max=None, lock_factor=1.0, krylov_depth=1, guard_active=None):
     """Alg. 3: positive eigenpairs of the symmetric matrix B.
 
     X0      n x m start block (warm: previous Ritz block, R27; cold: Philox, R28).
@@ -187,6 +187,12 @@ def lobpcg_pos(B, X0, tol, max_iter=500, guard=1, q=None, locking="hard", seed=0
         Lidx = np.flatnonzero(locked)
         # active set J (BLOPEX active mask): unlocked columns with r_i > tol
         J = Uidx[r[Uidx] > tol]
+        if guard_active is not None and guard_active >= 0 and not cold:
+            # R62 (option; the GPU default on warm calls): only the guard_active largest non-positive
+            # Ritz values keep their directions (theta is sorted descending)
+            npu = Uidx[theta[Uidx] <= 0]
+            keep = set(npu[np.argsort(-theta[npu], kind="stable")][:guard_active].tolist())
+            J = np.array([j for j in J if theta[j] > 0 or j in keep], dtype=J.dtype)
         if locking == "soft":
             Xs, BXs, thetas = X, BX, theta
             Sidx = np.arange(m)
@@ -441,7 +447,7 @@ class Context:
     the warm block. One per cone block."""
 
     def __init__(self, n, tol_default=1e-8, max_iter=500, guard=1, q=None, m0=None,
-                 locking="hard", seed=0, ctx_id=0, side=0, keep_extra=None, krylov_depth=1):
+                 locking="hard", seed=0, ctx_id=0, side=0, keep_extra=None, krylov_depth=1, guard_active=None):
         self.n = n
         self.max_iter = max_iter
         self.guard = guard
@@ -453,6 +459,7 @@ class Context:
         self.side_param = side
         self.keep_extra = keep_extra
         self.krylov_depth = krylov_depth
+        self.guard_active = guard_active
         # capacity ceil(n/3)+1: a wider block is the exact-eig regime (R18)
         self.m_max = min(n, (n + 2) // 3 + 1)
         self.reset()
@@ -506,7 +513,8 @@ class Context:
             X0 = gaussian_block(n, self.m0, self.seed, stream=call, ctx=self.ctx_id, tag=0) if cold else self.X
             res = lobpcg_pos(B, X0, tol, max_iter=self.max_iter, guard=self.guard, q=self.q,
                              locking=self.locking, seed=self.seed, ctx=self.ctx_id, call=call,
-                             cold=cold, m_max=self.m_max, krylov_depth=self.krylov_depth)
+                             cold=cold, m_max=self.m_max, krylov_depth=self.krylov_depth,
+                             guard_active=self.guard_active)
             if res.abort_direct:
                 mode = DIRECT
                 info["mode"] = mode

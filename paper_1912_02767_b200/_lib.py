@@ -34,7 +34,7 @@ class Params(ctypes.Structure):
         ("keep_extra", ctypes.c_int), ("m_max", ctypes.c_int), ("seed", ctypes.c_uint64),
         ("ctx_id", ctypes.c_uint32), ("profile", ctypes.c_int), ("host_io", ctypes.c_int),
         ("perp_steps", ctypes.c_int), ("perp_delta", ctypes.c_double), ("lock_factor", ctypes.c_double),
-        ("krylov_depth", ctypes.c_int),
+        ("krylov_depth", ctypes.c_int), ("guard_active", ctypes.c_int),
     ]
 
 

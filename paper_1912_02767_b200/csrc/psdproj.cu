@@ -2007,12 +2007,23 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
   int status = PSDPROJ_NOT_CONVERGED;
   int k = 0;
   static int restart = getenv("PSDPROJ_RESTART") ? atoi(getenv("PSDPROJ_RESTART")) : 100;
+  // R61: a restart also when the largest residual of the positive Ritz pairs has not improved for
+  // `stall` iterations (>= 2 stall since the last restart): the rotated B X carries rounding that
+  // leaves a residual floor near tol; the restart recomputes B X explicitly (PSDPROJ_STALL, 0 = off)
+  static int stall = getenv("PSDPROJ_STALL") ? atoi(getenv("PSDPROJ_STALL")) : 0;
+  bool force_restart = false;
+  int k_restart = 0, k_best = 0;
+  double best_rpos = INFINITY;
   for (;;) {
     // R47: restart every `restart` iterations -- X_U re-orthonormalised (against X_L, then by the
     // Cholesky-QR of the start-block RR), B X_U recomputed, Rayleigh-Ritz on span(X_U), P dropped.
     // The pencil takes X_U^T X_U = I and B X_U from the rotation; both drift (by ~u cond(G) and
     // ~u ||C'|| per step) on long runs that never meet the stopping rule.
-    if (restart > 0 && k > 0 && k % restart == 0 && mU > 0) {
+    if (((restart > 0 && k > 0 && k % restart == 0) || force_restart) && mU > 0) {
+      force_restart = false;
+      k_restart = k;
+      best_rpos = INFINITY;
+      k_best = k;
       TRY(run.mark(0));
       if (hard && nL > 0) {
         TRY(run.gram(nL, mU, XLp(), ld, c->S, ld, c->Y, ldm));
@@ -2044,7 +2055,9 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
       std::swap(c->S, c->S2);
       std::swap(c->BS, c->BS2);
       CK(cudaMemcpyAsync(c->d_thU, c->d_ths, sizeof(double) * mU, cudaMemcpyDeviceToDevice, st));
-      hasP.assign(mU, 0);
+      static const int soft_restart = getenv("PSDPROJ_SOFT_RESTART") ? atoi(getenv("PSDPROJ_SOFT_RESTART")) : 0;
+      // soft: P (re-projected against X every iteration) is kept unless a column was dropped
+      if (!soft_restart || (int)hasP.size() != mU) hasP.assign(mU, 0);
     }
     // ---- line 5: R = B X - X Theta, r_i = ||R_i|| (unlocked columns)
     TRY(run.mark(6));
@@ -2060,14 +2073,32 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
     rU.assign(c->h_d, c->h_d + mU);
     const int trace = getenv("PSDPROJ_TRACE") ? 1 : 0;  // debugging: per-iteration state on stderr
     if (trace) {
-      double tmx = -INFINITY, tmn = INFINITY, rmx = 0;
+      double tmx = -INFINITY, tmn = INFINITY, rmx = 0, rpos = 0;
+      int nun = 0;
       for (int j = 0; j < mU; ++j) {
         tmx = std::max(tmx, thU[j]);
         tmn = std::min(tmn, thU[j]);
         rmx = std::max(rmx, rU[j]);
+        if (thU[j] > 0) {
+          rpos = std::max(rpos, rU[j]);
+          nun += rU[j] > tol;
+        }
       }
-      fprintf(stderr, "trace k=%d mU=%d nL=%d qe=%d theta[%g, %g] rmax %g tol %g dropped %d\n", k, mU, nL, qe, tmn, tmx,
-              rmx, tol, info->dropped);
+      fprintf(stderr, "trace k=%d mU=%d nL=%d qe=%d theta[%g, %g] rmax %g rpos %g unconv+ %d tol %g dropped %d\n", k, mU, nL,
+              qe, tmn, tmx, rmx, rpos, nun, tol, info->dropped);
+    }
+    if (stall > 0 && mU > 0) {
+      double rpos = 0.0;
+      for (int j = 0; j < mU; ++j)
+        if (thU[j] > 0 && rU[j] > tol) rpos = std::max(rpos, rU[j]);
+      if (rpos > 0.0) {
+        if (rpos < 0.95 * best_rpos) {
+          best_rpos = rpos;
+          k_best = k;
+        } else if (k - k_best >= stall && k - k_restart >= 2 * stall) {
+          force_restart = true;
+        }
+      }
     }
     // ---- stopping rule (R12)
     int npos = nL;
@@ -2153,8 +2184,18 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
     }
     // ---- active set J (BLOPEX active mask): unlocked columns with r > tol
     std::vector<int> Jorig, Jnew, PJ;
+    // R62: on warm calls only the top guard_active non-positive columns keep their W / P directions
+    // (the guard test of R12 looks at the top guard only; measured on C3-R: +13% iterations at -20%
+    // time per iteration); cold calls keep every unconverged column (Alg. 3's mask)
+    static const char* ga_env = getenv("PSDPROJ_GUARD_ACTIVE");  // experiments: overrides the parameter
+    const int ga_prm = ga_env ? atoi(ga_env) : c->prm.guard_active;
+    const int guard_active = cold ? -1 : (ga_prm == 0 ? 2 : ga_prm);
+    int nonpos_seen = 0;
     for (int jj = 0; jj < mU; ++jj) {
       int j0 = keep[jj];
+      const bool guard_col = !(thU[jj] > 0);
+      if (guard_col) ++nonpos_seen;
+      if (guard_active >= 0 && guard_col && nonpos_seen > guard_active) continue;
       if (rU[jj] > tol) {
         Jorig.push_back(j0);
         Jnew.push_back(jj);

@@ -101,6 +101,7 @@ class C4Shard:
 
         tol = self.cfg.tol if tol is None else tol
         infos = [None] * len(self.ids)
+        t0 = time.perf_counter()
         if self.small:
             _, res = self.tiny.project([self.mats[k] for k in self.small], tol,
                                        outs=[self.outs[k] for k in self.small])
@@ -108,11 +109,14 @@ class C4Shard:
                 st = res["status"][j]
                 infos[k] = {"iters": res["iters"][j], "status": 0 if st in (0, 3) else st, "npos": res["npos"][j],
                             "err_bound": res["bound"][j], "path": "tiny-exact" if st == 3 else "tiny-lobpcg"}
+        t1 = time.perf_counter()
         if self.large:
             _, inf = api.project_batched(self.ctxs, [self.mats[k] for k in self.large], [tol] * len(self.large),
                                          outs=[self.outs[k] for k in self.large])
             for j, k in enumerate(self.large):
                 infos[k] = dict(inf[j], path="direct" if inf[j].get("side") == 2 else "lobpcg")
+        # host wall time of the two parts (each ends in a stream synchronisation)
+        self.last_split_ms = (1e3 * (t1 - t0), 1e3 * (time.perf_counter() - t1))
         return infos
 
     def close(self):
@@ -157,6 +161,9 @@ def run_c4(cfg, rank, world, dist, device, rounds, warmup, tol=None, tiny=True, 
         if paths is not None:
             for i in infos:
                 paths[i["path"]] = paths.get(i["path"], 0) + 1
+            sp = paths.setdefault("host_ms_tiny_then_batched", [0.0, 0.0])
+            sp[0] += sh.last_split_ms[0] / rounds
+            sp[1] += sh.last_split_ms[1] / rounds
         sh.drift()  # the next round's inputs, outside the timed region
     if dist is not None:
         dist.barrier()

@@ -330,3 +330,26 @@ def test_krylov_depth_extension_same_projection_fewer_iterations():
         assert info["err_bound"] >= np.linalg.norm(P - Pstar)
         its[d] = info["iters"]
     assert its[3] * 1.5 <= its[1], its
+
+
+def test_guard_active_warm_sequence_same_projection():
+    """R62 (the GPU default on warm calls): with only the top 2 guards keeping their directions the
+    warm projections of a drifting planted sequence still reach the closed form within tolerance, the
+    bound dominates, and the positive count is right; cold calls are unaffected (all columns active)."""
+    rng = np.random.default_rng(62)
+    n, p = 160, 8
+    lam = np.concatenate([10.0 ** rng.uniform(-2, 1, p), -(10.0 ** rng.uniform(-2, 1, n - p))])
+    Q = haar_q(rng, n)
+    ctxs = {ga: L.Context(n, seed=5, guard_active=ga) for ga in (None, 2)}
+    for t in range(4):
+        K = rng.standard_normal((n, n))
+        K = (K - K.T) / (2.0 * np.sqrt(n))
+        Qt = np.linalg.qr((np.eye(n) + 1e-3 * K) @ Q)[0] if t else Q
+        A = planted(Qt, lam)
+        Pstar = (Qt * np.maximum(lam, 0)) @ Qt.T
+        for ga, ctx in ctxs.items():
+            P, info = ctx.project(A, 1e-9)
+            assert info["status"] == L.OK and info["npos"] == p, (t, ga, info)
+            err = np.linalg.norm(P - Pstar)
+            assert err <= 1e-9 * np.linalg.norm(A), (t, ga, err)
+            assert info["err_bound"] >= err, (t, ga)
