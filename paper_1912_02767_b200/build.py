@@ -6,7 +6,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = os.path.join(HERE, "csrc", "psdproj.cu")
-DEPS = [os.path.join(HERE, "csrc", f) for f in ("psdproj.cu", "gemm.cuh", "kernels.cuh", "common.cuh", "tridiag.cuh", "cluster_la.cuh", "tridiag_tile.cuh", "gemm_tma.cuh", "tiny_lobpcg.cuh", "sbr.cuh")] + [
+DEPS = [os.path.join(HERE, "csrc", f) for f in ("psdproj.cu", "gemm.cuh", "kernels.cuh", "common.cuh", "tridiag.cuh", "cluster_la.cuh", "tridiag_tile.cuh", "gemm_tma.cuh", "tiny_lobpcg.cuh", "sbr.cuh", "tridiag_rep.cuh")] + [
     os.path.join(ROOT, "include", "psdproj.h")]
 SO = os.path.join(HERE, "libpsdproj.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

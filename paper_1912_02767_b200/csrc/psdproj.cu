@@ -38,6 +38,7 @@
 #include "gemm_tma.cuh"
 #include "tiny_lobpcg.cuh"
 #include "sbr.cuh"
+#include "tridiag_rep.cuh"
 
 using namespace psd;
 
@@ -531,7 +532,9 @@ static int cla_attrs() {
   CK(cudaFuncSetAttribute(tridiag_cluster_kernel<64, 256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
 #define TRI_REG_ATTR(KR, CR)                                                                                          \
   CK(cudaFuncSetAttribute(tridiag_reg_kernel<KR, CR>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)); \
-  CK(cudaFuncSetAttribute(tridiag_reg_kernel<KR, CR>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  CK(cudaFuncSetAttribute(tridiag_reg_kernel<KR, CR>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));   \
+  CK(cudaFuncSetAttribute(tridiag_rep_kernel<KR, CR>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)); \
+  CK(cudaFuncSetAttribute(tridiag_rep_kernel<KR, CR>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   TRI_REG_ATTR(3, 5)
   TRI_REG_ATTR(4, 4)
   TRI_REG_ATTR(6, 6)
@@ -727,8 +730,15 @@ static int eigh_top(cudaStream_t st, int s, const double* Hs, int ldh, int m, do
   } else if (tcs && tri_reg && kr <= 8 && cr <= 8 &&
       tri_reg_smem_doubles(s, tcs) * sizeof(double) <= (size_t)CLA_SMEM_BYTES) {
     const size_t tsm = tri_reg_smem_doubles(s, tcs) * sizeof(double);
-#define TRI_REG(KR, CR) \
-  TRY(launch_cluster(tridiag_reg_kernel<KR, CR>, tcs, 256, tsm, st, s, Hs, ldh, w.td, w.te, w.ttau, w.Vh, w.ldv, dprof, tri_dbg))
+    // one-hop variant (tridiag_rep.cuh): the step's column replicated in every CTA a step ahead
+    static const int tri_rep = getenv("PSDPROJ_TRI_REP") ? atoi(getenv("PSDPROJ_TRI_REP")) : 0;
+    const size_t tsm_rep = tri_rep_smem_doubles(s, tcs) * sizeof(double);
+    const bool rep = tri_rep && !want_prof && tsm_rep <= (size_t)CLA_SMEM_BYTES;
+#define TRI_REG(KR, CR)                                                                                              \
+  if (rep)                                                                                                          \
+    TRY(launch_cluster(tridiag_rep_kernel<KR, CR>, tcs, 256, tsm_rep, st, s, Hs, ldh, w.td, w.te, w.ttau, w.Vh, w.ldv)); \
+  else                                                                                                              \
+    TRY(launch_cluster(tridiag_reg_kernel<KR, CR>, tcs, 256, tsm, st, s, Hs, ldh, w.td, w.te, w.ttau, w.Vh, w.ldv, dprof, tri_dbg))
     if (kr <= 3 && cr <= 5)
       TRI_REG(3, 5);
     else if (kr <= 4 && cr <= 4)
