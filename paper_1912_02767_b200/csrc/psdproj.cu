@@ -2021,6 +2021,11 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
   // `stall` iterations (>= 2 stall since the last restart): the rotated B X carries rounding that
   // leaves a residual floor near tol; the restart recomputes B X explicitly (PSDPROJ_STALL, 0 = off)
   static int stall = getenv("PSDPROJ_STALL") ? atoi(getenv("PSDPROJ_STALL")) : 0;
+  // R61 (default): a restart when every unconverged positive pair has r < near_c * tol and the largest
+  // of them has not improved by 5% for near_win iterations (at most once per 2 near_win iterations):
+  // the warm calls otherwise sit just above tol until the next periodic restart (DESIGN R61)
+  static double near_c = getenv("PSDPROJ_NEAR_RESTART") ? atof(getenv("PSDPROJ_NEAR_RESTART")) : 3.0;
+  static int near_win = getenv("PSDPROJ_NEAR_WIN") ? atoi(getenv("PSDPROJ_NEAR_WIN")) : 5;
   bool force_restart = false;
   int k_restart = 0, k_best = 0;
   double best_rpos = INFINITY;
@@ -2097,15 +2102,16 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
       fprintf(stderr, "trace k=%d mU=%d nL=%d qe=%d theta[%g, %g] rmax %g rpos %g unconv+ %d tol %g dropped %d\n", k, mU, nL,
               qe, tmn, tmx, rmx, rpos, nun, tol, info->dropped);
     }
-    if (stall > 0 && mU > 0) {
+    if ((stall > 0 || near_c > 0.0) && mU > 0) {
       double rpos = 0.0;
       for (int j = 0; j < mU; ++j)
         if (thU[j] > 0 && rU[j] > tol) rpos = std::max(rpos, rU[j]);
       if (rpos > 0.0) {
+        const int win = stall > 0 ? stall : near_win;
         if (rpos < 0.95 * best_rpos) {
           best_rpos = rpos;
           k_best = k;
-        } else if (k - k_best >= stall && k - k_restart >= 2 * stall) {
+        } else if (k - k_best >= win && k - k_restart >= 2 * win && (near_c <= 0.0 || rpos < near_c * tol)) {
           force_restart = true;
         }
       }
