@@ -130,7 +130,11 @@ void psdproj_default_params(psdproj_params* p);
 /* Device workspace needed by a context of order n with these params (NULL = defaults). */
 size_t psdproj_workspace_bytes(int n, const psdproj_params* p);
 
-/* Create a context over caller-owned device workspace ws (>= workspace_bytes, 256-B aligned). */
+/* Create a context over caller-owned device workspace ws (>= workspace_bytes, 256-B aligned): the
+ * state that persists between the projections of one cone block across ADMM iterations -- the warm
+ * LOBPCG block (warm starting of multiple Ritz pairs) and the previous sign
+ * counts for the one-third rule (:505, ProjectionContext). Returns PSDPROJ_OK or a
+ * negative error; *out is untouched on error. */
 int psdproj_create(int n, const psdproj_params* p, void* ws, size_t ws_bytes, psdproj_ctx* out);
 
 /* Project A (device, n x n, lda) into Pi (device, ldpi). tol: absolute per-pair residual
@@ -191,14 +195,17 @@ int psdproj_project_tiny_lobpcg(int count, const int* n, const double* const* A,
                                 int m0, uint64_t seed, uint32_t call, void* ws, size_t ws_bytes, int* status,
                                 int* iters, int* npos, double* bound, void* stream);
 
-/* Warm block of the last call: vals_host (cap values, descending Ritz values of the side used,
- * sign as computed on B = side*A), vecs_dev (n x cap, ldv) may be NULL. Returns the count. */
+/* Warm block of the last call (the warm start the next call uses): vals_host (cap
+ * values, descending Ritz values of the side used, sign as computed on B = side*A), vecs_dev (n x cap,
+ * ldv, device, caller-owned) may be NULL. Returns the count (>= 0) or a negative error. */
 int psdproj_get_ritz(psdproj_ctx ctx, double* vals_host, int cap, double* vecs_dev, int ldv);
 
-/* Drop the warm state: the next call is cold and uses the side hint / positive side. */
+/* Drop the warm state (`warm` optional): the next call is cold -- Philox start block,
+ * side hint / positive side (PAPER.md:505 needs the previous counts). Returns PSDPROJ_OK or < 0. */
 int psdproj_reset(psdproj_ctx ctx);
 
-/* Free the host-side context (never the caller's workspace). */
+/* Free the host-side context and the streams / events it created (never the caller's workspace).
+ * Returns PSDPROJ_OK, or PSDPROJ_E_INVALID for NULL. */
 int psdproj_destroy(psdproj_ctx ctx);
 
 /* Thread-local message of the last error ("" if none). */
