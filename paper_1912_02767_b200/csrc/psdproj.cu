@@ -314,6 +314,64 @@ static int gemm_tma_launch(cudaStream_t st, int n, int k, double alpha, const do
   return 0;
 }
 
+// 3-D fp64 tensor map {16, cols, k tiles} over a column-major matrix with `rows` = 16 * ktiles rows:
+// element (r, c, t) at ptr[16 t + r + c ld] (strides ld * 8 and 128 bytes), box {16, box_cols, box_t},
+// 128-byte swizzle
+static int make_tmap3(CUtensorMap* m, const double* ptr, int ktiles, int cols, int ld, int box_cols, int box_t) {
+  TmapEncodeFn f = tmap_encode();
+  if (!f) return set_err(PSDPROJ_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {16, (cuuint64_t)cols, (cuuint64_t)ktiles};
+  cuuint64_t strides[2] = {(cuuint64_t)ld * sizeof(double), 16 * sizeof(double)};
+  cuuint32_t box[3] = {16, (cuuint32_t)box_cols, (cuuint32_t)box_t};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = f(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)ptr, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : 1;
+}
+
+// Row-panel variant (gemm_tma.cuh: dgemm_tma_panel_kernel): 32 rows x the whole k range per CTA, no
+// split-K partials; 3-D tensor maps (one TMA per operand per stage, contiguous 128 KG-byte runs per
+// column) when n % 16 == 0, else 2-D maps (one TMA per 16-wide k tile)
+template <int BN>
+static int gemm_tma_panel_launch(cudaStream_t st, int n, int k, double alpha, const double* A, int lda,
+                                 const double* Z, int ldz, double* Y, int ldy) {
+  using Cfg = PanelGemmCfg<BN>;
+  static const int t3_env = getenv("PSDPROJ_A3_PANEL3D") ? atoi(getenv("PSDPROJ_A3_PANEL3D")) : 1;
+  CUtensorMap ma, mb;
+  bool t3 = t3_env && n % 16 == 0;
+  if (t3) t3 = make_tmap3(&ma, A, n / 16, n, lda, Cfg::BM, Cfg::KG) == 0 && make_tmap3(&mb, Z, n / 16, k, ldz, BN, Cfg::KG) == 0;
+  auto kern = t3 ? dgemm_tma_panel_kernel<BN, true> : dgemm_tma_panel_kernel<BN, false>;
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(dgemm_tma_panel_kernel<BN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM));
+    CK(cudaFuncSetAttribute(dgemm_tma_panel_kernel<BN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM));
+    attr = true;
+  }
+  if (!t3) {
+    TRY(make_tmap(&ma, A, n, n, lda, Cfg::BM));
+    TRY(make_tmap(&mb, Z, n, k, ldz, BN));
+  }
+  TRY(launch_pdl(kern, dim3(cdiv(n, Cfg::BM)), dim3(Cfg::THREADS), Cfg::SMEM, st, ma, mb, n, k, n, alpha, Y, ldy));
+  return 0;
+}
+
+// a3 tile choice: the row-panel kernel when k <= 64 and its cdiv(n, 32) CTAs fill at least 3/4
+// of the SMs left (one CTA per SM); otherwise 64-row tiles with split-K -- 16 columns for k <= 16
+// (HBM-bound: no DMMA on zero padding), 32 when the last 64-tile would be at most half full, else 64
+static int a3_multiply_tma(cudaStream_t st, int n, int k, double alpha, const double* A, int lda, const double* Z, int ldz,
+                  double* Y, int ldy, double* part, size_t part_elems) {
+  static const int panel_on = getenv("PSDPROJ_A3_PANEL") ? atoi(getenv("PSDPROJ_A3_PANEL")) : 1;
+  const int free_sms = std::max(1, sms() - g_sm_reserve);
+  if (panel_on && k <= 64 && 4 * cdiv(n, 32) >= 3 * free_sms)
+    return k <= 16   ? gemm_tma_panel_launch<16>(st, n, k, alpha, A, lda, Z, ldz, Y, ldy)
+           : k <= 32 ? gemm_tma_panel_launch<32>(st, n, k, alpha, A, lda, Z, ldz, Y, ldy)
+                     : gemm_tma_panel_launch<64>(st, n, k, alpha, A, lda, Z, ldz, Y, ldy);
+  const bool narrow = k <= 96 && (k % 64) != 0 && (k % 64) <= 32;
+  if (k <= 16) return gemm_tma_launch<64, 16, 6>(st, n, k, alpha, A, lda, Z, ldz, Y, ldy, part, part_elems);
+  if (narrow) return gemm_tma_launch<64, 32, 4>(st, n, k, alpha, A, lda, Z, ldz, Y, ldy, part, part_elems);
+  return gemm_tma_launch<64, 64, 4>(st, n, k, alpha, A, lda, Z, ldz, Y, ldy, part, part_elems);
+}
+
 // Two products C = alpha A B + beta C and C2 = alpha A2 B + beta C2 (same B, shapes and leading
 // dimensions) in one launch (k-paired kernel, 64 x 64 or 64 x 32 tiles).
 static int dgemm2(cudaStream_t st, int M, int N, int K, double alpha, const double* A, const double* A2, int lda,
@@ -1427,12 +1485,7 @@ struct Run {
     const bool tma_ok = a3_tma && !c->sharded && lda % 2 == 0 && ldz % 2 == 0 && ((uintptr_t)A & 15) == 0 &&
                         ((uintptr_t)Z & 15) == 0;
     if (tma_ok) {
-      // column tile: 16 for k <= 16 (HBM-bound: no DMMA on zero padding), 32 when the last 64-tile
-      // would be at most half full, else 64
-      const bool narrow = k <= 96 && (k % 64) != 0 && (k % 64) <= 32;
-      int rc_ = k <= 16 ? gemm_tma_launch<64, 16, 6>(st, n, k, sgn, A, lda, Z, ldz, Y, ldy, c->part, c->part_elems)
-                : narrow ? gemm_tma_launch<64, 32, 4>(st, n, k, sgn, A, lda, Z, ldz, Y, ldy, c->part, c->part_elems)
-                         : gemm_tma_launch<64, 64, 4>(st, n, k, sgn, A, lda, Z, ldz, Y, ldy, c->part, c->part_elems);
+      int rc_ = a3_multiply_tma(st, n, k, sgn, A, lda, Z, ldz, Y, ldy, c->part, c->part_elems);
       if (rc_ < 0) return rc_;
     } else {
       const bool narrow = k <= 96 && (k % 64) != 0 && (k % 64) <= 32;
@@ -2912,11 +2965,7 @@ extern "C" int psdproj_symm_multiply(int n, int k, double alpha, const double* A
     return set_err(PSDPROJ_E_INVALID, "invalid symm_multiply arguments");
   if (lda % 2 || ldz % 2 || ((uintptr_t)A & 15) || ((uintptr_t)Z & 15))
     return set_err(PSDPROJ_E_INVALID, "symm_multiply needs even leading dimensions and 16-byte aligned A, Z");
-  cudaStream_t st = (cudaStream_t)stream;
-  const bool narrow = k <= 96 && (k % 64) != 0 && (k % 64) <= 32;
-  if (k <= 16) return gemm_tma_launch<64, 16, 6>(st, n, k, alpha, A, lda, Z, ldz, Y, ldy, ws, ws ? ws_elems : 0);
-  if (narrow) return gemm_tma_launch<64, 32, 4>(st, n, k, alpha, A, lda, Z, ldz, Y, ldy, ws, ws ? ws_elems : 0);
-  return gemm_tma_launch<64, 64, 4>(st, n, k, alpha, A, lda, Z, ldz, Y, ldy, ws, ws ? ws_elems : 0);
+  return a3_multiply_tma((cudaStream_t)stream, n, k, alpha, A, lda, Z, ldz, Y, ldy, ws, ws ? ws_elems : 0);
 }
 
 extern "C" size_t psdproj_jacobi_ws_elems(int s) {

@@ -168,11 +168,12 @@ def test_eigh_extreme_scales(api, s, scale):
 
 
 @pytest.mark.parametrize("n,k", [(64, 1), (130, 7), (1000, 33), (1000, 64), (2048, 100), (4000, 70), (4000, 200),
-                                 (998, 17)])
+                                 (998, 17), (4000, 17), (4000, 32), (4000, 56), (4002, 64), (3998, 45), (4096, 33), (4000, 9)])
 @pytest.mark.parametrize("split", [False, True])
 def test_symm_multiply_tma(api, n, k, split):
     """a3 block multiply on TMA-staged swizzled tiles (psdproj_symm_multiply, the kernel the path
-    runs) against an fp64 reference: ragged m / k / column tiles come from the TMA zero fill."""
+    runs) against an fp64 reference: ragged m / k / column tiles come from the TMA zero fill. n >= 3520
+    with 16 < k <= 64 takes the row-panel kernel (whole k range per CTA, in-CTA k-group sums)."""
     rng = np.random.default_rng(n + k)
     M = rng.standard_normal((n, n))
     A = (M + M.T) / 2
