@@ -35,6 +35,7 @@
 #include "tridiag.cuh"
 #include "cluster_la.cuh"
 #include "tridiag_tile.cuh"
+#include "tridiag_warp.cuh"
 #include "gemm_tma.cuh"
 #include "tiny_lobpcg.cuh"
 #include "sbr.cuh"
@@ -765,7 +766,21 @@ static int eigh_top(cudaStream_t st, int s, const double* Hs, int ldh, int m, do
     CKL();
     tcs = 0;
   }
-  const bool use_tile = !use_sbr && tri_mode == 0 && s >= 3 && s <= std::min(tri_tile, TT_SMAX);
+  // one-CTA warp-cyclic register kernel (tridiag_warp.cuh: two CTA barriers per column, no DSMEM hop)
+  // up to s = PSDPROJ_TRI_WARP (default 64: 87 vs 145 us for the tiled kernel at s = 64; its 4 x 8
+  // register variant measured 216 / 276 us at s = 100 / 128 against 170 / 230 us for the 16-CTA
+  // cluster kernel, so s > 64 stays on the cluster -- DESIGN.md §6)
+  static const int tri_warp = getenv("PSDPROJ_TRI_WARP") ? atoi(getenv("PSDPROJ_TRI_WARP")) : 64;
+  const bool use_warp = !use_sbr && tri_mode == 0 && s >= 3 && s <= std::min(tri_warp, 128);
+  if (use_warp) {
+    if (s <= 64)
+      tridiag_warp_kernel<2, 4><<<1, TW_NT, 0, st>>>(s, Hs, ldh, w.td, w.te, w.ttau, w.Vh, w.ldv);
+    else
+      tridiag_warp_kernel<4, 8><<<1, TW_NT, 0, st>>>(s, Hs, ldh, w.td, w.te, w.ttau, w.Vh, w.ldv);
+    CKL();
+    tcs = 0;
+  }
+  const bool use_tile = !use_warp && !use_sbr && tri_mode == 0 && s >= 3 && s <= std::min(tri_tile, TT_SMAX);
   if (use_tile) {
     static bool tattr = false;
     if (!tattr) {
@@ -783,7 +798,7 @@ static int eigh_top(cudaStream_t st, int s, const double* Hs, int ldh, int m, do
                      w.ldv, dprof, w.tG, tri_dbg))
   static int tri_reg = getenv("PSDPROJ_TRI_NOREG") ? 0 : 1;
   const int kr = cdiv(s, 64), cr = tcs ? cdiv(cdiv(s, tcs), TRI_TCG) : 99;
-  if (use_tile || use_sbr) {
+  if (use_warp || use_tile || use_sbr) {
     // done above
   } else if (tcs && tri_reg && kr <= 8 && cr <= 8 &&
       tri_reg_smem_doubles(s, tcs) * sizeof(double) <= (size_t)CLA_SMEM_BYTES) {

@@ -208,3 +208,22 @@ def test_eigh_two_stage_reduction_subprocess():
         assert float(f["orth"]) <= 1e-12 * max(1, s / 20), l
         assert float(f["resid"]) <= 1e-11 * max(1, s / 20), l
         assert f["npos_ok"] == "True", l
+
+
+@pytest.mark.parametrize("env", [{"PSDPROJ_TRI_WARP": "128"}, {"PSDPROJ_TRI_WARP": "0"}])
+def test_eigh_alternative_tridiagonalisations_subprocess(env):
+    """The non-default small-s tridiagonalisations against LAPACK eigenvalues: the one-CTA warp-cyclic
+    kernel's 4 x 8 register variant (s <= 128, PSDPROJ_TRI_WARP=128) and the tiled one-CTA kernel
+    (PSDPROJ_TRI_WARP=0). The switches are read once per process, hence the subprocess."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "tools", "eigh_probe.py"), "3:3,17:17,64:50,65:65,100:80,128:128"],
+                         env=dict(os.environ, **env), capture_output=True, text=True, timeout=300, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    recs = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(recs) == 6, out.stdout
+    for r in recs:
+        assert r["max_err"] <= 1e-12 * max(1, r["s"] / 20) * 3.0 * r["s"] ** 0.5, r
