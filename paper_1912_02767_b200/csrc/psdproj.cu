@@ -22,6 +22,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <initializer_list>
 #include <numeric>
 #include <string>
@@ -1399,6 +1400,11 @@ struct Run {
   int ntev = 0;  // timed tridiagonalisation launches (profile & 4)
   double anorm = 0.0;
   std::vector<int> marks;  // phase id of each recorded phase event (profile & 2)
+  // issued by rr() right before its host sync (the next iteration's rotation and residual norms,
+  // speculatively: one sync per LOBPCG iteration instead of two); spec_redo: rr() changed C' or the
+  // Ritz values after that point (second Newton-Schulz step / robust path), the speculative work is void
+  std::function<int()> spec_fn;
+  bool spec_redo = false;
 
   // phase boundary: the GPU time from this mark to the next is charged to phase ph
   int mark(int ph) {
@@ -1720,6 +1726,8 @@ struct Run {
     CK(cudaMemcpyAsync(c->h_d, c->d_ths, sizeof(double) * mU, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(c->h_i + c->h_i_len - 16, c->d_status, sizeof(int) * 8, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(c->h_i + c->h_i_len - 24, c->tnpos, sizeof(int), cudaMemcpyDeviceToHost, st));
+    spec_redo = false;
+    if (spec_fn) TRY(spec_fn());
     TRY(sync());
     int chol = c->h_i[c->h_i_len - 16];
     int sweeps = c->h_i[c->h_i_len - 16 + 4];
@@ -1732,6 +1740,7 @@ struct Run {
       TRY(li_t_apply(s, kx, mU));
       CK(cudaMemcpyAsync(c->h_d + c->h_d_len - 16, c->d_scal + 16, sizeof(double), cudaMemcpyDeviceToHost, st));
       TRY(sync());
+      spec_redo = true;
     }
     if (!use_jacobi && !(c->h_d[c->h_d_len - 16] <= 1e-4)) {
       // Newton-Schulz could not restore orthonormality (near-multiple eigenvalues): robust path
@@ -1739,6 +1748,7 @@ struct Run {
       TRY(li_t_apply(s, kx, mU));
       CK(cudaMemcpyAsync(c->h_d, c->d_ths, sizeof(double) * mU, cudaMemcpyDeviceToHost, st));
       TRY(sync());
+      spec_redo = true;
     }
     if (use_jacobi && sweeps < 0) return set_err(PSDPROJ_E_DEGENERATE, "Jacobi did not converge (s=%d)", s);
     return 0;
@@ -2095,6 +2105,11 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
   static double near_c = getenv("PSDPROJ_NEAR_RESTART") ? atof(getenv("PSDPROJ_NEAR_RESTART")) : 3.0;
   static int near_win = getenv("PSDPROJ_NEAR_WIN") ? atoi(getenv("PSDPROJ_NEAR_WIN")) : 5;
   bool force_restart = false;
+  // residual norms of the current block already on the host (issued speculatively before the last
+  // Rayleigh-Ritz sync, Run::spec_fn), in the pinned slot h_d + h_d_len / 2
+  bool spec_ready = false;
+  static const int spec_env = getenv("PSDPROJ_SPEC") ? atoi(getenv("PSDPROJ_SPEC")) : 1;
+  const size_t rslot = c->h_d_len / 2;
   int k_restart = 0, k_best = 0;
   double best_rpos = INFINITY;
   for (;;) {
@@ -2104,6 +2119,7 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
     // ~u ||C'|| per step) on long runs that never meet the stopping rule.
     if (((restart > 0 && k > 0 && k % restart == 0) || force_restart) && mU > 0) {
       force_restart = false;
+      spec_ready = false;
       k_restart = k;
       best_rpos = INFINITY;
       k_best = k;
@@ -2144,16 +2160,21 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
     }
     // ---- line 5: R = B X - X Theta, r_i = ||R_i|| (unlocked columns)
     TRY(run.mark(6));
-    TRY(launch_pdl(resid_norm_kernel<256>, dim3(mU), dim3(256), 0, st, nl, (const double*)c->S, ld,
-                   (const double*)c->BS, ld, (const double*)c->d_thU, c->R, ld, c->d_r, c->sharded ? 1 : 0));
-    if (c->sharded) {  // column sums of squares over the ranks' rows
-      TRY(run.allreduce(c->d_r, mU));
-      sqrt_inplace_kernel<<<cdiv(mU, 256), 256, 0, st>>>(mU, c->d_r);
-      CKL();
+    if (spec_ready) {
+      rU.assign(c->h_d + rslot, c->h_d + rslot + mU);
+      spec_ready = false;
+    } else {
+      TRY(launch_pdl(resid_norm_kernel<256>, dim3(mU), dim3(256), 0, st, nl, (const double*)c->S, ld,
+                     (const double*)c->BS, ld, (const double*)c->d_thU, c->R, ld, c->d_r, c->sharded ? 1 : 0));
+      if (c->sharded) {  // column sums of squares over the ranks' rows
+        TRY(run.allreduce(c->d_r, mU));
+        sqrt_inplace_kernel<<<cdiv(mU, 256), 256, 0, st>>>(mU, c->d_r);
+        CKL();
+      }
+      CK(cudaMemcpyAsync(c->h_d, c->d_r, sizeof(double) * mU, cudaMemcpyDeviceToHost, st));
+      TRY(run.sync());
+      rU.assign(c->h_d, c->h_d + mU);
     }
-    CK(cudaMemcpyAsync(c->h_d, c->d_r, sizeof(double) * mU, cudaMemcpyDeviceToHost, st));
-    TRY(run.sync());
-    rU.assign(c->h_d, c->h_d + mU);
     const int trace = getenv("PSDPROJ_TRACE") ? 1 : 0;  // debugging: per-iteration state on stderr
     if (trace) {
       double tmx = -INFINITY, tmn = INFINITY, rmx = 0, rpos = 0;
@@ -2423,7 +2444,28 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
                    ldm));
     TRY(run.gram(s, s, c->S, ld, c->BS, ld, c->Hm, ldm));
     int sU = s;
+    // the rotation (a8) and the next iteration's residual norms (a4) are issued before the Rayleigh-
+    // Ritz sync, assuming it succeeds (they only read S, BS, C' and the new Ritz values): one host sync
+    // per iteration; a failed pivot or a corrective eigensolver pass voids them (issued again below)
+    const bool spec_arm = spec_env && !c->sharded;
+    const int mUn_spec = std::min(mU + qe, s);
+    if (spec_arm) {
+      run.spec_fn = [&, mUn_spec, s]() -> int {
+        TRY(run.mark(5));
+        TRY(dgemm2(st, nl, mUn_spec, s, 1.0, c->S, c->BS, ld, c->Cp, ldm, 0.0, c->S2, c->BS2, ld, c->part,
+                   c->part_elems));
+        TRY(dgemm2(st, nl, mUn_spec, s - mU, 1.0, c->S + (size_t)mU * ld, c->BS + (size_t)mU * ld, ld, c->Cp + mU,
+                   ldm, 0.0, c->Pb, c->BPb, ld, c->part, c->part_elems));
+        TRY(run.mark(6));
+        TRY(launch_pdl(resid_norm_kernel<256>, dim3(mUn_spec), dim3(256), 0, st, nl, (const double*)c->S2, ld,
+                       (const double*)c->BS2, ld, (const double*)c->d_ths, c->R, ld, c->d_r, 0));
+        CK(cudaMemcpyAsync(c->h_d + rslot, c->d_r, sizeof(double) * mUn_spec, cudaMemcpyDeviceToHost, st));
+        return run.mark(7);
+      };
+    }
     rc = run.rr(s, mU, mU, c->d_thU, std::min(mU + qe, s), ovl);
+    run.spec_fn = nullptr;
+    const bool spec_done = spec_arm && rc == 0 && !run.spec_redo;
     // a failed attempt still ran the eigensolver, which uses G / Hm as scratch: a retry forms the
     // pencil again from S, BS
     auto regram = [&](int sr) -> int {
@@ -2455,10 +2497,13 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
     const int rr_npos = run.rr_npos;
     // ---- rotation (a8): X <- S C', BX <- BS C', P <- S_[R P] C'_[R P], BP likewise
     TRY(run.mark(5));
-    // X and BX (S C', BS C') in one launch, P and BP likewise
-    TRY(dgemm2(st, nl, mUn, sU, 1.0, c->S, c->BS, ld, c->Cp, ldm, 0.0, c->S2, c->BS2, ld, c->part, c->part_elems));
-    TRY(dgemm2(st, nl, mUn, sU - mU, 1.0, c->S + (size_t)mU * ld, c->BS + (size_t)mU * ld, ld, c->Cp + mU, ldm, 0.0,
-               c->Pb, c->BPb, ld, c->part, c->part_elems));
+    // X and BX (S C', BS C') in one launch, P and BP likewise (already issued when spec_done)
+    if (!spec_done) {
+      TRY(dgemm2(st, nl, mUn, sU, 1.0, c->S, c->BS, ld, c->Cp, ldm, 0.0, c->S2, c->BS2, ld, c->part, c->part_elems));
+      TRY(dgemm2(st, nl, mUn, sU - mU, 1.0, c->S + (size_t)mU * ld, c->BS + (size_t)mU * ld, ld, c->Cp + mU, ldm,
+                 0.0, c->Pb, c->BPb, ld, c->part, c->part_elems));
+    }
+    spec_ready = spec_done;
     info->flops += 8.0 * nl * (double)mUn * sU;
     std::swap(c->S, c->S2);
     std::swap(c->BS, c->BS2);
