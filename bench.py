@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--workload", default="c3r", choices=["c3r", "c1", "c2", "c2cl", "c3", "c4", "c5", "bo"])
     ap.add_argument("--c4-blocks", type=int, default=512)
     ap.add_argument("--c4-no-tiny", action="store_true", help="C4: every block through its own context (no f4 routing)")
+    ap.add_argument("--c4-direct-n", type=int, default=0,
+                    help="C4: blocks with 112 < n <= this use the exact DIRECT path (side = 2) instead of LOBPCG")
     ap.add_argument("--shard", action="store_true",
                     help="row-shard the single matrix across the ranks (NCCL inside libpsdproj; strong scaling)")
     ap.add_argument("--n", type=int, default=None)
@@ -55,6 +57,9 @@ def parse():
     ap.add_argument("--admm-max-iter", type=int, default=5000)
     ap.add_argument("--adapt-every", type=int, default=0)
     ap.add_argument("--tol-ratio", type=float, default=0.0)
+    ap.add_argument("--late-t0", type=int, default=100, help="first step of the late-sequence companion (0: off)")
+    ap.add_argument("--krylov-depth", type=int, default=1, help="R57 block-Krylov depth (1 = Alg. 3)")
+    ap.add_argument("--krylov-max-active", type=int, default=0, help="R63: R57 directions only while |J| <= this")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-sample-iters", type=int, default=4)
     return ap.parse_args()
@@ -281,7 +286,8 @@ def run_c4_bench(args, rank, world, local, dist):
     clocks.start()
     paths = {}
     ms, proj, iters, worst = run_c4(cfg, rank, world, dist, dev, rounds=max(args.steps, 1),
-                                    warmup=max(args.warmup, 0), tiny=not args.c4_no_tiny, paths=paths)
+                                    warmup=max(args.warmup, 0), tiny=not args.c4_no_tiny, paths=paths,
+                                    direct_n=args.c4_direct_n)
     ck = clocks.stop()
     if rank == 0:
         line = {"metric": "PSD-cone projections/sec (warm LOBPCG), C4 batch of independent blocks",
@@ -291,7 +297,7 @@ def run_c4_bench(args, rank, world, local, dist):
                 "config": {"workload": f"C4 {cfg.count} blocks n in {{50,100,200,400}} (configs[3]), tol {cfg.tol:g}",
                            "parallelism": f"batch-sharded LPT x{world}", "l2": "per-round drift, no flush"},
                 "iters_per_projection": {"mean": iters}, "worst_status": worst, "clocks": ck,
-                "paths_rank0": paths,
+                "paths_rank0": paths, "direct_n": args.c4_direct_n,
                 "routing": ("n <= 112: one launch of the one-CTA warm LOBPCG (f4) for all of them, blocks whose smaller side "
                             "outgrows its 8 columns projected exactly in one CTA (R50); n > 112: one context each, "
                             "psdproj_project_batched") if not args.c4_no_tiny else "every block: one context, psdproj_project_batched"}
@@ -428,7 +434,9 @@ def run_sequence(args, rank, world, local, dist):
     dev = torch.device("cuda", local)
     steps = 3 if args.workload == "c3" else cfg.steps  # C3 literal: the first steps only
     mats = gen_matrices(cfg, steps, dev)
-    ctx = api.Context(cfg.n, params=api.default_params(max_iter=args.max_iter, seed=1912 + rank), device=dev)
+    ctx = api.Context(cfg.n, params=api.default_params(max_iter=args.max_iter, seed=1912 + rank,
+                                                       krylov_depth=args.krylov_depth,
+                                                       krylov_max_active=args.krylov_max_active), device=dev)
     out = torch.empty_like(mats[0])
     st = torch.cuda.current_stream()
     infos, ms = [], []
@@ -505,7 +513,8 @@ def run_c3r(args, rank, world, local, dist):
     mats = [x[0] for x in seq]
     torch.cuda.synchronize()
     st = torch.cuda.current_stream()
-    prm = api.default_params(max_iter=max_iter, profile=5, seed=1912 + rank, ctx_id=rank)
+    kry = dict(krylov_depth=args.krylov_depth, krylov_max_active=args.krylov_max_active)
+    prm = api.default_params(max_iter=max_iter, profile=5, seed=1912 + rank, ctx_id=rank, **kry)
     ctx = api.Context(cfg.n, params=prm, device=dev)
     outs = [torch.empty_like(mats[0]) for _ in range(K)]
     scratch = torch.empty_like(mats[0])
@@ -600,7 +609,7 @@ def run_c3r(args, rank, world, local, dist):
 
     e2e = None
     if not args.no_e2e:
-        hprm = api.default_params(max_iter=max_iter, seed=1912 + rank, ctx_id=rank, host_io=1)
+        hprm = api.default_params(max_iter=max_iter, seed=1912 + rank, ctx_id=rank, host_io=1, **kry)
         hctx = api.Context(cfg.n, params=hprm, device=dev)
         ke_n = min(K, 3)
         host_mats = [m.cpu().pin_memory() for m in mats[: 1 + W + ke_n]]
@@ -634,6 +643,9 @@ def run_c3r(args, rank, world, local, dist):
             "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": name, "n": cfg.n, "tol": tol, "max_iter": max_iter, "locking": "hard",
+                       "trial_space": ("Alg. 3 span(X, R, dX)" if args.krylov_depth <= 1 else
+                                       f"R57/R63 span(X, R, .., B^{args.krylov_depth - 1} R, dX) while |J| <= "
+                                       f"{args.krylov_max_active or 'inf'}, else Alg. 3"),
                        "steps_timed": f"t={1 + W}..{total - 1} of the sequence (t=0 cold, untimed)",
                        "parallelism": f"independent sequences x{world} (one per GPU, no collective)" if world > 1 else "single",
                        "l2": "distinct 128 MB input matrix per step (> 126 MB L2), no flush"},
@@ -674,7 +686,8 @@ def side_lines(args, cfg, tol, mats, seq, W, K, dev, api):
     import torch
     out = {}
     st = torch.cuda.current_stream()
-    prm = api.default_params(max_iter=args.max_iter, profile=2, seed=1912, ctx_id=0)
+    kry = dict(krylov_depth=args.krylov_depth, krylov_max_active=args.krylov_max_active)
+    prm = api.default_params(max_iter=args.max_iter, profile=2, seed=1912, ctx_id=0, **kry)
     pctx = api.Context(cfg.n, params=prm, device=dev)
     scratch = torch.empty_like(mats[0])
     infos = []
@@ -687,6 +700,32 @@ def side_lines(args, cfg, tol, mats, seq, W, K, dev, api):
     out["phase_ms_per_step"] = tot
     dom = max(tot, key=tot.get)
     out["dominant_phase"] = {"phase": dom, "ms_per_step": tot[dom], "share": round(tot[dom] / max(ms, 1e-9), 4)}
+    # late: the drift magnitudes of t = 100.. (eps_t = 1e-2/t) applied from the state of the last timed
+    # step (Haar-invariant rotation: statistically the t = 100 state), warm from that step's block
+    if args.late_t0 > 0:
+        from workloads import generators as G
+        lseq = [(A.contiguous(), Q, lam) for _, A, Q, lam in
+                G.rotation_sequence(cfg, steps=4, device=dev, start=(seq[-1][1], seq[-1][2]), t0=args.late_t0 - 1)][1:]
+        louts = [torch.empty_like(mats[0]) for _ in lseq]
+        levs = [torch.cuda.Event(enable_timing=True) for _ in range(len(lseq) + 1)]
+        linf = []
+        torch.cuda.synchronize()
+        levs[0].record(st)
+        for j, (A, _, _) in enumerate(lseq):
+            _, inf = pctx.project(A, tol, out=louts[j])
+            linf.append(inf)
+            levs[j + 1].record(st)
+        torch.cuda.synchronize()
+        lms = [levs[j].elapsed_time(levs[j + 1]) for j in range(len(lseq))]
+        lrel = accuracy(louts, lseq, cfg)
+        del louts
+        out["late_sequence"] = {
+            "definition": "drift eps_t = 1e-2/t of t = %d..%d applied after the last timed step (same tol, warm)"
+                          % (args.late_t0, args.late_t0 + len(lseq) - 1),
+            "value": len(lseq) / (sum(lms) / 1e3), "unit": "projections/s", "ms": [round(x, 3) for x in lms],
+            "iters": [i["iters"] for i in linf], "status": [i["status"] for i in linf],
+            "npos": [i["npos"] for i in linf], "rel_err_vs_closed_form": lrel,
+            "err_bound_rel": [i["err_bound"] / i["anorm_f"] for i in linf]}
     # cold: same matrix as the first timed step, fresh context
     pctx.reset()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -698,7 +737,7 @@ def side_lines(args, cfg, tol, mats, seq, W, K, dev, api):
                                "cold": ci["cold"]}
     pctx.close()
     # C3-R-sched: tol_t = 10 / t^1.01 over the first steps of the same sequence (t >= 1)
-    sprm = api.default_params(max_iter=args.max_iter, seed=1912, ctx_id=0)
+    sprm = api.default_params(max_iter=args.max_iter, seed=1912, ctx_id=0, **kry)
     sctx = api.Context(cfg.n, params=sprm, device=dev)
     _, _ = sctx.project(mats[0], 10.0, out=scratch)
     souts = [torch.empty_like(mats[0]) for _ in range(1, len(mats))]

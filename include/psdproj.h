@@ -77,6 +77,11 @@ typedef struct {
                     /* their residual / dX directions in span(X, R, dX) (the stopping   */
                     /* rule tests the top guard only, R12); 0 => 2; < 0 => every unconverged column   */
                     /* (the BLOPEX active mask of Alg. 3 as printed). Cold calls always use all.      */
+  int krylov_max_active; /* R63 (with krylov_depth > 1): the block-Krylov directions of R57 join the   */
+                    /* trial subspace only on iterations whose active set J has at most this many     */
+                    /* columns (the Rayleigh-Ritz cost grows with the basis width, the fixed launch   */
+                    /* latency of an iteration does not); wider active sets use Alg. 3's span(X, R,   */
+                    /* dX). 0 => no limit (R57 on every iteration)                     */
 } psdproj_params;
 
 typedef struct {

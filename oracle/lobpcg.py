@@ -111,7 +111,8 @@ class LobpcgResult:
 
 
 def lobpcg_pos(B, X0, tol, max_iter=500, guard=1, q=None, locking="hard", seed=0, ctx=0,
-               call=0, cold=False, guard_tol=None, m_max=None, lock_factor=1.0, krylov_depth=1, guard_active=None):
+               call=0, cold=False, guard_tol=None, m_max=None, lock_factor=1.0, krylov_depth=1, guard_active=None,
+               krylov_max_active=0):
     """Alg. 3: positive eigenpairs of the symmetric matrix B.
 
     X0      n x m start block (warm: previous Ritz block, R27; cold: Philox, R28).
@@ -220,7 +221,9 @@ def lobpcg_pos(B, X0, tol, max_iter=500, guard=1, q=None, locking="hard", seed=0
         a = len(J)
         Kb, BKb = [], []
         prev = BW[:, :a]
-        for _ in range(1, krylov_depth if a else 1):
+        # R63: only on iterations whose active set has at most krylov_max_active columns (0: always)
+        depth = 1 if (krylov_max_active > 0 and a > krylov_max_active) else krylov_depth
+        for _ in range(1, depth if a else 1):
             K = prev.copy()
             if locking == "hard" and XL.shape[1]:
                 K = K - XL @ (XL.T @ K)
@@ -447,7 +450,8 @@ class Context:
     the warm block. One per cone block."""
 
     def __init__(self, n, tol_default=1e-8, max_iter=500, guard=1, q=None, m0=None,
-                 locking="hard", seed=0, ctx_id=0, side=0, keep_extra=None, krylov_depth=1, guard_active=None):
+                 locking="hard", seed=0, ctx_id=0, side=0, keep_extra=None, krylov_depth=1, guard_active=None,
+                 krylov_max_active=0):
         self.n = n
         self.max_iter = max_iter
         self.guard = guard
@@ -460,6 +464,7 @@ class Context:
         self.keep_extra = keep_extra
         self.krylov_depth = krylov_depth
         self.guard_active = guard_active
+        self.krylov_max_active = krylov_max_active
         # capacity ceil(n/3)+1: a wider block is the exact-eig regime (R18)
         self.m_max = min(n, (n + 2) // 3 + 1)
         self.reset()
@@ -514,7 +519,7 @@ class Context:
             res = lobpcg_pos(B, X0, tol, max_iter=self.max_iter, guard=self.guard, q=self.q,
                              locking=self.locking, seed=self.seed, ctx=self.ctx_id, call=call,
                              cold=cold, m_max=self.m_max, krylov_depth=self.krylov_depth,
-                             guard_active=self.guard_active)
+                             guard_active=self.guard_active, krylov_max_active=self.krylov_max_active)
             if res.abort_direct:
                 mode = DIRECT
                 info["mode"] = mode

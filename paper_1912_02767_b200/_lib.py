@@ -35,6 +35,7 @@ class Params(ctypes.Structure):
         ("ctx_id", ctypes.c_uint32), ("profile", ctypes.c_int), ("host_io", ctypes.c_int),
         ("perp_steps", ctypes.c_int), ("perp_delta", ctypes.c_double), ("lock_factor", ctypes.c_double),
         ("krylov_depth", ctypes.c_int), ("guard_active", ctypes.c_int),
+        ("krylov_max_active", ctypes.c_int),
     ]
 
 

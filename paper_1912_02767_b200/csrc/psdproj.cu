@@ -2333,7 +2333,10 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
     }
     int offW = mU, offE = mU + a, offP = mU + a + qe;
     // R57 (krylov_depth d > 1): d - 1 block-Krylov directions B^k R_J follow P in the basis
-    const int depth = std::max(1, c->prm.krylov_depth);
+    // R63: only while the active set is at most krylov_max_active columns wide (0: always)
+    static const char* kma_env = getenv("PSDPROJ_KRYLOV_MAX_ACTIVE");  // experiments: overrides the parameter
+    const int kma = kma_env ? atoi(kma_env) : c->prm.krylov_max_active;
+    const int depth = (kma > 0 && a > kma) ? 1 : std::max(1, c->prm.krylov_depth);
     const int aK = depth > 1 ? a : 0;
     int s = offP + ap + (depth - 1) * aK;
     if (getenv("PSDPROJ_TRACE")) fprintf(stderr, "basis k=%d s=%d mU=%d a=%d ap=%d qe=%d nL=%d\n", k, s, mU, a, ap, qe, nL);

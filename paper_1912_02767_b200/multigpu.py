@@ -59,9 +59,12 @@ class C4Shard:
     projected together by ONE launch of the one-CTA warm LOBPCG (psdproj_project_tiny_lobpcg, f4),
     which hands the blocks whose smaller side outgrows its 8-column block to the exact one-CTA
     projection (the DIRECT branch; R50); the others run one psdproj context each
-    through psdproj_project_batched."""
+    through psdproj_project_batched. direct_n > 0 (a routing option, off by default): the contexts of
+    blocks with n <= direct_n are created with side = PSDPROJ_SIDE_DIRECT, i.e. the library's exact
+    one-sided projection (a13) instead of LOBPCG -- at these sizes a round of the batch is bound by
+    kernel launches (~50 per LOBPCG iteration), not by arithmetic (C4)."""
 
-    def __init__(self, cfg, block_ids, device, seed=1912, max_iter=500, tiny=True):
+    def __init__(self, cfg, block_ids, device, seed=1912, max_iter=500, tiny=True, direct_n=0):
         import torch
 
         from . import api
@@ -81,7 +84,8 @@ class C4Shard:
         self.ctxs = []
         for k in self.large:
             i = self.ids[k]
-            prm = api.default_params(max_iter=max_iter, seed=seed, ctx_id=i)
+            prm = api.default_params(max_iter=max_iter, seed=seed, ctx_id=i,
+                                     side=2 if cfg.sizes[i] <= direct_n else 0)
             self.ctxs.append(api.Context(cfg.sizes[i], params=prm, device=device))
         self.tiny = (api.TinyLobpcgBatch([cfg.sizes[self.ids[k]] for k in self.small], device=device, seed=seed,
                                          max_iter=max_iter) if self.small else None)
@@ -130,7 +134,7 @@ def shard_c4(cfg, rank, world):
     return parts[rank], loads
 
 
-def run_c4(cfg, rank, world, dist, device, rounds, warmup, tol=None, tiny=True, paths=None):
+def run_c4(cfg, rank, world, dist, device, rounds, warmup, tol=None, tiny=True, paths=None, direct_n=0):
     """Sharded C4 rounds on this rank; returns (device ms of the timed rounds, max over ranks),
     projections done by all ranks, and the per-rank mean LOBPCG iterations. `paths` (a dict, if
     given) receives this rank's count of timed projections per path (lobpcg / direct / tiny-lobpcg /
@@ -138,7 +142,7 @@ def run_c4(cfg, rank, world, dist, device, rounds, warmup, tol=None, tiny=True, 
     import torch
 
     ids, _ = shard_c4(cfg, rank, world)
-    sh = C4Shard(cfg, ids, device, tiny=tiny)
+    sh = C4Shard(cfg, ids, device, tiny=tiny, direct_n=direct_n)
     st = torch.cuda.current_stream()
     for _ in range(warmup):
         sh.project(tol)

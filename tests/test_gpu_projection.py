@@ -335,6 +335,56 @@ def test_krylov_depth_parity(api, depth):
     assert its[depth] * 1.4 <= its[1], its
 
 
+def test_krylov_max_active_parity(api):
+    """R63: block-Krylov directions only while the active set is narrow (krylov_max_active). C3-R
+    (n = 1000) warm sequence: closed-form projection, dominating bound, right positive count, fewer
+    iterations than Alg. 3; a limit wider than any block equals R57 on every iteration bit for bit."""
+    from workloads.generators import C3R, rotation_sequence
+    cfg = C3R(1000)
+    its, last = {}, {}
+    for name, kw in (("alg3", dict(krylov_depth=1)), ("r57", dict(krylov_depth=2)),
+                     ("wide", dict(krylov_depth=2, krylov_max_active=100000)),
+                     ("mid", dict(krylov_depth=2, krylov_max_active=24))):
+        ctx = api.Context(cfg.n, params=api.default_params(seed=4, max_iter=6000, **kw))
+        tot = 0
+        for t, A, Q, lam in rotation_sequence(cfg, steps=3, device="cuda"):
+            Pi, info = ctx.project(A.contiguous(), cfg.tol)
+            Pstar = (Q * torch.clamp(lam, min=0)) @ Q.T
+            err = float(torch.linalg.norm(Pi - Pstar))
+            nA = float(torch.linalg.norm(A))
+            assert info["status"] == 0 and info["npos"] == 50, (name, t, info["iters"])
+            assert info["err_bound"] >= err and err / nA <= 2e-9, (name, t, err / nA)
+            if t > 0:
+                tot += info["iters"]
+        its[name] = tot
+        last[name] = Pi.clone()
+        ctx.close()
+    assert torch.equal(last["wide"], last["r57"]) and its["wide"] == its["r57"], its
+    assert its["r57"] <= its["mid"] < its["alg3"], its
+
+
+def test_krylov_max_active_matches_oracle_iterates(api):
+    """R63 against the oracle's LOBPCG with the same option (small planted problem, cold call): same
+    iteration count and Ritz values to 1e-10 relative (R34 form)."""
+    import oracle.lobpcg as L
+    rng = np.random.default_rng(163)
+    n, p = 240, 12
+    lam = np.concatenate([10.0 ** rng.uniform(-1, 1, p), -(10.0 ** rng.uniform(-1, 1, n - p))])
+    A = planted(haar_q(rng, n), lam)
+    octx = L.Context(n, seed=9, ctx_id=0, krylov_depth=2, krylov_max_active=10)
+    Po, io = octx.project(A, 1e-9)
+    ctx = api.Context(n, params=api.default_params(seed=9, ctx_id=0, krylov_depth=2, krylov_max_active=10))
+    Pi, info = ctx.project(torch.from_numpy(A).cuda(), 1e-9)
+    th = np.sort(ctx.get_ritz().numpy())[::-1][:p]
+    ctx.close()
+    assert info["status"] == 0 and io["status"] == L.OK
+    assert info["npos"] == io["npos"] == p
+    assert abs(info["iters"] - io["iters"]) <= max(3, io["iters"] // 20), (info["iters"], io["iters"])
+    top = np.sort(lam)[::-1][:p]
+    assert np.max(np.abs(th - top) / np.maximum(np.abs(top), 1.0)) <= 1e-10
+    assert np.linalg.norm(Pi.cpu().numpy() - Po) <= 1e-9 * np.linalg.norm(A)
+
+
 def test_direct_path_large_order(api):
     """DIRECT on the tridiagonal eigensolver at n = 2000 (n <= EIG_MAX but > 3 m_max: the eigensolver
     scratch must be sized for n, not for the LOBPCG basis): a half-positive planted spectrum, cold

@@ -332,6 +332,32 @@ def test_krylov_depth_extension_same_projection_fewer_iterations():
     assert its[3] * 1.5 <= its[1], its
 
 
+def test_krylov_max_active_switches_depth_by_active_width():
+    """R63: with krylov_max_active the R57 directions join the basis only on iterations whose active
+    set is narrow. A limit at least as wide as the block reproduces R57 on every iteration, a limit
+    of 0 columns' worth (1 here, below every active width > 1) stays close to Alg. 3's iteration
+    count, an intermediate limit lands in between; every variant reaches the planted projection."""
+    rng = np.random.default_rng(63)
+    n, p = 300, 15
+    lam = np.concatenate([10.0 ** rng.uniform(-2, 1, p), -(10.0 ** rng.uniform(-2, 1, n - p))])
+    Q = haar_q(rng, n)
+    A = planted(Q, lam)
+    Pstar = (Q * np.maximum(lam, 0)) @ Q.T
+    its = {}
+    for name, kw in (("alg3", dict(krylov_depth=1)), ("r57", dict(krylov_depth=2)),
+                     ("wide", dict(krylov_depth=2, krylov_max_active=n)),
+                     ("mid", dict(krylov_depth=2, krylov_max_active=22))):
+        ctx = L.Context(n, seed=3, **kw)
+        P, info = ctx.project(A, 1e-9)
+        assert info["status"] == L.OK and info["npos"] == p, name
+        assert np.linalg.norm(P - Pstar) <= 1e-9 * np.linalg.norm(A), name
+        assert info["err_bound"] >= np.linalg.norm(P - Pstar), name
+        its[name] = info["iters"]
+    assert its["wide"] == its["r57"], its
+    assert its["r57"] <= its["mid"] <= its["alg3"], its
+    assert its["mid"] < its["alg3"], its
+
+
 def test_guard_active_warm_sequence_same_projection():
     """R62 (the GPU default on warm calls): with only the top 2 guards keeping their directions the
     warm projections of a drifting planted sequence still reach the closed form within tolerance, the

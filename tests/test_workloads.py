@@ -33,6 +33,22 @@ def test_c3r_keeps_five_percent():
     assert np.all(np.abs(lam) >= 1e-3 * (1 - 1e-12)) and np.all(np.abs(lam) <= 1e2)
 
 
+def test_c3r_continue_from_state():
+    """rotation_sequence(start=(Q_t, lam), t0=t) continues the same sequence (bench.py's late-sequence
+    companion applies the drift of t = 100.. from the last timed state)."""
+    cfg = C3R(n=120)
+    full = list(rotation_sequence(cfg, steps=5))
+    cont = list(rotation_sequence(cfg, steps=3, start=(full[2][2], full[2][3]), t0=2))
+    assert [c[0] for c in cont] == [2, 3, 4]
+    for c, f in zip(cont, full[2:]):
+        assert np.array_equal(c[1], f[1])
+    # the drift of step t rotates by ~eps(t + 1): a late start moves the matrix less
+    late = list(rotation_sequence(cfg, steps=2, start=(full[2][2], full[2][3]), t0=99))
+    d_late = np.linalg.norm(late[1][1] - late[0][1])
+    d_early = np.linalg.norm(full[3][1] - full[2][1])
+    assert d_late < d_early * (3.0 / 100.0) * 1.5
+
+
 def test_c3_literal_loses_five_percent():
     """F4 of SURVEY.md: the literal additive drift of configs[2] smears the near-zero spectrum
     (measured at n = 400 here: positive count grows well beyond 5%)."""

@@ -123,14 +123,17 @@ def drift_sequence(cfg, steps=None, start=None):
         A = A + cfg.eps(t + 1) * sym(G)
 
 
-def rotation_sequence(cfg, steps=None, device=None):
+def rotation_sequence(cfg, steps=None, device=None, start=None, t0=0):
     """Yields (t, A_t, Q_t, lam) for the spectrum-preserving C3-R drift. With device (a torch
-    device string) the Cayley step and products run in torch float64 there (same recipe)."""
+    device string) the Cayley step and products run in torch float64 there (same recipe).
+    start = (Q, lam) with t0: continue from that state with the drift of steps t0, t0 + 1, ...
+    (eps(t + 1) and the seed stream [seed, t]); the Cayley rotation is Haar-invariant, so a state
+    reached after t0 steps and any other orthogonal Q are statistically the same start."""
     steps = cfg.steps if steps is None else steps
-    Q, lam = initial(cfg)
+    Q, lam = initial(cfg) if start is None else start
     n = cfg.n
     if device is None:
-        for t in range(steps):
+        for t in range(t0, t0 + steps):
             yield t, planted(Q, lam), Q, lam
             G = np.random.default_rng([cfg.seed, t]).standard_normal((n, n))
             K = (G - G.T) / (2.0 * math.sqrt(n)) * cfg.eps(t + 1)
@@ -144,7 +147,7 @@ def rotation_sequence(cfg, steps=None, device=None):
         Qd = torch.as_tensor(Q, device=device)
         lamd = torch.as_tensor(lam, device=device)
         I = torch.eye(n, dtype=torch.float64, device=device)
-        for t in range(steps):
+        for t in range(t0, t0 + steps):
             A = (Qd * lamd) @ Qd.T
             A = 0.5 * (A + A.T)
             yield t, A, Qd, lamd
