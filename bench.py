@@ -60,6 +60,7 @@ def parse():
     ap.add_argument("--late-t0", type=int, default=100, help="first step of the late-sequence companion (0: off)")
     ap.add_argument("--krylov-depth", type=int, default=1, help="R57 block-Krylov depth (1 = Alg. 3)")
     ap.add_argument("--krylov-max-active", type=int, default=0, help="R63: R57 directions only while |J| <= this")
+    ap.add_argument("--no-r63", action="store_true", help="skip the R63 block-Krylov companion line")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-sample-iters", type=int, default=4)
     return ap.parse_args()
@@ -736,6 +737,33 @@ def side_lines(args, cfg, tol, mats, seq, W, K, dev, api):
     out["cold_after_reset"] = {"t": 1 + W, "iters": ci["iters"], "ms": e0.elapsed_time(e1), "status": ci["status"],
                                "cold": ci["cold"]}
     pctx.close()
+    # R63 companion: the same warm steps with block-Krylov directions while the active set is narrow
+    # (krylov_depth 2, krylov_max_active 96; an extension of Alg. 3, off in the headline)
+    if args.krylov_depth <= 1 and not args.no_r63:
+        kprm = api.default_params(max_iter=args.max_iter, seed=1912, ctx_id=0, krylov_depth=2, krylov_max_active=96)
+        kctx = api.Context(cfg.n, params=kprm, device=dev)
+        kouts = [torch.empty_like(mats[0]) for _ in range(K)]
+        kinf = []
+        for k in range(1 + W):
+            kctx.project(mats[k], tol, out=scratch)
+        torch.cuda.synchronize()
+        e0.record(st)
+        for j, k in enumerate(range(1 + W, 1 + W + K)):
+            _, inf = kctx.project(mats[k], tol, out=kouts[j])
+            kinf.append(inf)
+        e1.record(st)
+        torch.cuda.synchronize()
+        kms = e0.elapsed_time(e1)
+        krel = accuracy(kouts, seq[1 + W:1 + W + K], cfg)
+        del kouts
+        kctx.close()
+        out["r63_block_krylov"] = {
+            "definition": "same timed steps, trial space span(X, R, B R, dX) on iterations with |J| <= 96 "
+                          "(krylov_depth 2, krylov_max_active 96; DESIGN R57/R63), Alg. 3 otherwise",
+            "value": K / (kms / 1e3), "unit": "projections/s", "ms_per_step": kms / K,
+            "iters": [i["iters"] for i in kinf], "status": [i["status"] for i in kinf],
+            "npos": [i["npos"] for i in kinf], "rel_err_vs_closed_form": krel,
+            "err_bound_rel": [i["err_bound"] / i["anorm_f"] for i in kinf]}
     # C3-R-sched: tol_t = 10 / t^1.01 over the first steps of the same sequence (t >= 1)
     sprm = api.default_params(max_iter=args.max_iter, seed=1912, ctx_id=0, **kry)
     sctx = api.Context(cfg.n, params=sprm, device=dev)

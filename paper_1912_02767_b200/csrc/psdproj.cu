@@ -2377,8 +2377,10 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
     // block of G is needed (X^T X = I, X^T [W P] = 0 by construction); it does not depend on B W, so
     // its Gram and Cholesky run on the side stream, overlapping the block multiply (unsharded mode)
     static int ovl_env = getenv("PSDPROJ_NO_OVERLAP") ? 0 : 1;
-    const bool ovl = ovl_env && !c->sharded && s > mU && depth == 1;
-    if (ovl) {
+    // (R57 / R63 iterations: the last Krylov block is known only after the multiply before it, so the
+    // fork sits before the LAST block multiply of the iteration)
+    const bool ovl = ovl_env && !c->sharded && s > mU;
+    auto fork_chol = [&]() -> int {
       if (!c->st2) {
         // high priority: the 16-CTA cluster Cholesky is dispatched before the block multiply's
         // CTAs, which would otherwise occupy every SM until the multiply ends
@@ -2408,11 +2410,14 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
         wait_flag_kernel<<<1, 32, 0, st>>>(c->d_flag, seq, 200000LL);
         CKL();
       }
-    }
+      return 0;
+    };
+    const bool krylov_it = depth > 1 && aK > 0;
+    if (ovl && !krylov_it) TRY(fork_chol());
     TRY(run.mark(0));
     static int hold_env = getenv("PSDPROJ_CHOL_HOLD") ? atoi(getenv("PSDPROJ_CHOL_HOLD")) : 1;
     static const int chol_sms = getenv("PSDPROJ_CHOL_CS") ? std::max(1, atoi(getenv("PSDPROJ_CHOL_CS"))) : 8;
-    g_sm_reserve = (ovl && hold_env) ? chol_sms : 0;  // the Cholesky cluster's CTAs (one SM each)
+    g_sm_reserve = (ovl && !krylov_it && hold_env) ? chol_sms : 0;  // the Cholesky cluster's CTAs (one SM each)
     rc = run.amul(sgn, A, lda, W, ld, aw, c->BS + (size_t)offW * ld, ld);
     g_sm_reserve = 0;
     TRY(rc);
@@ -2426,17 +2431,21 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
         double* K = c->S + (size_t)offK * ld;
         double* BK = c->BS + (size_t)offK * ld;
         TRY(copy_block_pdl(st, nl, aK, K, ld, BKprev, ld));
-        if (hard && nL > 0) {
-          TRY(run.gram(nL, aK, XLp(), ld, K, ld, c->Y, ldm));
-          TRY(run.gemm(OP_N, OP_N, nl, aK, nL, -1.0, XLp(), ld, c->Y, ldm, 1.0, K, ld));
-        }
-        TRY(run.gram(mU, aK, c->S, ld, K, ld, c->Y, ldm));
-        TRY(run.gemm(OP_N, OP_N, nl, aK, mU, -1.0, c->S, ld, c->Y, ldm, 1.0, K, ld));
-        TRY(run.gram(aK, aK, W, ld, K, ld, c->Y, ldm));
-        TRY(run.gemm(OP_N, OP_N, nl, aK, aK, -1.0, W, ld, c->Y, ldm, 1.0, K, ld));
+        // K <- K - [X_L X_U R_J] ([X_L X_U R_J]^T K): the three blocks are contiguous in S and R_J is
+        // orthogonal to X (projected above), so one Gram + one update equal the oracle's three
+        // successive projections up to rounding
+        const int nXW = ((hard && nL > 0) ? nL : 0) + mU + aK;
+        const double* XW = (hard && nL > 0) ? XLp() : c->S;
+        TRY(run.gram(nXW, aK, XW, ld, K, ld, c->Y, ldm));
+        TRY(run.gemm(OP_N, OP_N, nl, aK, nXW, -1.0, XW, ld, c->Y, ldm, 1.0, K, ld));
         TRY(run.normalize(nl, aK, K, ld, nullptr, 0));
+        const bool fork_here = ovl && dk == depth;
+        if (fork_here) TRY(fork_chol());
         TRY(run.mark(0));
-        TRY(run.amul(sgn, A, lda, K, ld, aK, BK, ld));
+        g_sm_reserve = (fork_here && hold_env) ? chol_sms : 0;
+        rc = run.amul(sgn, A, lda, K, ld, aK, BK, ld);
+        g_sm_reserve = 0;
+        TRY(rc);
         BKprev = BK;
       }
       TRY(run.mark(2));

@@ -1,5 +1,5 @@
 # R63 sweep on the headline command (no companions): krylov_depth x krylov_max_active
-for cfg in "1 0" "2 32" "2 48" "2 64" "2 96" "3 32" "3 48"; do
+for cfg in ${KMA_CFGS:-"1 0" "2 48" "2 96" "3 48" "3 64" "4 48" "2 0"}; do
   set -- $cfg
   python bench.py --no-extra --no-e2e --no-cpu --krylov-depth $1 --krylov-max-active $2 > gpurun_out/kma_$1_$2.log 2> gpurun_out/kma_$1_$2.err
   python - <<PY
