@@ -288,7 +288,9 @@ def run_c4_bench(args, rank, world, local, dist):
     paths = {}
     ms, proj, iters, worst = run_c4(cfg, rank, world, dist, dev, rounds=max(args.steps, 1),
                                     warmup=max(args.warmup, 0), tiny=not args.c4_no_tiny, paths=paths,
-                                    direct_n=args.c4_direct_n)
+                                    direct_n=args.c4_direct_n,
+                                    params=dict(krylov_depth=args.krylov_depth,
+                                                krylov_max_active=args.krylov_max_active))
     ck = clocks.stop()
     if rank == 0:
         line = {"metric": "PSD-cone projections/sec (warm LOBPCG), C4 batch of independent blocks",
@@ -298,7 +300,7 @@ def run_c4_bench(args, rank, world, local, dist):
                 "config": {"workload": f"C4 {cfg.count} blocks n in {{50,100,200,400}} (configs[3]), tol {cfg.tol:g}",
                            "parallelism": f"batch-sharded LPT x{world}", "l2": "per-round drift, no flush"},
                 "iters_per_projection": {"mean": iters}, "worst_status": worst, "clocks": ck,
-                "paths_rank0": paths, "direct_n": args.c4_direct_n,
+                "paths_rank0": paths, "direct_n": args.c4_direct_n, "krylov_depth": args.krylov_depth,
                 "routing": ("n <= 112: one launch of the one-CTA warm LOBPCG (f4) for all of them, blocks whose smaller side "
                             "outgrows its 8 columns projected exactly in one CTA (R50); n > 112: one context each, "
                             "psdproj_project_batched") if not args.c4_no_tiny else "every block: one context, psdproj_project_batched"}
@@ -317,7 +319,10 @@ def run_c5_bench(args, rank, world, local, dist):
     from workloads.generators import maxcut_graph
     n = args.n or 2000
     L = maxcut_graph(n=n, p_edge=0.01, seed=501)
-    solver = MaxCutADMM(L, device=f"cuda:{local}", adapt_every=args.adapt_every, tol_ratio=args.tol_ratio)
+    from paper_1912_02767_b200 import api
+    kprm = (api.default_params(seed=1912, krylov_depth=args.krylov_depth, krylov_max_active=args.krylov_max_active)
+            if args.krylov_depth > 1 else None)
+    solver = MaxCutADMM(L, device=f"cuda:{local}", adapt_every=args.adapt_every, tol_ratio=args.tol_ratio, params=kprm)
     for _ in range(max(args.warmup, 0)):
         solver.step()
     torch.cuda.synchronize()
@@ -384,7 +389,8 @@ def run_sharded_bench(args, rank, world, local, dist):
     obj = [uid if rank == 0 else None]
     if dist is not None:
         dist.broadcast_object_list(obj, src=0)
-    prm = api.default_params(max_iter=args.max_iter, profile=1, seed=1912, ctx_id=0)
+    prm = api.default_params(max_iter=args.max_iter, profile=1, seed=1912, ctx_id=0,
+                             krylov_depth=args.krylov_depth, krylov_max_active=args.krylov_max_active)
     ctx = api.ShardedContext(cfg.n, r0, nr, obj[0], rank, world, params=prm, device=dev)
     out = api.colmajor(nr, cfg.n, device=dev)
     for k in range(1 + W):

@@ -64,7 +64,7 @@ class C4Shard:
     one-sided projection (a13) instead of LOBPCG -- at these sizes a round of the batch is bound by
     kernel launches (~50 per LOBPCG iteration), not by arithmetic (C4)."""
 
-    def __init__(self, cfg, block_ids, device, seed=1912, max_iter=500, tiny=True, direct_n=0):
+    def __init__(self, cfg, block_ids, device, seed=1912, max_iter=500, tiny=True, direct_n=0, params=None):
         import torch
 
         from . import api
@@ -85,7 +85,7 @@ class C4Shard:
         for k in self.large:
             i = self.ids[k]
             prm = api.default_params(max_iter=max_iter, seed=seed, ctx_id=i,
-                                     side=2 if cfg.sizes[i] <= direct_n else 0)
+                                     side=2 if cfg.sizes[i] <= direct_n else 0, **(params or {}))
             self.ctxs.append(api.Context(cfg.sizes[i], params=prm, device=device))
         self.tiny = (api.TinyLobpcgBatch([cfg.sizes[self.ids[k]] for k in self.small], device=device, seed=seed,
                                          max_iter=max_iter) if self.small else None)
@@ -134,7 +134,8 @@ def shard_c4(cfg, rank, world):
     return parts[rank], loads
 
 
-def run_c4(cfg, rank, world, dist, device, rounds, warmup, tol=None, tiny=True, paths=None, direct_n=0):
+def run_c4(cfg, rank, world, dist, device, rounds, warmup, tol=None, tiny=True, paths=None, direct_n=0,
+           params=None):
     """Sharded C4 rounds on this rank; returns (device ms of the timed rounds, max over ranks),
     projections done by all ranks, and the per-rank mean LOBPCG iterations. `paths` (a dict, if
     given) receives this rank's count of timed projections per path (lobpcg / direct / tiny-lobpcg /
@@ -142,7 +143,7 @@ def run_c4(cfg, rank, world, dist, device, rounds, warmup, tol=None, tiny=True, 
     import torch
 
     ids, _ = shard_c4(cfg, rank, world)
-    sh = C4Shard(cfg, ids, device, tiny=tiny, direct_n=direct_n)
+    sh = C4Shard(cfg, ids, device, tiny=tiny, direct_n=direct_n, params=params)
     st = torch.cuda.current_stream()
     for _ in range(warmup):
         sh.project(tol)
