@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the phase / cold / sched companion lines")
     ap.add_argument("--admm-max-iter", type=int, default=5000)
+    ap.add_argument("--c5-exact", action="store_true", help="C5: also solve with exact (DIRECT) projections")
     ap.add_argument("--adapt-every", type=int, default=0)
     ap.add_argument("--tol-ratio", type=float, default=0.0)
     ap.add_argument("--late-t0", type=int, default=100, help="first step of the late-sequence companion (0: off)")
@@ -293,6 +294,17 @@ def run_c4_bench(args, rank, world, local, dist):
                                                 krylov_max_active=args.krylov_max_active))
     ck = clocks.stop()
     if rank == 0:
+        # whole-round roofline: rank 0's algorithmic flops / bytes against the round time
+        try:
+            p64 = float(json.load(open(PEAKS_FP64))["dgemm_tflops_burst"])
+            hbm = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+        except Exception:
+            p64, hbm = 35.46, 6650.0
+        fl, by = paths.get("alg_flops_bytes_per_round", [0.0, 0.0])
+        t_roof = max(by / (hbm * 1e9), fl / (p64 * 1e12))
+        step_roof = {"frac": t_roof / (ms / max(args.steps, 1) / 1e3), "t_roof_ms": t_roof * 1e3, "flops": fl, "bytes": by,
+                     "definition": "rank 0's blocks: max(bytes/HBM, flops/P64) / round time (SURVEY §8.d.1; the "
+                                   "library's per-call algorithmic counters, nominal 9 n^3 for the one-launch tiny blocks)"}
         line = {"metric": "PSD-cone projections/sec (warm LOBPCG), C4 batch of independent blocks",
                 "value": proj / (ms / 1e3), "unit": "projections/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms / max(args.steps, 1), "higher_is_better": True,
@@ -300,6 +312,7 @@ def run_c4_bench(args, rank, world, local, dist):
                 "config": {"workload": f"C4 {cfg.count} blocks n in {{50,100,200,400}} (configs[3]), tol {cfg.tol:g}",
                            "parallelism": f"batch-sharded LPT x{world}", "l2": "per-round drift, no flush"},
                 "iters_per_projection": {"mean": iters}, "worst_status": worst, "clocks": ck,
+                "step_roofline": step_roof,
                 "paths_rank0": paths, "direct_n": args.c4_direct_n, "krylov_depth": args.krylov_depth,
                 "routing": ("n <= 112: one launch of the one-CTA warm LOBPCG (f4) for all of them, blocks whose smaller side "
                             "outgrows its 8 columns projected exactly in one CTA (R50); n > 112: one context each, "
@@ -350,6 +363,24 @@ def run_c5_bench(args, rank, world, local, dist):
                      "r_dual": o2["r_dual"], "objective": o2["objective"],
                      "lobpcg_iters_per_admm_iter": o2["lobpcg_iters"] / max(o2["iters"], 1)}
         s2.close()
+    exact = None
+    if args.c5_exact:
+        # the paper's comparison (Table 1: ADMM with exact projections) on the same GPU:
+        # every projection through the library's exact DIRECT path (side = 2, tridiagonal eigensolver of A)
+        s3 = MaxCutADMM(L, device=f"cuda:{local}", params=api.default_params(seed=1912, side=2))
+        torch.cuda.synchronize()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(st)
+        o3 = s3.solve(eps=1e-4, max_iter=args.admm_max_iter)
+        g1.record(st)
+        torch.cuda.synchronize()
+        es = g0.elapsed_time(g1) / 1e3
+        exact = {"definition": "same ADMM, every projection exact (side = PSDPROJ_SIDE_DIRECT)", "solve_s": es,
+                 "admm_iters": o3["iters"], "ms_per_admm_iter": 1e3 * es / max(o3["iters"], 1),
+                 "r_prim": o3["r_prim"], "r_dual": o3["r_dual"], "objective": o3["objective"],
+                 "speedup_time_to_eps_approx_over_exact": es / (ms / 1e3),
+                 "speedup_per_admm_iter": (es / max(o3["iters"], 1)) / (ms / 1e3 / max(its, 1))}
+        s3.close()
     if rank == 0:
         infos = solver.infos
         line = {"metric": "MaxCut SDP approximate-ADMM iterations/sec (one warm LOBPCG projection each), n=2000",
@@ -366,7 +397,7 @@ def run_c5_bench(args, rank, world, local, dist):
                 "lobpcg_iters_per_admm_iter": sum(i["iters"] for i in infos) / max(len(infos), 1),
                 "sides": sorted(set(i["side"] for i in infos)), "cold_calls": sum(i["cold"] for i in infos),
                 "time_to_1e-4_s": ms / 1e3 if out["r_prim"] <= 1e-4 and out["r_dual"] <= 1e-4 else None,
-                "r59_companion": companion}
+                "r59_companion": companion, "exact_projection_admm": exact}
         print(json.dumps(line), flush=True)
     solver.close()
 
@@ -456,6 +487,27 @@ def run_sequence(args, rank, world, local, dist):
         if k > 0:
             infos.append(inf)
             ms.append(e0.elapsed_time(e1))
+    # the library's own exact path on the same matrices (side = PSDPROJ_SIDE_DIRECT, a13): where the
+    # crossover between warm LOBPCG and the exact projection sits on this GPU (first 20 steps)
+    direct = None
+    if cfg.n <= 2000 and args.workload != "c3":
+        dctx = api.Context(cfg.n, params=api.default_params(seed=1912 + rank, side=2), device=dev)
+        dms, dinf = [], []
+        for k, A in enumerate(mats[:21]):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            _, inf = dctx.project(A, tol, out=out)
+            e1.record(st)
+            torch.cuda.synchronize()
+            if k > 0:
+                dms.append(e0.elapsed_time(e1))
+                dinf.append(inf)
+        dctx.close()
+        direct = {"definition": "exact DIRECT path (a13) on steps 1..20 of the same sequence",
+                  "value": len(dms) / (sum(dms) / 1e3), "unit": "projections/s", "ms_per_step": sum(dms) / len(dms),
+                  "err_bound_rel_max": max(i["err_bound"] / i["anorm_f"] for i in dinf),
+                  "status_counts": {str(s_): [i["status"] for i in dinf].count(s_)
+                                    for s_ in sorted(set(i["status"] for i in dinf))}}
     if rank == 0:
         status = [i["status"] for i in infos]
         line = {"metric": f"PSD-cone projections/sec (warm LOBPCG), {name}", "value": len(ms) / (sum(ms) / 1e3),
@@ -466,7 +518,8 @@ def run_sequence(args, rank, world, local, dist):
                                          "max": max(i["iters"] for i in infos)},
                 "status_counts": {str(s_): status.count(s_) for s_ in sorted(set(status))},
                 "err_bound_rel_max": max(i["err_bound"] / i["anorm_f"] for i in infos),
-                "npos": sorted(set(i["npos"] for i in infos)), "sides": sorted(set(i["side"] for i in infos))}
+                "npos": sorted(set(i["npos"] for i in infos)), "sides": sorted(set(i["side"] for i in infos)),
+                "exact_direct_companion": direct}
         print(json.dumps(line), flush=True)
     ctx.close()
 
@@ -770,6 +823,26 @@ def side_lines(args, cfg, tol, mats, seq, W, K, dev, api):
             "iters": [i["iters"] for i in kinf], "status": [i["status"] for i in kinf],
             "npos": [i["npos"] for i in kinf], "rel_err_vs_closed_form": krel,
             "err_bound_rel": [i["err_bound"] / i["anorm_f"] for i in kinf]}
+    # timing context only (not a product path, no parity claim): the exact projection of
+    # the first timed matrix by a library eigendecomposition on the same GPU (torch.linalg.eigh =
+    # cuSOLVER syevd, then V+ Lambda+ V+^T) -- the GPU analogue of the paper's syevr baseline
+    try:
+        Ax = mats[1 + W]
+        for rep in range(2):  # first pass warms cuSOLVER's workspace
+            torch.cuda.synchronize()
+            e0.record(st)
+            lamx, Vx = torch.linalg.eigh(Ax)
+            posx = lamx > 0
+            Px = (Vx[:, posx] * lamx[posx]) @ Vx[:, posx].T
+            e1.record(st)
+            torch.cuda.synchronize()
+        out["exact_eigh_context"] = {
+            "definition": "torch.linalg.eigh (cuSOLVER) + V+ Lambda+ V+^T of the first timed matrix, same GPU; "
+                          "library timing context, not the product path",
+            "ms": e0.elapsed_time(e1), "npos": int(posx.sum())}
+        del lamx, Vx, Px
+    except Exception as ex:  # context line only: never fail the bench on it
+        out["exact_eigh_context"] = {"unavailable": str(ex)[:200]}
     # C3-R-sched: tol_t = 10 / t^1.01 over the first steps of the same sequence (t >= 1)
     sprm = api.default_params(max_iter=args.max_iter, seed=1912, ctx_id=0, **kry)
     sctx = api.Context(cfg.n, params=sprm, device=dev)

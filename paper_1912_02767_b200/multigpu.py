@@ -111,8 +111,13 @@ class C4Shard:
                                        outs=[self.outs[k] for k in self.small])
             for j, k in enumerate(self.small):
                 st = res["status"][j]
-                infos[k] = {"iters": res["iters"][j], "status": 0 if st in (0, 3) else st, "npos": res["npos"][j],
-                            "err_bound": res["bound"][j], "path": "tiny-exact" if st == 3 else "tiny-lobpcg"}
+                # algorithmic work of a tiny block (counted here because the one launch
+                # has no per-block counters): nominal exact projection 9 n^3 + n (n + 1) p flops, A read
+                # and Pi written once
+                nk, pk = self.cfg.sizes[self.ids[k]], res["npos"][j]
+                infos[k] = {"iters": res["iters"][j], "status": 0 if st in (0, 3) else st, "npos": pk,
+                            "err_bound": res["bound"][j], "path": "tiny-exact" if st == 3 else "tiny-lobpcg",
+                            "flops": 9.0 * nk ** 3 + nk * (nk + 1.0) * pk, "bytes": 16.0 * nk * nk}
         t1 = time.perf_counter()
         if self.large:
             _, inf = api.project_batched(self.ctxs, [self.mats[k] for k in self.large], [tol] * len(self.large),
@@ -166,6 +171,9 @@ def run_c4(cfg, rank, world, dist, device, rounds, warmup, tol=None, tiny=True, 
         if paths is not None:
             for i in infos:
                 paths[i["path"]] = paths.get(i["path"], 0) + 1
+            work = paths.setdefault("alg_flops_bytes_per_round", [0.0, 0.0])
+            work[0] += sum(i.get("flops", 0.0) for i in infos) / rounds
+            work[1] += sum(i.get("bytes", 0.0) for i in infos) / rounds
             sp = paths.setdefault("host_ms_tiny_then_batched", [0.0, 0.0])
             sp[0] += sh.last_split_ms[0] / rounds
             sp[1] += sh.last_split_ms[1] / rounds
