@@ -430,3 +430,30 @@ def test_c4_tiny_routing_parity(api):
         sh.drift()
     sh.close()
     assert "tiny-exact" in paths and "lobpcg" in paths, paths
+
+
+def test_c4_direct_routing_parity(api):
+    """C4 shard with direct_n = 200: the n = 200 contexts are created with side = DIRECT (the exact
+    path a13), the n = 400 ones keep the one-third rule; every block matches the oracle's exact
+    projection over two rounds, every bound dominates its error, and no n <= 200 context ran LOBPCG."""
+    import torch
+    from paper_1912_02767_b200.multigpu import C4Shard
+    from workloads.generators import C4
+    cfg = C4(24)
+    sh = C4Shard(cfg, list(range(24)), torch.device("cuda", 0), direct_n=200)
+    seen = {}
+    for rnd in range(2):
+        infos = sh.project(1e-10)
+        for k, i in enumerate(sh.ids):
+            A = sh.mats[k].cpu().numpy()
+            err = np.linalg.norm(sh.outs[k].cpu().numpy() - project_exact(A))
+            assert infos[k]["status"] == 0, (rnd, i, infos[k])
+            assert err <= 1e-9 * np.linalg.norm(A), (rnd, i, cfg.sizes[i], infos[k]["path"])
+            if infos[k]["path"] in ("lobpcg", "direct"):
+                assert infos[k]["err_bound"] >= err, (rnd, i, err, infos[k])
+            if 112 < cfg.sizes[i] <= 200:
+                assert infos[k]["path"] == "direct", (rnd, i, infos[k])
+            seen.setdefault(cfg.sizes[i], set()).add(infos[k]["path"])
+        sh.drift()
+    sh.close()
+    assert 200 in seen and seen[200] == {"direct"}, seen
