@@ -2308,6 +2308,11 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
       }
     }
     int a = (int)Jorig.size();
+    // experiment (PSDPROJ_WIDE_NO_P = a0, default off): iterations whose active set is wider than a0
+    // leave dX out of the trial space (s = mU + a instead of mU + 2a; the Rayleigh-Ritz cost of the
+    // few wide iterations at the start of a warm call is several times that of a late one)
+    static const int wide_no_p = getenv("PSDPROJ_WIDE_NO_P") ? atoi(getenv("PSDPROJ_WIDE_NO_P")) : 0;
+    if (wide_no_p > 0 && !cold && a > wide_no_p) PJ.clear();
     int ap = (int)PJ.size();
     if (mU + a + qe + ap == 0) {
       // every column is locked and no direction is left, but the guard test (R12) is not met: the
