@@ -2307,6 +2307,32 @@ static int lobpcg_path(Run& run, int side, const double* A, int lda, double* Pi,
         if (hasP[jj]) PJ.push_back(jj);
       }
     }
+    // experiment (PSDPROJ_S_CAP = +-cap, default off): on warm calls keep the basis within the
+    // register tridiagonalisation's range (s <= cap) by giving directions only to the (cap - mU) / 2
+    // active columns with the smallest (cap > 0) or largest (cap < 0) residuals
+    static const int s_cap = getenv("PSDPROJ_S_CAP") ? atoi(getenv("PSDPROJ_S_CAP")) : 0;
+    if (s_cap != 0 && !cold && mU + 2 * (int)Jorig.size() > std::abs(s_cap)) {
+      const int keep_a = std::max(16, (std::abs(s_cap) - mU) / 2);
+      if ((int)Jnew.size() > keep_a) {
+        std::vector<int> ord(Jnew.size());
+        for (size_t i = 0; i < ord.size(); ++i) ord[i] = (int)i;
+        std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) {
+          return s_cap > 0 ? rU[Jnew[x]] < rU[Jnew[y]] : rU[Jnew[x]] > rU[Jnew[y]];
+        });
+        std::vector<char> sel(Jnew.size(), 0);
+        for (int i = 0; i < keep_a; ++i) sel[ord[i]] = 1;
+        std::vector<int> Jo2, Jn2, PJ2;
+        for (size_t i = 0; i < Jnew.size(); ++i)
+          if (sel[i]) {
+            Jo2.push_back(Jorig[i]);
+            Jn2.push_back(Jnew[i]);
+            if (hasP[Jnew[i]]) PJ2.push_back(Jnew[i]);
+          }
+        Jorig.swap(Jo2);
+        Jnew.swap(Jn2);
+        PJ.swap(PJ2);
+      }
+    }
     int a = (int)Jorig.size();
     // experiment (PSDPROJ_WIDE_NO_P = a0, default off): iterations whose active set is wider than a0
     // leave dX out of the trial space (s = mU + a instead of mU + 2a; the Rayleigh-Ritz cost of the
